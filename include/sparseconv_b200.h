@@ -1,0 +1,185 @@
+/*
+ * sparseconv_b200.h -- C ABI of the B200 (sm_100a) direct sparse convolution
+ * engine.  Plain pointers and sizes only: no torch, no C++ types.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to /root/reference/pkg/src/sparseconv).  The Python drop-in
+ * (paper_2011_06295_b200/) binds these with ctypes; INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Every function returns an scb_status; on failure scb_last_error() returns
+ *    a thread-local message.  SCB_ERR_SHAPE maps to the reference ShapeError
+ *    (errors.py:8), SCB_ERR_FORMAT to FormatError (errors.py:12),
+ *    SCB_ERR_CUDA / SCB_ERR_UNSUPPORTED to SparseConvError (errors.py:4).
+ *  - Host arrays are C-contiguous.  Device arrays are device pointers in the
+ *    current CUDA context of `device`.  `stream` is a cudaStream_t (NULL =
+ *    legacy default stream).  Launch functions never allocate or synchronise.
+ *  - dtype codes: the element type of activations/bias/values.
+ */
+#ifndef SPARSECONV_B200_H
+#define SPARSECONV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SCB_API __attribute__((visibility("default")))
+#else
+#define SCB_API
+#endif
+
+typedef enum {
+    SCB_OK = 0,
+    SCB_ERR_SHAPE = 1,       /* -> ShapeError   (errors.py:8)  */
+    SCB_ERR_FORMAT = 2,      /* -> FormatError  (errors.py:12) */
+    SCB_ERR_INTEGRITY = 3,   /* -> IntegrityError (errors.py:16) */
+    SCB_ERR_CUDA = 4,        /* -> SparseConvError */
+    SCB_ERR_ARG = 5,         /* -> SparseConvError (bad pointer / size) */
+    SCB_ERR_UNSUPPORTED = 6  /* -> SparseConvError */
+} scb_status;
+
+typedef enum { SCB_F32 = 0, SCB_F64 = 1, SCB_F16 = 2 } scb_dtype;
+
+/* Weight payload formats of the device tap program.
+ *  NATIVE : values stored in the activation dtype (f32 / f16 / f64)
+ *  CB4    : 4-bit codebook index + a 16-entry table (the paper's "4b/16b",
+ *           quantize.py:194-246; table = the layer's distinct values)
+ *  LIN16  : int16 fixed-point code * 2^-frac (quantize.py:28-71)          */
+typedef enum { SCB_W_NATIVE = 0, SCB_W_CB4 = 1, SCB_W_LIN16 = 2 } scb_wfmt;
+
+/* Geometry of one layer: ConvShape (shapes.py:17-77).  n is ignored by the
+ * layer object (the batch comes from each call, engine.py:52-54). */
+typedef struct {
+    int32_t n, c, h, w, k, r, s, stride, padding;
+} scb_shape;
+
+/* Arithmetic modes (flags for scb_conv_sparse). */
+#define SCB_FLAG_RELU      0x1u   /* fused max(.,0) epilogue (store.py:284)          */
+#define SCB_FLAG_FAST      0x2u   /* f32: single-rounding FFMA instead of mul+add   */
+#define SCB_FLAG_POOL2     0x4u   /* fused 2x2/2 max-pool epilogue (VGG stage glue) */
+#define SCB_FLAG_GENERIC   0x8u   /* force the generic (any-geometry) kernel        */
+
+/* Launch configuration: replaces EnginePlan.sub_batch_size (engine.py:28-39)
+ * and the timed tune_sub_batch (engine.py:143-166). variant < 0 = generic. */
+typedef struct {
+    int32_t variant;   /* index into the compiled tiled-kernel table, -1 = generic */
+    int32_t warps_k;   /* warp groups per CTA along output channels               */
+    int32_t imgs;      /* images per CTA                                          */
+    int32_t bh, bw;    /* output block per CTA                                    */
+    int32_t cc;        /* input channels staged per pipeline stage                */
+} scb_launch;
+
+/* Static description of a compiled tiled variant (for the tuner). */
+typedef struct {
+    int32_t r, s;        /* kernel extent it is specialised for */
+    int32_t kt;          /* output channels per warp group (accumulator rows) */
+    int32_t nbt, th, tw; /* images x rows x cols per thread */
+    int32_t io;          /* scb_dtype of activations */
+    int32_t wf;          /* payload: 0 f32, 1 f16, 2 codebook-4bit, 3 int16 fixed-point */
+    int32_t mode;        /* 0 exact mul+add, 1 fma */
+} scb_variant_info;
+
+/* ---------------------------------------------------------------------- */
+/* host-side weight-format builder (csr.py)                               */
+/* ---------------------------------------------------------------------- */
+
+/* analyze_sparsity (csr.py:80-91): per-channel nonzero counts of a KCRS
+ * tensor viewed as k rows of vol elements. */
+SCB_API scb_status scb_channel_nnz(const void* w, scb_dtype dt, int32_t k, int64_t vol,
+                                   int64_t* nnz_out);
+
+/* select_padding_zeros (csr.py:94-117). out has room for `deficit`. */
+SCB_API scb_status scb_select_padding_zeros(const void* flat, scb_dtype dt, int64_t len,
+                                            int64_t deficit, int64_t* out);
+
+/* build_csr (csr.py:120-165), two phases: count, then fill.  values are
+ * raw element copies (sign of promoted -0.0 preserved). */
+SCB_API scb_status scb_csr_count(const void* w, scb_dtype dt, const scb_shape* shape,
+                                 int32_t unify, int64_t* nnz_out, int32_t* level_out);
+SCB_API scb_status scb_build_csr(const void* w, scb_dtype dt, const scb_shape* shape,
+                                 int32_t unify, int64_t nnz_cap, void* values,
+                                 int32_t* colidx, int32_t* rowptr);
+
+/* CsrKernel.validate (csr.py:50-73). */
+SCB_API scb_status scb_validate_csr(const scb_shape* shape, const int32_t* colidx,
+                                    const int32_t* rowptr, int64_t nnz,
+                                    int32_t unified, int32_t level);
+
+/* decompress (csr.py:168-178) into a zeroed dense KCRS buffer. */
+SCB_API scb_status scb_decompress(const scb_shape* shape, scb_dtype dt, const void* values,
+                                  const int32_t* colidx, const int32_t* rowptr,
+                                  int64_t nnz, void* dense_out);
+
+/* ---------------------------------------------------------------------- */
+/* device layer: the uploaded, kernel-ready weights of one CsrKernel      */
+/* ---------------------------------------------------------------------- */
+
+typedef struct scb_layer scb_layer;
+
+/* Upload a validated CSR (values in `dt`) as a device tap program.
+ *  wfmt = CB4  : values must hold <= 16 distinct bit patterns
+ *  wfmt = LIN16: values must be exactly code * 2^-frac with |code| < 2^15
+ * (SCB_ERR_UNSUPPORTED otherwise). Allocates device memory on `device`. */
+SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wfmt wfmt,
+                                    const void* values, const int32_t* colidx,
+                                    const int32_t* rowptr, int64_t nnz, int32_t unified,
+                                    int32_t device, scb_layer** out);
+SCB_API scb_status scb_layer_destroy(scb_layer* layer);
+/* device bytes of the tap program used by `variant` (-1 = generic arrays). */
+SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t variant,
+                                          int64_t* bytes);
+
+/* conv_sparse (engine.py:68-87) on device buffers.
+ *  x: (n, C, H, W) in the layer dtype; bias: (K,) in the COMPUTE dtype
+ *  (f32 for f16/f32 layers, f64 for f64; engine.py:55-60) or NULL (zeros);
+ *  y: (n, K, E, F), or (n, K, E/2, F/2) with SCB_FLAG_POOL2.
+ *  cfg NULL = the heuristic default launch for this shape.
+ * Replaces _kernels.conv_sparse_kernel (_kernels.py:53-85) and
+ * conv_sparse1d_kernel (_kernels.py:88-114). Asynchronous on `stream`. */
+SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
+                                   void* y, int32_t n, uint32_t flags,
+                                   const scb_launch* cfg, void* stream);
+
+/* Launch candidates for the tuner (replaces SUB_BATCH_CANDIDATES,
+ * engine.py:25): writes up to `cap` configs valid for batch n. */
+SCB_API scb_status scb_launch_candidates(const scb_layer* layer, int32_t n, uint32_t flags,
+                                         scb_launch* out, int32_t cap, int32_t* count);
+/* Heuristic default launch; prefer_imgs > 1 restricts it to configs with that
+ * many images per CTA when one exists (EnginePlan.sub_batch_size: the
+ * paper's images-per-block). */
+SCB_API scb_status scb_default_launch(const scb_layer* layer, int32_t n, uint32_t flags,
+                                      int32_t prefer_imgs, scb_launch* out);
+
+SCB_API int32_t scb_variant_count(void);
+SCB_API scb_status scb_variant_get(int32_t idx, scb_variant_info* out);
+
+/* ---------------------------------------------------------------------- */
+/* glue for network runners (Model.forward, store.py:263-292)             */
+/* ---------------------------------------------------------------------- */
+
+/* 2x2 stride-2 max pool over (n*c) planes of h x w (h, w even). */
+SCB_API scb_status scb_maxpool2(scb_dtype dt, const void* x, void* y, int64_t planes,
+                                int32_t h, int32_t w, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* measurement                                                            */
+/* ---------------------------------------------------------------------- */
+
+/* CUDA-core arithmetic peak microbenchmark on `device`.  For each probe i
+ * writes name (<=15 chars) and MAC/s (multiply-accumulates per second) into
+ * names[i*16] and macs_per_s[i].  Probes: ffma, ffma2, fmul_fadd,
+ * fmul2_fadd, fmul_fadd2, fhfma, hfma2. Synchronous. */
+SCB_API scb_status scb_fma_peaks(int32_t device, char* names, double* macs_per_s,
+                                 int32_t cap, int32_t* count);
+
+SCB_API const char* scb_last_error(void);
+SCB_API const char* scb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSECONV_B200_H */

@@ -1,0 +1,143 @@
+"""ctypes binding of the C ABI in include/sparseconv_b200.h.
+
+The shared library is built in-tree (paper_2011_06295_b200/_lib/) by
+``paper_2011_06295_b200/csrc/Makefile`` (``__graft_entry__.build()``).  There
+is no CPU fallback: if the library is missing every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from pathlib import Path
+
+from .errors import FormatError, IntegrityError, ShapeError, SparseConvError
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "_lib" / "libsparseconv_b200.so"
+CSRC = PKG / "csrc"
+
+SCB_OK, SCB_ERR_SHAPE, SCB_ERR_FORMAT, SCB_ERR_INTEGRITY = 0, 1, 2, 3
+SCB_ERR_CUDA, SCB_ERR_ARG, SCB_ERR_UNSUPPORTED = 4, 5, 6
+
+SCB_F32, SCB_F64, SCB_F16 = 0, 1, 2
+SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16 = 0, 1, 2
+
+FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC = 0x1, 0x2, 0x4, 0x8
+
+# every symbol include/sparseconv_b200.h declares
+EXPORTS = (
+    "scb_channel_nnz", "scb_select_padding_zeros", "scb_csr_count", "scb_build_csr",
+    "scb_validate_csr", "scb_decompress", "scb_layer_create", "scb_layer_destroy",
+    "scb_layer_weight_bytes", "scb_conv_sparse", "scb_launch_candidates",
+    "scb_default_launch", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
+    "scb_fma_peaks", "scb_last_error", "scb_version",
+)
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("n", "c", "h", "w", "k", "r", "s", "stride", "padding")]
+
+
+class Launch(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("variant", "warps_k", "imgs", "bh", "bw", "cc")]
+
+    def as_tuple(self):
+        return (self.variant, self.warps_k, self.imgs, self.bh, self.bw, self.cc)
+
+    @classmethod
+    def from_tuple(cls, t):
+        return cls(*[int(v) for v in t])
+
+
+class VariantInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("r", "s", "kt", "nbt", "th", "tw", "io", "wf", "mode")]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(quiet: bool = True) -> Path:
+    """Compile the CUDA library for sm_100a in place (nvcc cross-compiles; no GPU needed)."""
+    cmd = ["make", "-C", str(CSRC), f"-j{min(8, os.cpu_count() or 1)}"]
+    subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL if quiet else None)
+    return LIB_PATH
+
+
+def lib():
+    """Load libsparseconv_b200.so; raise loudly if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise SparseConvError(
+                f"CUDA library {LIB_PATH} is missing: run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        vp, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+        P = ctypes.POINTER
+        sig = {
+            "scb_channel_nnz": [vp, i32, i32, i64, vp],
+            "scb_select_padding_zeros": [vp, i32, i64, i64, vp],
+            "scb_csr_count": [vp, i32, P(Shape), i32, P(i64), P(i32)],
+            "scb_build_csr": [vp, i32, P(Shape), i32, i64, vp, vp, vp],
+            "scb_validate_csr": [P(Shape), vp, vp, i64, i32, i32],
+            "scb_decompress": [P(Shape), i32, vp, vp, vp, i64, vp],
+            "scb_layer_create": [P(Shape), i32, i32, vp, vp, vp, i64, i32, i32, P(vp)],
+            "scb_layer_destroy": [vp],
+            "scb_layer_weight_bytes": [vp, i32, P(i64)],
+            "scb_conv_sparse": [vp, vp, vp, vp, i32, u32, P(Launch), vp],
+            "scb_launch_candidates": [vp, i32, u32, P(Launch), i32, P(i32)],
+            "scb_default_launch": [vp, i32, u32, i32, P(Launch)],
+            "scb_variant_get": [i32, P(VariantInfo)],
+            "scb_maxpool2": [i32, vp, vp, i64, i32, i32, vp],
+            "scb_fma_peaks": [i32, vp, vp, i32, P(i32)],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.scb_variant_count.restype = i32
+        L.scb_variant_count.argtypes = []
+        L.scb_last_error.restype = ctypes.c_char_p
+        L.scb_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().scb_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a C status onto the reference exception hierarchy (errors.py)."""
+    if status == SCB_OK:
+        return
+    msg = last_error() or what
+    if status == SCB_ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == SCB_ERR_FORMAT:
+        raise FormatError(msg)
+    if status == SCB_ERR_INTEGRITY:
+        raise IntegrityError(msg)
+    raise SparseConvError(f"{what}: {msg}" if what else msg)
+
+
+def shape_struct(sh) -> Shape:
+    return Shape(int(sh.n), int(sh.c), int(sh.h), int(sh.w), int(sh.k), int(sh.r), int(sh.s),
+                 int(sh.stride), int(sh.padding))
+
+
+def variants():
+    L = lib()
+    out = []
+    for i in range(L.scb_variant_count()):
+        v = VariantInfo()
+        check(L.scb_variant_get(i, ctypes.byref(v)))
+        out.append({f: getattr(v, f) for f, _ in VariantInfo._fields_})
+    return out

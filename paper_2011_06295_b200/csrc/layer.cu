@@ -1,0 +1,522 @@
+// Device layer objects, the tap-program builder, launch-configuration rules
+// and the C-ABI launch entry points.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "variants.h"
+
+using namespace scb;
+
+namespace {
+
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kMaxThreads = 256;
+const int kKtChoices[] = {4, 8};
+
+scb_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Tap program of one KT: taps of group g (channels g*KT .. g*KT+KT-1)
+// ordered (c, kk, r, s); ptr[g][c] = first tap of channel c in group g.
+struct Program {
+    int kt = 0;
+    int groups = 0;
+    std::vector<int32_t> h_ptr;   // groups x (C+1)
+    int32_t* d_ptr = nullptr;
+    Tap* d_taps = nullptr;
+    int64_t ntaps = 0;
+    std::map<int, int> tap_cap;   // cc -> max taps per (group, chunk) + 1
+};
+
+}  // namespace
+
+struct scb_layer {
+    Geom g{};
+    scb_dtype dt = SCB_F32;
+    scb_wfmt wfmt = SCB_W_NATIVE;
+    int wf = WF_F32;
+    int device = 0;
+    bool unified = true;
+    int64_t nnz = 0;
+    QuantAux q{};
+    // generic-kernel arrays
+    void* d_values = nullptr;
+    int32_t* d_dec = nullptr;
+    int32_t* d_rowptr = nullptr;
+    std::vector<Program> progs;
+    std::mutex mu;
+
+    ~scb_layer() {
+        DeviceGuard dg(device);
+        cudaFree(d_values);
+        cudaFree(d_dec);
+        cudaFree(d_rowptr);
+        for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); }
+    }
+    Program* prog(int kt) {
+        for (auto& p : progs) if (p.kt == kt) return &p;
+        return nullptr;
+    }
+    const Program* prog(int kt) const {
+        for (auto& p : progs) if (p.kt == kt) return &p;
+        return nullptr;
+    }
+    int cap_for(Program& p, int cc) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = p.tap_cap.find(cc);
+        if (it != p.tap_cap.end()) return it->second;
+        const int C = g.c;
+        int mx = 0;
+        for (int gg = 0; gg < p.groups; ++gg)
+            for (int c0 = 0; c0 < C; c0 += cc) {
+                int c1 = std::min(c0 + cc, C);
+                mx = std::max(mx, p.h_ptr[(size_t)gg * (C + 1) + c1] - p.h_ptr[(size_t)gg * (C + 1) + c0]);
+            }
+        p.tap_cap[cc] = mx + 1;  // one slot of slack for the software prefetch
+        return mx + 1;
+    }
+};
+
+namespace {
+
+// Derive the device payload of every nonzero for the requested format.
+// Returns false (with error set) if the values do not fit the format exactly.
+bool encode_payloads(scb_layer* L, const unsigned char* vals, std::vector<uint32_t>& pay,
+                     std::vector<float>& as_f32) {
+    const int es = dtype_size(L->dt);
+    const int64_t nnz = L->nnz;
+    pay.resize(nnz);
+    as_f32.resize(nnz);
+    for (int64_t t = 0; t < nnz; ++t) {
+        float f;
+        if (L->dt == SCB_F32) std::memcpy(&f, vals + t * es, 4);
+        else if (L->dt == SCB_F16) { uint16_t h; std::memcpy(&h, vals + t * 2, 2); __half_raw hr; hr.x = h; f = __half2float(__half(hr)); }
+        else { double d; std::memcpy(&d, vals + t * 8, 8); f = (float)d; }
+        as_f32[t] = f;
+    }
+    if (L->wfmt == SCB_W_NATIVE) {
+        for (int64_t t = 0; t < nnz; ++t) {
+            if (L->dt == SCB_F16) { uint16_t h; std::memcpy(&h, vals + t * 2, 2); pay[t] = h; }
+            else { uint32_t b; std::memcpy(&b, &as_f32[t], 4); pay[t] = b; }
+        }
+        return true;
+    }
+    if (L->wfmt == SCB_W_CB4) {
+        // codebook: the layer's distinct values (bit patterns) form the table
+        std::vector<uint32_t> table;
+        for (int64_t t = 0; t < nnz; ++t) {
+            uint32_t b; std::memcpy(&b, &as_f32[t], 4);
+            auto it = std::find(table.begin(), table.end(), b);
+            if (it == table.end()) {
+                if (table.size() == 16) { set_error("CB4 needs <= 16 distinct weight values"); return false; }
+                table.push_back(b);
+                it = table.end() - 1;
+            }
+            pay[t] = (uint32_t)(it - table.begin());
+        }
+        for (size_t i = 0; i < 16; ++i) {
+            uint32_t b = i < table.size() ? table[i] : 0u;
+            std::memcpy(&L->q.cb[i], &b, 4);
+        }
+        return true;
+    }
+    // LIN16: v = code * 2^-frac; find the coarsest power-of-two grid holding all values
+    int frac = -126;
+    for (int64_t t = 0; t < nnz; ++t) {
+        float v = as_f32[t];
+        if (v == 0.f) continue;
+        if (!std::isfinite(v)) { set_error("LIN16 needs finite weights"); return false; }
+        int ex;
+        float m = std::frexp(v, &ex);  // v = m * 2^ex, |m| in [0.5,1)
+        // trailing precision: smallest power of two dividing v
+        uint32_t mant = (uint32_t)std::ldexp(std::fabs(m), 24);
+        int tz = 0;
+        while (tz < 24 && !(mant & (1u << tz))) ++tz;
+        int lsb = ex - 24 + tz;  // v is a multiple of 2^lsb
+        frac = std::max(frac, -lsb);
+    }
+    if (frac == -126) frac = 0;
+    const float scale = std::ldexp(1.0f, -frac);
+    for (int64_t t = 0; t < nnz; ++t) {
+        double code = std::ldexp((double)as_f32[t], frac);
+        if (std::fabs(code) > 32767.0 || code != std::floor(code)) {
+            set_error("LIN16 needs |code| < 2^15 on a common power-of-two grid");
+            return false;
+        }
+        int c = (int)code;
+        if ((float)c * scale != as_f32[t]) { set_error("LIN16 decode is not exact"); return false; }
+        pay[t] = (uint32_t)(uint16_t)(int16_t)c;
+    }
+    L->q.scale = scale;
+    return true;
+}
+
+scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int32_t* rowptr,
+                         const std::vector<uint32_t>& pay) {
+    const Geom& g = L->g;
+    Program P;
+    P.kt = kt;
+    P.groups = (g.k + kt - 1) / kt;
+    const int C = g.c, RS = g.r * g.s;
+    const int64_t plane = (int64_t)g.hp * g.wp;
+    P.h_ptr.assign((size_t)P.groups * (C + 1), 0);
+    std::vector<Tap> taps;
+    taps.reserve(L->nnz);
+    std::vector<int32_t> cur(kt);
+    for (int gg = 0; gg < P.groups; ++gg) {
+        for (int kk = 0; kk < kt; ++kk) {
+            int k = gg * kt + kk;
+            cur[kk] = k < g.k ? rowptr[k] : 0;
+        }
+        for (int c = 0; c < C; ++c) {
+            P.h_ptr[(size_t)gg * (C + 1) + c] = (int32_t)taps.size();
+            for (int kk = 0; kk < kt; ++kk) {
+                int k = gg * kt + kk;
+                if (k >= g.k) break;
+                while (cur[kk] < rowptr[k + 1] && colidx[cur[kk]] / plane == c) {
+                    int64_t rem = colidx[cur[kk]] % plane;
+                    int r = (int)(rem / g.wp), s = (int)(rem % g.wp);
+                    Tap tp;
+                    tp.meta = (uint32_t)(kk * RS + r * g.s + s);
+                    tp.payload = pay[cur[kk]];
+                    taps.push_back(tp);
+                    ++cur[kk];
+                }
+            }
+        }
+        P.h_ptr[(size_t)gg * (C + 1) + C] = (int32_t)taps.size();
+    }
+    if ((int64_t)taps.size() != L->nnz) return fail(SCB_ERR_FORMAT, "tap program lost entries (colidx order?)");
+    taps.push_back(Tap{0u, 0u});  // slack slot for the prefetch at the very end
+    P.ntaps = L->nnz;
+    cudaError_t e;
+    if ((e = cudaMalloc(&P.d_ptr, P.h_ptr.size() * sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&P.d_taps, taps.size() * sizeof(Tap))) != cudaSuccess) { cudaFree(P.d_ptr); return cuda_fail(e, "cudaMalloc"); }
+    cudaMemcpy(P.d_ptr, P.h_ptr.data(), P.h_ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(P.d_taps, taps.data(), taps.size() * sizeof(Tap), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(P.d_ptr); cudaFree(P.d_taps); return cuda_fail(e, "cudaMemcpy"); }
+    L->progs.push_back(std::move(P));
+    return SCB_OK;
+}
+
+int wf_of(const scb_layer* L) {
+    if (L->wfmt == SCB_W_CB4) return WF_CB4;
+    if (L->wfmt == SCB_W_LIN16) return WF_LIN16;
+    return L->dt == SCB_F16 ? WF_F16 : WF_F32;
+}
+
+bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t flags) {
+    const Geom& g = L->g;
+    if (L->dt == SCB_F64) return false;
+    if (g.stride != 1 || v.r != g.r || v.s != g.s) return false;
+    if (v.io != L->dt || v.wf != L->wf) return false;
+    const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
+    if (v.mode != mode) return false;
+    if (!L->prog(v.kt)) return false;
+    if ((flags & SCB_FLAG_POOL2) && ((v.th & 1) || (v.tw & 1))) return false;
+    return true;
+}
+
+int pix_bytes(const scb_variant_info& v) { return v.nbt == 2 ? 8 : 4; }
+
+int row_pitch(const scb_variant_info& v, int bw) {
+    int need = bw + v.s - 1 + 3;
+    return (need + 3) & ~3;
+}
+
+// Validate a launch and compute its derived quantities.
+struct Derived {
+    int wp, threads, row, tap_cap, n_ey, n_fx, kblocks, nb;
+    size_t smem;
+    unsigned grid;
+};
+
+scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    if (c.variant < 0 || c.variant >= g_num_variants) return fail(SCB_ERR_SHAPE, "bad variant index");
+    const scb_variant_info& v = g_variants[c.variant].info;
+    if (!variant_matches(L, v, flags)) return fail(SCB_ERR_SHAPE, "variant does not match the layer");
+    const Geom& g = L->g;
+    if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 || c.warps_k < 1)
+        return fail(SCB_ERR_SHAPE, "launch tile not a multiple of the thread tile");
+    const int px = (c.imgs / v.nbt) * (c.bh / v.th) * (c.bw / v.tw);
+    if (px % 32) return fail(SCB_ERR_SHAPE, "pixel threads per warp group must be a multiple of 32");
+    d->wp = px / 32;
+    d->threads = c.warps_k * px;
+    if (d->threads > kMaxThreads) return fail(SCB_ERR_SHAPE, "too many threads per CTA");
+    if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1))) return fail(SCB_ERR_SHAPE, "pool needs even output extents");
+    Program* P = L->prog(v.kt);
+    d->row = row_pitch(v, c.bw);
+    d->tap_cap = L->cap_for(*P, c.cc);
+    d->smem = (size_t)2 * (c.imgs / v.nbt) * c.cc * (c.bh + v.r - 1) * d->row * pix_bytes(v) +
+              (size_t)2 * c.warps_k * d->tap_cap * sizeof(Tap);
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    d->n_ey = (g.e + c.bh - 1) / c.bh;
+    d->n_fx = (g.f + c.bw - 1) / c.bw;
+    d->kblocks = (P->groups + c.warps_k - 1) / c.warps_k;
+    d->nb = (n + c.imgs - 1) / c.imgs;
+    const int64_t grid = (int64_t)d->kblocks * d->n_fx * d->n_ey * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
+int ceil_to(int a, int m) { return (a + m - 1) / m * m; }
+
+// Enumerate launch candidates for a layer and batch.
+void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out) {
+    const Geom& g = L->g;
+    for (int vi = 0; vi < g_num_variants; ++vi) {
+        const scb_variant_info& v = g_variants[vi].info;
+        if (!variant_matches(L, v, flags)) continue;
+        // spatial blocks: whole plane (rounded to the thread tile) when small,
+        // otherwise 32-wide / 16-high strips
+        std::vector<std::pair<int, int>> blocks;
+        const int eh = ceil_to(g.e, v.th), fw = ceil_to(g.f, v.tw);
+        blocks.push_back({std::min(eh, 32), std::min(fw, 32)});
+        if (eh > 16) blocks.push_back({16, std::min(fw, 32)});
+        if (eh > 8 && fw >= 8) blocks.push_back({8, std::min(fw, 32)});
+        for (auto& b : blocks) {
+            int bh = ceil_to(std::min(b.first, eh), v.th), bw = ceil_to(std::min(b.second, fw), v.tw);
+            const int tiles = (bh / v.th) * (bw / v.tw);
+            // smallest image count making the warp group a whole number of warps
+            int slots = 1;
+            while ((slots * tiles) % 32) ++slots;
+            for (int mult : {1, 2, 4}) {
+                int imgs = slots * mult * v.nbt;
+                if (imgs > std::max(v.nbt, ceil_to(n, v.nbt)) && mult > 1) break;
+                for (int wk : {1, 2, 4}) {
+                    for (int cc : {2, 4, 8}) {
+                        scb_launch c{vi, wk, imgs, bh, bw, cc};
+                        Derived d;
+                        if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                        out.push_back(c);
+                    }
+                }
+            }
+        }
+    }
+    set_error("");
+}
+
+// Heuristic default: prefer the largest accumulator tile that still puts
+// >= 2 CTAs' worth of warps on every SM, then 2 warp groups, 4-channel stages.
+bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_launch* out) {
+    std::vector<scb_launch> cands;
+    enumerate(L, n, flags, cands);
+    if (cands.empty()) return false;
+    if (prefer_imgs > 1) {
+        std::vector<scb_launch> pref;
+        for (auto& c : cands) if (c.imgs == prefer_imgs) pref.push_back(c);
+        if (!pref.empty()) cands.swap(pref);
+    }
+    double best = -1e30;
+    for (auto& c : cands) {
+        Derived d;
+        if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+        const scb_variant_info& v = g_variants[c.variant].info;
+        const double acc = (double)v.kt * v.nbt * v.th * v.tw;          // reuse per tap
+        const double warps = (double)d.grid * d.threads / 32.0;
+        const double fill = std::min(1.0, warps / (148.0 * 12.0));        // occupancy proxy
+        const double stage_cost = 1.0 / (c.warps_k * v.kt);              // input restaging per channel
+        double score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * stage_cost;
+        if (c.cc == 4) score += 0.05;
+        if (c.warps_k == 2) score += 0.05;
+        if (score > best) { best = score; *out = c; }
+    }
+    set_error("");
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wfmt wfmt,
+                                    const void* values, const int32_t* colidx,
+                                    const int32_t* rowptr, int64_t nnz, int32_t unified,
+                                    int32_t device, scb_layer** out) {
+    if (!out) return fail(SCB_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    Geom g;
+    scb_status st = make_geom(shape, &g);
+    if (st != SCB_OK) return st;
+    if (dtype_size(dt) == 0) return fail(SCB_ERR_ARG, "bad dtype");
+    if (!rowptr || (nnz > 0 && (!values || !colidx))) return fail(SCB_ERR_ARG, "NULL arrays");
+    if (g.r > 63 || g.s > 63 || g.c >= (1 << 19)) return fail(SCB_ERR_UNSUPPORTED, "kernel extent > 63 or C >= 2^19");
+    if (dt == SCB_F64 && wfmt != SCB_W_NATIVE) return fail(SCB_ERR_UNSUPPORTED, "f64 supports native weights only");
+    int level = 0;
+    for (int k = 0; k < g.k; ++k) level = std::max(level, rowptr[k + 1] - rowptr[k]);
+    st = scb_validate_csr(shape, colidx, rowptr, nnz, unified ? 1 : 0, level);
+    if (st != SCB_OK) return st;
+
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(SCB_ERR_CUDA, "cannot select device");
+    std::unique_ptr<scb_layer> L(new scb_layer());
+    L->g = g;
+    L->dt = dt;
+    L->wfmt = wfmt;
+    L->device = device;
+    L->unified = unified != 0;
+    L->nnz = nnz;
+    L->wf = wf_of(L.get());
+
+    std::vector<uint32_t> pay;
+    std::vector<float> as_f32;
+    if (!encode_payloads(L.get(), static_cast<const unsigned char*>(values), pay, as_f32))
+        return SCB_ERR_UNSUPPORTED;
+
+    // generic arrays: native values + decoded (c, r, s)
+    const int es = dtype_size(dt);
+    const int64_t plane = (int64_t)g.hp * g.wp;
+    std::vector<int32_t> dec(std::max<int64_t>(nnz, 1));
+    for (int64_t t = 0; t < nnz; ++t) {
+        int64_t c = colidx[t] / plane, rem = colidx[t] % plane;
+        dec[t] = (int32_t)((c << 12) | ((rem / g.wp) << 6) | (rem % g.wp));
+    }
+    cudaError_t e;
+    if ((e = cudaMalloc(&L->d_values, std::max<int64_t>(nnz, 1) * es)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&L->d_dec, dec.size() * 4)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&L->d_rowptr, (g.k + 1) * 4)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if (nnz > 0) cudaMemcpy(L->d_values, values, nnz * es, cudaMemcpyHostToDevice);
+    cudaMemcpy(L->d_dec, dec.data(), dec.size() * 4, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(L->d_rowptr, rowptr, (g.k + 1) * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
+
+    // tiled tap programs for every KT a compiled variant of this (R, S) uses
+    if (dt != SCB_F64 && g.stride == 1) {
+        for (int kt : kKtChoices) {
+            bool used = false;
+            for (int vi = 0; vi < g_num_variants; ++vi) {
+                const auto& v = g_variants[vi].info;
+                used |= (v.kt == kt && v.r == g.r && v.s == g.s && v.io == dt && v.wf == L->wf);
+            }
+            if (!used) continue;
+            st = build_program(L.get(), kt, colidx, rowptr, pay);
+            if (st != SCB_OK) return st;
+        }
+    }
+    *out = L.release();
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_layer_destroy(scb_layer* layer) {
+    delete layer;
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t variant, int64_t* bytes) {
+    if (!layer || !bytes) return fail(SCB_ERR_ARG, "NULL");
+    auto* L = const_cast<scb_layer*>(layer);
+    if (variant < 0) {
+        *bytes = L->nnz * (dtype_size(L->dt) + 4) + (int64_t)(L->g.k + 1) * 4;
+        return SCB_OK;
+    }
+    if (variant >= g_num_variants) return fail(SCB_ERR_ARG, "bad variant");
+    Program* P = L->prog(g_variants[variant].info.kt);
+    if (!P) return fail(SCB_ERR_ARG, "no program for this variant");
+    *bytes = P->ntaps * (int64_t)sizeof(Tap) + (int64_t)P->h_ptr.size() * 4;
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_launch_candidates(const scb_layer* layer, int32_t n, uint32_t flags,
+                                         scb_launch* out, int32_t cap, int32_t* count) {
+    if (!layer || !count) return fail(SCB_ERR_ARG, "NULL");
+    std::vector<scb_launch> c;
+    enumerate(const_cast<scb_layer*>(layer), std::max(n, 1), flags, c);
+    *count = (int32_t)c.size();
+    for (int i = 0; i < (int)c.size() && i < cap; ++i) out[i] = c[i];
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_default_launch(const scb_layer* layer, int32_t n, uint32_t flags,
+                                      int32_t prefer_imgs, scb_launch* out) {
+    if (!layer || !out) return fail(SCB_ERR_ARG, "NULL");
+    if ((flags & SCB_FLAG_GENERIC) ||
+        !pick_default(const_cast<scb_layer*>(layer), std::max(n, 1), flags, prefer_imgs, out)) {
+        *out = scb_launch{-1, 0, 0, 0, 0, 0};
+    }
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
+                                   void* y, int32_t n, uint32_t flags,
+                                   const scb_launch* cfg, void* stream) {
+    if (!layer) return fail(SCB_ERR_ARG, "layer is NULL");
+    auto* L = const_cast<scb_layer*>(layer);
+    if (n < 0) return fail(SCB_ERR_SHAPE, "negative batch");
+    if (n == 0) return SCB_OK;
+    if (!x || !y) return fail(SCB_ERR_ARG, "NULL activation buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DeviceGuard dg(L->device);
+    if (!dg.ok) return fail(SCB_ERR_CUDA, "cannot select device");
+
+    scb_launch c;
+    if (cfg) c = *cfg;
+    else scb_default_launch(layer, n, flags, 0, &c);
+    const Geom& g = L->g;
+    if (c.variant < 0 || (flags & SCB_FLAG_GENERIC)) {
+        if (flags & SCB_FLAG_POOL2) return fail(SCB_ERR_UNSUPPORTED, "fused pool needs a tiled variant");
+        GenericParams p;
+        p.x = x; p.bias = bias; p.y = y; p.values = L->d_values; p.dec = L->d_dec; p.rowptr = L->d_rowptr;
+        p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f;
+        p.stride = g.stride; p.pad = g.pad; p.flags = flags;
+        cudaError_t e = launch_generic(p, L->dt, (flags & SCB_FLAG_FAST) != 0, st);
+        return e == cudaSuccess ? SCB_OK : cuda_fail(e, "generic kernel launch");
+    }
+    Derived d;
+    scb_status s = derive(L, c, n, flags, &d);
+    if (s != SCB_OK) return s;
+    const VariantEntry& ve = g_variants[c.variant];
+    Program* P = L->prog(ve.info.kt);
+    TiledParams p;
+    p.x = x; p.bias = bias; p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps; p.q = L->q;
+    p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f; p.pad = g.pad;
+    p.imgs = c.imgs; p.bh = c.bh; p.bw = c.bw; p.cc = c.cc; p.wk = c.warps_k;
+    p.wp = d.wp; p.row = d.row; p.tap_cap = d.tap_cap;
+    p.n_ey = d.n_ey; p.n_fx = d.n_fx; p.kblocks = d.kblocks; p.groups = P->groups;
+    p.flags = flags;
+    cudaError_t e = ve.launch(p, d.grid, (unsigned)d.threads, d.smem, st);
+    return e == cudaSuccess ? SCB_OK : cuda_fail(e, "tiled kernel launch");
+}
+
+SCB_API int32_t scb_variant_count(void) { return g_num_variants; }
+
+SCB_API scb_status scb_variant_get(int32_t idx, scb_variant_info* out) {
+    if (idx < 0 || idx >= g_num_variants || !out) return fail(SCB_ERR_ARG, "bad variant index");
+    *out = g_variants[idx].info;
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_maxpool2(scb_dtype dt, const void* x, void* y, int64_t planes, int32_t h,
+                                int32_t w, void* stream) {
+    if ((h & 1) || (w & 1)) return fail(SCB_ERR_SHAPE, "pool needs even extents");
+    cudaError_t e = launch_maxpool2(dt, x, y, planes, h, w, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SCB_OK : cuda_fail(e, "maxpool launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+"""Operator API: direct sparse convolution on B200 (drop-in for the
+reference's engine.py).
+
+``conv_sparse(x, kernel, bias, plan)`` keeps the reference's contract
+(engine.py:68-87): batch taken from ``x`` (``kernel.shape.n`` ignored), bias
+optional (zeros), output dtype = input dtype, f16 storage computed in f32,
+outputs independent of ``sub_batch_size`` / ``worker_count``.  What changes is
+where it runs: one asynchronous launch of an sm_100a kernel from
+libsparseconv_b200 (no CPU fallback).
+
+Inputs may be
+  * numpy arrays  -> copied to the GPU, result copied back (numpy out);
+  * torch CUDA tensors -> zero-copy on their device and current stream
+    (torch tensor out, nothing synchronised).
+"""
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .device import device_layer
+from .errors import ShapeError
+from .geometry import check_nchw, compute_dtype, dtype_of
+from .weights import CsrKernel
+
+log = logging.getLogger(__name__)
+
+SUB_BATCH_CANDIDATES = (1, 2, 4, 8, 16)
+WEIGHT_FORMATS = ("native", "cb4", "lin16")
+
+
+@dataclass(frozen=True)
+class EnginePlan:
+    """Execution plan.  ``sub_batch_size`` and ``worker_count`` keep the
+    reference's validation (engine.py:28-39).  On the GPU, ``sub_batch_size``
+    > 1 asks for that many images per CTA (the paper's subBatchSize,
+    PAPER.md:151) and ``worker_count`` is accepted and ignored.
+
+    GPU-only fields: ``launch`` (explicit scb_launch tuple, see
+    tuner.tune_launch), ``fast_math`` (f32 single-rounding FMA instead of the
+    reference's separately rounded multiply and add), ``weight_format``
+    ("native" | "cb4" 4-bit codebook | "lin16" int16 fixed point, decoded in
+    registers) and ``device`` (CUDA device for numpy inputs)."""
+
+    sub_batch_size: int = 1
+    worker_count: int = 1
+    launch: tuple | None = None
+    fast_math: bool = False
+    weight_format: str = "native"
+    device: int | None = None
+
+    def __post_init__(self):
+        if self.sub_batch_size not in SUB_BATCH_CANDIDATES:
+            raise ShapeError(f"sub_batch_size must be in {SUB_BATCH_CANDIDATES}")
+        if self.worker_count < 1:
+            raise ShapeError("worker_count must be >= 1")
+        if self.weight_format not in WEIGHT_FORMATS:
+            raise ShapeError(f"weight_format must be in {WEIGHT_FORMATS}")
+
+
+# launches chosen by tuner.tune_launch: (layer signature, n, flags) -> launch
+TUNED: dict = {}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+_TORCH_DT = None
+
+
+def _torch_dtype(dt: np.dtype):
+    global _TORCH_DT
+    torch = _torch()
+    if _TORCH_DT is None:
+        _TORCH_DT = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+                     np.dtype(np.float16): torch.float16}
+    return _TORCH_DT[np.dtype(dt)]
+
+
+def _io_dtype(x_dtype: np.dtype, kernel: CsrKernel) -> np.dtype:
+    """Activation dtype the device kernel runs in.  f16 activations with f16
+    values use the f16 kernels (f16*f16 products are exact in f32, so FFMA is
+    bit-equal to the reference); any other f16 combination computes on f32
+    copies exactly like the reference's astype(f32) (engine.py:62-64)."""
+    if x_dtype == np.float16 and kernel.values.dtype != np.float16:
+        return np.dtype(np.float32)
+    return compute_dtype(x_dtype)
+
+
+def _flags(plan: EnginePlan, relu: bool, pool: bool, generic: bool) -> int:
+    f = 0
+    if relu:
+        f |= _abi.FLAG_RELU
+    if pool:
+        f |= _abi.FLAG_POOL2
+    if plan.fast_math:
+        f |= _abi.FLAG_FAST
+    if generic:
+        f |= _abi.FLAG_GENERIC
+    return f
+
+
+def _check_geometry(x, kernel: CsrKernel):
+    sh = kernel.shape
+    if tuple(x.shape[1:]) != (sh.c, sh.h, sh.w):
+        raise ShapeError(f"input {tuple(x.shape)} does not match kernel geometry "
+                         f"(C,H,W)=({sh.c},{sh.h},{sh.w})")
+
+
+def _run(x, kernel: CsrKernel, bias, plan: EnginePlan, *, relu=False, pool=False,
+         generic=False, out=None):
+    torch = _torch()
+    x = check_nchw(x)
+    _check_geometry(x, kernel)
+    sh = kernel.shape
+    x_dt = dtype_of(x)
+    ct = compute_dtype(x_dt)
+    io = _io_dtype(x_dt, kernel)
+    n = int(x.shape[0])
+    is_torch = not isinstance(x, np.ndarray)
+    if is_torch and x.is_cuda:
+        dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    else:
+        if not torch.cuda.is_available():
+            from .errors import SparseConvError
+            raise SparseConvError("no CUDA device: the B200 engine has no CPU fallback")
+        dev = plan.device if plan.device is not None else torch.cuda.current_device()
+    tdev = torch.device("cuda", dev)
+    # bias in the compute dtype (engine.py:55-60)
+    if bias is None:
+        b_dev = None
+    else:
+        b_np = bias.detach().cpu().numpy() if hasattr(bias, "detach") else np.asarray(bias)
+        b_np = np.ascontiguousarray(b_np, dtype=ct if io != np.float64 else np.float64)
+        if b_np.shape != (sh.k,):
+            raise ShapeError(f"bias must have shape ({sh.k},)")
+        if io == np.float16:
+            b_np = b_np.astype(np.float32)
+        b_dev = torch.from_numpy(b_np).to(tdev)
+    layer = device_layer(kernel, dev, io, plan.weight_format)
+    flags = _flags(plan, relu, pool, generic)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        if is_torch:
+            x_dev = x.to(tdev)
+        else:
+            x_dev = torch.from_numpy(np.ascontiguousarray(x)).to(tdev, non_blocking=False)
+        if dtype_of(x_dev) != io:
+            x_dev = x_dev.to(_torch_dtype(io))
+        x_dev = x_dev.contiguous()
+        e, f = (sh.e // 2, sh.f // 2) if pool else (sh.e, sh.f)
+        if out is None or io != x_dt:
+            y = torch.empty((n, sh.k, e, f), dtype=_torch_dtype(io), device=tdev)
+        else:
+            y = out
+        launch = _choose_launch(layer, n, flags, plan)
+        layer.launch(x_dev.data_ptr(), b_dev.data_ptr() if b_dev is not None else 0,
+                     y.data_ptr(), n, flags, launch, stream.cuda_stream)
+        if io != x_dt:
+            y = y.to(_torch_dtype(x_dt))
+            if out is not None:
+                out.copy_(y)
+                y = out
+    if is_torch:
+        return y
+    return y.cpu().numpy()
+
+
+def _choose_launch(layer, n, flags, plan: EnginePlan):
+    if flags & _abi.FLAG_GENERIC:
+        return None
+    if plan.launch is not None:
+        return tuple(plan.launch)
+    hit = TUNED.get((layer.signature(), n, flags))
+    if hit is not None:
+        return hit
+    if plan.sub_batch_size > 1:
+        return layer.default_launch(n, flags, plan.sub_batch_size)
+    return None  # C heuristic default
+
+
+def conv_sparse(x, kernel: CsrKernel, bias=None, plan: EnginePlan = EnginePlan(), *,
+                relu: bool = False, pool: bool = False, out=None):
+    """Direct sparse convolution of an NCHW batch against a CsrKernel
+    (engine.py:68-87).  ``relu`` / ``pool`` fuse Model.forward's ReLU
+    (store.py:284) and a 2x2 max-pool into the epilogue."""
+    return _run(x, kernel, bias, plan, relu=relu, pool=pool, out=out)
+
+
+def conv_sparse_1d(x, kernel: CsrKernel, bias=None, plan: EnginePlan = EnginePlan(), *,
+                   relu: bool = False, out=None):
+    """1D specialisation: H=1, R=1 (engine.py:90-106); bit-identical to
+    conv_sparse on the same inputs."""
+    sh = kernel.shape
+    if sh.h != 1 or sh.r != 1:
+        raise ShapeError("conv_sparse_1d requires H=1 and R=1")
+    return _run(x, kernel, bias, plan, relu=relu, out=out)
+
+
+def conv_sparse_reference(x, kernel: CsrKernel, bias=None):
+    """Instrumented path (engine.py:109-128): runs the generic one-thread-
+    per-output kernel -- independent of the tiled kernels -- and returns
+    (output, exact multiply-accumulate count)."""
+    out = _run(x, kernel, bias, EnginePlan(), generic=True)
+    sh = kernel.shape
+    per_ch = np.diff(np.asarray(kernel.rowptr, np.int64))
+    macs = int(x.shape[0]) * int(per_ch.sum()) * sh.e * sh.f
+    return out, macs
+
+
+def sparse_mac_count(kernel: CsrKernel, batch: int) -> int:
+    """Executed MACs: N*K*E*F*L for unified kernels (engine.py:131-136)."""
+    sh = kernel.shape
+    if kernel.unified:
+        return batch * sh.k * sh.e * sh.f * kernel.sparse_level
+    return batch * sh.e * sh.f * int(kernel.nnz)
+
+
+def dense_mac_count(shape, batch: int) -> int:
+    return batch * shape.k * shape.e * shape.f * shape.kernel_volume
+
+
+def tune_sub_batch(x, kernel: CsrKernel, bias=None, candidates=SUB_BATCH_CANDIDATES,
+                   worker_count: int = 1, repetitions: int = 5,
+                   warmups: int = 2) -> tuple[int, dict[int, float]]:
+    """Timed argmin over images-per-CTA candidates (engine.py:143-166
+    contract: median of `repetitions` after `warmups`, ties to the smaller).
+    Timing uses CUDA events around each launch.  For the full launch search
+    see tuner.tune_launch."""
+    if not candidates:
+        raise ShapeError("candidate set must be non-empty")
+    from .tuner import time_call
+    timings: dict[int, float] = {}
+    for sb in sorted(candidates):
+        plan = EnginePlan(sub_batch_size=sb, worker_count=worker_count)
+        timings[sb] = time_call(lambda: conv_sparse(x, kernel, bias, plan),
+                                repetitions=max(repetitions, 1), warmups=warmups)
+    best = min(timings, key=lambda sb: (timings[sb], sb))
+    return best, timings

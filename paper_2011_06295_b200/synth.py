@@ -1,0 +1,96 @@
+"""Synthetic workloads of BASELINE.json (weights and inputs are synthetic:
+there is no network for datasets or checkpoints).
+
+* ``make_layer_weights`` restates the reference generator bench.py:105-116:
+  every output channel gets exactly ``vol - round(sparsity*vol)`` N(0,1)
+  nonzeros at ``rng.choice`` positions, same rng call order, so the weights
+  are bit-identical to the reference's for the same seed
+  (tests/test_gpu_parity.py checks the digest recorded from the reference).
+* ``bench_inputs`` restates bench.py:175-177 (x, bias ~ N(0,1) from
+  ``default_rng(seed+1)``).
+* The CIFAR-10 stacks are builder-defined: the reference only
+  ships ImageNet shapes (bench.py:74-102).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ShapeError
+from .geometry import ConvShape
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    """One benchmark subject: geometry (batch replaced at run time) + sparsity."""
+
+    name: str
+    shape: ConvShape
+    sparsity: float
+    source: str = "builder-defined"
+
+    def __post_init__(self):
+        if not 0.0 <= self.sparsity <= 1.0:
+            raise ShapeError(f"sparsity must be in [0,1], got {self.sparsity}")
+
+
+def make_layer_weights(spec: LayerSpec, seed: int = 0) -> np.ndarray:
+    sh = spec.shape
+    rng = np.random.default_rng(seed)
+    vol = sh.c * sh.r * sh.s
+    keep = vol - int(round(spec.sparsity * vol))
+    w = np.zeros((sh.k, vol), np.float32)
+    for k in range(sh.k):
+        pos = rng.choice(vol, size=keep, replace=False)
+        w[k, pos] = rng.standard_normal(keep)
+    return w.reshape(sh.k, sh.c, sh.r, sh.s)
+
+
+def bench_inputs(shape: ConvShape, batch: int, seed: int = 0):
+    rng = np.random.default_rng(seed + 1)
+    x = rng.standard_normal((batch, shape.c, shape.h, shape.w)).astype(np.float32)
+    bias = rng.standard_normal(shape.k).astype(np.float32)
+    return x, bias
+
+
+def _vgg(c, hw, k):
+    return ConvShape(n=1, c=c, h=hw, w=hw, k=k, r=3, s=3, stride=1, padding=1)
+
+
+# (name, C, H, K, pool after)
+VGG16_CIFAR_LAYERS = [
+    ("conv1_1", 3, 32, 64, False), ("conv1_2", 64, 32, 64, True),
+    ("conv2_1", 64, 16, 128, False), ("conv2_2", 128, 16, 128, True),
+    ("conv3_1", 128, 8, 256, False), ("conv3_2", 256, 8, 256, False), ("conv3_3", 256, 8, 256, True),
+    ("conv4_1", 256, 4, 512, False), ("conv4_2", 512, 4, 512, False), ("conv4_3", 512, 4, 512, True),
+    ("conv5_1", 512, 2, 512, False), ("conv5_2", 512, 2, 512, False), ("conv5_3", 512, 2, 512, True),
+]
+
+# AlexNet-style CIFAR-10 stack: 5x5 then 3x3, "same" padding
+ALEXNET_CIFAR_LAYERS = [
+    ("conv1", 3, 32, 64, 5, True), ("conv2", 64, 16, 192, 5, True),
+    ("conv3", 192, 8, 384, 3, False), ("conv4", 384, 8, 256, 3, False),
+    ("conv5", 256, 8, 256, 3, False),
+]
+
+
+def vgg16_cifar(sparsity: float = 0.9):
+    """[(LayerSpec, pool_after)] of the 13 VGG-16 convs on 32x32 inputs."""
+    return [(LayerSpec(n, _vgg(c, h, k), sparsity), pool) for n, c, h, k, pool in VGG16_CIFAR_LAYERS]
+
+
+def alexnet_cifar(sparsity: float = 0.9):
+    out = []
+    for n, c, h, k, ks, pool in ALEXNET_CIFAR_LAYERS:
+        sh = ConvShape(n=1, c=c, h=h, w=h, k=k, r=ks, s=ks, stride=1, padding=ks // 2)
+        out.append((LayerSpec(n, sh, sparsity), pool))
+    return out
+
+
+SWEEP_SPARSITIES = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.97, 0.98, 0.99)
+
+
+def sweep_layer(sparsity: float) -> LayerSpec:
+    """BASELINE config 5: 256->256, 3x3, 32x32."""
+    return LayerSpec(f"sweep256_s{sparsity:g}", _vgg(256, 32, 256), sparsity)

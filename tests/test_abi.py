@@ -1,0 +1,64 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol the
+public header declares (no compute calls)."""
+import re
+import subprocess
+from pathlib import Path
+
+from paper_2011_06295_b200 import _abi
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "sparseconv_b200.h"
+
+
+def declared():
+    return sorted(set(re.findall(r"SCB_API\s+[\w\s\*]+?\b(scb_\w+)\s*\(", HEADER.read_text())))
+
+
+def test_header_lists_match_binding():
+    assert declared() == sorted(_abi.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = _abi.lib()
+    for name in declared():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_abi.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (scb_\w+)", out))
+    assert set(declared()) <= exported
+    assert all(s.startswith("scb_") for s in exported)
+
+
+def test_variant_table():
+    vs = _abi.variants()
+    assert len(vs) >= 10
+    for v in vs:
+        assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (4, 8)
+        assert v["nbt"] in (1, 2) and v["mode"] in (0, 1)
+
+
+def test_sm100a_cubin_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_abi.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_exact_kernels_never_fuse():
+    """Exact-mode kernels must not contain FFMA/FFMA2: the reference rounds the
+    product and the sum separately (sc/_kernels.py:73-84)."""
+    sass = subprocess.run(["cuobjdump", "-sass", str(_abi.LIB_PATH)],
+                          capture_output=True, text=True, check=True).stdout
+    funcs = re.split(r"\n\s*Function : ", sass)
+    checked = 0
+    for body in funcs[1:]:
+        name = body.split("\n", 1)[0].strip()
+        m = re.match(r"_ZN3scb7k_tiledILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi(\d)ELi0EE", name)
+        g = re.match(r"_ZN3scb9k_genericI([fd])Li0EE", name)
+        if not (m or g):
+            continue
+        ops = re.findall(r"\b(FFMA2?|DFMA|FMUL2?|FADD2?|DMUL|DADD)\b", body)
+        assert "FFMA" not in ops and "FFMA2" not in ops and "DFMA" not in ops, name
+        assert any(o.startswith(("FMUL", "DMUL")) for o in ops), name
+        checked += 1
+    assert checked >= 8

@@ -1,0 +1,350 @@
+"""Parity of the sm_100a engine with the reference (GPU).
+
+Every comparison is bitwise unless stated: the engine's exact mode performs
+the reference's arithmetic (bias first, then product and sum separately
+rounded in colidx order; sc/_kernels.py:53-85), and f16 storage is exact with
+FFMA because f16*f16 products are exact in f32.  References used:
+  * golden outputs recorded from the reference package (tests/golden/),
+  * the C oracle (oracle/, itself pinned to those goldens),
+  * the reference's tolerance rule |out-ref| <= tol*(|ref|+1) where the
+    contract is a tolerance (fast-math mode, north star 1e-5 / 1e-2).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from golden_gen import c1_configs, make_case, random_sparse_weights, sha256
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view({2: np.uint16, 4: np.uint32, 8: np.uint64}[a.dtype.itemsize])
+
+
+def beq(a, b):
+    return a.dtype == b.dtype and a.shape == b.shape and np.array_equal(bits(a), bits(b))
+
+
+@pytest.fixture(scope="module")
+def sc():
+    import paper_2011_06295_b200 as sc
+    return sc
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle
+    return oracle
+
+
+def _shape(sc, x, w, stride=1, padding=0):
+    k, c, r, s = w.shape
+    return sc.ConvShape(n=x.shape[0], c=c, h=x.shape[2], w=x.shape[3], k=k, r=r, s=s,
+                        stride=stride, padding=padding)
+
+
+# ---------------------------------------------------------------------------
+# golden vectors from the reference
+# ---------------------------------------------------------------------------
+
+def test_golden_conv_cases(sc):
+    z = np.load(GOLDEN / "conv_cases.npz")
+    meta = json.loads(str(z["meta"]))
+    for i, m in enumerate(meta):
+        x, w = z[f"x{i}"], z[f"w{i}"]
+        b = z[f"b{i}"] if m["has_bias"] else None
+        sh = _shape(sc, x, w, m["stride"], m["padding"])
+        kern = sc.build_csr(w, sh, unify=m["unify"])
+        fn = sc.conv_sparse_1d if m["name"].startswith("seq1d") else sc.conv_sparse
+        out = fn(x, kern, b, sc.EnginePlan(sub_batch_size=m["sb"]))
+        assert beq(out, z[f"out{i}"]), m["name"]
+        # the independent generic kernel agrees bitwise as well
+        ref_out, macs = sc.conv_sparse_reference(x, kern, b)
+        assert beq(ref_out, z[f"out{i}"]), m["name"]
+        assert macs == x.shape[0] * kern.nnz * sh.e * sh.f
+
+
+def test_c1_random_configs_bitwise(sc):
+    """Acceptance C1 (tests/test_acceptance.py:63-92): 200 random configs,
+    f32 and the every-5th f16 subset, bit-identical to the reference."""
+    recs = json.loads((GOLDEN / "c1_digests.json").read_text())
+    for cfg, rec in zip(c1_configs(), recs):
+        x, w, bias = cfg["x"], cfg["w"], cfg["bias"]
+        assert sha256(x, w, bias) == rec["in_sha"]
+        sh = sc.ConvShape(**cfg["shape"])
+        kern = sc.build_csr(w, sh)
+        out = sc.conv_sparse(x, kern, bias)
+        assert sha256(out) == rec["out_sha"], cfg["shape"]
+        if "out16_sha" in rec:
+            k16 = sc.build_csr(w.astype(np.float16), sh)
+            o16 = sc.conv_sparse(x.astype(np.float16), k16, bias.astype(np.float16))
+            assert sha256(o16) == rec["out16_sha"], cfg["shape"]
+
+
+def test_baseline_layer_digests(sc):
+    """BASELINE layer shapes (batch 2) through make_layer_weights: weights,
+    CSR and outputs (f32 and f16) bit-identical to the reference's."""
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    for rec in json.loads((GOLDEN / "layer_digests.json").read_text()):
+        sh = sc.ConvShape(n=2, c=rec["c"], h=rec["hw"], w=rec["hw"], k=rec["k"], r=3, s=3, padding=1)
+        w = make_layer_weights(LayerSpec(rec["name"], sh, rec["sparsity"]), seed=0)
+        x, b = bench_inputs(sh, 2)
+        assert sha256(w) == rec["w_sha"] and sha256(x, b) == rec["x_sha"]
+        kern = sc.build_csr(w, sh)
+        assert sha256(kern.values, kern.colidx, kern.rowptr) == rec["csr_sha"]
+        assert sha256(sc.conv_sparse(x, kern, b)) == rec["out_sha"], rec["name"]
+        k16 = sc.build_csr(w.astype(np.float16), sh)
+        o16 = sc.conv_sparse(x.astype(np.float16), k16, b.astype(np.float16))
+        assert sha256(o16) == rec["out16_sha"], rec["name"]
+
+
+# ---------------------------------------------------------------------------
+# reference test_engine.py behaviour (pkg/tests/test_engine.py:20-170)
+# ---------------------------------------------------------------------------
+
+class TestEngineContract:
+    def test_dense_special_case_bit_exact(self, sc, orc):
+        x, wt, bias, _ = make_case(0, sparsity=0.0)
+        sh = _shape(sc, x, wt, 1, 1)
+        out = sc.conv_sparse(x, sc.build_csr(wt, sh), bias)
+        assert beq(out, orc.conv_dense_direct(x, wt, bias, 1, 1))
+
+    def test_all_zero_kernel_is_bias(self, sc):
+        x, wt, bias, _ = make_case(1)
+        sh = _shape(sc, x, wt, 1, 1)
+        out = sc.conv_sparse(x, sc.build_csr(np.zeros_like(wt), sh), bias)
+        assert np.array_equal(out, np.broadcast_to(bias[None, :, None, None], out.shape))
+
+    def test_plan_invariance_and_oracle(self, sc, orc):
+        x, wt, bias, _ = make_case(2, n=8, c=4, h=16, w=16, k=8, sparsity=0.9)
+        sh = _shape(sc, x, wt, 1, 1)
+        kern = sc.build_csr(wt, sh)
+        outs = [sc.conv_sparse(x, kern, bias, sc.EnginePlan(sub_batch_size=sb)) for sb in (1, 2, 4, 8, 16)]
+        for o in outs[1:]:
+            assert beq(o, outs[0])
+        ref = orc.conv_oracle_f64(x, wt, bias, 1, 1)
+        assert orc.rel_ok(outs[0], ref, 1e-4)
+
+    def test_worker_invariance(self, sc):
+        x, wt, bias, _ = make_case(3, n=4, sparsity=0.8)
+        kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+        outs = [sc.conv_sparse(x, kern, bias, sc.EnginePlan(worker_count=wc)) for wc in (1, 2, 64)]
+        assert beq(outs[0], outs[1]) and beq(outs[0], outs[2])
+
+    def test_odd_batch(self, sc):
+        x, wt, bias, _ = make_case(4, n=3)
+        kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+        o4 = sc.conv_sparse(x, kern, bias, sc.EnginePlan(sub_batch_size=4))
+        o1 = sc.conv_sparse(x, kern, bias, sc.EnginePlan(sub_batch_size=1))
+        assert o4.shape[0] == 3 and beq(o4, o1)
+
+    def test_f16_storage(self, sc, orc):
+        x, wt, bias, _ = make_case(6, dtype=np.float16, sparsity=0.5)
+        kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+        out = sc.conv_sparse(x, kern, bias)
+        assert out.dtype == np.float16
+        assert orc.rel_ok(out, orc.conv_oracle_f64(x, wt, bias, 1, 1), 1e-2)
+
+    def test_shape_mismatch(self, sc):
+        x, wt, bias, _ = make_case(7)
+        kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+        with pytest.raises(sc.ShapeError):
+            sc.conv_sparse(x[:, :2], kern, bias)
+
+    def test_bad_plan(self, sc):
+        with pytest.raises(sc.ShapeError):
+            sc.EnginePlan(sub_batch_size=3)
+        with pytest.raises(sc.ShapeError):
+            sc.EnginePlan(worker_count=0)
+
+    def test_1d_pair_kernel(self, sc):
+        x = np.full((1, 1, 1, 10), 3.0, np.float32)
+        w = np.ones((1, 1, 1, 2), np.float32)
+        kern = sc.build_csr(w, sc.ConvShape(n=1, c=1, h=1, w=10, k=1, r=1, s=2))
+        assert np.all(sc.conv_sparse_1d(x, kern) == np.float32(6.0))
+
+    def test_1d_requires_geometry(self, sc):
+        x, wt, bias, _ = make_case(10)
+        kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+        with pytest.raises(sc.ShapeError):
+            sc.conv_sparse_1d(x, kern, bias)
+
+    def test_mac_counts(self, sc):
+        x, wt, bias, _ = make_case(11, sparsity=0.8)
+        sh = _shape(sc, x, wt, 1, 1)
+        kern = sc.build_csr(wt, sh)
+        _, macs = sc.conv_sparse_reference(x, kern, bias)
+        assert macs == sc.sparse_mac_count(kern, 2) == 2 * sh.k * sh.e * sh.f * kern.sparse_level
+        assert sc.dense_mac_count(sh, 2) == 2 * sh.k * sh.e * sh.f * sh.c * sh.r * sh.s
+
+    def test_tune_sub_batch(self, sc):
+        x, wt, bias, _ = make_case(15, n=8)
+        kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+        best, timings = sc.tune_sub_batch(x, kern, bias, candidates=(1, 2, 4), repetitions=2, warmups=1)
+        assert timings[best] <= min(timings.values()) and set(timings) == {1, 2, 4}
+
+
+# ---------------------------------------------------------------------------
+# launch-configuration invariance (acceptance C3, tests/test_acceptance.py:127-144)
+# ---------------------------------------------------------------------------
+
+def _all_launch_outputs(sc, x, kern, bias, max_cands=None):
+    import torch
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.engine import _io_dtype
+    xd = torch.from_numpy(x).cuda()
+    io = _io_dtype(x.dtype, kern)
+    layer = device_layer(kern, 0, io)
+    cands = layer.candidates(x.shape[0])
+    assert cands, "no tiled variant for this geometry"
+    if max_cands:
+        cands = cands[:: max(1, len(cands) // max_cands)]
+    outs = []
+    for c in cands + [None]:
+        plan = sc.EnginePlan(launch=c)
+        if c is None:
+            o, _ = sc.conv_sparse_reference(xd, kern, bias)
+        else:
+            o = sc.conv_sparse(xd, kern, bias, plan)
+        outs.append((c, o.cpu().numpy()))
+    return outs
+
+
+def test_c3_launch_invariance(sc, orc):
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((4, 8, 16, 16)).astype(np.float32)
+    w = random_sparse_weights(rng, 16, 8, 3, 3, 0.9)
+    b = rng.standard_normal(16).astype(np.float32)
+    sh = sc.ConvShape(n=4, c=8, h=16, w=16, k=16, r=3, s=3, padding=1)
+    kern = sc.build_csr(w, sh)
+    v, ci, rp, _ = orc.build_csr(w, 16, 16, 1)
+    ref = orc.conv_sparse(x, v, ci, rp, 16, 3, 3, 1, 1, b)
+    for c, o in _all_launch_outputs(sc, x, kern, b):
+        assert beq(o, ref), c
+
+
+@pytest.mark.parametrize("c,hw,k,sp,n", [(64, 32, 64, 0.9, 4), (128, 16, 128, 0.9, 6),
+                                         (256, 8, 256, 0.9, 10), (512, 4, 512, 0.95, 34),
+                                         (512, 2, 512, 0.9, 130), (3, 32, 64, 0.9, 3)])
+def test_vgg_layer_all_launches_bitwise(sc, orc, c, hw, k, sp, n):
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, sp), seed=0)
+    x, b = bench_inputs(sh, n)
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+    for cfg, o in _all_launch_outputs(sc, x, kern, b, max_cands=24):
+        assert beq(o, ref), cfg
+
+
+@pytest.mark.parametrize("dtype", [np.float16])
+def test_f16_all_launches_bitwise(sc, orc, dtype):
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=6, c=64, h=16, w=16, k=64, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, 0.9), seed=0).astype(dtype)
+    x, b = bench_inputs(sh, 6)
+    x, b = x.astype(dtype), b.astype(dtype)
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 64, 3, 3, 1, 1, b)
+    for cfg, o in _all_launch_outputs(sc, x, kern, b, max_cands=24):
+        assert beq(o, ref), cfg
+
+
+# ---------------------------------------------------------------------------
+# quantised weights dequantised in registers
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("key,fmt", [("codebook16_float32", "cb4"), ("codebook16_float16", "cb4"),
+                                     ("codebook4_float32", "cb4"), ("fixed16_float32", "lin16"),
+                                     ("fixed8_float32", "lin16"), ("fixed16_float16", "lin16"),
+                                     ("fixed8_float16", "lin16")])
+def test_quantized_formats_bitwise(sc, orc, key, fmt):
+    z = np.load(GOLDEN / "quant_cases.npz")
+    wq = z[key]                              # reference quantize_weights_array output
+    rng = np.random.default_rng(11)
+    n = 6
+    x = rng.standard_normal((n, 6, 12, 12)).astype(wq.dtype)
+    b = rng.standard_normal(8).astype(wq.dtype)
+    sh = sc.ConvShape(n=n, c=6, h=12, w=12, k=8, r=3, s=3, padding=1)
+    kern = sc.build_csr(wq, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 8, 3, 3, 1, 1, b)
+    native = sc.conv_sparse(x, kern, b)
+    quant = sc.conv_sparse(x, kern, b, sc.EnginePlan(weight_format=fmt))
+    assert beq(native, ref) and beq(quant, ref)
+
+
+def test_affine_weights_rejected_by_lin16(sc):
+    z = np.load(GOLDEN / "quant_cases.npz")
+    wq = z["affine16_float32"]
+    sh = sc.ConvShape(n=1, c=6, h=12, w=12, k=8, r=3, s=3, padding=1)
+    kern = sc.build_csr(wq, sh)
+    x = np.ones((1, 6, 12, 12), np.float32)
+    with pytest.raises(sc.SparseConvError):
+        sc.conv_sparse(x, kern, None, sc.EnginePlan(weight_format="lin16"))
+
+
+# ---------------------------------------------------------------------------
+# modes and epilogues
+# ---------------------------------------------------------------------------
+
+def test_fast_math_within_north_star_tolerance(sc, orc):
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=8, c=128, h=16, w=16, k=128, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, 0.9), seed=0)
+    x, b = bench_inputs(sh, 8)
+    kern = sc.build_csr(w, sh)
+    out = sc.conv_sparse(x, kern, b, sc.EnginePlan(fast_math=True))
+    ref = orc.conv_oracle_f64(x, w, b, 1, 1)
+    assert orc.rel_ok(out, ref, 1e-5)
+
+
+def test_fused_relu_pool_epilogue(sc):
+    import torch
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=8, c=64, h=16, w=16, k=64, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, 0.9), seed=0)
+    x, b = bench_inputs(sh, 8)
+    kern = sc.build_csr(w, sh)
+    xd = torch.from_numpy(x).cuda()
+    y = sc.conv_sparse(xd, kern, b)
+    want = torch.nn.functional.max_pool2d(torch.relu(y), 2)
+    got = sc.conv_sparse(xd, kern, b, relu=True, pool=True)
+    assert torch.equal(got, want)
+    got_relu = sc.conv_sparse(xd, kern, b, relu=True)
+    assert torch.equal(got_relu, torch.relu(y))
+
+
+def test_torch_input_zero_copy_path(sc):
+    import torch
+    x, wt, bias, _ = make_case(2, n=8, c=4, h=16, w=16, k=8, sparsity=0.9)
+    kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+    a = sc.conv_sparse(x, kern, bias)
+    t = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, torch.from_numpy(bias).cuda())
+    assert t.is_cuda and beq(t.cpu().numpy(), a)
+
+
+def test_f64_generic(sc, orc):
+    x, wt, bias, _ = make_case(20, dtype=np.float64, sparsity=0.6)
+    kern = sc.build_csr(wt, _shape(sc, x, wt, 1, 1))
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, wt.shape[0], 3, 3, 1, 1, bias)
+    assert beq(sc.conv_sparse(x, kern, bias), ref)
+
+
+def test_tune_launch_picks_valid_and_identical(sc, orc):
+    import torch
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    from paper_2011_06295_b200.tuner import tune_launch
+    sh = sc.ConvShape(n=32, c=128, h=8, w=8, k=128, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, 0.9), seed=0)
+    x, b = bench_inputs(sh, 32)
+    kern = sc.build_csr(w, sh)
+    best, timings = tune_launch(torch.from_numpy(x).cuda(), kern, b, repetitions=2, warmups=1,
+                                max_candidates=16)
+    assert best in timings and timings[best] == min(timings.values())
+    out = sc.conv_sparse(x, kern, b)  # now uses the tuned launch
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 128, 3, 3, 1, 1, b)
+    assert beq(out, ref)
