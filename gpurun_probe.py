@@ -35,5 +35,5 @@ for spec, pool in vgg16_cifar(0.9):
     macs = sc.sparse_mac_count(kern, N)
     t = res[0][0] if res else tg
     tot += t
-    print(f"{spec.name:8s} L={kern.sparse_level:4d} ncand={len(cands):3d} best={t*1e6:8.1f}us {macs/t/1e12:6.2f}TMAC/s default={td*1e6:8.1f}us generic={tg*1e6:9.1f}us best_cfg={res[0][1] if res else None} top3={[ (round(a*1e6,1), c) for a,c in res[1:3]]}", flush=True)
+    print(f"{spec.name:8s} L={kern.sparse_level:4d} ncand={len(cands):3d} best={t*1e6:8.1f}us {macs/t/1e12:6.2f}TMAC/s default={td*1e6:8.1f}us generic={tg*1e6:9.1f}us best_cfg={res[0][1] if res else None} v={_abi.variants()[res[0][1][0]] if res else None} top3={[ (round(a*1e6,1), c) for a,c in res[1:3]]}", flush=True)
 print("TOTAL_us", tot*1e6, "img/s", N/tot)

@@ -50,7 +50,6 @@ struct Program {
     int32_t* d_ptr = nullptr;
     Tap* d_taps = nullptr;
     int64_t ntaps = 0;
-    std::map<int, int> tap_cap;   // cc -> max taps per (group, chunk) + 1
 };
 
 }  // namespace
@@ -85,20 +84,6 @@ struct scb_layer {
     const Program* prog(int kt) const {
         for (auto& p : progs) if (p.kt == kt) return &p;
         return nullptr;
-    }
-    int cap_for(Program& p, int cc) {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = p.tap_cap.find(cc);
-        if (it != p.tap_cap.end()) return it->second;
-        const int C = g.c;
-        int mx = 0;
-        for (int gg = 0; gg < p.groups; ++gg)
-            for (int c0 = 0; c0 < C; c0 += cc) {
-                int c1 = std::min(c0 + cc, C);
-                mx = std::max(mx, p.h_ptr[(size_t)gg * (C + 1) + c1] - p.h_ptr[(size_t)gg * (C + 1) + c0]);
-            }
-        p.tap_cap[cc] = mx + 1;  // one slot of slack for the software prefetch
-        return mx + 1;
     }
 };
 
@@ -242,26 +227,32 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     return true;
 }
 
-int pix_bytes(const scb_variant_info& v) { return v.nbt == 2 ? 8 : 4; }
+int elem_bytes(const scb_variant_info& v) { return v.io == SCB_F16 ? 2 : 4; }
 
+// smem row pitch (elements) of a TMA / cp.async stage: covers bw + S - 1
+// columns, a multiple of 16 bytes (TMA box inner extent), and the widest
+// vector read of the last thread's patch row.
 int row_pitch(const scb_variant_info& v, int bw) {
-    int need = bw + v.s - 1 + 3;
-    return (need + 3) & ~3;
+    const int es = elem_bytes(v), q = 16 / es;
+    int need = std::max(bw + v.s - 1, bw - v.tw + ((v.tw + v.s - 1 + q - 1) / q) * q);
+    return (need + q - 1) / q * q;
 }
 
 // Validate a launch and compute its derived quantities.
 struct Derived {
-    int wp, threads, row, tap_cap, n_ey, n_fx, kblocks, nb;
+    int wp, threads, row, n_ey, n_fx, kblocks, nb;
     size_t smem;
     unsigned grid;
 };
 
 scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
-    if (c.variant < 0 || c.variant >= g_num_variants) return fail(SCB_ERR_SHAPE, "bad variant index");
-    const scb_variant_info& v = g_variants[c.variant].info;
+    if (c.variant < 0 || c.variant >= num_variants()) return fail(SCB_ERR_SHAPE, "bad variant index");
+    const scb_variant_info& v = variant(c.variant).info;
     if (!variant_matches(L, v, flags)) return fail(SCB_ERR_SHAPE, "variant does not match the layer");
     const Geom& g = L->g;
-    if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 || c.warps_k < 1)
+    const int es = elem_bytes(v);
+    if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
+        c.warps_k < 1)
         return fail(SCB_ERR_SHAPE, "launch tile not a multiple of the thread tile");
     const int px = (c.imgs / v.nbt) * (c.bh / v.th) * (c.bw / v.tw);
     if (px % 32) return fail(SCB_ERR_SHAPE, "pixel threads per warp group must be a multiple of 32");
@@ -269,12 +260,28 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     d->threads = c.warps_k * px;
     if (d->threads > kMaxThreads) return fail(SCB_ERR_SHAPE, "too many threads per CTA");
     if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1))) return fail(SCB_ERR_SHAPE, "pool needs even output extents");
-    Program* P = L->prog(v.kt);
-    d->row = row_pitch(v, c.bw);
-    d->tap_cap = L->cap_for(*P, c.cc);
-    d->smem = (size_t)2 * (c.imgs / v.nbt) * c.cc * (c.bh + v.r - 1) * d->row * pix_bytes(v) +
-              (size_t)2 * c.warps_k * d->tap_cap * sizeof(Tap);
+    size_t plane;  // elements per (image, channel) in a stage
+    if (v.stage == STAGE_BULK) {
+        // thread tile == whole output plane == whole input plane ("same" padding)
+        if (v.th != g.e || v.tw != g.f || g.h != g.e || g.w != g.f || c.bh != v.th || c.bw != v.tw ||
+            2 * g.pad != g.r - 1 || 2 * g.pad != g.s - 1)
+            return fail(SCB_ERR_SHAPE, "bulk staging needs thread tile == full plane, same padding");
+        if ((g.h * g.w * es) % 16) return fail(SCB_ERR_SHAPE, "bulk staging needs 16-byte planes");
+        d->row = g.w;
+        plane = (size_t)g.h * g.w;
+    } else {
+        d->row = row_pitch(v, c.bw);
+        plane = (size_t)(c.bh + v.r - 1) * d->row;
+        if (v.stage == STAGE_TMA) {
+            if (((int64_t)g.w * es) % 16) return fail(SCB_ERR_SHAPE, "TMA needs 16-byte input rows");
+            if (d->row > 256 || c.bh + v.r - 1 > 256 || c.cc > 256 || c.imgs > 256)
+                return fail(SCB_ERR_SHAPE, "TMA box extent over 256");
+        }
+    }
+    const size_t stage_bytes = ((size_t)c.imgs * c.cc * plane * es + 127) & ~(size_t)127;
+    d->smem = 2 * stage_bytes;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    const Program* P = L->prog(v.kt);
     d->n_ey = (g.e + c.bh - 1) / c.bh;
     d->n_fx = (g.f + c.bw - 1) / c.bw;
     d->kblocks = (P->groups + c.warps_k - 1) / c.warps_k;
@@ -290,27 +297,30 @@ int ceil_to(int a, int m) { return (a + m - 1) / m * m; }
 // Enumerate launch candidates for a layer and batch.
 void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out) {
     const Geom& g = L->g;
-    for (int vi = 0; vi < g_num_variants; ++vi) {
-        const scb_variant_info& v = g_variants[vi].info;
+    const int nv = num_variants();
+    for (int vi = 0; vi < nv; ++vi) {
+        const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
-        // spatial blocks: whole plane (rounded to the thread tile) when small,
-        // otherwise 32-wide / 16-high strips
         std::vector<std::pair<int, int>> blocks;
         const int eh = ceil_to(g.e, v.th), fw = ceil_to(g.f, v.tw);
-        blocks.push_back({std::min(eh, 32), std::min(fw, 32)});
-        if (eh > 16) blocks.push_back({16, std::min(fw, 32)});
-        if (eh > 8 && fw >= 8) blocks.push_back({8, std::min(fw, 32)});
+        if (v.stage == STAGE_BULK) {
+            blocks.push_back({v.th, v.tw});
+        } else {
+            blocks.push_back({std::min(eh, 32), std::min(fw, 32)});
+            if (eh > 16) blocks.push_back({16, std::min(fw, 32)});
+            if (eh > 8 && fw >= 8) blocks.push_back({8, std::min(fw, 32)});
+            if (fw > 64) blocks.push_back({std::min(eh, 4), 64});
+        }
         for (auto& b : blocks) {
-            int bh = ceil_to(std::min(b.first, eh), v.th), bw = ceil_to(std::min(b.second, fw), v.tw);
+            const int bh = ceil_to(std::min(b.first, eh), v.th), bw = ceil_to(std::min(b.second, fw), v.tw);
             const int tiles = (bh / v.th) * (bw / v.tw);
-            // smallest image count making the warp group a whole number of warps
-            int slots = 1;
+            int slots = 1;  // smallest image count making the group a whole number of warps
             while ((slots * tiles) % 32) ++slots;
             for (int mult : {1, 2, 4}) {
-                int imgs = slots * mult * v.nbt;
-                if (imgs > std::max(v.nbt, ceil_to(n, v.nbt)) && mult > 1) break;
-                for (int wk : {1, 2, 4}) {
-                    for (int cc : {2, 4, 8}) {
+                const int imgs = slots * mult * v.nbt;
+                if (mult > 1 && imgs > ceil_to(n, v.nbt)) break;
+                for (int wk : {1, 2, 4, 8}) {
+                    for (int cc : {2, 4, 8, 16}) {
                         scb_launch c{vi, wk, imgs, bh, bw, cc};
                         Derived d;
                         if (derive(L, c, n, flags, &d) != SCB_OK) continue;
@@ -323,8 +333,8 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     set_error("");
 }
 
-// Heuristic default: prefer the largest accumulator tile that still puts
-// >= 2 CTAs' worth of warps on every SM, then 2 warp groups, 4-channel stages.
+// Heuristic default (used when the tuner has not run): favour large
+// accumulator tiles and enough resident warps, then TMA/bulk staging.
 bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_launch* out) {
     std::vector<scb_launch> cands;
     enumerate(L, n, flags, cands);
@@ -338,18 +348,54 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
     for (auto& c : cands) {
         Derived d;
         if (derive(L, c, n, flags, &d) != SCB_OK) continue;
-        const scb_variant_info& v = g_variants[c.variant].info;
-        const double acc = (double)v.kt * v.nbt * v.th * v.tw;          // reuse per tap
+        const scb_variant_info& v = variant(c.variant).info;
+        const double acc = (double)v.kt * v.nbt * v.th * v.tw;  // MACs per tap dispatch
         const double warps = (double)d.grid * d.threads / 32.0;
-        const double fill = std::min(1.0, warps / (148.0 * 12.0));        // occupancy proxy
-        const double stage_cost = 1.0 / (c.warps_k * v.kt);              // input restaging per channel
-        double score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * stage_cost;
-        if (c.cc == 4) score += 0.05;
-        if (c.warps_k == 2) score += 0.05;
+        const double fill = std::min(1.0, warps / (148.0 * 8.0));
+        const double restage = 1.0 / (c.warps_k * v.kt);        // input re-reads per channel
+        double score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * restage;
+        if (v.stage == STAGE_CPASYNC) score -= 1.0;
+        if (c.cc == 8) score += 0.05;
         if (score > best) { best = score; *out = c; }
     }
     set_error("");
     return true;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+scb_status encode_input_map(const scb_layer* L, const void* x, int n, const scb_launch& c, const Derived& d,
+                            const scb_variant_info& v, CUtensorMap* m) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return fail(SCB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const Geom& g = L->g;
+    const int es = elem_bytes(v);
+    cuuint64_t dims[4] = {(cuuint64_t)g.w, (cuuint64_t)g.h, (cuuint64_t)g.c, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)g.w * es, (cuuint64_t)g.h * g.w * es, (cuuint64_t)g.c * g.h * g.w * es};
+    cuuint32_t box[4] = {(cuuint32_t)d.row, (cuuint32_t)(c.bh + v.r - 1), (cuuint32_t)c.cc, (cuuint32_t)c.imgs};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, v.io == SCB_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                     const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SCB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return SCB_OK;
 }
 
 }  // namespace
@@ -411,8 +457,8 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
     if (dt != SCB_F64 && g.stride == 1) {
         for (int kt : kKtChoices) {
             bool used = false;
-            for (int vi = 0; vi < g_num_variants; ++vi) {
-                const auto& v = g_variants[vi].info;
+            for (int vi = 0; vi < num_variants(); ++vi) {
+                const auto& v = variant(vi).info;
                 used |= (v.kt == kt && v.r == g.r && v.s == g.s && v.io == dt && v.wf == L->wf);
             }
             if (!used) continue;
@@ -436,8 +482,8 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
         *bytes = L->nnz * (dtype_size(L->dt) + 4) + (int64_t)(L->g.k + 1) * 4;
         return SCB_OK;
     }
-    if (variant >= g_num_variants) return fail(SCB_ERR_ARG, "bad variant");
-    Program* P = L->prog(g_variants[variant].info.kt);
+    if (variant >= num_variants()) return fail(SCB_ERR_ARG, "bad variant");
+    Program* P = L->prog(scb::variant(variant).info.kt);
     if (!P) return fail(SCB_ERR_ARG, "no program for this variant");
     *bytes = P->ntaps * (int64_t)sizeof(Tap) + (int64_t)P->h_ptr.size() * 4;
     return SCB_OK;
@@ -491,24 +537,32 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     Derived d;
     scb_status s = derive(L, c, n, flags, &d);
     if (s != SCB_OK) return s;
-    const VariantEntry& ve = g_variants[c.variant];
-    Program* P = L->prog(ve.info.kt);
+    const VariantEntry& ve = variant(c.variant);
+    if ((ve.info.stage != STAGE_CPASYNC) && (reinterpret_cast<uintptr_t>(x) & 15))
+        return fail(SCB_ERR_UNSUPPORTED, "TMA/bulk staging needs a 16-byte aligned input");
+    const Program* P = L->prog(ve.info.kt);
     TiledParams p;
-    p.x = x; p.bias = bias; p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps; p.q = L->q;
+    std::memset(&p, 0, sizeof(p));
+    if (ve.info.stage == STAGE_TMA) {
+        s = encode_input_map(L, x, n, c, d, ve.info, &p.tmap);
+        if (s != SCB_OK) return s;
+    }
+    p.x = x; p.bias = static_cast<const float*>(bias); p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps;
+    p.q = L->q;
     p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f; p.pad = g.pad;
     p.imgs = c.imgs; p.bh = c.bh; p.bw = c.bw; p.cc = c.cc; p.wk = c.warps_k;
-    p.wp = d.wp; p.row = d.row; p.tap_cap = d.tap_cap;
+    p.wp = d.wp; p.row = d.row;
     p.n_ey = d.n_ey; p.n_fx = d.n_fx; p.kblocks = d.kblocks; p.groups = P->groups;
     p.flags = flags;
     cudaError_t e = ve.launch(p, d.grid, (unsigned)d.threads, d.smem, st);
     return e == cudaSuccess ? SCB_OK : cuda_fail(e, "tiled kernel launch");
 }
 
-SCB_API int32_t scb_variant_count(void) { return g_num_variants; }
+SCB_API int32_t scb_variant_count(void) { return num_variants(); }
 
 SCB_API scb_status scb_variant_get(int32_t idx, scb_variant_info* out) {
-    if (idx < 0 || idx >= g_num_variants || !out) return fail(SCB_ERR_ARG, "bad variant index");
-    *out = g_variants[idx].info;
+    if (idx < 0 || idx >= num_variants() || !out) return fail(SCB_ERR_ARG, "bad variant index");
+    *out = variant(idx).info;
     return SCB_OK;
 }
 

@@ -21,8 +21,11 @@ __global__ void __launch_bounds__(256) k_probe(float a, float b, float* out) {
     float acc[kChains], x[kChains];
 #pragma unroll
     for (int i = 0; i < kChains; ++i) { acc[i] = a * (threadIdx.x + i); x[i] = b + i; }
-    const float v = a + b;
+    float v = a + b;
     for (int it = 0; it < kIters; ++it) {
+        // the multiplicand rotates through the chains so products cannot be hoisted
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) x[i] = acc[(i + 1) % kChains];
 #pragma unroll
         for (int i = 0; i < kChains; i += 2) {
             if constexpr (OP == 0) {  // FFMA
