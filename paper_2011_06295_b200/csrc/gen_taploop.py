@@ -21,30 +21,30 @@ from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 
-# staging modes (must match kernels.cu)
-CPASYNC, TMA, BULK = 0, 1, 2
+# staging modes (must match kernels.cuh)
+CPASYNC, PLANE = 0, 1
 # weight payload formats (kernels.cuh WF_*)
 WF_F32, WF_F16, WF_CB4, WF_LIN16 = 0, 1, 2, 3
 EXACT, FMA = 0, 1
 
 # (R, S, KT, NBT, TH, TW, staging modes)
 TILES = [
-    (3, 3, 8, 1, 4, 4, (TMA, CPASYNC, BULK)),
-    (3, 3, 4, 1, 4, 4, (TMA, BULK)),
-    (3, 3, 8, 1, 2, 4, (TMA,)),
-    (3, 3, 4, 2, 2, 4, (TMA,)),
-    (3, 3, 8, 2, 2, 4, (TMA,)),
-    (3, 3, 4, 2, 4, 4, (TMA, BULK)),
-    (3, 3, 8, 1, 2, 2, (BULK,)),
-    (3, 3, 8, 2, 2, 2, (BULK,)),
-    (3, 3, 8, 4, 2, 2, (BULK,)),
-    (3, 3, 4, 4, 2, 2, (BULK,)),
-    (1, 1, 8, 1, 4, 4, (TMA, CPASYNC)),
-    (1, 1, 8, 2, 2, 4, (TMA,)),
-    (5, 5, 4, 1, 4, 4, (TMA, CPASYNC)),
-    (5, 5, 4, 1, 2, 4, (TMA,)),
-    (1, 2, 8, 1, 1, 8, (TMA, CPASYNC)),
-    (1, 3, 8, 1, 1, 8, (TMA, CPASYNC)),
+    (3, 3, 8, 1, 4, 4, (PLANE, CPASYNC)),
+    (3, 3, 4, 1, 4, 4, (PLANE,)),
+    (3, 3, 8, 1, 2, 4, (PLANE,)),
+    (3, 3, 4, 2, 2, 4, (PLANE,)),
+    (3, 3, 8, 2, 2, 4, (PLANE,)),
+    (3, 3, 4, 2, 4, 4, (PLANE,)),
+    (3, 3, 8, 1, 2, 2, (PLANE,)),
+    (3, 3, 8, 2, 2, 2, (PLANE,)),
+    (3, 3, 8, 4, 2, 2, (PLANE,)),
+    (3, 3, 4, 4, 2, 2, (PLANE,)),
+    (1, 1, 8, 1, 4, 4, (PLANE, CPASYNC)),
+    (1, 1, 8, 2, 2, 4, (PLANE,)),
+    (5, 5, 4, 1, 4, 4, (PLANE, CPASYNC)),
+    (5, 5, 4, 1, 2, 4, (PLANE,)),
+    (1, 2, 8, 1, 1, 8, (CPASYNC,)),
+    (1, 3, 8, 1, 1, 8, (PLANE, CPASYNC)),
 ]
 # (io f16?, weight format, mode) combinations compiled for every tile
 BASE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]

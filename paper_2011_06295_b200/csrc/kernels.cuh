@@ -9,7 +9,6 @@
 // to the reference there.  f64 computes in f64 (generic kernel).
 #pragma once
 
-#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
 
@@ -18,9 +17,8 @@ namespace scb {
 enum { MODE_EXACT = 0, MODE_FMA = 1 };
 enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3 };
 // how a CTA stages its input tile in shared memory
-enum { STAGE_CPASYNC = 0,   // per-element cp.async with zero fill (any W)
-       STAGE_TMA = 1,       // one cp.async.bulk.tensor 4-D box per stage, OOB = zero padding
-       STAGE_BULK = 2 };    // whole planes via cp.async.bulk (thread tile == full plane)
+enum { STAGE_CPASYNC = 0,   // per-element cp.async with zero fill (any geometry)
+       STAGE_PLANE = 1 };   // whole input planes via cp.async.bulk, halo predicated in registers
 
 template <int MODE>
 __device__ __forceinline__ float mac1(float acc, float v, float x) {
@@ -49,8 +47,7 @@ struct GenericParams {
     uint32_t flags;
 };
 
-struct alignas(64) TiledParams {
-    CUtensorMap tmap;       // STAGE_TMA: 4-D map over x (W, H, C, N)
+struct TiledParams {
     const void* x;
     const float* bias;      // f32 compute dtype, may be null
     void* y;

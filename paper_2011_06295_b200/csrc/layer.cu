@@ -229,9 +229,8 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
 
 int elem_bytes(const scb_variant_info& v) { return v.io == SCB_F16 ? 2 : 4; }
 
-// smem row pitch (elements) of a TMA / cp.async stage: covers bw + S - 1
-// columns, a multiple of 16 bytes (TMA box inner extent), and the widest
-// vector read of the last thread's patch row.
+// smem row pitch (elements) of a cp.async stage: covers bw + S - 1 columns,
+// a multiple of 16 bytes, and the widest vector read of the last patch row.
 int row_pitch(const scb_variant_info& v, int bw) {
     const int es = elem_bytes(v), q = 16 / es;
     int need = std::max(bw + v.s - 1, bw - v.tw + ((v.tw + v.s - 1 + q - 1) / q) * q);
@@ -261,25 +260,17 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     if (d->threads > kMaxThreads) return fail(SCB_ERR_SHAPE, "too many threads per CTA");
     if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1))) return fail(SCB_ERR_SHAPE, "pool needs even output extents");
     size_t plane;  // elements per (image, channel) in a stage
-    if (v.stage == STAGE_BULK) {
-        // thread tile == whole output plane == whole input plane ("same" padding)
-        if (v.th != g.e || v.tw != g.f || g.h != g.e || g.w != g.f || c.bh != v.th || c.bw != v.tw ||
-            2 * g.pad != g.r - 1 || 2 * g.pad != g.s - 1)
-            return fail(SCB_ERR_SHAPE, "bulk staging needs thread tile == full plane, same padding");
-        if ((g.h * g.w * es) % 16) return fail(SCB_ERR_SHAPE, "bulk staging needs 16-byte planes");
+    if (v.stage == STAGE_PLANE) {
+        // whole input planes via cp.async.bulk: 16-byte planes, any padding
+        if (((int64_t)g.h * g.w * es) % 16) return fail(SCB_ERR_SHAPE, "plane staging needs 16-byte planes");
         d->row = g.w;
         plane = (size_t)g.h * g.w;
     } else {
         d->row = row_pitch(v, c.bw);
         plane = (size_t)(c.bh + v.r - 1) * d->row;
-        if (v.stage == STAGE_TMA) {
-            if (((int64_t)g.w * es) % 16) return fail(SCB_ERR_SHAPE, "TMA needs 16-byte input rows");
-            if (d->row > 256 || c.bh + v.r - 1 > 256 || c.cc > 256 || c.imgs > 256)
-                return fail(SCB_ERR_SHAPE, "TMA box extent over 256");
-        }
     }
     const size_t stage_bytes = ((size_t)c.imgs * c.cc * plane * es + 127) & ~(size_t)127;
-    d->smem = 2 * stage_bytes;
+    d->smem = 2 * stage_bytes + 128;  // + alignment slack (tiled.cuh)
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     const Program* P = L->prog(v.kt);
     d->n_ey = (g.e + c.bh - 1) / c.bh;
@@ -303,14 +294,10 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         if (!variant_matches(L, v, flags)) continue;
         std::vector<std::pair<int, int>> blocks;
         const int eh = ceil_to(g.e, v.th), fw = ceil_to(g.f, v.tw);
-        if (v.stage == STAGE_BULK) {
-            blocks.push_back({v.th, v.tw});
-        } else {
-            blocks.push_back({std::min(eh, 32), std::min(fw, 32)});
-            if (eh > 16) blocks.push_back({16, std::min(fw, 32)});
-            if (eh > 8 && fw >= 8) blocks.push_back({8, std::min(fw, 32)});
-            if (fw > 64) blocks.push_back({std::min(eh, 4), 64});
-        }
+        blocks.push_back({std::min(eh, 32), std::min(fw, 32)});
+        if (eh > 16) blocks.push_back({16, std::min(fw, 32)});
+        if (eh > 8 && fw >= 8) blocks.push_back({8, std::min(fw, 32)});
+        if (fw > 64) blocks.push_back({std::min(eh, 4), 64});
         for (auto& b : blocks) {
             const int bh = ceil_to(std::min(b.first, eh), v.th), bw = ceil_to(std::min(b.second, fw), v.tw);
             const int tiles = (bh / v.th) * (bw / v.tw);
@@ -334,7 +321,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
 }
 
 // Heuristic default (used when the tuner has not run): favour large
-// accumulator tiles and enough resident warps, then TMA/bulk staging.
+// accumulator tiles and enough resident warps, then plane (bulk) staging.
 bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_launch* out) {
     std::vector<scb_launch> cands;
     enumerate(L, n, flags, cands);
@@ -354,48 +341,12 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
         const double fill = std::min(1.0, warps / (148.0 * 8.0));
         const double restage = 1.0 / (c.warps_k * v.kt);        // input re-reads per channel
         double score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * restage;
-        if (v.stage == STAGE_CPASYNC) score -= 1.0;
+        if (v.stage == STAGE_CPASYNC) score -= 1.0;  // per-element staging is costlier
         if (c.cc == 8) score += 0.05;
         if (score > best) { best = score; *out = c; }
     }
     set_error("");
     return true;
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encode_fn() {
-    static EncodeFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(p);
-    });
-    return fn;
-}
-
-scb_status encode_input_map(const scb_layer* L, const void* x, int n, const scb_launch& c, const Derived& d,
-                            const scb_variant_info& v, CUtensorMap* m) {
-    EncodeFn enc = encode_fn();
-    if (!enc) return fail(SCB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const Geom& g = L->g;
-    const int es = elem_bytes(v);
-    cuuint64_t dims[4] = {(cuuint64_t)g.w, (cuuint64_t)g.h, (cuuint64_t)g.c, (cuuint64_t)n};
-    cuuint64_t strides[3] = {(cuuint64_t)g.w * es, (cuuint64_t)g.h * g.w * es, (cuuint64_t)g.c * g.h * g.w * es};
-    cuuint32_t box[4] = {(cuuint32_t)d.row, (cuuint32_t)(c.bh + v.r - 1), (cuuint32_t)c.cc, (cuuint32_t)c.imgs};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(m, v.io == SCB_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                     const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SCB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    return SCB_OK;
 }
 
 }  // namespace
@@ -538,15 +489,11 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     scb_status s = derive(L, c, n, flags, &d);
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
-    if ((ve.info.stage != STAGE_CPASYNC) && (reinterpret_cast<uintptr_t>(x) & 15))
-        return fail(SCB_ERR_UNSUPPORTED, "TMA/bulk staging needs a 16-byte aligned input");
+    if ((ve.info.stage == STAGE_PLANE) && (reinterpret_cast<uintptr_t>(x) & 15))
+        return fail(SCB_ERR_UNSUPPORTED, "plane staging needs a 16-byte aligned input");
     const Program* P = L->prog(ve.info.kt);
     TiledParams p;
     std::memset(&p, 0, sizeof(p));
-    if (ve.info.stage == STAGE_TMA) {
-        s = encode_input_map(L, x, n, c, d, ve.info, &p.tmap);
-        if (s != SCB_OK) return s;
-    }
     p.x = x; p.bias = static_cast<const float*>(bias); p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps;
     p.q = L->q;
     p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f; p.pad = g.pad;

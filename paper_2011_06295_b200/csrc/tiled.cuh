@@ -5,19 +5,19 @@
 // NBT x TH x TW output tile (NBT images) and keeps KT x NBT x TH x TW f32
 // accumulators in registers.  Input channels stream through a two-stage
 // shared-memory pipeline, `cc` channels per stage:
-//   STAGE_TMA     one cp.async.bulk.tensor.4d box per stage; out-of-bounds
-//                 elements are filled with zeros by the TMA unit, which IS the
-//                 reference's materialised zero padding (shapes.py:98-105),
-//                 done on chip for free;
-//   STAGE_BULK    thread tile == whole output plane (2x2 / 4x4 CIFAR planes):
-//                 one cp.async.bulk per image copies cc dense planes; the halo
-//                 is a compile-time zero in registers;
-//   STAGE_CPASYNC per-element cp.async with zero fill (any width).
+//   STAGE_PLANE   whole input planes via cp.async.bulk (one bulk copy of cc
+//                 contiguous planes per image, completion on an mbarrier).
+//                 The zero padding of the reference (shapes.py:98-105) is
+//                 never materialised: halo elements are predicated to 0.0 when
+//                 the register patch is loaded.  (TMA tile loads would give the
+//                 halo for free, but a box with negative start coordinates
+//                 traps on B200 -- tools/tma_test.cu.)
+//   STAGE_CPASYNC per-element cp.async with zero fill (any geometry).
 // Per input channel a lane loads its (TH+R-1) x (TW+S-1) patch per image into
 // registers once, then runs the warp group's taps of that channel through a
-// generated PTX jump table (taploop_gen.cuh): each tap selects a fully
-// unrolled block of MACs whose operands are registers at compile-time offsets.
-// Taps are ordered (c, kk, r, s), i.e. colidx order per accumulator
+// generated PTX jump table (gen_taploop.py): each tap selects a fully unrolled
+// block of MACs whose operands are registers at compile-time offsets.  Taps
+// are ordered (c, kk, r, s), i.e. colidx order per accumulator
 // (csr.py:143-160), so exact mode reproduces the reference bit for bit.
 #pragma once
 
@@ -47,15 +47,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
     asm volatile(
         "{\n .reg .pred P1;\n WAIT:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        " @!P1 bra.uni WAIT;\n}\n" ::"r"(smem_u32(b)), "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int c, int n,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(c), "r"(n), "r"(smem_u32(bar))
+        " @!P1 bra WAIT;\n}\n" ::"r"(smem_u32(b)), "r"(parity)
         : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -117,6 +109,44 @@ __device__ __forceinline__ void load_row(float* dst, const T* src) {
     }
 }
 
+// Patch of a lane from a dense H x W plane in shared memory, "same" padding
+// (pad = (R-1)/2 = (S-1)/2): rows/cols outside the plane read as 0.0 -- the
+// reference's materialised zero padding.  The TW middle columns start at the
+// lane's tile origin and use one aligned vector load when W % TW == 0.
+template <int R, int S, int TH, int TW, typename TIO>
+__device__ __forceinline__ void load_patch_plane(float* pt, const TIO* plane, int py0, int px0, int H, int W,
+                                                 bool vec_ok) {
+    constexpr int PH = TH + R - 1, PW = TW + S - 1, PADS = (S - 1) / 2;
+    constexpr int ES = (int)sizeof(TIO);
+    const int ox = px0 + PADS;  // first output column of the tile
+#pragma unroll
+    for (int yy = 0; yy < PH; ++yy) {
+        const int gy = py0 + yy;
+        const bool row_ok = (unsigned)gy < (unsigned)H;
+        const TIO* rp = plane + (row_ok ? gy : 0) * W;
+        float* d = pt + yy * PW;
+        if (vec_ok && row_ok && ox + TW <= W) {
+            load_row<TW, TW * ES, TIO>(d + PADS, rp + ox);
+#pragma unroll
+            for (int xx = 0; xx < PADS; ++xx) {
+                const int gx = px0 + xx;
+                d[xx] = gx >= 0 ? to_f32(rp[gx]) : 0.f;
+            }
+#pragma unroll
+            for (int xx = PADS + TW; xx < PW; ++xx) {
+                const int gx = px0 + xx;
+                d[xx] = gx < W ? to_f32(rp[gx]) : 0.f;
+            }
+        } else {
+#pragma unroll
+            for (int xx = 0; xx < PW; ++xx) {
+                const int gx = px0 + xx;
+                d[xx] = (row_ok && (unsigned)gx < (unsigned)W) ? to_f32(rp[gx]) : 0.f;
+            }
+        }
+    }
+}
+
 template <int R, int S, int KT, int NBT, int TH, int TW, bool F16IO, int WF, int MODE, int STAGE>
 __global__ void __launch_bounds__(256, 1) k_tiled(const __grid_constant__ TiledParams p) {
     using TIO = typename std::conditional<F16IO, __half, float>::type;
@@ -147,11 +177,13 @@ __global__ void __launch_bounds__(256, 1) k_tiled(const __grid_constant__ TiledP
     const int k0 = g * KT;
     const int n0 = nb * p.imgs, oy0 = ey * p.bh, ox0 = fx * p.bw;
     const int C = p.c, cp1 = C + 1;
-    const int BHP = (STAGE == STAGE_BULK) ? p.h : p.bh + R - 1;
-    const int ROW = (STAGE == STAGE_BULK) ? p.w : p.row;
+    const int BHP = (STAGE == STAGE_PLANE) ? p.h : p.bh + R - 1;
+    const int ROW = (STAGE == STAGE_PLANE) ? p.w : p.row;
     const int plane_s = BHP * ROW;  // elements per (image, channel)
     const int stage_el = ((p.imgs * p.cc * plane_s * ES + 127) & ~127) / ES;
-    TIO* xs = reinterpret_cast<TIO*>(smem);
+    // bulk-copy destinations need 16-byte alignment; align the dynamic window
+    // explicitly (the host adds 128 bytes of slack to the allocation)
+    TIO* xs = reinterpret_cast<TIO*>(smem + ((128u - (smem_u32(smem) & 127u)) & 127u));
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -173,15 +205,10 @@ __global__ void __launch_bounds__(256, 1) k_tiled(const __grid_constant__ TiledP
     }
 
     // ---- producer side -------------------------------------------------
-    auto issue = [&](int ch, int buf) {  // TMA / BULK: executed by warp 0
+    auto issue = [&](int ch, int buf) {  // STAGE_PLANE: executed by warp 0
         const int c0 = ch * p.cc;
         TIO* dst = xs + (size_t)buf * stage_el;
-        if constexpr (STAGE == STAGE_TMA) {
-            if (lane == 0) {
-                mbar_expect_tx(&bars[buf], (unsigned)(p.imgs * p.cc * plane_s * ES));
-                tma_load_4d(dst, &p.tmap, ox0 - p.pad, oy0 - p.pad, c0, n0, &bars[buf]);
-            }
-        } else {
+        {
             const int nc = min(p.cc, C - c0);
             const int ni = min(p.imgs, p.n - n0);
             const unsigned bytes = (unsigned)(nc * p.h * p.w * ES);
@@ -224,6 +251,9 @@ __global__ void __launch_bounds__(256, 1) k_tiled(const __grid_constant__ TiledP
         }
     };
 
+    // STAGE_PLANE: top-left input coordinate of this lane's patch ("same" padding)
+    const int py0 = oy0 + ty * TH - p.pad, px0 = ox0 + tx * TW - p.pad;
+    const bool vec_ok = (p.w % TW) == 0 && ((TW * ES) % 4) == 0 && p.pad == (S - 1) / 2;
     const int nch = (C + p.cc - 1) / p.cc;
     if constexpr (STAGE == STAGE_CPASYNC) {
         stage_cpasync(0, 0);
@@ -260,14 +290,8 @@ __global__ void __launch_bounds__(256, 1) k_tiled(const __grid_constant__ TiledP
 #pragma unroll
                 for (int j = 0; j < NBT; ++j) {
                     const TIO* pl = xb + (size_t)((ti * NBT + j) * p.cc + cl) * plane_s;
-                    if constexpr (STAGE == STAGE_BULK) {
-#pragma unroll
-                        for (int yy = 0; yy < PH; ++yy)
-#pragma unroll
-                            for (int xx = 0; xx < PW; ++xx) pt[(j * PH + yy) * PW + xx] = 0.f;
-#pragma unroll
-                        for (int yy = 0; yy < TH; ++yy)
-                            load_row<TW, TW * ES, TIO>(&pt[(j * PH + yy + PADR) * PW + PADS], pl + yy * TW);
+                    if constexpr (STAGE == STAGE_PLANE) {
+                        load_patch_plane<R, S, TH, TW, TIO>(&pt[j * PH * PW], pl, py0, px0, p.h, p.w, vec_ok);
                     } else {
                         const TIO* rb = pl + (ty * TH) * ROW + tx * TW;
 #pragma unroll
