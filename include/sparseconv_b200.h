@@ -81,7 +81,8 @@ typedef struct {
     int32_t io;          /* scb_dtype of activations */
     int32_t wf;          /* payload: 0 f32, 1 f16, 2 codebook-4bit, 3 int16 fixed-point */
     int32_t mode;        /* 0 exact mul+add, 1 fma */
-    int32_t stage;       /* input staging: 0 per-element cp.async, 1 whole planes via cp.async.bulk */
+    int32_t dispatch;    /* tap dispatch: 0 brx.idx jump table, 1 per-channel mask walk */
+    int32_t pad;         /* padding the variant is specialised for */
 } scb_variant_info;
 
 /* ---------------------------------------------------------------------- */

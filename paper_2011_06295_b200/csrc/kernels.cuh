@@ -16,9 +16,9 @@ namespace scb {
 
 enum { MODE_EXACT = 0, MODE_FMA = 1 };
 enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3 };
-// how a CTA stages its input tile in shared memory
-enum { STAGE_CPASYNC = 0,   // per-element cp.async with zero fill (any geometry)
-       STAGE_PLANE = 1 };   // whole input planes via cp.async.bulk, halo predicated in registers
+// how the tiled kernel dispatches a tap to its unrolled MAC block (gen_taploop.py)
+enum { DISPATCH_JUMP = 0,   // brx.idx jump table, one indirect branch per tap
+       DISPATCH_MASK = 1 }; // per-channel KT x 16-bit masks walked in order
 
 template <int MODE>
 __device__ __forceinline__ float mac1(float acc, float v, float x) {
@@ -52,12 +52,15 @@ struct TiledParams {
     const float* bias;      // f32 compute dtype, may be null
     void* y;
     const int32_t* tap_ptr; // [G][C+1] absolute tap offsets
-    const Tap* taps;
+    const Tap* taps;        // (c, kk, r, s)-ordered taps per group, two slack slots at the end
+    const uint32_t* masks;  // DISPATCH_MASK: [G][C][KT/2] 16-bit tap masks per kk
     QuantAux q;
     int n, c, h, w, k, e, f, pad;
     int imgs, bh, bw, cc, wk;   // launch shape
     int wp;                     // pixel warps per warp group
     int row;                    // smem row pitch (elements)
+    int stage_el;               // elements per pipeline stage
+    int chunk;                  // cp.async size in bytes (16, 8 or 4)
     int n_ey, n_fx, kblocks, groups;
     uint32_t flags;
 };

@@ -49,6 +49,7 @@ struct Program {
     std::vector<int32_t> h_ptr;   // groups x (C+1)
     int32_t* d_ptr = nullptr;
     Tap* d_taps = nullptr;
+    uint32_t* d_masks = nullptr;  // groups x C x ceil(KT/2): bit r*S+s of half-word kk
     int64_t ntaps = 0;
 };
 
@@ -75,7 +76,7 @@ struct scb_layer {
         cudaFree(d_values);
         cudaFree(d_dec);
         cudaFree(d_rowptr);
-        for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); }
+        for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); cudaFree(p.d_masks); }
     }
     Program* prog(int kt) {
         for (auto& p : progs) if (p.kt == kt) return &p;
@@ -167,11 +168,13 @@ scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int3
     Program P;
     P.kt = kt;
     P.groups = (g.k + kt - 1) / kt;
-    const int C = g.c, RS = g.r * g.s;
+    const int C = g.c, RS = g.r * g.s, NW = (kt + 1) / 2;
     const int64_t plane = (int64_t)g.hp * g.wp;
     P.h_ptr.assign((size_t)P.groups * (C + 1), 0);
+    std::vector<uint32_t> masks((size_t)P.groups * C * NW, 0u);
+    const bool mask_ok = RS <= 16;
     std::vector<Tap> taps;
-    taps.reserve(L->nnz);
+    taps.reserve(L->nnz + 2);
     std::vector<int32_t> cur(kt);
     for (int gg = 0; gg < P.groups; ++gg) {
         for (int kk = 0; kk < kt; ++kk) {
@@ -190,6 +193,8 @@ scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int3
                     tp.meta = (uint32_t)(kk * RS + r * g.s + s);
                     tp.payload = pay[cur[kk]];
                     taps.push_back(tp);
+                    if (mask_ok)
+                        masks[((size_t)gg * C + c) * NW + kk / 2] |= 1u << (16 * (kk % 2) + r * g.s + s);
                     ++cur[kk];
                 }
             }
@@ -197,14 +202,19 @@ scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int3
         P.h_ptr[(size_t)gg * (C + 1) + C] = (int32_t)taps.size();
     }
     if ((int64_t)taps.size() != L->nnz) return fail(SCB_ERR_FORMAT, "tap program lost entries (colidx order?)");
-    taps.push_back(Tap{0u, 0u});  // slack slot for the prefetch at the very end
+    taps.push_back(Tap{0u, 0u});  // two slack slots for the two-deep prefetch
+    taps.push_back(Tap{0u, 0u});
     P.ntaps = L->nnz;
     cudaError_t e;
     if ((e = cudaMalloc(&P.d_ptr, P.h_ptr.size() * sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&P.d_taps, taps.size() * sizeof(Tap))) != cudaSuccess) { cudaFree(P.d_ptr); return cuda_fail(e, "cudaMalloc"); }
+    if ((e = cudaMalloc(&P.d_masks, std::max<size_t>(masks.size(), 1) * sizeof(uint32_t))) != cudaSuccess) {
+        cudaFree(P.d_ptr); cudaFree(P.d_taps); return cuda_fail(e, "cudaMalloc");
+    }
     cudaMemcpy(P.d_ptr, P.h_ptr.data(), P.h_ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    cudaMemcpy(P.d_masks, masks.data(), masks.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
     e = cudaMemcpy(P.d_taps, taps.data(), taps.size() * sizeof(Tap), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) { cudaFree(P.d_ptr); cudaFree(P.d_taps); return cuda_fail(e, "cudaMemcpy"); }
+    if (e != cudaSuccess) { cudaFree(P.d_ptr); cudaFree(P.d_taps); cudaFree(P.d_masks); return cuda_fail(e, "cudaMemcpy"); }
     L->progs.push_back(std::move(P));
     return SCB_OK;
 }
@@ -218,7 +228,7 @@ int wf_of(const scb_layer* L) {
 bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t flags) {
     const Geom& g = L->g;
     if (L->dt == SCB_F64) return false;
-    if (g.stride != 1 || v.r != g.r || v.s != g.s) return false;
+    if (g.stride != 1 || v.r != g.r || v.s != g.s || v.pad != g.pad) return false;
     if (v.io != L->dt || v.wf != L->wf) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
@@ -229,17 +239,17 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
 
 int elem_bytes(const scb_variant_info& v) { return v.io == SCB_F16 ? 2 : 4; }
 
-// smem row pitch (elements) of a cp.async stage: covers bw + S - 1 columns,
-// a multiple of 16 bytes, and the widest vector read of the last patch row.
+// smem row pitch (elements) of a zero-halo window row: XOFF (16 bytes) +
+// block columns + right halo + one copy chunk of rounding slack, 16-byte rows.
 int row_pitch(const scb_variant_info& v, int bw) {
     const int es = elem_bytes(v), q = 16 / es;
-    int need = std::max(bw + v.s - 1, bw - v.tw + ((v.tw + v.s - 1 + q - 1) / q) * q);
+    const int need = q + bw + v.s - 1 - v.pad + q;
     return (need + q - 1) / q * q;
 }
 
 // Validate a launch and compute its derived quantities.
 struct Derived {
-    int wp, threads, row, n_ey, n_fx, kblocks, nb;
+    int wp, threads, row, stage_el, chunk, n_ey, n_fx, kblocks, nb;
     size_t smem;
     unsigned grid;
 };
@@ -259,19 +269,19 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     d->threads = c.warps_k * px;
     if (d->threads > kMaxThreads) return fail(SCB_ERR_SHAPE, "too many threads per CTA");
     if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1))) return fail(SCB_ERR_SHAPE, "pool needs even output extents");
-    size_t plane;  // elements per (image, channel) in a stage
-    if (v.stage == STAGE_PLANE) {
-        // whole input planes via cp.async.bulk: 16-byte planes, any padding
-        if (((int64_t)g.h * g.w * es) % 16) return fail(SCB_ERR_SHAPE, "plane staging needs 16-byte planes");
-        d->row = g.w;
-        plane = (size_t)g.h * g.w;
-    } else {
-        d->row = row_pitch(v, c.bw);
-        plane = (size_t)(c.bh + v.r - 1) * d->row;
-    }
+    d->row = row_pitch(v, c.bw);
+    const size_t plane = (size_t)(c.bh + v.r - 1) * d->row;  // elements per (image, channel)
     const size_t stage_bytes = ((size_t)c.imgs * c.cc * plane * es + 127) & ~(size_t)127;
-    d->smem = 2 * stage_bytes + 128;  // + alignment slack (tiled.cuh)
+    d->stage_el = (int)(stage_bytes / es);
+    d->smem = 2 * stage_bytes;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    // copy chunk: the widest of 16/8/4 bytes dividing the input row and the block stride
+    const int n_fx = (g.f + c.bw - 1) / c.bw;
+    d->chunk = 0;
+    for (int ch : {16, 8, 4})
+        if (((int64_t)g.w * es) % ch == 0 && (n_fx == 1 || ((int64_t)c.bw * es) % ch == 0)) { d->chunk = ch; break; }
+    if (d->chunk == 0) return fail(SCB_ERR_SHAPE, "input rows are not a multiple of 4 bytes");
+    if (v.dispatch == DISPATCH_MASK && v.r * v.s > 16) return fail(SCB_ERR_SHAPE, "mask dispatch needs R*S <= 16");
     const Program* P = L->prog(v.kt);
     d->n_ey = (g.e + c.bh - 1) / c.bh;
     d->n_fx = (g.f + c.bw - 1) / c.bw;
@@ -341,7 +351,6 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
         const double fill = std::min(1.0, warps / (148.0 * 8.0));
         const double restage = 1.0 / (c.warps_k * v.kt);        // input re-reads per channel
         double score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * restage;
-        if (v.stage == STAGE_CPASYNC) score -= 1.0;  // per-element staging is costlier
         if (c.cc == 8) score += 0.05;
         if (score > best) { best = score; *out = c; }
     }
@@ -489,16 +498,15 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     scb_status s = derive(L, c, n, flags, &d);
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
-    if ((ve.info.stage == STAGE_PLANE) && (reinterpret_cast<uintptr_t>(x) & 15))
-        return fail(SCB_ERR_UNSUPPORTED, "plane staging needs a 16-byte aligned input");
+    if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
     const Program* P = L->prog(ve.info.kt);
     TiledParams p;
     std::memset(&p, 0, sizeof(p));
-    p.x = x; p.bias = static_cast<const float*>(bias); p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps;
+    p.x = x; p.bias = static_cast<const float*>(bias); p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps; p.masks = P->d_masks;
     p.q = L->q;
     p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f; p.pad = g.pad;
     p.imgs = c.imgs; p.bh = c.bh; p.bw = c.bw; p.cc = c.cc; p.wk = c.warps_k;
-    p.wp = d.wp; p.row = d.row;
+    p.wp = d.wp; p.row = d.row; p.stage_el = d.stage_el; p.chunk = d.chunk;
     p.n_ey = d.n_ey; p.n_fx = d.n_fx; p.kblocks = d.kblocks; p.groups = P->groups;
     p.flags = flags;
     cudaError_t e = ve.launch(p, d.grid, (unsigned)d.threads, d.smem, st);

@@ -34,7 +34,7 @@ def test_variant_table():
     assert len(vs) >= 10
     for v in vs:
         assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (4, 8)
-        assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["stage"] in (0, 1)
+        assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["dispatch"] in (0, 1)
 
 
 def test_sm100a_cubin_only():
@@ -53,7 +53,7 @@ def test_exact_kernels_never_fuse():
     checked = 0
     for body in funcs[1:]:
         name = body.split("\n", 1)[0].strip()
-        m = re.match(r"_ZN3scb7k_tiledILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi(\d)ELi0ELi\dEE", name)
+        m = re.match(r"_ZN3scb7k_tiledILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi(\d)ELi0ELi\dELi\dEE", name)
         g = re.match(r"_ZN3scb9k_genericI([fd])Li0EE", name)
         if not (m or g):
             continue
