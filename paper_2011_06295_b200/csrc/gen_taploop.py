@@ -66,7 +66,7 @@ def decode_ptx(wf: int, src: str = "%%pc") -> str:
     if wf == WF_F16:
         return f"cvt.u16.u32 %%h, {src};\ncvt.f32.f16 %%v, %%h;\n"
     if wf == WF_CB4:
-        return f"shl.b32 %%o, {src}, 2;\nadd.u32 %%o, %%o, %%aux;\nld.shared.f32 %%v, [%%o];\n"
+        return f"and.b32 %%o, {src}, 15;\nshl.b32 %%o, %%o, 2;\nadd.u32 %%o, %%o, %%aux;\nld.shared.f32 %%v, [%%o];\n"
     return f"cvt.u16.u32 %%h, {src};\ncvt.rn.f32.s16 %%v, %%h;\nmul.rn.f32 %%v, %%v, %%scl;\n"
 
 
@@ -118,19 +118,69 @@ def emit(template_args, signature, asm, outs, ins) -> str:
 
 def regs_decl(P, MODE, with_end=True):
     t = ", ".join(f"%%t{i}" for i in range(P)) if MODE == EXACT else "%%t0"
-    q = ".reg .u64 %%q, %%end;\n" if with_end else ""
-    return (".reg .pred %%p;\n.reg .u32 %%m, %%mc, %%pb, %%pc, %%m2, %%pb2, %%o, %%aux, %%w;\n"
+    q = ".reg .u64 %%q, %%end;\n" if with_end else ".reg .u64 %%q;\n"
+    return (".reg .pred %%p;\n.reg .u32 %%m, %%mc, %%pb, %%pc, %%o, %%aux, %%w;\n"
             f"{q}.reg .f32 %%v, %%scl, {t};\n.reg .b16 %%h;\n")
 
 
-def gen_jump(R, S, KT, NBT, TH, TW, WF, MODE) -> str:
-    o = Ops(R, S, KT, NBT, TH, TW)
-    ob = o.nacc + o.npt
-    L = ["{\n", regs_decl(o.P, MODE),
-         f"mov.u64 %%q, %{ob};\nmov.u64 %%end, %{ob + 1};\nmov.u32 %%aux, %{ob + 2};\nmov.f32 %%scl, %{ob + 3};\n",
-         "setp.ge.u64 %%p, %%q, %%end;\n@%%p bra.uni DONE;\n",
+def patch_load_ptx(o: Ops, NBT, R, S, PAD, TW, f16: bool) -> str:
+    """Load the lane's NBT x PH x PW patch of channel %%cl from shared memory:
+    image j, row yy at %%a + j*%%imgb + yy*%%rowb; left halo (PAD elements),
+    aligned middle (TW elements), right halo (S-1-PAD elements)."""
+    es = 2 if f16 else 4
+    L = []
+    right = S - 1 - PAD
+    for j in range(NBT):
+        L.append("mov.u32 %%ra, %%a;\n" if j == 0 else "add.u32 %%a, %%a, %%imgb;\nmov.u32 %%ra, %%a;\n")
+        for yy in range(o.PH):
+            if yy:
+                L.append("add.u32 %%ra, %%ra, %%rowb;\n")
+            regs = [o.pt(j, yy, xx) for xx in range(o.PW)]
+            segs = []  # (first element, count, vector ok)
+            if PAD:
+                segs.append((0, PAD, False))
+            segs.append((PAD, TW, True))
+            if right:
+                segs.append((PAD + TW, right, True))
+            for first, cnt, vec in segs:
+                off0 = first * es
+                if not f16:
+                    k = 0
+                    while k < cnt:
+                        w = 4 if (vec and cnt - k >= 4 and (TW * 4) % 16 == 0 and ((k * 4) % 16 == 0)) else \
+                            (2 if (vec and cnt - k >= 2 and ((TW * 4) % 8 == 0) and ((k * 4) % 8 == 0)) else 1)
+                        dst = regs[first + k:first + k + w]
+                        if w == 1:
+                            L.append(f"ld.shared.f32 {dst[0]}, [%%ra+{off0 + 4 * k}];\n")
+                        else:
+                            L.append(f"ld.shared.v{w}.f32 {{{', '.join(dst)}}}, [%%ra+{off0 + 4 * k}];\n")
+                        k += w
+                else:
+                    for k in range(cnt):
+                        L.append(f"ld.shared.b16 %%h, [%%ra+{off0 + 2 * k}];\ncvt.f32.f16 {regs[first + k]}, %%h;\n")
+    return "".join(L)
+
+
+def gen_jump(R, S, PAD, KT, NBT, TH, TW, WF, MODE, f16) -> str:
+    """Jump-table tap loop over one stage.  The stream of a warp group holds,
+    per non-empty input channel, a sentinel (meta = KT*R*S, payload = channel)
+    followed by the channel's taps; the group ends with a sentinel of channel C.
+    A sentinel of a channel outside [c0, c0+cc) ends the stage with q pointing
+    at it; otherwise it (re)loads the lane's patch of that channel."""
+    nacc = KT * NBT * TH * TW
+    o = Ops(R, S, KT, NBT, TH, TW, pt_base=nacc)
+    npt = o.npt
+    oq = nacc + npt                                    # "+l" q
+    oin = oq + 1                                       # inputs
+    names = ["c0", "ccnt", "base", "planeb", "imgb", "rowb", "aux", "scl"]
+    op = {n: f"%{oin + i}" for i, n in enumerate(names)}
+    NC = KT * R * S
+    L = ["{\n", regs_decl(o.P, MODE, with_end=False),
+         ".reg .u32 %%cl, %%a, %%ra, %%c0, %%ccnt, %%base, %%planeb, %%imgb, %%rowb;\n",
+         f"mov.u32 %%c0, {op['c0']};\nmov.u32 %%ccnt, {op['ccnt']};\nmov.u32 %%base, {op['base']};\n"
+         f"mov.u32 %%planeb, {op['planeb']};\nmov.u32 %%imgb, {op['imgb']};\nmov.u32 %%rowb, {op['rowb']};\n"
+         f"mov.u32 %%aux, {op['aux']};\nmov.f32 %%scl, {op['scl']};\nmov.u64 %%q, %{oq};\n",
          "ld.global.nc.v2.u32 {%%m, %%pb}, [%%q];\n",
-         "ld.global.nc.v2.u32 {%%m2, %%pb2}, [%%q+8];\n",
          "bra.uni LOOP;\n"]
     labels = []
     for kk in range(KT):
@@ -138,21 +188,26 @@ def gen_jump(R, S, KT, NBT, TH, TW, WF, MODE) -> str:
             for s in range(S):
                 lab = f"C{(kk * R + r) * S + s}"
                 labels.append(lab)
-                L.append(f"{lab}:\n" + mac_block(o, kk, r, s, NBT, TH, TW, MODE) + "bra.uni NEXT;\n")
+                L.append(f"{lab}:\n" + mac_block(o, kk, r, s, NBT, TH, TW, MODE) + "bra.uni LOOP;\n")
+    labels.append("CS")
+    L.append("CS:\nsub.u32 %%cl, %%pc, %%c0;\nsetp.ge.u32 %%p, %%cl, %%ccnt;\n@%%p bra.uni EXIT;\n"
+             "mad.lo.u32 %%a, %%cl, %%planeb, %%base;\n")
+    L.append(patch_load_ptx(o, NBT, R, S, PAD, TW, f16))
+    L.append("bra.uni LOOP;\n")
     L.append("TBL: .branchtargets " + ", ".join(labels) + ";\n")
-    # two-deep prefetch of the tap stream (the device array has two slack slots)
-    L.append("LOOP:\nmov.u32 %%mc, %%m;\nmov.u32 %%pc, %%pb;\nmov.u32 %%m, %%m2;\nmov.u32 %%pb, %%pb2;\n"
-             "ld.global.nc.v2.u32 {%%m2, %%pb2}, [%%q+16];\nadd.u64 %%q, %%q, 8;\n")
+    L.append("LOOP:\nmov.u32 %%mc, %%m;\nmov.u32 %%pc, %%pb;\n"
+             "ld.global.nc.v2.u32 {%%m, %%pb}, [%%q+8];\nadd.u64 %%q, %%q, 8;\n")
     L.append(decode_ptx(WF))
-    L.append("brx.idx.uni %%mc, TBL;\nNEXT:\nsetp.lt.u64 %%p, %%q, %%end;\n@%%p bra.uni LOOP;\nDONE:\n}\n")
-    outs = [f'"+f"(a[{i}])' for i in range(o.nacc)]
-    ins = [f'"f"(pt[{i}])' for i in range(o.npt)] + ['"l"(beg)', '"l"(end)', '"r"(aux)', '"f"(scl)']
-    sig = (f"float (&a)[{o.nacc}], const float (&pt)[{o.npt}], const Tap* beg, const Tap* end, "
-           "unsigned aux, float scl")
-    return emit(f"{R}, {S}, {KT}, {NBT}, {TH}, {TW}, {WF}, {MODE}, {JUMP}", sig, "".join(L), outs, ins)
+    L.append("brx.idx.uni %%mc, TBL;\nEXIT:\nsub.u64 %%q, %%q, 8;\nmov.u64 %" + str(oq) + ", %%q;\n}\n")
+    outs = [f'"+f"(a[{i}])' for i in range(nacc)] + [f'"+f"(pt[{i}])' for i in range(npt)] + ['"+l"(q)']
+    ins = ['"r"(c0)', '"r"(ccnt)', '"r"(base)', '"r"(planeb)', '"r"(imgb)', '"r"(rowb)', '"r"(aux)', '"f"(scl)']
+    sig = (f"float (&a)[{nacc}], float (&pt)[{npt}], const Tap*& q, unsigned c0, unsigned ccnt, unsigned base, "
+           "unsigned planeb, unsigned imgb, unsigned rowb, unsigned aux, float scl")
+    return emit(f"{R}, {S}, {PAD}, {KT}, {NBT}, {TH}, {TW}, {WF}, {MODE}, {JUMP}, {'true' if f16 else 'false'}",
+                sig, "".join(L), outs, ins)
 
 
-def gen_mask(R, S, KT, NBT, TH, TW, WF, MODE) -> str:
+def gen_mask(R, S, PAD, KT, NBT, TH, TW, WF, MODE, f16) -> str:
     """Mask walk over one input channel.  In: mk (KT/2 u32 words; half-word kk
     holds bit r*S+s), vp = the channel's first Tap, pc = its payload
     (prefetched).  Out: vp / pc advanced past the channel's taps."""
@@ -187,7 +242,8 @@ def gen_mask(R, S, KT, NBT, TH, TW, WF, MODE) -> str:
     ins = [f'"f"(pt[{i}])' for i in range(o.npt)] + [f'"r"(mk[{i}])' for i in range(nw)] + ['"r"(aux)', '"f"(scl)']
     sig = (f"float (&a)[{o.nacc}], const float (&pt)[{o.npt}], const Tap*& vp, unsigned& pc, "
            f"const unsigned (&mk)[{nw}], unsigned aux, float scl")
-    return emit(f"{R}, {S}, {KT}, {NBT}, {TH}, {TW}, {WF}, {MODE}, {MASK}", sig, "".join(L), outs, ins)
+    return emit(f"{R}, {S}, {PAD}, {KT}, {NBT}, {TH}, {TW}, {WF}, {MODE}, {MASK}, {'true' if f16 else 'false'}",
+                sig, "".join(L), outs, ins)
 
 
 N_PARTS = 10
@@ -202,11 +258,11 @@ def main():
         loops, variants = [], []
         for f16, wf, mode in modes:
             for d in disps:
-                key = (R, S, KT, NBT, TH, TW, wf, mode, d)
+                key = (R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16)
                 if key not in loops:
                     loops.append(key)
                 variants.append((R, S, PAD, KT, NBT, TH, TW, f16, wf, mode, d, minb))
-        tile_key = (R, S, KT, NBT, TH, TW)
+        tile_key = (R, S, PAD, KT, NBT, TH, TW)
         g = groups.setdefault(tile_key, ([], []))
         for l in loops:
             if l not in g[0]:
@@ -226,8 +282,8 @@ def main():
         ents = []
         for loops, variants in part:
             for key in loops:
-                R, S, KT, NBT, TH, TW, wf, mode, d = key
-                src.append((gen_jump if d == JUMP else gen_mask)(R, S, KT, NBT, TH, TW, wf, mode))
+                R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
+                src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
                 R, S, PAD, KT, NBT, TH, TW, f16, wf, mode, d, minb = v
                 io = "SCB_F16" if f16 else "SCB_F32"

@@ -47,10 +47,12 @@ struct Program {
     int kt = 0;
     int groups = 0;
     std::vector<int32_t> h_ptr;   // groups x (C+1)
-    int32_t* d_ptr = nullptr;
-    Tap* d_taps = nullptr;
+    int32_t* d_ptr = nullptr;     // jump stream: ptr[g][c] -> sentinel of first non-empty channel >= c
+    Tap* d_taps = nullptr;        // jump stream: per channel a sentinel {KT*R*S, c} + taps; group ends with {., C}
+    int32_t* d_ptr_m = nullptr;   // mask stream (taps only)
+    Tap* d_taps_m = nullptr;
     uint32_t* d_masks = nullptr;  // groups x C x ceil(KT/2): bit r*S+s of half-word kk
-    int64_t ntaps = 0;
+    int64_t ntaps = 0, nentries = 0;
 };
 
 }  // namespace
@@ -76,7 +78,7 @@ struct scb_layer {
         cudaFree(d_values);
         cudaFree(d_dec);
         cudaFree(d_rowptr);
-        for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); cudaFree(p.d_masks); }
+        for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); cudaFree(p.d_ptr_m); cudaFree(p.d_taps_m); cudaFree(p.d_masks); }
     }
     Program* prog(int kt) {
         for (auto& p : progs) if (p.kt == kt) return &p;
@@ -162,6 +164,15 @@ bool encode_payloads(scb_layer* L, const unsigned char* vals, std::vector<uint32
     return true;
 }
 
+template <typename T>
+scb_status upload(T** dst, const std::vector<T>& v) {
+    cudaError_t e = cudaMalloc(dst, std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if (!v.empty() && (e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy");
+    return SCB_OK;
+}
+
 scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int32_t* rowptr,
                          const std::vector<uint32_t>& pay) {
     const Geom& g = L->g;
@@ -169,52 +180,64 @@ scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int3
     P.kt = kt;
     P.groups = (g.k + kt - 1) / kt;
     const int C = g.c, RS = g.r * g.s, NW = (kt + 1) / 2;
+    const uint32_t sentinel = (uint32_t)(kt * RS);
     const int64_t plane = (int64_t)g.hp * g.wp;
-    P.h_ptr.assign((size_t)P.groups * (C + 1), 0);
+    std::vector<int32_t> ptr_j((size_t)P.groups * (C + 1)), ptr_m((size_t)P.groups * (C + 1));
     std::vector<uint32_t> masks((size_t)P.groups * C * NW, 0u);
     const bool mask_ok = RS <= 16;
-    std::vector<Tap> taps;
-    taps.reserve(L->nnz + 2);
+    std::vector<Tap> tj, tm, chan;
+    tj.reserve(L->nnz + (size_t)P.groups * (C + 1) + 2);
+    tm.reserve(L->nnz + 2);
     std::vector<int32_t> cur(kt);
     for (int gg = 0; gg < P.groups; ++gg) {
         for (int kk = 0; kk < kt; ++kk) {
             int k = gg * kt + kk;
             cur[kk] = k < g.k ? rowptr[k] : 0;
         }
+        // ptr_j[g][c] must point at the sentinel of the first non-empty channel >= c:
+        // fill after the fact, walking channels backwards
+        std::vector<int32_t> first_sent(C + 1, -1);
         for (int c = 0; c < C; ++c) {
-            P.h_ptr[(size_t)gg * (C + 1) + c] = (int32_t)taps.size();
+            ptr_m[(size_t)gg * (C + 1) + c] = (int32_t)tm.size();
+            chan.clear();
             for (int kk = 0; kk < kt; ++kk) {
                 int k = gg * kt + kk;
                 if (k >= g.k) break;
                 while (cur[kk] < rowptr[k + 1] && colidx[cur[kk]] / plane == c) {
                     int64_t rem = colidx[cur[kk]] % plane;
                     int r = (int)(rem / g.wp), s = (int)(rem % g.wp);
-                    Tap tp;
-                    tp.meta = (uint32_t)(kk * RS + r * g.s + s);
-                    tp.payload = pay[cur[kk]];
-                    taps.push_back(tp);
+                    chan.push_back(Tap{(uint32_t)(kk * RS + r * g.s + s), pay[cur[kk]]});
                     if (mask_ok)
                         masks[((size_t)gg * C + c) * NW + kk / 2] |= 1u << (16 * (kk % 2) + r * g.s + s);
                     ++cur[kk];
                 }
             }
+            if (!chan.empty()) {
+                first_sent[c] = (int32_t)tj.size();
+                tj.push_back(Tap{sentinel, (uint32_t)c});
+                tj.insert(tj.end(), chan.begin(), chan.end());
+                tm.insert(tm.end(), chan.begin(), chan.end());
+            }
         }
-        P.h_ptr[(size_t)gg * (C + 1) + C] = (int32_t)taps.size();
+        first_sent[C] = (int32_t)tj.size();
+        tj.push_back(Tap{sentinel, (uint32_t)C});  // end-of-group sentinel
+        for (int c = C - 1; c >= 0; --c)
+            if (first_sent[c] < 0) first_sent[c] = first_sent[c + 1];
+        for (int c = 0; c <= C; ++c) ptr_j[(size_t)gg * (C + 1) + c] = first_sent[c];
+        ptr_m[(size_t)gg * (C + 1) + C] = (int32_t)tm.size();
     }
-    if ((int64_t)taps.size() != L->nnz) return fail(SCB_ERR_FORMAT, "tap program lost entries (colidx order?)");
-    taps.push_back(Tap{0u, 0u});  // two slack slots for the two-deep prefetch
-    taps.push_back(Tap{0u, 0u});
+    if ((int64_t)tm.size() != L->nnz) return fail(SCB_ERR_FORMAT, "tap program lost entries (colidx order?)");
+    for (auto* v : {&tj, &tm}) { v->push_back(Tap{sentinel, 0u}); v->push_back(Tap{sentinel, 0u}); }  // prefetch slack
     P.ntaps = L->nnz;
-    cudaError_t e;
-    if ((e = cudaMalloc(&P.d_ptr, P.h_ptr.size() * sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    if ((e = cudaMalloc(&P.d_taps, taps.size() * sizeof(Tap))) != cudaSuccess) { cudaFree(P.d_ptr); return cuda_fail(e, "cudaMalloc"); }
-    if ((e = cudaMalloc(&P.d_masks, std::max<size_t>(masks.size(), 1) * sizeof(uint32_t))) != cudaSuccess) {
-        cudaFree(P.d_ptr); cudaFree(P.d_taps); return cuda_fail(e, "cudaMalloc");
+    P.nentries = (int64_t)tj.size();
+    P.h_ptr = ptr_m;
+    scb_status st;
+    if ((st = upload(&P.d_ptr, ptr_j)) != SCB_OK || (st = upload(&P.d_taps, tj)) != SCB_OK ||
+        (st = upload(&P.d_ptr_m, ptr_m)) != SCB_OK || (st = upload(&P.d_taps_m, tm)) != SCB_OK ||
+        (st = upload(&P.d_masks, masks)) != SCB_OK) {
+        cudaFree(P.d_ptr); cudaFree(P.d_taps); cudaFree(P.d_ptr_m); cudaFree(P.d_taps_m); cudaFree(P.d_masks);
+        return st;
     }
-    cudaMemcpy(P.d_ptr, P.h_ptr.data(), P.h_ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
-    cudaMemcpy(P.d_masks, masks.data(), masks.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-    e = cudaMemcpy(P.d_taps, taps.data(), taps.size() * sizeof(Tap), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) { cudaFree(P.d_ptr); cudaFree(P.d_taps); cudaFree(P.d_masks); return cuda_fail(e, "cudaMemcpy"); }
     L->progs.push_back(std::move(P));
     return SCB_OK;
 }
@@ -445,7 +468,8 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
     if (variant >= num_variants()) return fail(SCB_ERR_ARG, "bad variant");
     Program* P = L->prog(scb::variant(variant).info.kt);
     if (!P) return fail(SCB_ERR_ARG, "no program for this variant");
-    *bytes = P->ntaps * (int64_t)sizeof(Tap) + (int64_t)P->h_ptr.size() * 4;
+    *bytes = (scb::variant(variant).info.dispatch == DISPATCH_JUMP ? P->nentries : P->ntaps) * (int64_t)sizeof(Tap) +
+             (int64_t)P->h_ptr.size() * 4;
     return SCB_OK;
 }
 
@@ -502,7 +526,10 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     const Program* P = L->prog(ve.info.kt);
     TiledParams p;
     std::memset(&p, 0, sizeof(p));
-    p.x = x; p.bias = static_cast<const float*>(bias); p.y = y; p.tap_ptr = P->d_ptr; p.taps = P->d_taps; p.masks = P->d_masks;
+    p.x = x; p.bias = static_cast<const float*>(bias); p.y = y; const bool jump = ve.info.dispatch == DISPATCH_JUMP;
+    p.tap_ptr = jump ? P->d_ptr : P->d_ptr_m;
+    p.taps = jump ? P->d_taps : P->d_taps_m;
+    p.masks = P->d_masks;
     p.q = L->q;
     p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f; p.pad = g.pad;
     p.imgs = c.imgs; p.bh = c.bh; p.bw = c.bw; p.cc = c.cc; p.wk = c.warps_k;

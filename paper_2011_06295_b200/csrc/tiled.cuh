@@ -33,7 +33,7 @@
 
 namespace scb {
 
-template <int R, int S, int KT, int NBT, int TH, int TW, int WF, int MODE, int DISPATCH>
+template <int R, int S, int PAD, int KT, int NBT, int TH, int TW, int WF, int MODE, int DISPATCH, bool F16IO>
 struct TapLoop;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -192,6 +192,10 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
     const float lin_scale = qs.scale;
     // lane's patch origin inside a window plane
     const int patch_off = (ty * TH) * ROW + XOFF - PAD + tx * TW;
+    float pt[NBT * PH * PW];
+#pragma unroll
+    for (int i = 0; i < NBT * PH * PW; ++i) pt[i] = 0.f;
+    const Tap* q = p.taps + (g < p.groups ? __ldg(p.tap_ptr + g * cp1) : 0);
     for (int ch = 0; ch < nch; ++ch) {
         const int buf = ch & 1;
         if (ch + 1 < nch) {
@@ -206,43 +210,37 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
             const int c0 = ch * p.cc;
             const int ncl = min(p.cc, C - c0);
             const TIO* xb = xs + (size_t)buf * stage_el + (size_t)ti * NBT * p.cc * plane_s + patch_off;
-            int tb = __ldg(p.tap_ptr + g * cp1 + c0);
-            const Tap* vp = p.taps + tb;
-            unsigned pc = 0;
-            if constexpr (DISPATCH == DISPATCH_MASK) pc = __ldg(&vp->payload);
-            for (int cl = 0; cl < ncl; ++cl) {
-                const int c = c0 + cl;
-                unsigned mk[NW];
-                int te = 0;
-                if constexpr (DISPATCH == DISPATCH_JUMP) {
-                    te = __ldg(p.tap_ptr + g * cp1 + c + 1);
-                    if (te == tb) continue;
-                } else {
+            if constexpr (DISPATCH == DISPATCH_JUMP) {
+                // sentinel-driven stream: the PTX loop loads patches and exits at the
+                // first sentinel of a channel beyond this stage (q then points at it)
+                TapLoop<R, S, PAD, KT, NBT, TH, TW, WF, MODE, DISPATCH, F16IO>::run(
+                    acc, pt, q, (unsigned)c0, (unsigned)ncl, smem_u32(xb), (unsigned)(plane_s * ES),
+                    (unsigned)(p.cc * plane_s * ES), (unsigned)(ROW * ES), cb_addr, lin_scale);
+            } else {
+                const Tap* vp = p.taps + __ldg(p.tap_ptr + g * cp1 + c0);
+                unsigned pc = __ldg(&vp->payload);
+                for (int cl = 0; cl < ncl; ++cl) {
+                    const int c = c0 + cl;
+                    unsigned mk[NW];
                     const unsigned* mp = p.masks + ((size_t)g * C + c) * NW;
                     unsigned any = 0;
 #pragma unroll
                     for (int i = 0; i < NW; ++i) { mk[i] = __ldg(mp + i); any |= mk[i]; }
                     if (any == 0) continue;
-                }
-                float pt[NBT * PH * PW];
 #pragma unroll
-                for (int j = 0; j < NBT; ++j) {
-                    const TIO* pl = xb + (size_t)(j * p.cc + cl) * plane_s;
+                    for (int j = 0; j < NBT; ++j) {
+                        const TIO* pl = xb + (size_t)(j * p.cc + cl) * plane_s;
 #pragma unroll
-                    for (int yy = 0; yy < PH; ++yy) {
-                        float* d = &pt[(j * PH + yy) * PW];
-                        const TIO* rp = pl + yy * ROW;
-                        if constexpr (PAD > 0) load_row<PAD, ES, TIO>(d, rp);
-                        load_row<TW, MID_ALIGN, TIO>(d + PAD, rp + PAD);
-                        if constexpr (RIGHT > 0) load_row<RIGHT, MID_ALIGN, TIO>(d + PAD + TW, rp + PAD + TW);
+                        for (int yy = 0; yy < PH; ++yy) {
+                            float* d = &pt[(j * PH + yy) * PW];
+                            const TIO* rp = pl + yy * ROW;
+                            if constexpr (PAD > 0) load_row<PAD, ES, TIO>(d, rp);
+                            load_row<TW, MID_ALIGN, TIO>(d + PAD, rp + PAD);
+                            if constexpr (RIGHT > 0) load_row<RIGHT, MID_ALIGN, TIO>(d + PAD + TW, rp + PAD + TW);
+                        }
                     }
-                }
-                if constexpr (DISPATCH == DISPATCH_JUMP) {
-                    TapLoop<R, S, KT, NBT, TH, TW, WF, MODE, DISPATCH>::run(acc, pt, p.taps + tb, p.taps + te, cb_addr,
-                                                                            lin_scale);
-                    tb = te;
-                } else {
-                    TapLoop<R, S, KT, NBT, TH, TW, WF, MODE, DISPATCH>::run(acc, pt, vp, pc, mk, cb_addr, lin_scale);
+                    TapLoop<R, S, PAD, KT, NBT, TH, TW, WF, MODE, DISPATCH, F16IO>::run(acc, pt, vp, pc, mk, cb_addr,
+                                                                                       lin_scale);
                 }
             }
         }

@@ -50,4 +50,4 @@ print(json.dumps(device_layer(kern, 0, dt).candidates({n})))
         r = subprocess.run([sys.executable, __file__, 'one', str(c), str(hw), str(k), str(n), str(f16), str(i)],
                            capture_output=True, text=True, env=dict(os.environ, CUDA_LAUNCH_BLOCKING='1'), timeout=120)
         tail = (r.stdout.strip().splitlines() or [''])[-1] if r.returncode == 0 else ('CRASH ' + (r.stderr.strip().splitlines() or [''])[-1][:150])
-        print(f"layer c{c} hw{hw} f16={f16} v{cf[0]} stage={v['stage']} tile=({v['kt']},{v['nbt']},{v['th']},{v['tw']}) mode={v['mode']} cfg={cf}: {tail}", flush=True)
+        print(f"layer c{c} hw{hw} f16={f16} v{cf[0]} disp={v['dispatch']} tile=({v['kt']},{v['nbt']},{v['th']},{v['tw']}) mode={v['mode']} cfg={cf}: {tail}", flush=True)
