@@ -8,8 +8,9 @@ the launch tuner picks per layer:
 * DISPATCH_JUMP (0): one PTX ``brx.idx`` per tap through a jump table of the
   KT*R*S MAC blocks (SASS LDC + BRX).  NVVM would lower a C++ switch into a
   compare tree (~7 compare+branch per tap, ncu: profiles/r01_*); brx.idx
-  costs a constant handful of instructions per tap.  The tap stream is
-  prefetched two entries ahead.
+  costs a constant handful of instructions per tap.  Channel switches are
+  sentinel entries of the stream that reload the register patch inside the
+  same PTX loop; the stream segment of a stage is staged in shared memory.
 * DISPATCH_MASK (1): per input channel the warp group reads KT 16-bit masks
   (bit r*S+s of half-word kk = tap present) and walks the MAC blocks in order
   with warp-uniform forward branches over absent kk / rows / taps.  No
@@ -37,17 +38,20 @@ JUMP, MASK = 0, 1                                # kernels.cuh DISPATCH_*
 
 # (R, S, PAD, KT, NBT, TH, TW, dispatches, min CTAs/SM)
 TILES = [
-    (3, 3, 1, 8, 1, 4, 4, (JUMP, MASK), 1),
-    (3, 3, 1, 4, 1, 4, 4, (JUMP, MASK), 2),
-    (3, 3, 1, 8, 1, 2, 4, (JUMP, MASK), 2),
-    (3, 3, 1, 4, 2, 2, 4, (JUMP, MASK), 2),
-    (3, 3, 1, 4, 2, 4, 4, (JUMP, MASK), 1),
-    (3, 3, 1, 8, 2, 2, 2, (JUMP, MASK), 2),
-    (3, 3, 1, 8, 4, 2, 2, (JUMP, MASK), 1),
-    (3, 3, 1, 4, 4, 2, 2, (JUMP, MASK), 2),
-    (1, 1, 0, 8, 1, 4, 4, (JUMP, MASK), 1),
+    (3, 3, 1, 8, 1, 4, 4, (JUMP,), 1),
+    (3, 3, 1, 4, 1, 4, 4, (JUMP,), 2),
+    (3, 3, 1, 8, 1, 2, 4, (JUMP,), 2),
+    (3, 3, 1, 4, 2, 2, 4, (JUMP,), 2),
+    (3, 3, 1, 4, 2, 4, 4, (JUMP,), 1),
+    (3, 3, 1, 8, 2, 2, 2, (JUMP,), 2),
+    (3, 3, 1, 8, 4, 2, 2, (JUMP,), 1),
+    (3, 3, 1, 4, 4, 2, 2, (JUMP,), 2),
+    (3, 3, 1, 4, 1, 2, 2, (JUMP,), 2),
+    (3, 3, 1, 4, 2, 2, 2, (JUMP,), 2),
+    (3, 3, 1, 2, 2, 2, 2, (JUMP,), 2),
+    (1, 1, 0, 8, 1, 4, 4, (JUMP,), 1),
     (1, 1, 0, 8, 1, 2, 4, (JUMP,), 2),
-    (5, 5, 2, 4, 1, 4, 4, (JUMP, MASK), 1),
+    (5, 5, 2, 4, 1, 4, 4, (JUMP,), 1),
     (5, 5, 0, 4, 1, 4, 4, (JUMP,), 1),
     (5, 5, 2, 4, 1, 2, 4, (JUMP,), 2),
     (1, 2, 0, 8, 1, 1, 8, (JUMP,), 2),
@@ -165,22 +169,23 @@ def gen_jump(R, S, PAD, KT, NBT, TH, TW, WF, MODE, f16) -> str:
     """Jump-table tap loop over one stage.  The stream of a warp group holds,
     per non-empty input channel, a sentinel (meta = KT*R*S, payload = channel)
     followed by the channel's taps; the group ends with a sentinel of channel C.
-    A sentinel of a channel outside [c0, c0+cc) ends the stage with q pointing
-    at it; otherwise it (re)loads the lane's patch of that channel."""
+    The stage's segment of the stream sits in shared memory at `qs`.  A
+    sentinel of a channel outside [c0, c0+cc) ends the stage; any other
+    sentinel (re)loads the lane's patch of that channel."""
     nacc = KT * NBT * TH * TW
     o = Ops(R, S, KT, NBT, TH, TW, pt_base=nacc)
     npt = o.npt
-    oq = nacc + npt                                    # "+l" q
-    oin = oq + 1                                       # inputs
+    oq = nacc + npt                                    # shared address of the stage's tap segment
+    oin = oq + 1                                       # remaining inputs
     names = ["c0", "ccnt", "base", "planeb", "imgb", "rowb", "aux", "scl"]
     op = {n: f"%{oin + i}" for i, n in enumerate(names)}
     NC = KT * R * S
     L = ["{\n", regs_decl(o.P, MODE, with_end=False),
-         ".reg .u32 %%cl, %%a, %%ra, %%c0, %%ccnt, %%base, %%planeb, %%imgb, %%rowb;\n",
+         ".reg .u32 %%cl, %%a, %%ra, %%c0, %%ccnt, %%base, %%planeb, %%imgb, %%rowb, %%qs;\n",
          f"mov.u32 %%c0, {op['c0']};\nmov.u32 %%ccnt, {op['ccnt']};\nmov.u32 %%base, {op['base']};\n"
          f"mov.u32 %%planeb, {op['planeb']};\nmov.u32 %%imgb, {op['imgb']};\nmov.u32 %%rowb, {op['rowb']};\n"
-         f"mov.u32 %%aux, {op['aux']};\nmov.f32 %%scl, {op['scl']};\nmov.u64 %%q, %{oq};\n",
-         "ld.global.nc.v2.u32 {%%m, %%pb}, [%%q];\n",
+         f"mov.u32 %%aux, {op['aux']};\nmov.f32 %%scl, {op['scl']};\nmov.u32 %%qs, %{oq};\n",
+         "ld.shared.v2.u32 {%%m, %%pb}, [%%qs];\n",
          "bra.uni LOOP;\n"]
     labels = []
     for kk in range(KT):
@@ -196,12 +201,13 @@ def gen_jump(R, S, PAD, KT, NBT, TH, TW, WF, MODE, f16) -> str:
     L.append("bra.uni LOOP;\n")
     L.append("TBL: .branchtargets " + ", ".join(labels) + ";\n")
     L.append("LOOP:\nmov.u32 %%mc, %%m;\nmov.u32 %%pc, %%pb;\n"
-             "ld.global.nc.v2.u32 {%%m, %%pb}, [%%q+8];\nadd.u64 %%q, %%q, 8;\n")
+             "ld.shared.v2.u32 {%%m, %%pb}, [%%qs+8];\nadd.u32 %%qs, %%qs, 8;\n")
     L.append(decode_ptx(WF))
-    L.append("brx.idx.uni %%mc, TBL;\nEXIT:\nsub.u64 %%q, %%q, 8;\nmov.u64 %" + str(oq) + ", %%q;\n}\n")
-    outs = [f'"+f"(a[{i}])' for i in range(nacc)] + [f'"+f"(pt[{i}])' for i in range(npt)] + ['"+l"(q)']
-    ins = ['"r"(c0)', '"r"(ccnt)', '"r"(base)', '"r"(planeb)', '"r"(imgb)', '"r"(rowb)', '"r"(aux)', '"f"(scl)']
-    sig = (f"float (&a)[{nacc}], float (&pt)[{npt}], const Tap*& q, unsigned c0, unsigned ccnt, unsigned base, "
+    L.append("brx.idx.uni %%mc, TBL;\nEXIT:\n}\n")
+    outs = [f'"+f"(a[{i}])' for i in range(nacc)] + [f'"+f"(pt[{i}])' for i in range(npt)]
+    ins = ['"r"(qs)', '"r"(c0)', '"r"(ccnt)', '"r"(base)', '"r"(planeb)', '"r"(imgb)', '"r"(rowb)', '"r"(aux)',
+           '"f"(scl)']
+    sig = (f"float (&a)[{nacc}], float (&pt)[{npt}], unsigned qs, unsigned c0, unsigned ccnt, unsigned base, "
            "unsigned planeb, unsigned imgb, unsigned rowb, unsigned aux, float scl")
     return emit(f"{R}, {S}, {PAD}, {KT}, {NBT}, {TH}, {TW}, {WF}, {MODE}, {JUMP}, {'true' if f16 else 'false'}",
                 sig, "".join(L), outs, ins)

@@ -61,6 +61,7 @@ struct TiledParams {
     int row;                    // smem row pitch (elements)
     int stage_el;               // elements per pipeline stage
     int chunk;                  // cp.async size in bytes (16, 8 or 4)
+    int tap_cap;                // tap entries per (stage, warp group) in shared memory
     int n_ey, n_fx, kblocks, groups;
     uint32_t flags;
 };

@@ -46,7 +46,9 @@ struct DeviceGuard {
 struct Program {
     int kt = 0;
     int groups = 0;
-    std::vector<int32_t> h_ptr;   // groups x (C+1)
+    std::vector<int32_t> h_ptr;   // groups x (C+1), mask stream
+    std::vector<int32_t> h_ptr_j; // groups x (C+1), jump stream
+    std::map<int, int> tap_cap;   // cc -> smem tap entries per (stage, group)
     int32_t* d_ptr = nullptr;     // jump stream: ptr[g][c] -> sentinel of first non-empty channel >= c
     Tap* d_taps = nullptr;        // jump stream: per channel a sentinel {KT*R*S, c} + taps; group ends with {., C}
     int32_t* d_ptr_m = nullptr;   // mask stream (taps only)
@@ -83,6 +85,23 @@ struct scb_layer {
     Program* prog(int kt) {
         for (auto& p : progs) if (p.kt == kt) return &p;
         return nullptr;
+    }
+    int cap_for(Program& p, int cc) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = p.tap_cap.find(cc);
+        if (it != p.tap_cap.end()) return it->second;
+        const int C = g.c;
+        int mx = 0;
+        for (int gg = 0; gg < p.groups; ++gg)
+            for (int c0 = 0; c0 < C; c0 += cc) {
+                const int c1 = std::min(c0 + cc, C);
+                const int a0 = p.h_ptr_j[(size_t)gg * (C + 1) + c0] & ~1;
+                const int a1 = p.h_ptr_j[(size_t)gg * (C + 1) + c1] + 2;
+                mx = std::max(mx, a1 - a0);
+            }
+        mx = (mx + 1) & ~1;  // whole 16-byte chunks
+        p.tap_cap[cc] = mx;
+        return mx;
     }
     const Program* prog(int kt) const {
         for (auto& p : progs) if (p.kt == kt) return &p;
@@ -231,6 +250,7 @@ scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int3
     P.ntaps = L->nnz;
     P.nentries = (int64_t)tj.size();
     P.h_ptr = ptr_m;
+    P.h_ptr_j = ptr_j;
     scb_status st;
     if ((st = upload(&P.d_ptr, ptr_j)) != SCB_OK || (st = upload(&P.d_taps, tj)) != SCB_OK ||
         (st = upload(&P.d_ptr_m, ptr_m)) != SCB_OK || (st = upload(&P.d_taps_m, tm)) != SCB_OK ||
@@ -272,7 +292,7 @@ int row_pitch(const scb_variant_info& v, int bw) {
 
 // Validate a launch and compute its derived quantities.
 struct Derived {
-    int wp, threads, row, stage_el, chunk, n_ey, n_fx, kblocks, nb;
+    int wp, threads, row, stage_el, chunk, tap_cap, n_ey, n_fx, kblocks, nb;
     size_t smem;
     unsigned grid;
 };
@@ -296,7 +316,9 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     const size_t plane = (size_t)(c.bh + v.r - 1) * d->row;  // elements per (image, channel)
     const size_t stage_bytes = ((size_t)c.imgs * c.cc * plane * es + 127) & ~(size_t)127;
     d->stage_el = (int)(stage_bytes / es);
-    d->smem = 2 * stage_bytes;
+    d->tap_cap = 0;
+    if (v.dispatch == DISPATCH_JUMP) d->tap_cap = L->cap_for(*L->prog(v.kt), c.cc);
+    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * d->tap_cap * sizeof(Tap);
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     // copy chunk: the widest of 16/8/4 bytes dividing the input row and the block stride
     const int n_fx = (g.f + c.bw - 1) / c.bw;
@@ -533,7 +555,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     p.q = L->q;
     p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f; p.pad = g.pad;
     p.imgs = c.imgs; p.bh = c.bh; p.bw = c.bw; p.cc = c.cc; p.wk = c.warps_k;
-    p.wp = d.wp; p.row = d.row; p.stage_el = d.stage_el; p.chunk = d.chunk;
+    p.wp = d.wp; p.row = d.row; p.stage_el = d.stage_el; p.chunk = d.chunk; p.tap_cap = d.tap_cap;
     p.n_ey = d.n_ey; p.n_fx = d.n_fx; p.kblocks = d.kblocks; p.groups = P->groups;
     p.flags = flags;
     cudaError_t e = ve.launch(p, d.grid, (unsigned)d.threads, d.smem, st);

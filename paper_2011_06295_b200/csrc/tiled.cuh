@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
     const int plane_s = RT * ROW;    // elements per (image, channel)
     const int stage_el = p.stage_el; // elements per stage (128-byte multiple)
     TIO* xs = reinterpret_cast<TIO*>(smem);
+    // tap segments of the stage: [buf][warp group][tap_cap] entries after the x stages
+    Tap* tsm = reinterpret_cast<Tap*>(smem + (size_t)2 * stage_el * ES);
 
     // zero both stages once: positions outside the image are never written again
     {
@@ -183,6 +185,19 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
             pc += dpc;
             if (yy >= RT) { yy -= RT; ++pc; }
         }
+        if constexpr (DISPATCH == DISPATCH_JUMP) {
+            // each warp group's stream segment for channels [c0, c0+cc) plus the exit
+            // sentinel and one prefetch slot, copied from its 16-byte-aligned floor
+            const int c1 = min(c0 + p.cc, C);
+            for (int w = 0; w < p.wk; ++w) {
+                const int gg = kb * p.wk + w;
+                if (gg >= p.groups) break;
+                const int a0 = __ldg(p.tap_ptr + gg * cp1 + c0) & ~1;
+                const int a1 = __ldg(p.tap_ptr + gg * cp1 + c1) + 2;
+                Tap* d = tsm + ((size_t)buf * p.wk + w) * p.tap_cap;
+                for (int i = 2 * tid; i < a1 - a0; i += 2 * nthreads) cp_async<16>(d + i, p.taps + a0 + i);
+            }
+        }
     };
 
     const int nch = (C + p.cc - 1) / p.cc;
@@ -195,7 +210,7 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
     float pt[NBT * PH * PW];
 #pragma unroll
     for (int i = 0; i < NBT * PH * PW; ++i) pt[i] = 0.f;
-    const Tap* q = p.taps + (g < p.groups ? __ldg(p.tap_ptr + g * cp1) : 0);
+
     for (int ch = 0; ch < nch; ++ch) {
         const int buf = ch & 1;
         if (ch + 1 < nch) {
@@ -212,9 +227,11 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
             const TIO* xb = xs + (size_t)buf * stage_el + (size_t)ti * NBT * p.cc * plane_s + patch_off;
             if constexpr (DISPATCH == DISPATCH_JUMP) {
                 // sentinel-driven stream: the PTX loop loads patches and exits at the
-                // first sentinel of a channel beyond this stage (q then points at it)
+                // first sentinel of a channel beyond this stage
+                const int t0 = __ldg(p.tap_ptr + g * cp1 + c0);
+                const Tap* seg = tsm + ((size_t)buf * p.wk + wg) * p.tap_cap + (t0 & 1);
                 TapLoop<R, S, PAD, KT, NBT, TH, TW, WF, MODE, DISPATCH, F16IO>::run(
-                    acc, pt, q, (unsigned)c0, (unsigned)ncl, smem_u32(xb), (unsigned)(plane_s * ES),
+                    acc, pt, smem_u32(seg), (unsigned)c0, (unsigned)ncl, smem_u32(xb), (unsigned)(plane_s * ES),
                     (unsigned)(p.cc * plane_s * ES), (unsigned)(ROW * ES), cb_addr, lin_scale);
             } else {
                 const Tap* vp = p.taps + __ldg(p.tap_ptr + g * cp1 + c0);
