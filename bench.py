@@ -1,0 +1,451 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 direct sparse convolution engine (BASELINE.json).
+
+Metric: "Sparse conv layer us & achieved HBM GB/s vs sparsity; images/sec at
+1-8 GPUs".  One *step* is one forward pass of the 13-layer VGG-16/CIFAR-10
+conv stack (BASELINE config 3: 3x3 convs, 90% unified per-channel sparsity,
+bias + ReLU fused, 2x2 max-pool fused at the end of each stage) over a batch
+of 256 synthetic 32x32 images per GPU, fp32 in the reference's exact
+arithmetic (separately rounded multiply and add, bit-identical to the CPU
+reference).  ``value`` = images/s of the whole job (weak scaling: every rank
+runs its own 256-image batch, no data-path collective).
+
+Per-layer microseconds, achieved FLOP/s and HBM GB/s are reported in
+``layers``; ``roofline`` describes the layer kernel with the largest share of
+the step.  ``e2e`` runs the same stack through the host-facing call
+(SparseConvNet.forward: pinned host batch -> H2D -> 13 kernels -> D2H).
+``cpu_baseline`` times the reference algorithm's CPU restatement
+(oracle/, C + OpenMP) on a bounded sample of the same workload on this box's
+host cores.  ``dense_cudnn`` times torch/cuDNN dense fp32 (IEEE, no TF32)
+convolutions of the same stack, the comparator the paper uses.
+
+``--impl reference`` times only the reference's CPU path (the oracle port)
+and prints the same metric with ``"impl": "reference"``.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Sparse conv layer µs & achieved HBM GB/s vs sparsity; images/sec at 1–8 GPUs"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU")
+    ap.add_argument("--sparsity", type=float, default=0.9)
+    ap.add_argument("--no-tune", action="store_true", help="C heuristic launches instead of the tuner")
+    ap.add_argument("--launches", default="", help="JSON of per-layer launches: loaded if present "
+                    "(tuner skipped), else written after tuning")
+    ap.add_argument("--cpu-images", type=int, default=8, help="images per CPU-baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline time budget")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def workload(sparsity: float):
+    from paper_2011_06295_b200.synth import vgg16_cifar
+    return vgg16_cifar(sparsity)
+
+
+def layer_work(spec, L: int, batch: int, pool: bool):
+    """Algorithmic FLOPs and bytes of one layer launch:
+    FLOPs = 2*N*K*E*F*L (executed MACs incl. unification padding,
+    engine.py:131-136); bytes = unpadded input + output (pooled when fused)
+    + values + column indices + rowptr + bias, each counted once."""
+    sh = spec.shape
+    flops = 2 * batch * sh.k * sh.e * sh.f * L
+    e, f = (sh.e // 2, sh.f // 2) if pool else (sh.e, sh.f)
+    byts = 4 * (batch * sh.c * sh.h * sh.w + batch * sh.k * e * f) + sh.k * L * (4 + 4) + 4 * (sh.k + 1) + 4 * sh.k
+    return flops, byts
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = self.proc.communicate()[0]
+
+    def summary(self):
+        rows = []
+        for ln in self.out.splitlines():
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), p[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the oracle: reference algorithm restated in C, OpenMP threads)
+# ---------------------------------------------------------------------------
+
+def cpu_stack_time(specs, kernels, biases, images: int, budget_s: float, seed: int = 7):
+    """Run the reference algorithm over the conv stack on `images` images
+    (conv_sparse -> ReLU -> 2x2 max-pool, store.py:276-284) until `budget_s`
+    is spent; returns (seconds per pass, passes, threads)."""
+    from oracle import oracle as orc
+    rng = np.random.default_rng(seed)
+    x0 = rng.standard_normal((images, specs[0][0].shape.c, 32, 32)).astype(np.float32)
+
+    def one_pass():
+        a = x0
+        for (spec, pool), kern, b in zip(specs, kernels, biases):
+            sh = spec.shape
+            z = orc.conv_sparse(a, kern.values, kern.colidx, kern.rowptr, sh.k, sh.r, sh.s, sh.stride,
+                                sh.padding, b)
+            a = np.maximum(z, 0)
+            if pool:
+                n, k, e, f = a.shape
+                a = a.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
+        return a
+
+    one_pass()  # warm (threads, page faults)
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        one_pass()
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or passes >= 1000:
+            break
+    return el / passes, passes, orc.max_threads()
+
+
+def build_kernels(specs, seed: int = 0):
+    import paper_2011_06295_b200 as sc
+    from paper_2011_06295_b200.synth import bench_inputs, make_layer_weights
+    kernels, biases = [], []
+    for spec, _ in specs:
+        kernels.append(sc.build_csr(make_layer_weights(spec, seed), spec.shape))
+        biases.append(bench_inputs(spec.shape, 1, seed)[1])
+    return kernels, biases
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    specs = workload(args.sparsity)
+    kernels, biases = build_kernels(specs)
+    per_pass, passes, threads = cpu_stack_time(specs, kernels, biases, args.cpu_images,
+                                               max(args.cpu_seconds, 1.0))
+    ips = args.cpu_images / per_pass
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ips, 3), "unit": "images/s",
+        "n_gpus": args.gpus, "steps": passes, "warmup": 1, "ms_per_step": round(per_pass * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (make_layer_weights bench.py:105-116 restated; N(0,1) inputs)",
+        "config": {"workload": f"VGG-16 CIFAR-10 13-conv stack, {args.sparsity:g} unified sparsity, "
+                               f"fp32, conv+bias+ReLU(+2x2 max-pool)", "images_per_sample": args.cpu_images,
+                   "global_batch": args.cpu_images, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(ips, 3), "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{passes} passes of the 13-layer stack over {args.cpu_images} images "
+                                   f"(oracle/oracle.c conv_sparse restatement, OpenMP {threads} threads)"},
+        "e2e": {"value": round(ips, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+def fma_peak_tflops(device: int):
+    """Measured CUDA-core peaks (scb_fma_peaks): MAC/s per probe -> FLOP/s."""
+    import ctypes
+    from paper_2011_06295_b200 import _abi
+    names = ctypes.create_string_buffer(16 * 8)
+    vals = (ctypes.c_double * 8)()
+    cnt = ctypes.c_int32()
+    _abi.check(_abi.lib().scb_fma_peaks(device, names, vals, 8, ctypes.byref(cnt)))
+    return {names.raw[16 * i:16 * i + 16].split(b"\0")[0].decode(): 2 * vals[i] / 1e12 for i in range(cnt.value)}
+
+
+def integrity_gate(net, x_dev):
+    """Every tuned layer launch must agree bit for bit with the independent
+    generic kernel on the benchmark input (the reference gates every timed
+    result, bench.py:139-147)."""
+    import torch
+    from paper_2011_06295_b200 import engine
+    from paper_2011_06295_b200.errors import IntegrityError
+    cur = x_dev
+    stream = torch.cuda.current_stream().cuda_stream
+    for i, L in enumerate(net.layers):
+        got = torch.empty(net.out_shape(i, net.batch), dtype=net.tdtype, device=net.tdev)
+        net.launch_layer(i, cur, got, stream)
+        want = torch.empty_like(got)
+        b = net.biases[i]
+        engine.run_layer(net.dlayers[i], cur.data_ptr(), b.data_ptr() if b is not None else 0, want, net.batch,
+                         net.flags(i), None, stream)
+        torch.cuda.synchronize()
+        if not torch.equal(got.view(torch.int32), want.view(torch.int32)):
+            raise IntegrityError(f"{L.name}: tuned launch {net.launches[i]} differs from the generic kernel")
+        cur = got
+
+
+def dense_cudnn(specs, kernels, biases, batch: int, dev, reps: int = 10):
+    """Dense torch/cuDNN fp32 (IEEE) conv + bias + ReLU (+ max-pool) stack time."""
+    import torch
+    import paper_2011_06295_b200 as sc
+    torch.backends.cudnn.benchmark = True
+    old = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        ws = [torch.from_numpy(sc.decompress(k)).to(dev) for k in kernels]
+        bs = [torch.from_numpy(b).to(dev) for b in biases]
+        x = torch.randn((batch, 3, 32, 32), device=dev)
+
+        def step():
+            a = x
+            for (spec, pool), w, b in zip(specs, ws, bs):
+                a = torch.relu(torch.nn.functional.conv2d(a, w, b, padding=spec.shape.padding))
+                if pool:
+                    a = torch.nn.functional.max_pool2d(a, 2)
+            return a
+
+        per_layer = []
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ts = []
+        for _ in range(reps):
+            evs[0].record()
+            step()
+            evs[1].record()
+            evs[1].synchronize()
+            ts.append(evs[0].elapsed_time(evs[1]))
+        return {"ms_per_step": round(statistics.median(ts), 4),
+                "images_per_s": round(batch / (statistics.median(ts) * 1e-3), 1),
+                "precision": "fp32 ieee (cudnn.allow_tf32=False), cudnn.benchmark", "per_layer": per_layer}
+    finally:
+        torch.backends.cudnn.allow_tf32 = old
+
+
+def load_traffic():
+    """Per-layer DRAM traffic (dram__bytes_read.sum + write.sum) from the
+    committed ncu --set full capture summary, if any."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return {}
+    return {}
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    from paper_2011_06295_b200.network import build_net
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    specs = workload(args.sparsity)
+    net = build_net(specs, seed=0, device=local_rank)
+    t0 = time.perf_counter()
+    lf = Path(args.launches) if args.launches else None
+    if lf is not None and lf.exists():
+        net.plan(args.batch, tune=False)
+        net.set_launches([None if l is None else tuple(l) for l in json.loads(lf.read_text())])
+    else:
+        net.plan(args.batch, tune=not args.no_tune)
+        if lf is not None and rank == 0:
+            lf.parent.mkdir(parents=True, exist_ok=True)
+            lf.write_text(json.dumps([None if l is None else list(l) for l in net.launches]))
+    launches = list(net.launches)
+    tune_s = time.perf_counter() - t0
+
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    x_host = torch.randn((args.batch, 3, 32, 32), generator=g).pin_memory()
+    x_dev = x_host.to(dev)
+    integrity_gate(net, x_dev)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    nl = len(net.layers)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        return net.forward_device(x_dev, events=evs)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
+    with Clocks(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            step(ev[k])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [ev[k][0].elapsed_time(ev[k][nl]) for k in range(args.steps)]
+    layer_ms = [[ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(args.steps)] for i in range(nl)]
+    total_s = sum(step_ms) * 1e-3
+
+    # e2e: the host-facing call, H2D + 13 kernels + D2H every step
+    out_host = torch.empty(net.out_shape(nl - 1, args.batch), dtype=torch.float32, pin_memory=True)
+    for _ in range(2):
+        net.forward(x_host, out_host)
+    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e_ev[0].record(stream)
+    for _ in range(args.steps):
+        net.forward(x_host, out_host)
+    e_ev[1].record(stream)
+    e_ev[1].synchronize()
+    e2e_s = e_ev[0].elapsed_time(e_ev[1]) * 1e-3
+
+    # max over ranks
+    t = torch.tensor([total_s, e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_s, e2e_s = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+
+    images = args.batch * args.steps * world
+    value = images / total_s
+    peaks = fma_peak_tflops(local_rank)
+    peak_exact = peaks.get("fmul_fadd")
+    hbm_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    traffic = load_traffic()
+    layers = []
+    for i, ((spec, pool), kern) in enumerate(zip(specs, [L.kernel for L in net.layers])):
+        us = statistics.median(layer_ms[i]) * 1e3
+        fl, by = layer_work(spec, kern.sparse_level, args.batch, pool)
+        layers.append({"layer": spec.name, "L": int(kern.sparse_level), "us": round(us, 2),
+                       "tflops": round(fl / (us * 1e-6) / 1e12, 3), "hbm_gbs": round(by / (us * 1e-6) / 1e9, 1),
+                       "fma_frac": round(fl / (us * 1e-6) / 1e12 / peak_exact, 4) if peak_exact else None,
+                       "launch": list(launches[i]) if launches[i] is not None else "generic"})
+    top = max(range(nl), key=lambda i: layers[i]["us"])
+    fl, by = layer_work(specs[top][0], layers[top]["L"], args.batch, specs[top][1])
+    mean_us = statistics.mean(layer_ms[top]) * 1e3
+    ach = fl / (mean_us * 1e-6) / 1e12
+    roof = {"bound": "fma", "kernel": specs[top][0].name, "achieved": round(ach, 3), "peak": round(peak_exact, 3),
+            "unit": "TFLOP/s", "frac": round(ach / peak_exact, 4),
+            "peak_source": "measured live: scb_fma_peaks 'fmul_fadd' (exact mode = FMUL+FADD per MAC); "
+                           "MEASURED_PEAKS.json has no CUDA-core peak",
+            "ffma_peak_tflops": round(peaks.get("ffma", 0), 2),
+            "algorithmic_flops": fl, "algorithmic_bytes": by,
+            "hbm_achieved_gbs": round(by / (mean_us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
+            "traffic": traffic.get(specs[top][0].name)}
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(total_s / args.steps * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: make_layer_weights (bench.py:105-116 restated), N(0,1) activations",
+        "config": {"workload": f"VGG-16 CIFAR-10, 13 sparse 3x3 convs at {args.sparsity:g} unified sparsity, "
+                               "bias+ReLU fused, 2x2 max-pool fused per stage, exact fp32 (mul+add)",
+                   "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                   "parallelism": f"batch-sharded x{world} (weak, no collective)",
+                   "l2": "flushed between timed steps (256 MB write, untimed)",
+                   "tuned": not args.no_tune, "tune_seconds": round(tune_s, 1)},
+        "e2e": {"value": round(args.batch * args.steps * world / e2e_s, 1), "unit": "images/s",
+                "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
+                "api": "SparseConvNet.forward (pinned host in/out)"},
+        "gpu_launches": net.kernels_per_step() * args.steps,
+        "clocks": clk.summary(),
+        "roofline": roof,
+        "layers": layers,
+        "fma_peaks_tflops": {k: round(v, 2) for k, v in peaks.items()},
+    }
+    if not args.no_dense:
+        line["dense_cudnn"] = dense_cudnn(specs, [L.kernel for L in net.layers], [L.bias for L in net.layers],
+                                          args.batch, dev)
+    if not args.no_cpu and world == 1:
+        per_pass, passes, threads = cpu_stack_time(specs, [L.kernel for L in net.layers],
+                                                   [L.bias for L in net.layers], args.cpu_images,
+                                                   args.cpu_seconds)
+        line["cpu_baseline"] = {"value": round(args.cpu_images / per_pass, 3), "unit": "images/s",
+                                "cores": threads, "kind": "port",
+                                "sample": f"{passes} passes of the 13-layer stack over {args.cpu_images} images "
+                                          "(oracle/oracle.c restatement of conv_sparse_kernel, OpenMP)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

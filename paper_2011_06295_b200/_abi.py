@@ -141,3 +141,14 @@ def variants():
         check(L.scb_variant_get(i, ctypes.byref(v)))
         out.append({f: getattr(v, f) for f, _ in VariantInfo._fields_})
     return out
+
+
+_DT_CODE = {"float32": SCB_F32, "float64": SCB_F64, "float16": SCB_F16}
+
+
+def maxpool2(dtype, x_ptr: int, y_ptr: int, planes: int, h: int, w: int, stream: int = 0) -> None:
+    """2x2 stride-2 max pool over `planes` h x w planes (scb_maxpool2)."""
+    import numpy as np
+    check(lib().scb_maxpool2(_DT_CODE[str(np.dtype(dtype))], ctypes.c_void_p(x_ptr),
+                             ctypes.c_void_p(y_ptr), int(planes), int(h), int(w),
+                             ctypes.c_void_p(stream)), "scb_maxpool2")

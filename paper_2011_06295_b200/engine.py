@@ -160,8 +160,8 @@ def _run(x, kernel: CsrKernel, bias, plan: EnginePlan, *, relu=False, pool=False
         else:
             y = out
         launch = _choose_launch(layer, n, flags, plan)
-        layer.launch(x_dev.data_ptr(), b_dev.data_ptr() if b_dev is not None else 0,
-                     y.data_ptr(), n, flags, launch, stream.cuda_stream)
+        run_layer(layer, x_dev.data_ptr(), b_dev.data_ptr() if b_dev is not None else 0,
+                  y, n, flags, launch, stream.cuda_stream)
         if io != x_dt:
             y = y.to(_torch_dtype(x_dt))
             if out is not None:
@@ -172,17 +172,34 @@ def _run(x, kernel: CsrKernel, bias, plan: EnginePlan, *, relu=False, pool=False
     return y.cpu().numpy()
 
 
+def run_layer(layer, x_ptr: int, b_ptr: int, y, n: int, flags: int, launch, stream: int,
+              scratch=None) -> None:
+    """One layer on `stream`: a tiled launch (tuple), or the generic kernel
+    (launch None) followed by scb_maxpool2 when the pool is requested (the
+    generic kernel has no fused pool epilogue)."""
+    if launch is None and flags & _abi.FLAG_POOL2:
+        sh = layer.shape
+        tmp = scratch if scratch is not None else \
+            _torch().empty((n, sh.k, sh.e, sh.f), dtype=y.dtype, device=y.device)
+        layer.launch(x_ptr, b_ptr, tmp.data_ptr(), n, (flags & ~_abi.FLAG_POOL2) | _abi.FLAG_GENERIC,
+                     None, stream)
+        _abi.maxpool2(layer.io_dtype, tmp.data_ptr(), y.data_ptr(), n * sh.k, sh.e, sh.f, stream)
+        return
+    layer.launch(x_ptr, b_ptr, y.data_ptr(), n, flags | (_abi.FLAG_GENERIC if launch is None else 0),
+                 launch, stream)
+
+
 def _choose_launch(layer, n, flags, plan: EnginePlan):
+    """tuple = tiled launch, None = generic kernel."""
     if flags & _abi.FLAG_GENERIC:
         return None
     if plan.launch is not None:
         return tuple(plan.launch)
-    hit = TUNED.get((layer.signature(), n, flags))
-    if hit is not None:
-        return hit
-    if plan.sub_batch_size > 1:
-        return layer.default_launch(n, flags, plan.sub_batch_size)
-    return None  # C heuristic default
+    key = (layer.signature(), n, flags)
+    if key in TUNED:
+        return TUNED[key]
+    d = layer.default_launch(n, flags, plan.sub_batch_size if plan.sub_batch_size > 1 else 0)
+    return None if d[0] < 0 else d
 
 
 def conv_sparse(x, kernel: CsrKernel, bias=None, plan: EnginePlan = EnginePlan(), *,

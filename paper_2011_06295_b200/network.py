@@ -1,0 +1,244 @@
+"""Network runner: the conv loop of the reference's ``Model.forward``
+(store.py:263-286) on one B200.
+
+``Model.forward`` walks its conv layers, calling ``conv_sparse`` with the
+layer's CsrKernel and bias, then ``np.maximum(z, 0)`` for ReLU layers
+(store.py:276,284).  ``SparseConvNet`` does the same walk with every layer
+resident on the device:
+
+* each layer's CsrKernel is uploaded once (device.DeviceLayer) -- the
+  reference rebuilds CSR on every forward for dense-stored layers
+  (store.py:178-182);
+* ReLU, and the 2x2/2 max-pool that the CIFAR stacks put between stages
+  (the reference has no pooling: SURVEY.md 7.4 #9), are fused into the conv
+  kernel's epilogue (SCB_FLAG_RELU / SCB_FLAG_POOL2), so one layer is one
+  kernel launch and nothing else;
+* activations live in preallocated device buffers; the whole stack can be
+  captured into one CUDA graph (``capture``) so replays pay no launch cost;
+* ``forward`` is the host-facing call: pinned host batch -> H2D -> layers ->
+  D2H of the final activations, all on one stream.
+
+Outputs are bit-identical to running the reference layer by layer
+(conv_sparse -> maximum -> pool) in exact mode; tests/test_gpu_parity.py
+checks that against the CPU oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi, engine
+from .device import device_layer
+from .errors import ShapeError
+from .weights import CsrKernel
+
+
+@dataclass
+class NetLayer:
+    """One conv layer of the stack (cf. ConvLayerRecord, store.py:127-181)."""
+
+    name: str
+    kernel: CsrKernel
+    bias: np.ndarray | None = None
+    relu: bool = True
+    pool: bool = False  # fused 2x2 stride-2 max-pool after the activation
+
+
+class SparseConvNet:
+    """A sequential sparse-conv stack resident on one GPU.
+
+    ``plan(batch)`` allocates the activation buffers for a batch size and
+    (optionally) runs the measured launch tuner on every layer;
+    ``forward_device`` runs the stack asynchronously on the current stream;
+    ``forward`` adds the host copies.  ``dtype`` is the activation dtype
+    (f32, or f16 with f16 weights); ``weight_format`` selects in-register
+    dequantisation ("cb4" / "lin16")."""
+
+    def __init__(self, layers: list[NetLayer], device: int = 0, dtype=np.float32,
+                 weight_format: str = "native", fast_math: bool = False):
+        import torch
+        if not layers:
+            raise ShapeError("empty network")
+        self.torch = torch
+        self.layers = list(layers)
+        self.device = int(device)
+        self.dtype = np.dtype(dtype)
+        self.weight_format = weight_format
+        self.fast_math = bool(fast_math)
+        self.tdev = torch.device("cuda", self.device)
+        self.tdtype = engine._torch_dtype(self.dtype)
+        self.batch = None
+        self.graph = None
+        # geometry chain check: each layer's input is the previous output
+        for a, b in zip(self.layers, self.layers[1:]):
+            sa, sb = a.kernel.shape, b.kernel.shape
+            e, f = (sa.e // 2, sa.f // 2) if a.pool else (sa.e, sa.f)
+            if (sa.k, e, f) != (sb.c, sb.h, sb.w):
+                raise ShapeError(f"{a.name} -> {b.name}: output ({sa.k},{e},{f}) does not "
+                                 f"match input ({sb.c},{sb.h},{sb.w})")
+        self.dlayers = []
+        self.biases = []
+        for L in self.layers:
+            if self.dtype == np.float16 and L.kernel.values.dtype != np.float16:
+                raise ShapeError(f"{L.name}: f16 activations need f16 weights")
+            self.dlayers.append(device_layer(L.kernel, self.device, self.dtype, weight_format))
+            if L.bias is None:
+                self.biases.append(None)
+            else:
+                b = np.ascontiguousarray(L.bias, dtype=np.float32)
+                if b.shape != (L.kernel.shape.k,):
+                    raise ShapeError(f"{L.name}: bias must have shape ({L.kernel.shape.k},)")
+                self.biases.append(torch.from_numpy(b).to(self.tdev))
+        self.launches = [None] * len(self.layers)
+
+    # ---- shapes ---------------------------------------------------------
+    def flags(self, i: int) -> int:
+        L = self.layers[i]
+        f = 0
+        if L.relu:
+            f |= _abi.FLAG_RELU
+        if L.pool:
+            f |= _abi.FLAG_POOL2
+        if self.fast_math:
+            f |= _abi.FLAG_FAST
+        return f
+
+    def out_shape(self, i: int, n: int):
+        sh = self.layers[i].kernel.shape
+        e, f = (sh.e // 2, sh.f // 2) if self.layers[i].pool else (sh.e, sh.f)
+        return (n, sh.k, e, f)
+
+    @property
+    def in_shape(self):
+        sh = self.layers[0].kernel.shape
+        return (sh.c, sh.h, sh.w)
+
+    # ---- planning -------------------------------------------------------
+    def plan(self, batch: int, tune: bool = True, repetitions: int = 3, warmups: int = 1,
+             max_candidates: int | None = None) -> list:
+        """Allocate activations for `batch` images and pick every layer's
+        launch (measured when `tune`, else the C heuristic)."""
+        torch = self.torch
+        self.batch = int(batch)
+        self.graph = None
+        self.x_in = torch.zeros((self.batch, *self.in_shape), dtype=self.tdtype, device=self.tdev)
+        self.acts = [torch.empty(self.out_shape(i, self.batch), dtype=self.tdtype, device=self.tdev)
+                     for i in range(len(self.layers))]
+        self.scratch = [None] * len(self.layers)
+        if tune:
+            from .tuner import tune_launch
+            gen = torch.Generator(device="cpu").manual_seed(0)
+            x = torch.randn((self.batch, *self.in_shape), generator=gen).to(self.tdev, self.tdtype)
+            plan = engine.EnginePlan(fast_math=self.fast_math, weight_format=self.weight_format,
+                                     device=self.device)
+            with torch.cuda.device(self.device):
+                for i, L in enumerate(self.layers):
+                    best, _ = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
+                                          repetitions=repetitions, warmups=warmups,
+                                          max_candidates=max_candidates, include_generic=True)
+                    self.launches[i] = best
+                    x = torch.relu(torch.randn(self.out_shape(i, self.batch), generator=gen)).to(
+                        self.tdev, self.tdtype)
+        else:
+            self.launches = [self.dlayers[i].default_launch(self.batch, self.flags(i))
+                             for i in range(len(self.layers))]
+            self.launches = [None if l[0] < 0 else l for l in self.launches]
+        self.set_launches(self.launches)
+        return list(self.launches)
+
+    def set_launches(self, launches) -> None:
+        """Install explicit per-layer launches (tuple, or None = generic)."""
+        if len(launches) != len(self.layers):
+            raise ShapeError("one launch per layer")
+        self.launches = list(launches)
+        self.graph = None
+        for i, L in enumerate(self.layers):
+            self.scratch[i] = None
+            if self.launches[i] is None and L.pool:
+                sh = L.kernel.shape
+                self.scratch[i] = self.torch.empty((self.batch, sh.k, sh.e, sh.f), dtype=self.tdtype,
+                                                   device=self.tdev)
+
+    # ---- execution ------------------------------------------------------
+    def launch_layer(self, i: int, x_dev, y_dev, stream: int) -> None:
+        b = self.biases[i]
+        engine.run_layer(self.dlayers[i], x_dev.data_ptr(), b.data_ptr() if b is not None else 0,
+                         y_dev, self.batch, self.flags(i), self.launches[i], stream,
+                         scratch=self.scratch[i])
+
+    def kernels_per_step(self) -> int:
+        """Kernel launches of one forward (a generic layer with a pool is two)."""
+        return sum(2 if (l is None and L.pool) else 1 for l, L in zip(self.launches, self.layers))
+
+    def forward_device(self, x_dev=None, events=None):
+        """Run the stack on the current stream of the device; returns the last
+        activation buffer (no synchronisation).  ``events``: optional list of
+        len(layers)+1 CUDA events recorded between layers."""
+        torch = self.torch
+        if self.batch is None:
+            raise ShapeError("call plan(batch) first")
+        if x_dev is not None and x_dev is not self.x_in:
+            self.x_in.copy_(x_dev)
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            if self.graph is not None and events is None:
+                self.graph.replay()
+                return self.acts[-1]
+            s = stream.cuda_stream
+            cur = self.x_in
+            if events is not None:
+                events[0].record(stream)
+            for i in range(len(self.layers)):
+                self.launch_layer(i, cur, self.acts[i], s)
+                if events is not None:
+                    events[i + 1].record(stream)
+                cur = self.acts[i]
+        return self.acts[-1]
+
+    def capture(self) -> None:
+        """Capture the whole stack into one CUDA graph (replayed by
+        forward_device when no per-layer events are requested)."""
+        torch = self.torch
+        with torch.cuda.device(self.device):
+            self.graph = None
+            s = torch.cuda.Stream(self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                self.forward_device()  # warm (lazy attribute setup outside capture)
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.forward_device()
+            self.graph = g
+
+    def forward(self, x_host, out_host=None):
+        """Host batch in, host activations out (the call a user makes):
+        H2D of `x_host` (pinned for an async copy), the stack, D2H."""
+        torch = self.torch
+        xt = x_host if isinstance(x_host, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x_host))
+        if tuple(xt.shape) != (self.batch, *self.in_shape):
+            raise ShapeError(f"input {tuple(xt.shape)} != planned {(self.batch, *self.in_shape)}")
+        with torch.cuda.device(self.device):
+            self.x_in.copy_(xt, non_blocking=True)
+            y = self.forward_device()
+            if out_host is None:
+                out_host = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+            out_host.copy_(y, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+        return out_host if isinstance(x_host, torch.Tensor) else out_host.numpy()
+
+
+def build_net(specs_pools, seed: int = 0, dtype=np.float32, device: int = 0,
+              weight_format: str = "native", fast_math: bool = False):
+    """SparseConvNet of synthetic unified-sparsity layers
+    (synth.make_layer_weights / bench_inputs, bench.py:105-116,175-177)."""
+    from .synth import bench_inputs, make_layer_weights
+    from .weights import build_csr
+    layers = []
+    for spec, pool in specs_pools:
+        w = make_layer_weights(spec, seed).astype(dtype)
+        _, b = bench_inputs(spec.shape, 1, seed)
+        layers.append(NetLayer(spec.name, build_csr(w, spec.shape), b, relu=True, pool=pool))
+    return SparseConvNet(layers, device=device, dtype=dtype, weight_format=weight_format,
+                         fast_math=fast_math)

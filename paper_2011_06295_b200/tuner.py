@@ -17,7 +17,7 @@ from pathlib import Path
 
 import numpy as np
 
-from . import engine
+from . import _abi, engine
 from .device import device_layer
 from .geometry import check_nchw, dtype_of
 
@@ -76,20 +76,26 @@ def tune_launch(x, kernel, bias=None, plan: engine.EnginePlan = engine.EnginePla
     for c in cands:
         timings[c] = time_call(lambda: layer.launch(xin.data_ptr(), bptr, y.data_ptr(), n, flags,
                                                     c, stream), repetitions, warmups)
-    if include_generic and not pool:
-        timings[None] = time_call(lambda: layer.launch(xin.data_ptr(), bptr, y.data_ptr(), n,
-                                                       flags | 0x8, None, stream),
-                                  repetitions, warmups)
+    if include_generic:
+        # the generic kernel has no fused pool: conv + ReLU, then scb_maxpool2
+        yfull = torch.empty((n, sh.k, sh.e, sh.f), dtype=engine._torch_dtype(io), device=x.device) \
+            if pool else y
+        gflags = (flags & ~_abi.FLAG_POOL2) | _abi.FLAG_GENERIC
+
+        def run_generic():
+            layer.launch(xin.data_ptr(), bptr, yfull.data_ptr(), n, gflags, None, stream)
+            if pool:
+                _abi.maxpool2(io, yfull.data_ptr(), y.data_ptr(), n * sh.k, sh.e, sh.f, stream)
+        timings[None] = time_call(run_generic, repetitions, warmups)
     if not timings:
         return None, {}
     best = min(timings, key=lambda c: timings[c])
-    if best is not None:
-        engine.TUNED[(layer.signature(), n, flags)] = best
+    engine.TUNED[(layer.signature(), n, flags)] = best
     return best, timings
 
 
 def save_tuned(path) -> None:
-    rows = [{"sig": list(k[0]), "n": k[1], "flags": k[2], "launch": list(v)}
+    rows = [{"sig": list(k[0]), "n": k[1], "flags": k[2], "launch": None if v is None else list(v)}
             for k, v in engine.TUNED.items()]
     Path(path).write_text(json.dumps(rows, indent=1))
 
@@ -97,5 +103,5 @@ def save_tuned(path) -> None:
 def load_tuned(path) -> int:
     rows = json.loads(Path(path).read_text())
     for r in rows:
-        engine.TUNED[(tuple(r["sig"]), r["n"], r["flags"])] = tuple(r["launch"])
+        engine.TUNED[(tuple(r["sig"]), r["n"], r["flags"])] = None if r["launch"] is None else tuple(r["launch"])
     return len(rows)

@@ -33,7 +33,7 @@ def test_variant_table():
     vs = _abi.variants()
     assert len(vs) >= 10
     for v in vs:
-        assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (4, 8)
+        assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (2, 4, 8)
         assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["dispatch"] in (0, 1)
 
 

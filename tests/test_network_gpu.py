@@ -1,0 +1,102 @@
+"""SparseConvNet (Model.forward's conv loop on the GPU, store.py:263-286) vs
+the CPU oracle run layer by layer: conv_sparse -> ReLU -> 2x2 max-pool.
+Exact fp32 mode must be bit-identical, for tuned tiled launches, the generic
+kernel (+ separate pool kernel) and CUDA-graph replay."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+def oracle_stack(net, x):
+    from oracle import oracle as orc
+    a = x
+    for L in net.layers:
+        sh = L.kernel.shape
+        z = orc.conv_sparse(a, L.kernel.values, L.kernel.colidx, L.kernel.rowptr, sh.k, sh.r, sh.s,
+                            sh.stride, sh.padding, L.bias)
+        a = np.maximum(z, 0) if L.relu else z
+        if L.pool:
+            n, k, e, f = a.shape
+            a = a.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
+    return a
+
+
+@pytest.fixture(scope="module")
+def vgg_small(torch):
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import vgg16_cifar
+    net = build_net(vgg16_cifar(0.9), seed=0)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((3, 3, 32, 32)).astype(np.float32)
+    return net, x, oracle_stack(net, x)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def test_tuned_stack_bitwise(torch, vgg_small):
+    net, x, ref = vgg_small
+    net.plan(3, tune=True, repetitions=1, warmups=0, max_candidates=12)
+    out = net.forward(x)
+    assert out.shape == ref.shape == (3, 512, 1, 1)
+    assert np.array_equal(_bits(out), _bits(ref))
+
+
+def test_generic_stack_bitwise(torch, vgg_small):
+    net, x, ref = vgg_small
+    net.plan(3, tune=False)
+    net.set_launches([None] * len(net.layers))  # generic kernel + separate max-pool kernel
+    assert net.kernels_per_step() == len(net.layers) + sum(L.pool for L in net.layers)
+    out = net.forward(x)
+    assert np.array_equal(_bits(out), _bits(ref))
+
+
+def test_graph_replay_bitwise(torch, vgg_small):
+    net, x, ref = vgg_small
+    net.plan(3, tune=False)
+    net.capture()
+    out = net.forward(x)
+    assert np.array_equal(_bits(out), _bits(ref))
+    x2 = np.random.default_rng(6).standard_normal(x.shape).astype(np.float32)
+    out2 = net.forward(x2)  # replay reads the refreshed input buffer
+    assert np.array_equal(_bits(out2), _bits(oracle_stack(net, x2)))
+
+
+def test_alexnet_stack_5x5(torch):
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import alexnet_cifar
+    net = build_net(alexnet_cifar(0.9), seed=0)
+    x = np.random.default_rng(2).standard_normal((2, 3, 32, 32)).astype(np.float32)
+    net.plan(2, tune=False)
+    out = net.forward(x)
+    assert np.array_equal(_bits(out), _bits(oracle_stack(net, x)))
+
+
+def test_generic_pool_through_conv_sparse(torch):
+    """conv_sparse(pool=True) with the generic kernel chosen (launch None in
+    the tuner cache) goes through scb_maxpool2."""
+    import paper_2011_06295_b200 as sc
+    from paper_2011_06295_b200 import engine
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=4, c=64, h=4, w=4, k=64, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, 0.9), 0)
+    x, b = bench_inputs(sh, 4)
+    kern = sc.build_csr(w, sh)
+    layer = device_layer(kern, 0, np.float32)
+    flags = engine._flags(sc.EnginePlan(), True, True, False)
+    engine.TUNED[(layer.signature(), 4, flags)] = None
+    try:
+        got = sc.conv_sparse(x, kern, b, relu=True, pool=True)
+    finally:
+        engine.TUNED.pop((layer.signature(), 4, flags), None)
+    want = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, b, relu=True, pool=True).cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(want))
