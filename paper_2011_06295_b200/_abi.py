@@ -52,7 +52,7 @@ class Launch(ctypes.Structure):
 
 
 class VariantInfo(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int32) for n in ("r", "s", "kt", "nbt", "th", "tw", "io", "wf", "mode", "dispatch", "pad")]
+    _fields_ = [(n, ctypes.c_int32) for n in ("r", "s", "kt", "nbt", "th", "tw", "io", "wf", "mode", "dispatch", "pad", "kind")]
 
 
 _lock = threading.Lock()

@@ -252,6 +252,102 @@ def gen_mask(R, S, PAD, KT, NBT, TH, TW, WF, MODE, f16) -> str:
                 sig, "".join(L), outs, ins)
 
 
+def gen_plane(H, W, R, S, PAD, KT, NBT, WF, MODE, f16) -> str:
+    """Whole-plane tap loop (plane.cuh).  Same stream format as gen_jump; the
+    lane's patch is the H x W plane of each of its NBT images (registers
+    %%x*), the zero padding around it is the literal 0f00000000, and every
+    MAC block ends with its own copy of the dispatch (direct threading: no
+    branch back to a loop head)."""
+    E, F = H + 2 * PAD - R + 1, W + 2 * PAD - S + 1
+    HW, EF = H * W, E * F
+    P = NBT * EF
+    nacc = KT * P
+    names = ["qs", "c0", "ccnt", "base", "planeb", "imgb", "aux", "scl"]
+    op = {n: f"%{nacc + i}" for i, n in enumerate(names)}
+
+    def acc(kk, j, y, x):
+        return f"%{kk * P + j * EF + y * F + x}"
+
+    def pt(j, y, x):  # padded-plane coordinates
+        yy, xx = y - PAD, x - PAD
+        if 0 <= yy < H and 0 <= xx < W:
+            return f"%%x{j * HW + yy * W + xx}"
+        return "0f00000000"
+
+    def mac(kk, r, s):
+        body = []
+        for j in range(NBT):
+            for y in range(E):
+                for x in range(F):
+                    a, q = acc(kk, j, y, x), pt(j, y + r, x + s)
+                    if MODE == EXACT:
+                        t = f"%%t{(j * E + y) * F + x}"
+                        body.append(f"mul.rn.f32 {t}, %%v, {q};\nadd.rn.f32 {a}, {a}, {t};\n")
+                    else:
+                        body.append(f"fma.rn.f32 {a}, %%v, {q}, {a};\n")
+        return "".join(body)
+
+    dispatch = ("mov.u32 %%mc, %%m;\nmov.u32 %%pc, %%pb;\n"
+                "ld.shared.v2.u32 {%%m, %%pb}, [%%qs+8];\nadd.u32 %%qs, %%qs, 8;\n"
+                + decode_ptx(WF) + "brx.idx.uni %%mc, TBL;\n")
+    t = ", ".join(f"%%t{i}" for i in range(P)) if MODE == EXACT else "%%t0"
+    L = ["{\n", ".reg .pred %%p;\n.reg .u32 %%m, %%mc, %%pb, %%pc, %%o, %%aux, %%w;\n",
+         f".reg .f32 %%v, %%scl, {t};\n.reg .b16 %%h, %%h0, %%h1, %%h2, %%h3;\n",
+         f".reg .f32 %%x<{NBT * HW}>;\n",
+         ".reg .u32 %%cl, %%a, %%ra, %%c0, %%ccnt, %%base, %%planeb, %%imgb, %%qs;\n",
+         f"mov.u32 %%qs, {op['qs']};\nmov.u32 %%c0, {op['c0']};\nmov.u32 %%ccnt, {op['ccnt']};\n"
+         f"mov.u32 %%base, {op['base']};\nmov.u32 %%planeb, {op['planeb']};\nmov.u32 %%imgb, {op['imgb']};\n"
+         f"mov.u32 %%aux, {op['aux']};\nmov.f32 %%scl, {op['scl']};\n"]
+    labels = [f"C{i}" for i in range(KT * R * S)] + ["CS"]
+    L.append("TBL: .branchtargets " + ", ".join(labels) + ";\n")
+    L.append("ld.shared.v2.u32 {%%m, %%pb}, [%%qs];\n" + dispatch)
+    for kk in range(KT):
+        for r in range(R):
+            for s_ in range(S):
+                L.append(f"C{(kk * R + r) * S + s_}:\n" + mac(kk, r, s_) + dispatch)
+    # channel sentinel: exit past the stage, else load the lane's planes of channel pc
+    L.append("CS:\nsub.u32 %%cl, %%pc, %%c0;\nsetp.ge.u32 %%p, %%cl, %%ccnt;\n@%%p bra.uni EXIT;\n"
+             "mad.lo.u32 %%a, %%cl, %%planeb, %%base;\n")
+    for j in range(NBT):
+        L.append("mov.u32 %%ra, %%a;\n" if j == 0 else "add.u32 %%ra, %%ra, %%imgb;\n")
+        for q in range(0, HW, 4):
+            regs = [f"%%x{j * HW + q + i}" for i in range(min(4, HW - q))]
+            if not f16:
+                if len(regs) == 4:
+                    L.append(f"ld.shared.v4.f32 {{{', '.join(regs)}}}, [%%ra+{4 * q}];\n")
+                else:
+                    for i, rg in enumerate(regs):
+                        L.append(f"ld.shared.f32 {rg}, [%%ra+{4 * (q + i)}];\n")
+            else:
+                if len(regs) == 4:
+                    L.append(f"ld.shared.v4.b16 {{%%h0, %%h1, %%h2, %%h3}}, [%%ra+{2 * q}];\n")
+                    for i, rg in enumerate(regs):
+                        L.append(f"cvt.f32.f16 {rg}, %%h{i};\n")
+                else:
+                    for i, rg in enumerate(regs):
+                        L.append(f"ld.shared.b16 %%h, [%%ra+{2 * (q + i)}];\ncvt.f32.f16 {rg}, %%h;\n")
+    L.append(dispatch)
+    L.append("EXIT:\n}\n")
+    outs = [f'"+f"(a[{i}])' for i in range(nacc)]
+    ins = ['"r"(qs)', '"r"(c0)', '"r"(ccnt)', '"r"(base)', '"r"(planeb)', '"r"(imgb)', '"r"(aux)', '"f"(scl)']
+    sig = (f"float (&a)[{nacc}], float (&pt)[{NBT * HW}], unsigned qs, unsigned c0, unsigned ccnt, unsigned base, "
+           "unsigned planeb, unsigned imgb, unsigned aux, float scl")
+    body = emit("", sig, "".join(L), outs, ins)
+    targs = f"{H}, {W}, {R}, {S}, {PAD}, {KT}, {NBT}, {WF}, {MODE}, {'true' if f16 else 'false'}"
+    return body.replace("struct TapLoop<>", f"struct PlaneLoop<{targs}>")
+
+
+# whole-plane variants: (H, W, R, S, PAD, KT, NBT, min CTAs/SM)
+PLANES = [
+    (2, 2, 3, 3, 1, 2, 4, 2), (2, 2, 3, 3, 1, 4, 2, 2), (2, 2, 3, 3, 1, 4, 4, 2), (2, 2, 3, 3, 1, 8, 2, 2),
+    (2, 2, 3, 3, 1, 2, 2, 2),
+    (4, 4, 3, 3, 1, 2, 2, 2), (4, 4, 3, 3, 1, 4, 1, 2), (4, 4, 3, 3, 1, 4, 2, 2), (4, 4, 3, 3, 1, 8, 1, 2),
+    (4, 4, 3, 3, 1, 2, 1, 2),
+]
+PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
+KIND_TILED, KIND_PLANE = 0, 1
+
+
 N_PARTS = 10
 
 
@@ -274,6 +370,12 @@ def main():
             if l not in g[0]:
                 g[0].append(l)
         g[1].extend(variants)
+    for H, W, R, S, PAD, KT, NBT, minb in PLANES:
+        loops, variants = [], []
+        for f16, wf, mode in PLANE_MODES:
+            loops.append(("plane", H, W, R, S, PAD, KT, NBT, wf, mode, f16))
+            variants.append(("plane", H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb))
+        groups[("plane", H, W, R, S, PAD, KT, NBT)] = (loops, variants)
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -283,20 +385,31 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
             for key in loops:
+                if key[0] == "plane":
+                    src.append(gen_plane(*key[1:]))
+                    continue
                 R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
                 src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
+                if v[0] == "plane":
+                    _, H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb = v
+                    io = "SCB_F16" if f16 else "SCB_F32"
+                    tf = "true" if f16 else "false"
+                    ents.append(f"    {{{{{R}, {S}, {KT}, {NBT}, {H}, {W}, {io}, {wf}, {mode}, {JUMP}, {PAD}, "
+                                f"{KIND_PLANE}}}, &launch_plane_t<{H}, {W}, {R}, {S}, {PAD}, {KT}, {NBT}, {tf}, "
+                                f"{wf}, {mode}, {minb}>}},\n")
+                    continue
                 R, S, PAD, KT, NBT, TH, TW, f16, wf, mode, d, minb = v
                 io = "SCB_F16" if f16 else "SCB_F32"
                 tf = "true" if f16 else "false"
-                ents.append(f"    {{{{{R}, {S}, {KT}, {NBT}, {TH}, {TW}, {io}, {wf}, {mode}, {d}, {PAD}}}, "
-                            f"&launch_tiled_t<{R}, {S}, {PAD}, {KT}, {NBT}, {TH}, {TW}, {tf}, {wf}, {mode}, "
-                            f"{d}, {minb}>}},\n")
+                ents.append(f"    {{{{{R}, {S}, {KT}, {NBT}, {TH}, {TW}, {io}, {wf}, {mode}, {d}, {PAD}, "
+                            f"{KIND_TILED}}}, &launch_tiled_t<{R}, {S}, {PAD}, {KT}, {NBT}, {TH}, {TW}, {tf}, "
+                            f"{wf}, {mode}, {d}, {minb}>}},\n")
         total_v += len(ents)
         src.append(f"extern const VariantEntry g_part_{i}[];\nextern const int g_part_{i}_n;\n")
         src.append(f"const VariantEntry g_part_{i}[] = {{\n" + "".join(ents) + "};\n")

@@ -22,7 +22,8 @@ namespace {
 
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxThreads = 256;
-const int kKtChoices[] = {4, 8};
+const int kKtChoices[] = {2, 4, 8};
+constexpr int KIND_TILED = 0, KIND_PLANE = 1;
 
 scb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -276,6 +277,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
     if (!L->prog(v.kt)) return false;
+    if (v.kind == KIND_PLANE) {
+        if (g.h != v.th || g.w != v.tw) return false;
+        if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1))) return false;
+        return true;
+    }
     if ((flags & SCB_FLAG_POOL2) && ((v.th & 1) || (v.tw & 1))) return false;
     return true;
 }
@@ -297,10 +303,44 @@ struct Derived {
     unsigned grid;
 };
 
+// Whole-plane variants (plane.cuh): imgs = wp * 32 * nbt, image pitch
+// = (cc*H*W elements rounded up to 128 B) + 16 B.
+scb_status derive_plane(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const int es = elem_bytes(v);
+    const int hw = g.h * g.w;
+    if (c.imgs < 32 * v.nbt || c.imgs % (32 * v.nbt) || c.cc < 1 || c.warps_k < 1)
+        return fail(SCB_ERR_SHAPE, "plane launch: imgs must be a multiple of 32*nbt");
+    if (((int64_t)c.cc * hw * es) % 16 || ((int64_t)g.c * hw * es) % 16)
+        return fail(SCB_ERR_SHAPE, "plane launch: channel runs must be 16-byte multiples");
+    d->wp = c.imgs / (32 * v.nbt);
+    d->threads = c.warps_k * d->wp * 32;
+    if (d->threads > kMaxThreads) return fail(SCB_ERR_SHAPE, "too many threads per CTA");
+    const size_t run = ((size_t)c.cc * hw * es + 127) & ~(size_t)127;
+    d->row = (int)((run + 16) / es);
+    const size_t stage_bytes = ((size_t)c.imgs * d->row * es + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / es);
+    d->chunk = 16;
+    d->tap_cap = L->cap_for(*L->prog(v.kt), c.cc);
+    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * d->tap_cap * sizeof(Tap);
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    const Program* P = L->prog(v.kt);
+    d->n_ey = 1;
+    d->n_fx = 1;
+    d->kblocks = (P->groups + c.warps_k - 1) / c.warps_k;
+    d->nb = (n + c.imgs - 1) / c.imgs;
+    const int64_t grid = (int64_t)d->kblocks * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
 scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     if (c.variant < 0 || c.variant >= num_variants()) return fail(SCB_ERR_SHAPE, "bad variant index");
     const scb_variant_info& v = variant(c.variant).info;
     if (!variant_matches(L, v, flags)) return fail(SCB_ERR_SHAPE, "variant does not match the layer");
+    if (v.kind == KIND_PLANE) return derive_plane(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -347,6 +387,20 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_PLANE) {
+            for (int wp : {1, 2, 4}) {
+                const int imgs = wp * 32 * v.nbt;
+                if (wp > 1 && imgs > ceil_to(n, 32 * v.nbt)) break;
+                for (int wk : {1, 2, 4, 8})
+                    for (int cc : {4, 8, 16, 32}) {
+                        scb_launch c{vi, wk, imgs, g.e, g.f, cc};
+                        Derived d;
+                        if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                        out.push_back(c);
+                    }
+            }
+            continue;
+        }
         std::vector<std::pair<int, int>> blocks;
         const int eh = ceil_to(g.e, v.th), fw = ceil_to(g.f, v.tw);
         blocks.push_back({std::min(eh, 32), std::min(fw, 32)});

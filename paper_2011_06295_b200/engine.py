@@ -88,9 +88,10 @@ def _io_dtype(x_dtype: np.dtype, kernel: CsrKernel) -> np.dtype:
     values use the f16 kernels (f16*f16 products are exact in f32, so FFMA is
     bit-equal to the reference); any other f16 combination computes on f32
     copies exactly like the reference's astype(f32) (engine.py:62-64)."""
-    if x_dtype == np.float16 and kernel.values.dtype != np.float16:
-        return np.dtype(np.float32)
-    return compute_dtype(x_dtype)
+    x_dtype = np.dtype(x_dtype)
+    if x_dtype == np.float16:
+        return np.dtype(np.float16) if kernel.values.dtype == np.float16 else np.dtype(np.float32)
+    return x_dtype
 
 
 def _flags(plan: EnginePlan, relu: bool, pool: bool, generic: bool) -> int:

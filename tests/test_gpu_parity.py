@@ -348,3 +348,42 @@ def test_tune_launch_picks_valid_and_identical(sc, orc):
     out = sc.conv_sparse(x, kern, b)  # now uses the tuned launch
     ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 128, 3, 3, 1, 1, b)
     assert beq(out, ref)
+
+
+# ---------------------------------------------------------------------------
+# whole-plane kernels (plane.cuh): small spatial extents
+# ---------------------------------------------------------------------------
+
+def _plane_cands(layer, n, flags=0):
+    from paper_2011_06295_b200 import _abi
+    vs = _abi.variants()
+    return [c for c in layer.candidates(n, flags) if vs[c[0]]["kind"] == 1]
+
+
+@pytest.mark.parametrize("c,hw,k,sp,n,dtype", [(512, 2, 512, 0.9, 130, np.float32), (64, 2, 72, 0.9, 33, np.float32),
+                                                (512, 4, 512, 0.95, 34, np.float32), (96, 4, 40, 0.8, 70, np.float32),
+                                                (64, 2, 64, 0.9, 40, np.float16), (64, 4, 64, 0.9, 40, np.float16)])
+def test_plane_kernels_bitwise(sc, orc, c, hw, k, sp, n, dtype):
+    import torch
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, sp), seed=0).astype(dtype)
+    x, b = bench_inputs(sh, n)
+    x = x.astype(dtype)
+    bq = b.astype(dtype) if dtype == np.float16 else b
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, bq)
+    xd = torch.from_numpy(x).cuda()
+    layer = device_layer(kern, 0, dtype)
+    cands = _plane_cands(layer, n)
+    assert cands, "no plane variant"
+    for cfg in cands[:: max(1, len(cands) // 40)]:
+        o = sc.conv_sparse(xd, kern, bq, sc.EnginePlan(launch=cfg)).cpu().numpy()
+        assert beq(o, ref), cfg
+    # fused ReLU + 2x2 max-pool epilogue
+    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref.astype(np.float32))), 2).numpy()
+    flags = 0x1 | 0x4
+    for cfg in _plane_cands(layer, n, flags)[:6]:
+        o = sc.conv_sparse(xd, kern, bq, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
+        assert beq(o, want.astype(dtype)), cfg
