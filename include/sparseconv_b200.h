@@ -84,7 +84,9 @@ typedef struct {
     int32_t dispatch;    /* tap dispatch: 0 brx.idx jump table, 1 per-channel mask walk */
     int32_t pad;         /* padding the variant is specialised for */
     int32_t kind;        /* 0 tiled (output blocks, halo patches); 1 whole plane (th x tw = the
-                            input plane a lane holds; small spatial extents) */
+                            input plane a lane holds; small spatial extents); 2 direct
+                            (dispatch-free: th rows x tw columns per lane group, kt = output
+                            channels per warp) */
 } scb_variant_info;
 
 /* ---------------------------------------------------------------------- */

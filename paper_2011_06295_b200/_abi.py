@@ -15,7 +15,7 @@ from pathlib import Path
 from .errors import FormatError, IntegrityError, ShapeError, SparseConvError
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_lib" / "libsparseconv_b200.so"
+LIB_PATH = Path(os.environ["SCB_LIB"]) if os.environ.get("SCB_LIB") else PKG / "_lib" / "libsparseconv_b200.so"
 CSRC = PKG / "csrc"
 
 SCB_OK, SCB_ERR_SHAPE, SCB_ERR_FORMAT, SCB_ERR_INTEGRITY = 0, 1, 2, 3

@@ -1,0 +1,215 @@
+// Dispatch-free direct sparse convolution kernel (sm_100a).
+//
+// The tiled/plane kernels keep an input patch in registers and jump to a
+// per-(channel, r, s) MAC block for every tap (PTX brx.idx).  ncu shows that
+// indirect branch -- LDC of the jump table, branch resolution, instruction
+// fetch -- dominating their stalls (profiles/r01_*).  This kernel has no
+// data-dependent control flow at all:
+//
+//  * a warp owns KW output channels (an unrolled, compile-time loop: the
+//    accumulator index is never dynamic) and TH output rows of LW columns of
+//    32/LW images -- lane = (column, image);
+//  * taps are warp-uniform: for output channel k and the stage's input
+//    channels the warp walks the reference's CSR row in colidx order
+//    (csr.py:143-160), so every output accumulates exactly like
+//    _kernels.py:73-84 (bias first, then v*x per nonzero, mul and add rounded
+//    separately in exact mode);
+//  * a tap is {v, off} with off = c*PLANE + r*ROW + s precomputed on upload;
+//    a lane's input is xs[lane_base - c0*PLANE + off + j*ROW] -- one shared
+//    load per MAC with an immediate row offset, lanes of a warp on 32
+//    distinct banks (consecutive columns; images at a pitch = LW mod 32);
+//  * input channels are staged `cc` at a time (two stages in flight,
+//    16-byte cp.async) into zero-halo windows: the zero padding
+//    (shapes.py:98-105) is the never-written halo of shared memory.
+//
+// Shared-memory bandwidth (4 B per MAC in fp32) bounds this kernel at about
+// half of the FMUL+FADD issue rate; it trades the dispatch stalls for that
+// predictable ceiling.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "kernels.cuh"
+#include "sparseconv_b200.h"
+#include "tiled.cuh"
+
+namespace scb {
+
+struct __align__(8) DirectTap {
+    float v;
+    int32_t off;  // byte offset (c*PLANE + r*ROW + s) * 4
+};
+
+struct DirectParams {
+    const void* x;
+    const float* bias;        // f32, may be null
+    void* y;
+    const DirectTap* taps;    // reference CSR order (rowptr[k] .. rowptr[k+1])
+    const int32_t* sptr;      // [K][nst+1]: first tap of channel k with c >= st*cc
+    int n, c, h, w, k, e, f;
+    int cc, nst, wk;          // channels per stage, stages, warps per CTA
+    int ip;                   // image pitch in shared memory (elements)
+    int stage_el;             // elements per stage (128-byte multiple)
+    int kblocks, n_ey, nb;
+    uint32_t flags;
+};
+
+// LW: output columns per lane group (= F when F <= 32), TH: output rows per
+// lane, XO: shared column of input column 0 (16-byte aligned interior).
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE>
+__global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ DirectParams p) {
+    constexpr int XO = 4;
+    // row pitch: interior + right halo, rounded to 16 bytes (cp.async destinations)
+    constexpr int ROW = ((XO + LW + (S - 1 - PAD > 0 ? S - 1 - PAD : 0)) + 3) / 4 * 4;
+    constexpr int RT = TH + R - 1;
+    constexpr int PLANE = RT * ROW;
+    constexpr int G = 32 / LW;  // images per CTA
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int tid = threadIdx.x, nthreads = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int lx = lane % LW, lg = lane / LW;
+    int bid = blockIdx.x;
+    const int kb = bid % p.kblocks;
+    bid /= p.kblocks;
+    const int ey = bid % p.n_ey;
+    const int nbk = bid / p.n_ey;
+    const int n0 = nbk * G, oy0 = ey * TH;
+    const int k0 = (kb * p.wk + warp) * KW;
+    const int C = p.c;
+    float* xs = reinterpret_cast<float*>(smem);
+
+    // zero both stages once: halo positions are never written again
+    {
+        float4* z = reinterpret_cast<float4*>(smem);
+        const int n16 = (2 * p.stage_el * 4) / 16;
+        for (int i = tid; i < n16; i += nthreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // row descriptors after the stages: {src element offset from (n0, channel 0), dst | cl << 24}
+    const int rows = G * p.cc * RT;
+    uint2* rdesc = reinterpret_cast<uint2*>(smem + (size_t)2 * p.stage_el * 4);
+    const int hw = p.h * p.w;
+    for (int rr = tid; rr < rows; rr += nthreads) {
+        const int yy = rr % RT, q = rr / RT;
+        const int cl = q % p.cc, g = q / p.cc;
+        const int gy = oy0 - PAD + yy;
+        const bool ok = n0 + g < p.n && (unsigned)gy < (unsigned)p.h;
+        rdesc[rr] = make_uint2((unsigned)((g * C + cl) * hw + gy * p.w),
+                               (unsigned)(g * p.ip + cl * PLANE + yy * ROW + XO) | ((unsigned)(ok ? cl : 255) << 24));
+    }
+    __syncthreads();
+
+    const float* xg = static_cast<const float*>(p.x) + (size_t)n0 * C * hw;
+    const int nchunk = p.w / 4;  // 16-byte chunks per input row (derive() requires w % 4 == 0)
+    auto stage = [&](int st, int buf) {
+        const int c0 = st * p.cc;
+        const unsigned ncl = (unsigned)min(p.cc, C - c0);
+        float* dst = xs + (size_t)buf * p.stage_el;
+        const float* src = xg + (size_t)c0 * hw;
+        for (int rr = tid; rr < rows; rr += nthreads) {
+            const uint2 rd = rdesc[rr];
+            if ((rd.y >> 24) < ncl) {
+                const float* s = src + rd.x;
+                float* d = dst + (rd.y & 0xffffffu);
+                for (int q = 0; q < nchunk; ++q) cp_async<16>(d + 4 * q, s + 4 * q);
+            }
+        }
+    };
+
+    float acc[KW][TH];
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+        const int k = k0 + kk;
+        const float b = (p.bias != nullptr && k < p.k) ? p.bias[k] : 0.f;
+#pragma unroll
+        for (int j = 0; j < TH; ++j) acc[kk][j] = b;
+    }
+
+    stage(0, 0);
+    cp_async_commit();
+    const int lane_off = lg * p.ip + XO - PAD + lx;  // + tap off - c0*PLANE
+    const int np1 = p.nst + 1;
+    for (int st = 0; st < p.nst; ++st) {
+        const int buf = st & 1;
+        if (st + 1 < p.nst) {
+            stage(st + 1, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk) {
+            const int k = k0 + kk;
+            if (k >= p.k) break;
+            int t = __ldg(p.sptr + (size_t)k * np1 + st);
+            const int t1 = __ldg(p.sptr + (size_t)k * np1 + st + 1);
+#pragma unroll 2
+            for (; t < t1; ++t) {
+                const DirectTap tp = p.taps[t];
+                const float* xp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(xl) + tp.off);
+#pragma unroll
+                for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * ROW]);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: lane (lx, lg) holds rows oy0..oy0+TH-1 of column lx of image n0+lg
+    const int n = n0 + lg;
+    const bool relu = p.flags & SCB_FLAG_RELU;
+    const bool pool = p.flags & SCB_FLAG_POOL2;
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+        const int k = k0 + kk;
+        if (k >= p.k) break;
+        if (!pool) {
+            if (n < p.n && lx < p.f) {
+                float* yp = static_cast<float*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * p.f + lx;
+#pragma unroll
+                for (int j = 0; j < TH; ++j) {
+                    if (oy0 + j >= p.e) break;
+                    float o = acc[kk][j];
+                    if (relu && o < 0.f) o = 0.f;
+                    yp[(int64_t)j * p.f] = o;
+                }
+            }
+        } else {
+            const int pe = p.e >> 1, pf = p.f >> 1;
+#pragma unroll
+            for (int j = 0; j < TH; j += 2) {
+                float o = fmaxf(acc[kk][j], acc[kk][j + 1]);
+                o = fmaxf(o, __shfl_xor_sync(0xffffffffu, o, 1));
+                if (relu && o < 0.f) o = 0.f;
+                const int py = (oy0 + j) >> 1;
+                if (n < p.n && !(lx & 1) && lx < p.f && py < pe)
+                    static_cast<float*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + (lx >> 1)] = o;
+            }
+        }
+    }
+}
+
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE>
+cudaError_t launch_direct_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
+    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE>;
+    static int max_dyn = -1;  // benign race: idempotent
+    if (max_dyn < 0) {
+        cudaFuncAttributes fa;
+        cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+        if (e != cudaSuccess) return e;
+        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        if (e != cudaSuccess) return e;
+        max_dyn = lim;
+    }
+    if ((int)smem > max_dyn) return cudaErrorInvalidValue;
+    kern<<<grid, threads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace scb

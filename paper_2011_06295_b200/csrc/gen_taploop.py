@@ -31,6 +31,9 @@ import sys
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
+# tiled tap loop dispatch: 1 = direct threaded (dispatch copied into every MAC
+# block), 0 = one shared loop head (smaller code)
+THREADED = int(__import__("os").environ.get("SCB_THREADED", "1"))
 
 WF_F32, WF_F16, WF_CB4, WF_LIN16 = 0, 1, 2, 3   # kernels.cuh WF_*
 EXACT, FMA = 0, 1                                # kernels.cuh MODE_*
@@ -72,6 +75,25 @@ def decode_ptx(wf: int, src: str = "%%pc") -> str:
     if wf == WF_CB4:
         return f"and.b32 %%o, {src}, 15;\nshl.b32 %%o, %%o, 2;\nadd.u32 %%o, %%o, %%aux;\nld.shared.f32 %%v, [%%o];\n"
     return f"cvt.u16.u32 %%h, {src};\ncvt.rn.f32.s16 %%v, %%h;\nmul.rn.f32 %%v, %%v, %%scl;\n"
+
+
+def dispatch_ptx(wf: int) -> str:
+    """Threaded dispatch at the end of every MAC block: take the prefetched
+    tap (%%m meta, %%pb payload), prefetch the following one, jump.  For f32
+    payloads the value register doubles as the raw payload (a sentinel's
+    channel number is read back from %%v in CS)."""
+    if wf == WF_F32:
+        return ("mov.b32 %%v, %%pb;\nmov.u32 %%mc, %%m;\n"
+                "ld.shared.v2.u32 {%%m, %%pb}, [%%qs+8];\nadd.u32 %%qs, %%qs, 8;\n"
+                "brx.idx.uni %%mc, TBL;\n")
+    return ("mov.u32 %%pc, %%pb;\nmov.u32 %%mc, %%m;\n"
+            "ld.shared.v2.u32 {%%m, %%pb}, [%%qs+8];\nadd.u32 %%qs, %%qs, 8;\n"
+            + decode_ptx(wf) + "brx.idx.uni %%mc, TBL;\n")
+
+
+def cs_head(wf: int) -> str:
+    pc = "mov.b32 %%pc, %%v;\n" if wf == WF_F32 else ""
+    return "CS:\n" + pc + "sub.u32 %%cl, %%pc, %%c0;\nsetp.ge.u32 %%p, %%cl, %%ccnt;\n@%%p bra.uni EXIT;\n"
 
 
 class Ops:
@@ -185,25 +207,22 @@ def gen_jump(R, S, PAD, KT, NBT, TH, TW, WF, MODE, f16) -> str:
          f"mov.u32 %%c0, {op['c0']};\nmov.u32 %%ccnt, {op['ccnt']};\nmov.u32 %%base, {op['base']};\n"
          f"mov.u32 %%planeb, {op['planeb']};\nmov.u32 %%imgb, {op['imgb']};\nmov.u32 %%rowb, {op['rowb']};\n"
          f"mov.u32 %%aux, {op['aux']};\nmov.f32 %%scl, {op['scl']};\nmov.u32 %%qs, %{oq};\n",
-         "ld.shared.v2.u32 {%%m, %%pb}, [%%qs];\n",
-         "bra.uni LOOP;\n"]
-    labels = []
+         "TBL: .branchtargets " + ", ".join([f"C{i}" for i in range(NC)] + ["CS"]) + ";\n",
+         "ld.shared.v2.u32 {%%m, %%pb}, [%%qs];\n", dispatch_ptx(WF)]
+    # THREADED: every block ends with its own dispatch; else one shared loop head
+    tail = dispatch_ptx(WF) if THREADED else "bra.uni LOOP;\n"
+    if not THREADED:
+        L[-1] = "bra.uni LOOP;\n"
     for kk in range(KT):
         for r in range(R):
             for s in range(S):
-                lab = f"C{(kk * R + r) * S + s}"
-                labels.append(lab)
-                L.append(f"{lab}:\n" + mac_block(o, kk, r, s, NBT, TH, TW, MODE) + "bra.uni LOOP;\n")
-    labels.append("CS")
-    L.append("CS:\nsub.u32 %%cl, %%pc, %%c0;\nsetp.ge.u32 %%p, %%cl, %%ccnt;\n@%%p bra.uni EXIT;\n"
-             "mad.lo.u32 %%a, %%cl, %%planeb, %%base;\n")
+                L.append(f"C{(kk * R + r) * S + s}:\n" + mac_block(o, kk, r, s, NBT, TH, TW, MODE) + tail)
+    L.append(cs_head(WF) + "mad.lo.u32 %%a, %%cl, %%planeb, %%base;\n")
     L.append(patch_load_ptx(o, NBT, R, S, PAD, TW, f16))
-    L.append("bra.uni LOOP;\n")
-    L.append("TBL: .branchtargets " + ", ".join(labels) + ";\n")
-    L.append("LOOP:\nmov.u32 %%mc, %%m;\nmov.u32 %%pc, %%pb;\n"
-             "ld.shared.v2.u32 {%%m, %%pb}, [%%qs+8];\nadd.u32 %%qs, %%qs, 8;\n")
-    L.append(decode_ptx(WF))
-    L.append("brx.idx.uni %%mc, TBL;\nEXIT:\n}\n")
+    L.append(tail)
+    if not THREADED:
+        L.append("LOOP:\n" + dispatch_ptx(WF))
+    L.append("EXIT:\n}\n")
     outs = [f'"+f"(a[{i}])' for i in range(nacc)] + [f'"+f"(pt[{i}])' for i in range(npt)]
     ins = ['"r"(qs)', '"r"(c0)', '"r"(ccnt)', '"r"(base)', '"r"(planeb)', '"r"(imgb)', '"r"(rowb)', '"r"(aux)',
            '"f"(scl)']
@@ -287,9 +306,7 @@ def gen_plane(H, W, R, S, PAD, KT, NBT, WF, MODE, f16) -> str:
                         body.append(f"fma.rn.f32 {a}, %%v, {q}, {a};\n")
         return "".join(body)
 
-    dispatch = ("mov.u32 %%mc, %%m;\nmov.u32 %%pc, %%pb;\n"
-                "ld.shared.v2.u32 {%%m, %%pb}, [%%qs+8];\nadd.u32 %%qs, %%qs, 8;\n"
-                + decode_ptx(WF) + "brx.idx.uni %%mc, TBL;\n")
+    dispatch = dispatch_ptx(WF)
     t = ", ".join(f"%%t{i}" for i in range(P)) if MODE == EXACT else "%%t0"
     L = ["{\n", ".reg .pred %%p;\n.reg .u32 %%m, %%mc, %%pb, %%pc, %%o, %%aux, %%w;\n",
          f".reg .f32 %%v, %%scl, {t};\n.reg .b16 %%h, %%h0, %%h1, %%h2, %%h3;\n",
@@ -306,8 +323,7 @@ def gen_plane(H, W, R, S, PAD, KT, NBT, WF, MODE, f16) -> str:
             for s_ in range(S):
                 L.append(f"C{(kk * R + r) * S + s_}:\n" + mac(kk, r, s_) + dispatch)
     # channel sentinel: exit past the stage, else load the lane's planes of channel pc
-    L.append("CS:\nsub.u32 %%cl, %%pc, %%c0;\nsetp.ge.u32 %%p, %%cl, %%ccnt;\n@%%p bra.uni EXIT;\n"
-             "mad.lo.u32 %%a, %%cl, %%planeb, %%base;\n")
+    L.append(cs_head(WF) + "mad.lo.u32 %%a, %%cl, %%planeb, %%base;\n")
     for j in range(NBT):
         L.append("mov.u32 %%ra, %%a;\n" if j == 0 else "add.u32 %%ra, %%ra, %%imgb;\n")
         for q in range(0, HW, 4):
@@ -345,7 +361,12 @@ PLANES = [
     (4, 4, 3, 3, 1, 2, 1, 2),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
-KIND_TILED, KIND_PLANE = 0, 1
+KIND_TILED, KIND_PLANE, KIND_DIRECT = 0, 1, 2
+
+# dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW)
+DIRECTS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
+          [(3, 3, 1, 4, 4, 4), (3, 3, 1, 4, 4, 8),
+           (5, 5, 2, 4, 32, 4), (5, 5, 2, 4, 16, 4), (5, 5, 2, 8, 8, 4)]
 
 
 N_PARTS = 10
@@ -376,6 +397,9 @@ def main():
             loops.append(("plane", H, W, R, S, PAD, KT, NBT, wf, mode, f16))
             variants.append(("plane", H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb))
         groups[("plane", H, W, R, S, PAD, KT, NBT)] = (loops, variants)
+    for R, S, PAD, TH, LW, KW in DIRECTS:
+        groups[("direct", R, S, PAD, TH, LW, KW)] = (
+            [], [("direct", R, S, PAD, TH, LW, KW, mode) for mode in (EXACT, FMA)])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -385,7 +409,7 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
@@ -396,6 +420,12 @@ def main():
                 R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
                 src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
+                if v[0] == "direct":
+                    _, R, S, PAD, TH, LW, KW, mode = v
+                    ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
+                                f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
+                                f"{mode}>}},\n")
+                    continue
                 if v[0] == "plane":
                     _, H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb = v
                     io = "SCB_F16" if f16 else "SCB_F32"

@@ -23,7 +23,7 @@ namespace {
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
-constexpr int KIND_TILED = 0, KIND_PLANE = 1;
+constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2;
 
 scb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -75,6 +75,11 @@ struct scb_layer {
     int32_t* d_rowptr = nullptr;
     std::vector<Program> progs;
     std::mutex mu;
+    // direct-kernel tables, built on first use: taps per (PLANE, ROW) layout, stage pointers per cc
+    std::vector<int32_t> h_colidx, h_rowptr;
+    std::vector<float> h_vals;  // values as f32 (exact for f16/f32 storage)
+    std::map<std::pair<int, int>, DirectTap*> d_dtaps;
+    std::map<int, int32_t*> d_sptr;
 
     ~scb_layer() {
         DeviceGuard dg(device);
@@ -82,6 +87,55 @@ struct scb_layer {
         cudaFree(d_dec);
         cudaFree(d_rowptr);
         for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); cudaFree(p.d_ptr_m); cudaFree(p.d_taps_m); cudaFree(p.d_masks); }
+        for (auto& kv : d_dtaps) cudaFree(kv.second);
+        for (auto& kv : d_sptr) cudaFree(kv.second);
+    }
+    // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
+    DirectTap* direct_taps(int plane, int row) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto key = std::make_pair(plane, row);
+        auto it = d_dtaps.find(key);
+        if (it != d_dtaps.end()) return it->second;
+        const int64_t pp = (int64_t)g.hp * g.wp;
+        std::vector<DirectTap> t(std::max<int64_t>(nnz, 1));
+        for (int64_t i = 0; i < nnz; ++i) {
+            const int64_t c = h_colidx[i] / pp, rem = h_colidx[i] % pp;
+            t[i].v = h_vals[i];
+            t[i].off = (int32_t)(4 * (c * plane + (rem / g.wp) * row + rem % g.wp));
+        }
+        DirectTap* d = nullptr;
+        if (cudaMalloc(&d, t.size() * sizeof(DirectTap)) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(d, t.data(), t.size() * sizeof(DirectTap), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        d_dtaps[key] = d;
+        return d;
+    }
+    // sptr[k][st] = first tap of row k whose input channel is >= st*cc (st = 0..nst)
+    int32_t* stage_ptr(int cc) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = d_sptr.find(cc);
+        if (it != d_sptr.end()) return it->second;
+        const int64_t pp = (int64_t)g.hp * g.wp;
+        const int nst = (g.c + cc - 1) / cc;
+        std::vector<int32_t> sp((size_t)g.k * (nst + 1));
+        for (int k = 0; k < g.k; ++k) {
+            int t = h_rowptr[k];
+            for (int st = 0; st <= nst; ++st) {
+                const int64_t cmin = (int64_t)st * cc;
+                while (t < h_rowptr[k + 1] && h_colidx[t] / pp < cmin) ++t;
+                sp[(size_t)k * (nst + 1) + st] = st == nst ? h_rowptr[k + 1] : t;
+            }
+        }
+        int32_t* d = nullptr;
+        if (cudaMalloc(&d, sp.size() * 4) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(d, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        d_sptr[cc] = d;
+        return d;
     }
     Program* prog(int kt) {
         for (auto& p : progs) if (p.kt == kt) return &p;
@@ -276,7 +330,12 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     if (v.io != L->dt || v.wf != L->wf) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
-    if (!L->prog(v.kt)) return false;
+    if (v.kind != KIND_DIRECT && !L->prog(v.kt)) return false;
+    if (v.kind == KIND_DIRECT) {
+        if (g.f != v.tw || (g.w % 4) != 0 || g.w > 32) return false;
+        if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
+        return true;
+    }
     if (v.kind == KIND_PLANE) {
         if (g.h != v.th || g.w != v.tw) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1))) return false;
@@ -336,11 +395,51 @@ scb_status derive_plane(scb_layer* L, const scb_launch& c, int n, uint32_t flags
     return SCB_OK;
 }
 
+// Direct variants (direct.cuh): 32/tw images per CTA, th output rows, warps_k warps.
+int direct_row(const scb_variant_info& v) {  // = direct.cuh ROW
+    const int right = v.s - 1 - v.pad > 0 ? v.s - 1 - v.pad : 0;
+    return (4 + v.tw + right + 3) / 4 * 4;
+}
+
+scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const int G = 32 / v.tw;
+    if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
+        return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32/tw, bh = th, bw = tw, 1..8 warps");
+    d->wp = 1;
+    d->threads = 32 * c.warps_k;
+    d->row = direct_row(v);
+    const int plane = (v.th + v.r - 1) * d->row;
+    int ip = c.cc * plane;
+    if (G > 1) {
+        ip = (ip + 3) & ~3;
+        while (ip % 32 != v.tw % 32) ip += 4;
+    }
+    d->chunk = ip;  // image pitch (elements) travels in `chunk`
+    const size_t stage_bytes = ((size_t)G * ip * 4 + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / 4);
+    d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
+    const int rows = G * c.cc * (v.th + v.r - 1);
+    d->smem = 2 * stage_bytes + (size_t)rows * 8;
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    if (2 * stage_bytes >= (1u << 24) * 4ull) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
+    d->n_ey = (g.e + v.th - 1) / v.th;
+    d->n_fx = 1;
+    d->kblocks = (g.k + c.warps_k * v.kt - 1) / (c.warps_k * v.kt);
+    d->nb = (n + G - 1) / G;
+    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
 scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     if (c.variant < 0 || c.variant >= num_variants()) return fail(SCB_ERR_SHAPE, "bad variant index");
     const scb_variant_info& v = variant(c.variant).info;
     if (!variant_matches(L, v, flags)) return fail(SCB_ERR_SHAPE, "variant does not match the layer");
     if (v.kind == KIND_PLANE) return derive_plane(L, c, n, flags, d);
+    if (v.kind == KIND_DIRECT) return derive_direct(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -358,8 +457,10 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = 0;
     if (v.dispatch == DISPATCH_JUMP) d->tap_cap = L->cap_for(*L->prog(v.kt), c.cc);
-    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * d->tap_cap * sizeof(Tap);
+    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * d->tap_cap * sizeof(Tap) +
+              (size_t)c.imgs * c.cc * (c.bh + v.r - 1) * 8;  // row descriptors
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    if (2 * stage_bytes >= (1u << 24)) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
     // copy chunk: the widest of 16/8/4 bytes dividing the input row and the block stride
     const int n_fx = (g.f + c.bw - 1) / c.bw;
     d->chunk = 0;
@@ -387,6 +488,16 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_DIRECT) {
+            for (int wk : {1, 2, 4, 8})
+                for (int cc : {4, 8, 16, 32, 64}) {
+                    scb_launch c{vi, wk, 32 / v.tw, v.th, v.tw, cc};
+                    Derived d;
+                    if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                    out.push_back(c);
+                }
+            continue;
+        }
         if (v.kind == KIND_PLANE) {
             for (int wp : {1, 2, 4}) {
                 const int imgs = wp * 32 * v.nbt;
@@ -512,6 +623,10 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
     e = cudaMemcpy(L->d_rowptr, rowptr, (g.k + 1) * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
 
+    L->h_colidx.assign(colidx, colidx + nnz);
+    L->h_rowptr.assign(rowptr, rowptr + g.k + 1);
+    L->h_vals = as_f32;
+
     // tiled tap programs for every KT a compiled variant of this (R, S) uses
     if (dt != SCB_F64 && g.stride == 1) {
         for (int kt : kKtChoices) {
@@ -542,6 +657,10 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
         return SCB_OK;
     }
     if (variant >= num_variants()) return fail(SCB_ERR_ARG, "bad variant");
+    if (scb::variant(variant).info.kind == KIND_DIRECT) {
+        *bytes = L->nnz * (int64_t)sizeof(DirectTap) + (int64_t)(L->g.k + 1) * 4;
+        return SCB_OK;
+    }
     Program* P = L->prog(scb::variant(variant).info.kt);
     if (!P) return fail(SCB_ERR_ARG, "no program for this variant");
     *bytes = (scb::variant(variant).info.dispatch == DISPATCH_JUMP ? P->nentries : P->ntaps) * (int64_t)sizeof(Tap) +
@@ -599,6 +718,20 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
     if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
+    if (ve.info.kind == KIND_DIRECT) {
+        DirectParams q;
+        std::memset(&q, 0, sizeof(q));
+        q.x = x; q.bias = static_cast<const float*>(bias); q.y = y;
+        q.taps = L->direct_taps(d.tap_cap, d.row);
+        q.sptr = L->stage_ptr(c.cc);
+        if (!q.taps || !q.sptr) return fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed");
+        q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
+        q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
+        q.ip = d.chunk; q.stage_el = d.stage_el;
+        q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nb = d.nb; q.flags = flags;
+        cudaError_t e = ve.dlaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
+        return e == cudaSuccess ? SCB_OK : cuda_fail(e, "direct kernel launch");
+    }
     const Program* P = L->prog(ve.info.kt);
     TiledParams p;
     std::memset(&p, 0, sizeof(p));

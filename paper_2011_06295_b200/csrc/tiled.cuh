@@ -154,36 +154,50 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
         for (int i = 0; i < P; ++i) acc[kk * P + i] = b;
     }
 
-    // ---- producer: copy the in-image part of every window row of a stage
+    // ---- producer: copy the in-image part of every window row of a stage.
+    // Row assignments (image, channel slot, window row) are the same for every
+    // stage, so each thread decodes its rows once: a 32-bit source offset from
+    // the CTA's first image (channel 0) and a shared-memory byte offset.
     const int ce = p.chunk / ES;  // elements per copy chunk
     const int gx_lo = max(0, ox0 - PAD) / ce * ce;
     const int gx_hi = (min(p.w, ox0 + p.bw + S - 1 - PAD) + ce - 1) / ce * ce;
     const int nchunk = (gx_hi - gx_lo) / ce;
     const int dcol = XOFF + gx_lo - ox0;  // smem column of gx_lo
+    const int rows = p.imgs * p.cc * RT;
+    const int hw = p.h * p.w;
+    const unsigned char* xcta = static_cast<const unsigned char*>(p.x) + (size_t)n0 * C * hw * ES;
+    // row descriptors after the tap segments: {source element offset from the
+    // CTA's first image at channel 0, smem byte offset | channel slot << 24}
+    uint2* rdesc = reinterpret_cast<uint2*>(smem + (size_t)2 * stage_el * ES +
+                                            (size_t)2 * p.wk * p.tap_cap * sizeof(Tap));
+    for (int rr = tid; rr < rows; rr += nthreads) {
+        const int yy = rr % RT, pc = rr / RT;
+        const int cl = pc % p.cc, img = pc / p.cc;
+        const int gy = oy0 - PAD + yy;
+        const bool ok = n0 + img < p.n && (unsigned)gy < (unsigned)p.h;
+        const unsigned dst = (unsigned)(((size_t)pc * plane_s + yy * ROW + dcol) * ES);
+        rdesc[rr] = make_uint2((unsigned)(((img * C + cl) * p.h + gy) * p.w + gx_lo),
+                               dst | ((unsigned)(ok ? cl : 255) << 24));
+    }
+    __syncthreads();
     auto stage = [&](int ch, int buf) {
         const int c0 = ch * p.cc;
-        TIO* dst = xs + (size_t)buf * stage_el;
-        const TIO* src = static_cast<const TIO*>(p.x);
-        const int rows = p.imgs * p.cc * RT;
-        int yy = tid % RT, pc = tid / RT;  // pc = img * cc + cl
-        const int dyy = nthreads % RT, dpc = nthreads / RT;
+        const unsigned ncl = (unsigned)min(p.cc, C - c0);
+        unsigned char* dst = smem + (size_t)buf * stage_el * ES;
+        const unsigned char* src = xcta + (size_t)c0 * hw * ES;
         for (int rr = tid; rr < rows; rr += nthreads) {
-            const int cl = pc % p.cc, img = pc / p.cc;
-            const int n = n0 + img, c = c0 + cl, gy = oy0 - PAD + yy;
-            if (n < p.n && c < C && (unsigned)gy < (unsigned)p.h) {
-                const TIO* s = src + (((size_t)n * C + c) * p.h + gy) * p.w + gx_lo;
-                TIO* d = dst + (size_t)pc * plane_s + yy * ROW + dcol;
+            const uint2 rd = rdesc[rr];
+            if ((rd.y >> 24) < ncl) {
+                const unsigned char* s = src + (size_t)rd.x * ES;
+                unsigned char* d = dst + (rd.y & 0xffffffu);
                 if (p.chunk == 16) {
-                    for (int q = 0; q < nchunk; ++q) cp_async<16>(d + q * ce, s + q * ce);
+                    for (int q = 0; q < nchunk; ++q) cp_async<16>(d + q * 16, s + q * 16);
                 } else if (p.chunk == 8) {
-                    for (int q = 0; q < nchunk; ++q) cp_async<8>(d + q * ce, s + q * ce);
+                    for (int q = 0; q < nchunk; ++q) cp_async<8>(d + q * 8, s + q * 8);
                 } else {
-                    for (int q = 0; q < nchunk; ++q) cp_async<4>(d + q * ce, s + q * ce);
+                    for (int q = 0; q < nchunk; ++q) cp_async<4>(d + q * 4, s + q * 4);
                 }
             }
-            yy += dyy;
-            pc += dpc;
-            if (yy >= RT) { yy -= RT; ++pc; }
         }
         if constexpr (DISPATCH == DISPATCH_JUMP) {
             // each warp group's stream segment for channels [c0, c0+cc) plus the exit
