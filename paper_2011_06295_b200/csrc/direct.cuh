@@ -54,6 +54,7 @@ struct DirectParams {
     int ip;                   // image pitch in shared memory (elements)
     int stage_el;             // elements per stage (128-byte multiple)
     int kblocks, n_ey, nb;
+    int segcap;               // taps per (output channel, stage) segment slot in shared memory
     uint32_t flags;
 };
 
@@ -102,6 +103,11 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
     }
     __syncthreads();
 
+    // tap segments after the row descriptors: [buf][warp][kk][segcap] (8-byte taps)
+    DirectTap* tsm = reinterpret_cast<DirectTap*>(
+        smem + (size_t)2 * p.stage_el * 4 + (((size_t)rows * 8 + 15) & ~(size_t)15));
+    const int np1 = p.nst + 1;
+
     const float* xg = static_cast<const float*>(p.x) + (size_t)n0 * C * hw;
     const int nchunk = p.w / 4;  // 16-byte chunks per input row (derive() requires w % 4 == 0)
     auto stage = [&](int st, int buf) {
@@ -117,6 +123,16 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
                 for (int q = 0; q < nchunk; ++q) cp_async<16>(d + 4 * q, s + 4 * q);
             }
         }
+        // this warp's KW tap segments of the stage (each lane copies every 32nd tap)
+        DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk) {
+            const int k = k0 + kk;
+            if (k >= p.k) break;
+            const int t0 = __ldg(p.sptr + (size_t)k * np1 + st);
+            const int t1 = __ldg(p.sptr + (size_t)k * np1 + st + 1);
+            for (int i = lane; i < t1 - t0; i += 32) cp_async<8>(tb + kk * p.segcap + i, p.taps + t0 + i);
+        }
     };
 
     float acc[KW][TH];
@@ -131,7 +147,6 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
     stage(0, 0);
     cp_async_commit();
     const int lane_off = lg * p.ip + XO - PAD + lx;  // + tap off - c0*PLANE
-    const int np1 = p.nst + 1;
     for (int st = 0; st < p.nst; ++st) {
         const int buf = st & 1;
         if (st + 1 < p.nst) {
@@ -143,15 +158,16 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
         }
         __syncthreads();
         const float* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
+        const DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
             if (k >= p.k) break;
-            int t = __ldg(p.sptr + (size_t)k * np1 + st);
-            const int t1 = __ldg(p.sptr + (size_t)k * np1 + st + 1);
+            const int nt = __ldg(p.sptr + (size_t)k * np1 + st + 1) - __ldg(p.sptr + (size_t)k * np1 + st);
+            const DirectTap* seg = tb + kk * p.segcap;
 #pragma unroll 2
-            for (; t < t1; ++t) {
-                const DirectTap tp = p.taps[t];
+            for (int t = 0; t < nt; ++t) {
+                const DirectTap tp = seg[t];
                 const float* xp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(xl) + tp.off);
 #pragma unroll
                 for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * ROW]);

@@ -80,6 +80,7 @@ struct scb_layer {
     std::vector<float> h_vals;  // values as f32 (exact for f16/f32 storage)
     std::map<std::pair<int, int>, DirectTap*> d_dtaps;
     std::map<int, int32_t*> d_sptr;
+    std::map<int, int> sptr_maxseg;  // cc -> longest (channel, stage) tap segment
 
     ~scb_layer() {
         DeviceGuard dg(device);
@@ -128,6 +129,11 @@ struct scb_layer {
                 sp[(size_t)k * (nst + 1) + st] = st == nst ? h_rowptr[k + 1] : t;
             }
         }
+        int mx = 1;
+        for (int k = 0; k < g.k; ++k)
+            for (int st = 0; st < nst; ++st)
+                mx = std::max(mx, sp[(size_t)k * (nst + 1) + st + 1] - sp[(size_t)k * (nst + 1) + st]);
+        sptr_maxseg[cc] = mx;
         int32_t* d = nullptr;
         if (cudaMalloc(&d, sp.size() * 4) != cudaSuccess) return nullptr;
         if (cudaMemcpy(d, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -407,7 +413,6 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     const int G = 32 / v.tw;
     if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
         return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32/tw, bh = th, bw = tw, 1..8 warps");
-    d->wp = 1;
     d->threads = 32 * c.warps_k;
     d->row = direct_row(v);
     const int plane = (v.th + v.r - 1) * d->row;
@@ -421,7 +426,11 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     d->stage_el = (int)(stage_bytes / 4);
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
     const int rows = G * c.cc * (v.th + v.r - 1);
-    d->smem = 2 * stage_bytes + (size_t)rows * 8;
+    if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
+    const int segcap = L->sptr_maxseg[c.cc];
+    d->wp = segcap;  // tap segment slot travels in `wp`
+    d->smem = 2 * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
+              (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap);
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     if (2 * stage_bytes >= (1u << 24) * 4ull) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
     d->n_ey = (g.e + v.th - 1) / v.th;
@@ -728,7 +737,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
-        q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nb = d.nb; q.flags = flags;
+        q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
         cudaError_t e = ve.dlaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
         return e == cudaSuccess ? SCB_OK : cuda_fail(e, "direct kernel launch");
     }
