@@ -86,7 +86,8 @@ typedef struct {
     int32_t kind;        /* 0 tiled (output blocks, halo patches); 1 whole plane (th x tw = the
                             input plane a lane holds; small spatial extents); 2 direct
                             (dispatch-free: th rows x tw columns per lane group, kt = output
-                            channels per warp) */
+                            channels per warp); 3 image-lane direct (lane = image, whole
+                            th x tw plane, shifted-copy vector loads) */
 } scb_variant_info;
 
 /* ---------------------------------------------------------------------- */

@@ -1,0 +1,202 @@
+// Image-lane direct kernel for small planes (sm_100a): VGG-CIFAR conv4_x
+// (4x4) and conv5_x (2x2), 3x3 taps, padding 1.
+//
+// Lane = image (32 images per CTA); a lane owns the whole H x H output plane
+// of its image for the KW output channels of its warp (compile-time unrolled,
+// as in direct.cuh -- no data-dependent control flow).  Taps are warp-uniform
+// and walked in the reference's colidx order per output channel
+// (_kernels.py:73-84), so exact mode is bit-identical to the reference.
+//
+// Shared layout per (image, channel): H+2 rows (top/bottom zero-padding rows
+// never written) x 3 column-shifted copies of each padded input row,
+// copy_s = padded_row[s .. s+H), each one H-float vector.  A tap (c, r, s)
+// then reads output row y's inputs as ONE aligned vector load
+// (ld.shared.v4 for H=4, .v2 for H=2) at c*BLK + (y+r)*3H + s*H: 4 B per MAC
+// but one instruction per H MACs.  Images sit at a pitch whose vector index
+// is odd, so the 8 (v4) / 16 (v2) lanes of a shared-memory wavefront hit
+// distinct banks.  copy_1 is the input row itself (one 16/8-byte cp.async);
+// copy_0 / copy_2 are built from it in shared memory after it lands.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "direct.cuh"
+#include "kernels.cuh"
+#include "sparseconv_b200.h"
+#include "tiled.cuh"
+
+namespace scb {
+
+template <int H>
+struct VecT;
+template <>
+struct VecT<4> { using T = float4; };
+template <>
+struct VecT<2> { using T = float2; };
+
+template <int H, int KW, int MODE>
+__global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectParams p) {
+    using V = typename VecT<H>::T;
+    constexpr int RW = 3 * H;            // one padded row: 3 shifted copies
+    constexpr int BLK = (H + 2) * RW;    // floats per (image, channel)
+    constexpr int HW = H * H;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int tid = threadIdx.x, nthreads = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int kb = blockIdx.x % p.kblocks;
+    const int n0 = (blockIdx.x / p.kblocks) * 32;
+    const int k0 = (kb * p.wk + warp) * KW;
+    const int C = p.c;
+    float* xs = reinterpret_cast<float*>(smem);
+    const int rows = 32 * p.cc * H;  // input rows per stage
+    DirectTap* tsm = reinterpret_cast<DirectTap*>(smem + (size_t)2 * p.stage_el * 4);
+    const int np1 = p.nst + 1;
+
+    {  // zero both stages: padding rows and the halo ends of copies 0 / 2 stay zero
+        float4* z = reinterpret_cast<float4*>(smem);
+        const int n16 = (2 * p.stage_el * 4) / 16;
+        for (int i = tid; i < n16; i += nthreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+
+    // row q of a stage: image q / (cc*H), channel slot (q / H) % cc, row q % H
+    const float* xg = static_cast<const float*>(p.x) + (size_t)n0 * C * HW;
+    auto stage = [&](int st, int buf) {
+        const int c0 = st * p.cc;
+        const int ncl = min(p.cc, C - c0);
+        float* dst = xs + (size_t)buf * p.stage_el;
+        for (int q = tid; q < rows; q += nthreads) {
+            const int y = q % H, t = q / H;
+            const int cl = t % p.cc, img = t / p.cc;
+            if (cl < ncl && n0 + img < p.n)
+                cp_async<H * 4>(dst + img * p.ip + cl * BLK + (y + 1) * RW + H,
+                                xg + ((size_t)img * C + c0 + cl) * HW + y * H);
+        }
+        DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk) {
+            const int k = k0 + kk;
+            if (k >= p.k) break;
+            const int t0 = __ldg(p.sptr + (size_t)k * np1 + st);
+            const int t1 = __ldg(p.sptr + (size_t)k * np1 + st + 1);
+            for (int i = lane; i < t1 - t0; i += 32) cp_async<8>(tb + kk * p.segcap + i, p.taps + t0 + i);
+        }
+    };
+    // copy_0 = (0, x0 .. x_{H-2}), copy_2 = (x1 .. x_{H-1}, 0) from copy_1
+    auto shift = [&](int st, int buf) {
+        const int ncl = min(p.cc, C - st * p.cc);
+        float* base = xs + (size_t)buf * p.stage_el;
+        for (int q = tid; q < rows; q += nthreads) {
+            const int y = q % H, t = q / H;
+            const int cl = t % p.cc, img = t / p.cc;
+            if (cl >= ncl) continue;
+            float* r = base + img * p.ip + cl * BLK + (y + 1) * RW;
+            const V m = *reinterpret_cast<const V*>(r + H);
+            if constexpr (H == 4) {
+                *reinterpret_cast<float4*>(r) = make_float4(0.f, m.x, m.y, m.z);
+                *reinterpret_cast<float4*>(r + 2 * H) = make_float4(m.y, m.z, m.w, 0.f);
+            } else {
+                *reinterpret_cast<float2*>(r) = make_float2(0.f, m.x);
+                *reinterpret_cast<float2*>(r + 2 * H) = make_float2(m.y, 0.f);
+            }
+        }
+    };
+
+    float acc[KW][HW];
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+        const int k = k0 + kk;
+        const float b = (p.bias != nullptr && k < p.k) ? p.bias[k] : 0.f;
+#pragma unroll
+        for (int j = 0; j < HW; ++j) acc[kk][j] = b;
+    }
+
+    stage(0, 0);
+    cp_async_commit();
+    for (int st = 0; st < p.nst; ++st) {
+        const int buf = st & 1;
+        if (st + 1 < p.nst) {
+            stage(st + 1, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        shift(st, buf);
+        __syncthreads();
+        // lane's image block, minus the stage's first channel (tap offsets are absolute)
+        const char* xl = reinterpret_cast<const char*>(xs + (size_t)buf * p.stage_el + lane * p.ip) -
+                         (size_t)st * p.cc * BLK * 4;
+        const DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk) {
+            const int k = k0 + kk;
+            if (k >= p.k) break;
+            const int nt = __ldg(p.sptr + (size_t)k * np1 + st + 1) - __ldg(p.sptr + (size_t)k * np1 + st);
+            const DirectTap* seg = tb + kk * p.segcap;
+#pragma unroll 2
+            for (int t = 0; t < nt; ++t) {
+                const DirectTap tp = seg[t];
+                const float* xp = reinterpret_cast<const float*>(xl + tp.off);
+#pragma unroll
+                for (int y = 0; y < H; ++y) {
+                    const V v = *reinterpret_cast<const V*>(xp + y * RW);
+                    const float* vf = reinterpret_cast<const float*>(&v);
+#pragma unroll
+                    for (int x = 0; x < H; ++x) acc[kk][y * H + x] = mac1<MODE>(acc[kk][y * H + x], tp.v, vf[x]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: lane's image plane per output channel is contiguous
+    const int n = n0 + lane;
+    if (n >= p.n) return;
+    const bool relu = p.flags & SCB_FLAG_RELU;
+    const bool pool = p.flags & SCB_FLAG_POOL2;
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+        const int k = k0 + kk;
+        if (k >= p.k) break;
+        float o[HW];
+#pragma unroll
+        for (int j = 0; j < HW; ++j) o[j] = (relu && acc[kk][j] < 0.f) ? 0.f : acc[kk][j];
+        if (!pool) {
+            float* yp = static_cast<float*>(p.y) + ((int64_t)n * p.k + k) * HW;
+#pragma unroll
+            for (int j = 0; j < HW; j += H) *reinterpret_cast<V*>(yp + j) = *reinterpret_cast<const V*>(&o[j]);
+        } else {
+            constexpr int PH = H / 2;
+            float* yp = static_cast<float*>(p.y) + ((int64_t)n * p.k + k) * PH * PH;
+#pragma unroll
+            for (int yy = 0; yy < PH; ++yy)
+#pragma unroll
+                for (int xx = 0; xx < PH; ++xx)
+                    yp[yy * PH + xx] = fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
+                                             fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1]));
+        }
+    }
+}
+
+template <int H, int KW, int MODE>
+cudaError_t launch_dimg_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
+    auto kern = k_dimg<H, KW, MODE>;
+    static int max_dyn = -1;  // benign race: idempotent
+    if (max_dyn < 0) {
+        cudaFuncAttributes fa;
+        cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+        if (e != cudaSuccess) return e;
+        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        if (e != cudaSuccess) return e;
+        max_dyn = lim;
+    }
+    if ((int)smem > max_dyn) return cudaErrorInvalidValue;
+    kern<<<grid, threads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace scb

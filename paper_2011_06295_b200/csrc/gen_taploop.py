@@ -361,7 +361,9 @@ PLANES = [
     (4, 4, 3, 3, 1, 2, 1, 2),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
-KIND_TILED, KIND_PLANE, KIND_DIRECT = 0, 1, 2
+KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG = 0, 1, 2, 3
+# image-lane direct variants (dimg.cuh): (H, KW)
+DIMGS = [(4, 2), (4, 4), (2, 2), (2, 4), (2, 8)]
 
 # dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW)
 DIRECTS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
@@ -400,6 +402,8 @@ def main():
     for R, S, PAD, TH, LW, KW in DIRECTS:
         groups[("direct", R, S, PAD, TH, LW, KW)] = (
             [], [("direct", R, S, PAD, TH, LW, KW, mode) for mode in (EXACT, FMA)])
+    for H, KW in DIMGS:
+        groups[("dimg", H, KW)] = ([], [("dimg", H, KW, mode) for mode in (EXACT, FMA)])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -409,7 +413,7 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
@@ -420,6 +424,11 @@ def main():
                 R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
                 src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
+                if v[0] == "dimg":
+                    _, H, KW, mode = v
+                    ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
+                                f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {mode}>}},\n")
+                    continue
                 if v[0] == "direct":
                     _, R, S, PAD, TH, LW, KW, mode = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "

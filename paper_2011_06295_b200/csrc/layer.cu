@@ -23,7 +23,7 @@ namespace {
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
-constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2;
+constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3;
 
 scb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -78,7 +78,7 @@ struct scb_layer {
     // direct-kernel tables, built on first use: taps per (PLANE, ROW) layout, stage pointers per cc
     std::vector<int32_t> h_colidx, h_rowptr;
     std::vector<float> h_vals;  // values as f32 (exact for f16/f32 storage)
-    std::map<std::pair<int, int>, DirectTap*> d_dtaps;
+    std::map<std::pair<int, int>, DirectTap*> d_dtaps;  // key (plane, row | scol << 20)
     std::map<int, int32_t*> d_sptr;
     std::map<int, int> sptr_maxseg;  // cc -> longest (channel, stage) tap segment
 
@@ -92,9 +92,9 @@ struct scb_layer {
         for (auto& kv : d_sptr) cudaFree(kv.second);
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
-    DirectTap* direct_taps(int plane, int row) {
+    DirectTap* direct_taps(int plane, int row, int scol = 1) {
         std::lock_guard<std::mutex> lk(mu);
-        auto key = std::make_pair(plane, row);
+        auto key = std::make_pair(plane, row | (scol << 20));
         auto it = d_dtaps.find(key);
         if (it != d_dtaps.end()) return it->second;
         const int64_t pp = (int64_t)g.hp * g.wp;
@@ -102,7 +102,7 @@ struct scb_layer {
         for (int64_t i = 0; i < nnz; ++i) {
             const int64_t c = h_colidx[i] / pp, rem = h_colidx[i] % pp;
             t[i].v = h_vals[i];
-            t[i].off = (int32_t)(4 * (c * plane + (rem / g.wp) * row + rem % g.wp));
+            t[i].off = (int32_t)(4 * (c * plane + (rem / g.wp) * row + (rem % g.wp) * scol));
         }
         DirectTap* d = nullptr;
         if (cudaMalloc(&d, t.size() * sizeof(DirectTap)) != cudaSuccess) return nullptr;
@@ -336,7 +336,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     if (v.io != L->dt || v.wf != L->wf) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
-    if (v.kind != KIND_DIRECT && !L->prog(v.kt)) return false;
+    if (v.kind != KIND_DIRECT && v.kind != KIND_DIMG && !L->prog(v.kt)) return false;
+    if (v.kind == KIND_DIMG) {
+        if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
+        return true;
+    }
     if (v.kind == KIND_DIRECT) {
         if (g.f != v.tw || (g.w % 4) != 0 || g.w > 32) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
@@ -443,12 +447,45 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     return SCB_OK;
 }
 
+// Image-lane direct variants (dimg.cuh): 32 images per CTA, (H+2) x 3H floats per (image, channel).
+scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const int H = v.th;
+    if (c.imgs != 32 || c.bh != H || c.bw != H || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
+        return fail(SCB_ERR_SHAPE, "image-lane launch: imgs = 32, bh = bw = plane, 1..8 warps");
+    d->threads = 32 * c.warps_k;
+    d->row = 3 * H;
+    const int blk = (H + 2) * 3 * H;
+    int ip = c.cc * blk;
+    const int vec = H;                      // floats per vector load
+    while ((ip / vec) % 2 == 0 || ip % vec) ++ip;  // odd vector index: conflict-free lanes
+    d->chunk = ip;
+    const size_t stage_bytes = ((size_t)32 * ip * 4 + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / 4);
+    d->tap_cap = blk;
+    if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
+    const int segcap = L->sptr_maxseg[c.cc];
+    d->wp = segcap;
+    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap);
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    d->n_ey = 1;
+    d->n_fx = 1;
+    d->kblocks = (g.k + c.warps_k * v.kt - 1) / (c.warps_k * v.kt);
+    d->nb = (n + 31) / 32;
+    const int64_t grid = (int64_t)d->kblocks * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
 scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     if (c.variant < 0 || c.variant >= num_variants()) return fail(SCB_ERR_SHAPE, "bad variant index");
     const scb_variant_info& v = variant(c.variant).info;
     if (!variant_matches(L, v, flags)) return fail(SCB_ERR_SHAPE, "variant does not match the layer");
     if (v.kind == KIND_PLANE) return derive_plane(L, c, n, flags, d);
     if (v.kind == KIND_DIRECT) return derive_direct(L, c, n, flags, d);
+    if (v.kind == KIND_DIMG) return derive_dimg(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -497,6 +534,16 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_DIMG) {
+            for (int wk : {1, 2, 4, 8})
+                for (int cc : {2, 4, 8, 16, 32}) {
+                    scb_launch c{vi, wk, 32, v.th, v.tw, cc};
+                    Derived d;
+                    if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                    out.push_back(c);
+                }
+            continue;
+        }
         if (v.kind == KIND_DIRECT) {
             for (int wk : {1, 2, 4, 8})
                 for (int cc : {4, 8, 16, 32, 64}) {
@@ -666,7 +713,7 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
         return SCB_OK;
     }
     if (variant >= num_variants()) return fail(SCB_ERR_ARG, "bad variant");
-    if (scb::variant(variant).info.kind == KIND_DIRECT) {
+    if (scb::variant(variant).info.kind == KIND_DIRECT || scb::variant(variant).info.kind == KIND_DIMG) {
         *bytes = L->nnz * (int64_t)sizeof(DirectTap) + (int64_t)(L->g.k + 1) * 4;
         return SCB_OK;
     }
@@ -727,11 +774,12 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
     if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
-    if (ve.info.kind == KIND_DIRECT) {
+    if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
         DirectParams q;
         std::memset(&q, 0, sizeof(q));
         q.x = x; q.bias = static_cast<const float*>(bias); q.y = y;
-        q.taps = L->direct_taps(d.tap_cap, d.row);
+        q.taps = ve.info.kind == KIND_DIMG ? L->direct_taps(d.tap_cap, d.row, ve.info.th)
+                                           : L->direct_taps(d.tap_cap, d.row);
         q.sptr = L->stage_ptr(c.cc);
         if (!q.taps || !q.sptr) return fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed");
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
