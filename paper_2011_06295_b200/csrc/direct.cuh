@@ -58,21 +58,35 @@ struct DirectParams {
     uint32_t flags;
 };
 
+// Shared row geometry of a direct variant (host and device agree on it).
+template <int S, int PAD, int LW, int VX>
+struct DirectRow {
+    static constexpr int XO = 4;  // shared column of input column 0 (16-byte aligned)
+    // one copy of a row: left halo, LW columns, right halo, rounded to 16 bytes
+    static constexpr int QW = VX == 1 ? ((XO + LW + (S - 1 - PAD > 0 ? S - 1 - PAD : 0)) + 3) / 4 * 4
+                                      : ((XO + LW + S) + 3) / 4 * 4;
+    static constexpr int ROW = VX * QW;
+    // shared column (relative to the lane's first output column) of tap column s
+    static constexpr int col(int s) {
+        return VX == 1 ? XO - PAD + s : (((s - PAD) % 2 == 0) ? XO + (s - PAD) : QW + XO + (s - PAD) + 1);
+    }
+};
+
 // LW: output columns per lane group (= F when F <= 32), TH: output rows per
-// lane, XO: shared column of input column 0 (16-byte aligned interior).
-template <int R, int S, int PAD, int TH, int LW, int KW, int MODE>
+// lane, VX: adjacent output columns per lane (1 or 2).
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX>
 __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ DirectParams p) {
-    constexpr int XO = 4;
-    // row pitch: interior + right halo, rounded to 16 bytes (cp.async destinations)
-    constexpr int ROW = ((XO + LW + (S - 1 - PAD > 0 ? S - 1 - PAD : 0)) + 3) / 4 * 4;
+    using RG = DirectRow<S, PAD, LW, VX>;
+    constexpr int XO = RG::XO, QW = RG::QW, ROW = RG::ROW;
     constexpr int RT = TH + R - 1;
     constexpr int PLANE = RT * ROW;
-    constexpr int G = 32 / LW;  // images per CTA
+    constexpr int LPI = LW / VX;   // lanes per image row
+    constexpr int G = 32 / LPI;    // images per CTA
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int tid = threadIdx.x, nthreads = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int lx = lane % LW, lg = lane / LW;
+    const int lx = (lane % LPI) * VX, lg = lane / LPI;
     int bid = blockIdx.x;
     const int kb = bid % p.kblocks;
     bid /= p.kblocks;
@@ -135,18 +149,36 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
         }
     };
 
-    float acc[KW][TH];
+    // VX = 2: P copy of every staged row = Q shifted right by one element
+    auto shift = [&](int st, int buf) {
+        const unsigned ncl = (unsigned)min(p.cc, C - st * p.cc);
+        float* base = xs + (size_t)buf * p.stage_el;
+        for (int rr = tid; rr < rows; rr += nthreads) {
+            const uint2 rd = rdesc[rr];
+            if ((rd.y >> 24) >= ncl) continue;
+            const float* q = base + (rd.y & 0xffffffu);  // Q[XO]
+            float* pr = const_cast<float*>(q) + QW;       // P[XO]
+            float4 prev = *reinterpret_cast<const float4*>(q - 4);
+            for (int i = 0; i <= nchunk; ++i) {
+                const float4 cur = *reinterpret_cast<const float4*>(q + 4 * i);
+                *reinterpret_cast<float4*>(pr + 4 * i) = make_float4(prev.w, cur.x, cur.y, cur.z);
+                prev = cur;
+            }
+        }
+    };
+
+    float acc[KW][TH * VX];
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
         const float b = (p.bias != nullptr && k < p.k) ? p.bias[k] : 0.f;
 #pragma unroll
-        for (int j = 0; j < TH; ++j) acc[kk][j] = b;
+        for (int j = 0; j < TH * VX; ++j) acc[kk][j] = b;
     }
 
     stage(0, 0);
     cp_async_commit();
-    const int lane_off = lg * p.ip + XO - PAD + lx;  // + tap off - c0*PLANE
+    const int lane_off = lg * p.ip + lx;  // + tap off - c0*PLANE
     for (int st = 0; st < p.nst; ++st) {
         const int buf = st & 1;
         if (st + 1 < p.nst) {
@@ -157,6 +189,10 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
             cp_async_wait<0>();
         }
         __syncthreads();
+        if constexpr (VX == 2) {
+            shift(st, buf);
+            __syncthreads();
+        }
         const float* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
         const DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
 #pragma unroll
@@ -169,14 +205,23 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
                 const float* xp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(xl) + tp.off);
+                if constexpr (VX == 1) {
 #pragma unroll
-                for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * ROW]);
+                    for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * ROW]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < TH; ++j) {
+                        const float2 v2 = *reinterpret_cast<const float2*>(xp + j * ROW);
+                        acc[kk][2 * j] = mac1<MODE>(acc[kk][2 * j], tp.v, v2.x);
+                        acc[kk][2 * j + 1] = mac1<MODE>(acc[kk][2 * j + 1], tp.v, v2.y);
+                    }
+                }
             }
         }
         __syncthreads();
     }
 
-    // ---- epilogue: lane (lx, lg) holds rows oy0..oy0+TH-1 of column lx of image n0+lg
+    // ---- epilogue: lane holds rows oy0..oy0+TH-1 of columns lx..lx+VX-1 of image n0+lg
     const int n = n0 + lg;
     const bool relu = p.flags & SCB_FLAG_RELU;
     const bool pool = p.flags & SCB_FLAG_POOL2;
@@ -190,17 +235,28 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
 #pragma unroll
                 for (int j = 0; j < TH; ++j) {
                     if (oy0 + j >= p.e) break;
-                    float o = acc[kk][j];
-                    if (relu && o < 0.f) o = 0.f;
-                    yp[(int64_t)j * p.f] = o;
+                    float o0 = acc[kk][j * VX];
+                    if (relu && o0 < 0.f) o0 = 0.f;
+                    if constexpr (VX == 1) {
+                        yp[(int64_t)j * p.f] = o0;
+                    } else {
+                        float o1 = acc[kk][j * VX + 1];
+                        if (relu && o1 < 0.f) o1 = 0.f;
+                        *reinterpret_cast<float2*>(yp + (int64_t)j * p.f) = make_float2(o0, o1);
+                    }
                 }
             }
         } else {
             const int pe = p.e >> 1, pf = p.f >> 1;
 #pragma unroll
             for (int j = 0; j < TH; j += 2) {
-                float o = fmaxf(acc[kk][j], acc[kk][j + 1]);
-                o = fmaxf(o, __shfl_xor_sync(0xffffffffu, o, 1));
+                float o;
+                if constexpr (VX == 1) {
+                    o = fmaxf(acc[kk][j], acc[kk][j + 1]);
+                    o = fmaxf(o, __shfl_xor_sync(0xffffffffu, o, 1));
+                } else {
+                    o = fmaxf(fmaxf(acc[kk][2 * j], acc[kk][2 * j + 1]), fmaxf(acc[kk][2 * j + 2], acc[kk][2 * j + 3]));
+                }
                 if (relu && o < 0.f) o = 0.f;
                 const int py = (oy0 + j) >> 1;
                 if (n < p.n && !(lx & 1) && lx < p.f && py < pe)
@@ -210,9 +266,9 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
     }
 }
 
-template <int R, int S, int PAD, int TH, int LW, int KW, int MODE>
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX>
 cudaError_t launch_direct_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE>;
+    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX>;
     static int max_dyn = -1;  // benign race: idempotent
     if (max_dyn < 0) {
         cudaFuncAttributes fa;

@@ -365,10 +365,11 @@ KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG = 0, 1, 2, 3
 # image-lane direct variants (dimg.cuh): (H, KW)
 DIMGS = [(4, 2), (4, 4), (2, 2), (2, 4), (2, 8)]
 
-# dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW)
-DIRECTS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
-          [(3, 3, 1, 4, 4, 4), (3, 3, 1, 4, 4, 8),
-           (5, 5, 2, 4, 32, 4), (5, 5, 2, 4, 16, 4), (5, 5, 2, 8, 8, 4)]
+# dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW, VX)
+DIRECTS = [(3, 3, 1, th, lw, kw, 1) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
+          [(3, 3, 1, th, lw, kw, 2) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)] + \
+          [(3, 3, 1, 4, 4, 4, 1), (3, 3, 1, 4, 4, 8, 1),
+           (5, 5, 2, 4, 32, 4, 1), (5, 5, 2, 4, 16, 4, 1), (5, 5, 2, 8, 8, 4, 1), (5, 5, 2, 4, 16, 4, 2)]
 
 
 N_PARTS = 10
@@ -399,9 +400,9 @@ def main():
             loops.append(("plane", H, W, R, S, PAD, KT, NBT, wf, mode, f16))
             variants.append(("plane", H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb))
         groups[("plane", H, W, R, S, PAD, KT, NBT)] = (loops, variants)
-    for R, S, PAD, TH, LW, KW in DIRECTS:
-        groups[("direct", R, S, PAD, TH, LW, KW)] = (
-            [], [("direct", R, S, PAD, TH, LW, KW, mode) for mode in (EXACT, FMA)])
+    for R, S, PAD, TH, LW, KW, VX in DIRECTS:
+        groups[("direct", R, S, PAD, TH, LW, KW, VX)] = (
+            [], [("direct", R, S, PAD, TH, LW, KW, VX, mode) for mode in (EXACT, FMA)])
     for H, KW in DIMGS:
         groups[("dimg", H, KW)] = ([], [("dimg", H, KW, mode) for mode in (EXACT, FMA)])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
@@ -430,10 +431,10 @@ def main():
                                 f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {mode}>}},\n")
                     continue
                 if v[0] == "direct":
-                    _, R, S, PAD, TH, LW, KW, mode = v
-                    ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
+                    _, R, S, PAD, TH, LW, KW, VX, mode = v
+                    ents.append(f"    {{{{{R}, {S}, {KW}, {VX}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
-                                f"{mode}>}},\n")
+                                f"{mode}, {VX}>}},\n")
                     continue
                 if v[0] == "plane":
                     _, H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb = v

@@ -78,7 +78,7 @@ struct scb_layer {
     // direct-kernel tables, built on first use: taps per (PLANE, ROW) layout, stage pointers per cc
     std::vector<int32_t> h_colidx, h_rowptr;
     std::vector<float> h_vals;  // values as f32 (exact for f16/f32 storage)
-    std::map<std::pair<int, int>, DirectTap*> d_dtaps;  // key (plane, row | scol << 20)
+    std::map<std::vector<int>, DirectTap*> d_dtaps;  // key (plane, row, column of each s)
     std::map<int, int32_t*> d_sptr;
     std::map<int, int> sptr_maxseg;  // cc -> longest (channel, stage) tap segment
 
@@ -92,9 +92,10 @@ struct scb_layer {
         for (auto& kv : d_sptr) cudaFree(kv.second);
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
-    DirectTap* direct_taps(int plane, int row, int scol = 1) {
+    DirectTap* direct_taps(int plane, int row, const std::vector<int>& col) {
         std::lock_guard<std::mutex> lk(mu);
-        auto key = std::make_pair(plane, row | (scol << 20));
+        std::vector<int> key{plane, row};
+        key.insert(key.end(), col.begin(), col.end());
         auto it = d_dtaps.find(key);
         if (it != d_dtaps.end()) return it->second;
         const int64_t pp = (int64_t)g.hp * g.wp;
@@ -102,7 +103,7 @@ struct scb_layer {
         for (int64_t i = 0; i < nnz; ++i) {
             const int64_t c = h_colidx[i] / pp, rem = h_colidx[i] % pp;
             t[i].v = h_vals[i];
-            t[i].off = (int32_t)(4 * (c * plane + (rem / g.wp) * row + (rem % g.wp) * scol));
+            t[i].off = (int32_t)(4 * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
         }
         DirectTap* d = nullptr;
         if (cudaMalloc(&d, t.size() * sizeof(DirectTap)) != cudaSuccess) return nullptr;
@@ -406,17 +407,28 @@ scb_status derive_plane(scb_layer* L, const scb_launch& c, int n, uint32_t flags
 }
 
 // Direct variants (direct.cuh): 32/tw images per CTA, th output rows, warps_k warps.
-int direct_row(const scb_variant_info& v) {  // = direct.cuh ROW
+// = direct.cuh DirectRow<S, PAD, LW = tw, VX = nbt>
+int direct_qw(const scb_variant_info& v) {
     const int right = v.s - 1 - v.pad > 0 ? v.s - 1 - v.pad : 0;
-    return (4 + v.tw + right + 3) / 4 * 4;
+    return v.nbt == 1 ? (4 + v.tw + right + 3) / 4 * 4 : (4 + v.tw + v.s + 3) / 4 * 4;
+}
+int direct_row(const scb_variant_info& v) { return v.nbt * direct_qw(v); }
+std::vector<int> direct_cols(const scb_variant_info& v) {
+    std::vector<int> col(v.s);
+    const int qw = direct_qw(v);
+    for (int s = 0; s < v.s; ++s) {
+        const int t = s - v.pad;
+        col[s] = v.nbt == 1 ? 4 - v.pad + s : ((t % 2 == 0) ? 4 + t : qw + 4 + t + 1);
+    }
+    return col;
 }
 
 scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
-    const int G = 32 / v.tw;
+    const int G = 32 * v.nbt / v.tw;
     if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
-        return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32/tw, bh = th, bw = tw, 1..8 warps");
+        return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32*vx/tw, bh = th, bw = tw, 1..8 warps");
     d->threads = 32 * c.warps_k;
     d->row = direct_row(v);
     const int plane = (v.th + v.r - 1) * d->row;
@@ -547,7 +559,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         if (v.kind == KIND_DIRECT) {
             for (int wk : {1, 2, 4, 8})
                 for (int cc : {4, 8, 16, 32, 64}) {
-                    scb_launch c{vi, wk, 32 / v.tw, v.th, v.tw, cc};
+                    scb_launch c{vi, wk, 32 * v.nbt / v.tw, v.th, v.tw, cc};
                     Derived d;
                     if (derive(L, c, n, flags, &d) != SCB_OK) continue;
                     out.push_back(c);
@@ -778,8 +790,12 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         DirectParams q;
         std::memset(&q, 0, sizeof(q));
         q.x = x; q.bias = static_cast<const float*>(bias); q.y = y;
-        q.taps = ve.info.kind == KIND_DIMG ? L->direct_taps(d.tap_cap, d.row, ve.info.th)
-                                           : L->direct_taps(d.tap_cap, d.row);
+        std::vector<int> col;
+        if (ve.info.kind == KIND_DIMG)
+            for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * ve.info.th);
+        else
+            col = direct_cols(ve.info);
+        q.taps = L->direct_taps(d.tap_cap, d.row, col);
         q.sptr = L->stage_ptr(c.cc);
         if (!q.taps || !q.sptr) return fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed");
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
