@@ -14,15 +14,16 @@ _abi.check(_abi.lib().scb_fma_peaks(0, names, vals, 8, ctypes.byref(cnt)))
 pk = {names.raw[16*i:16*i+16].split(b'\0')[0].decode(): vals[i] for i in range(cnt.value)}
 print("PEAKS_GMACS", json.dumps({k: round(v/1e9,1) for k,v in pk.items()}), flush=True)
 N = 256
+DT = np.float16 if '--f16' in sys.argv else np.float32
 tot = 0
 for spec, pool in vgg16_cifar(0.9):
     sh = spec.shape.with_batch(N)
     w = make_layer_weights(spec, 0); x, b = bench_inputs(sh, N)
-    kern = sc.build_csr(w, sh)
-    xd = torch.from_numpy(x).cuda(); bd = torch.from_numpy(b).cuda()
-    layer = device_layer(kern, 0, np.float32)
+    kern = sc.build_csr(w.astype(DT), sh)
+    xd = torch.from_numpy(x.astype(DT)).cuda(); bd = torch.from_numpy(b).cuda()
+    layer = device_layer(kern, 0, DT)
     cands = layer.candidates(N)
-    y = torch.empty((N, sh.k, sh.e, sh.f), device='cuda')
+    y = torch.empty((N, sh.k, sh.e, sh.f), device='cuda', dtype=xd.dtype)
     st = torch.cuda.current_stream().cuda_stream
     best = None
     res = []

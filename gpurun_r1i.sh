@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -p no:cacheprovider -k "f16 or direct" > gpurun_out/pytest_direct.log 2>&1
+timeout 900 python gpurun_probe.py --f16 > gpurun_out/probe_f16.log 2>&1
+echo done

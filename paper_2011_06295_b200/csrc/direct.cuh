@@ -59,12 +59,13 @@ struct DirectParams {
 };
 
 // Shared row geometry of a direct variant (host and device agree on it).
-template <int S, int PAD, int LW, int VX>
+template <int S, int PAD, int LW, int VX, int ES = 4>
 struct DirectRow {
-    static constexpr int XO = 4;  // shared column of input column 0 (16-byte aligned)
+    static constexpr int Q16 = 16 / ES;  // elements per 16 bytes
+    static constexpr int XO = Q16;       // shared column of input column 0 (16-byte aligned)
     // one copy of a row: left halo, LW columns, right halo, rounded to 16 bytes
-    static constexpr int QW = VX == 1 ? ((XO + LW + (S - 1 - PAD > 0 ? S - 1 - PAD : 0)) + 3) / 4 * 4
-                                      : ((XO + LW + S) + 3) / 4 * 4;
+    static constexpr int QW = VX == 1 ? ((XO + LW + (S - 1 - PAD > 0 ? S - 1 - PAD : 0)) + Q16 - 1) / Q16 * Q16
+                                      : ((XO + LW + S) + Q16 - 1) / Q16 * Q16;
     static constexpr int ROW = VX * QW;
     // shared column (relative to the lane's first output column) of tap column s
     static constexpr int col(int s) {
@@ -72,11 +73,22 @@ struct DirectRow {
     }
 };
 
+// f16 storage: acc += v * x with one FHFMA (fma.rn.f32.f16, f16 x f16 + f32):
+// the product of two f16 values is exact in f32, so this equals the
+// reference's f32 multiply then add (shapes.py:93-95, engine.py:62-64).
+__device__ __forceinline__ float fhfma(float acc, unsigned short v, unsigned short x) {
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(v), "h"(x));
+    return acc;
+}
+
 // LW: output columns per lane group (= F when F <= 32), TH: output rows per
-// lane, VX: adjacent output columns per lane (1 or 2).
-template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX>
-__global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ DirectParams p) {
-    using RG = DirectRow<S, PAD, LW, VX>;
+// lane, VX: adjacent output columns per lane (1 or 2; f16 storage needs 2).
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false>
+__global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ DirectParams p) {
+    static_assert(!F16IO || VX == 2, "f16 storage reads column pairs");
+    using TIO = typename std::conditional<F16IO, __half, float>::type;
+    constexpr int ES = (int)sizeof(TIO);
+    using RG = DirectRow<S, PAD, LW, VX, ES>;
     constexpr int XO = RG::XO, QW = RG::QW, ROW = RG::ROW;
     constexpr int RT = TH + R - 1;
     constexpr int PLANE = RT * ROW;
@@ -95,17 +107,17 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
     const int n0 = nbk * G, oy0 = ey * TH;
     const int k0 = (kb * p.wk + warp) * KW;
     const int C = p.c;
-    float* xs = reinterpret_cast<float*>(smem);
+    TIO* xs = reinterpret_cast<TIO*>(smem);
 
     // zero both stages once: halo positions are never written again
     {
         float4* z = reinterpret_cast<float4*>(smem);
-        const int n16 = (2 * p.stage_el * 4) / 16;
+        const int n16 = (2 * p.stage_el * ES) / 16;
         for (int i = tid; i < n16; i += nthreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     // row descriptors after the stages: {src element offset from (n0, channel 0), dst | cl << 24}
     const int rows = G * p.cc * RT;
-    uint2* rdesc = reinterpret_cast<uint2*>(smem + (size_t)2 * p.stage_el * 4);
+    uint2* rdesc = reinterpret_cast<uint2*>(smem + (size_t)2 * p.stage_el * ES);
     const int hw = p.h * p.w;
     for (int rr = tid; rr < rows; rr += nthreads) {
         const int yy = rr % RT, q = rr / RT;
@@ -119,22 +131,23 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
 
     // tap segments after the row descriptors: [buf][warp][kk][segcap] (8-byte taps)
     DirectTap* tsm = reinterpret_cast<DirectTap*>(
-        smem + (size_t)2 * p.stage_el * 4 + (((size_t)rows * 8 + 15) & ~(size_t)15));
+        smem + (size_t)2 * p.stage_el * ES + (((size_t)rows * 8 + 15) & ~(size_t)15));
     const int np1 = p.nst + 1;
 
-    const float* xg = static_cast<const float*>(p.x) + (size_t)n0 * C * hw;
-    const int nchunk = p.w / 4;  // 16-byte chunks per input row (derive() requires w % 4 == 0)
+    const TIO* xg = static_cast<const TIO*>(p.x) + (size_t)n0 * C * hw;
+    constexpr int Q16 = 16 / ES;
+    const int nchunk = p.w / Q16;  // 16-byte chunks per input row (derive() requires it exact)
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;
         const unsigned ncl = (unsigned)min(p.cc, C - c0);
-        float* dst = xs + (size_t)buf * p.stage_el;
-        const float* src = xg + (size_t)c0 * hw;
+        TIO* dst = xs + (size_t)buf * p.stage_el;
+        const TIO* src = xg + (size_t)c0 * hw;
         for (int rr = tid; rr < rows; rr += nthreads) {
             const uint2 rd = rdesc[rr];
             if ((rd.y >> 24) < ncl) {
-                const float* s = src + rd.x;
-                float* d = dst + (rd.y & 0xffffffu);
-                for (int q = 0; q < nchunk; ++q) cp_async<16>(d + 4 * q, s + 4 * q);
+                const TIO* s = src + rd.x;
+                TIO* d = dst + (rd.y & 0xffffffu);
+                for (int q = 0; q < nchunk; ++q) cp_async<16>(d + Q16 * q, s + Q16 * q);
             }
         }
         // this warp's KW tap segments of the stage (each lane copies every 32nd tap)
@@ -152,16 +165,23 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
     // VX = 2: P copy of every staged row = Q shifted right by one element
     auto shift = [&](int st, int buf) {
         const unsigned ncl = (unsigned)min(p.cc, C - st * p.cc);
-        float* base = xs + (size_t)buf * p.stage_el;
+        TIO* base = xs + (size_t)buf * p.stage_el;
         for (int rr = tid; rr < rows; rr += nthreads) {
             const uint2 rd = rdesc[rr];
             if ((rd.y >> 24) >= ncl) continue;
-            const float* q = base + (rd.y & 0xffffffu);  // Q[XO]
-            float* pr = const_cast<float*>(q) + QW;       // P[XO]
-            float4 prev = *reinterpret_cast<const float4*>(q - 4);
+            const TIO* q = base + (rd.y & 0xffffffu);  // Q[XO]
+            TIO* pr = const_cast<TIO*>(q) + QW;         // P[XO]
+            uint4 prev = *reinterpret_cast<const uint4*>(q - Q16);
             for (int i = 0; i <= nchunk; ++i) {
-                const float4 cur = *reinterpret_cast<const float4*>(q + 4 * i);
-                *reinterpret_cast<float4*>(pr + 4 * i) = make_float4(prev.w, cur.x, cur.y, cur.z);
+                const uint4 cur = *reinterpret_cast<const uint4*>(q + Q16 * i);
+                uint4 o;
+                if constexpr (ES == 4) {
+                    o = make_uint4(prev.w, cur.x, cur.y, cur.z);
+                } else {  // shift by one half: word w = (cur[w] << 16) | (prev word >> 16)
+                    o = make_uint4(__funnelshift_l(prev.w, cur.x, 16), __funnelshift_l(cur.x, cur.y, 16),
+                                   __funnelshift_l(cur.y, cur.z, 16), __funnelshift_l(cur.z, cur.w, 16));
+                }
+                *reinterpret_cast<uint4*>(pr + Q16 * i) = o;
                 prev = cur;
             }
         }
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
             shift(st, buf);
             __syncthreads();
         }
-        const float* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
+        const TIO* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
         const DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
@@ -204,8 +224,16 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
 #pragma unroll 2
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
-                const float* xp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(xl) + tp.off);
-                if constexpr (VX == 1) {
+                const TIO* xp = reinterpret_cast<const TIO*>(reinterpret_cast<const char*>(xl) + tp.off);
+                if constexpr (F16IO) {
+                    const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
+#pragma unroll
+                    for (int j = 0; j < TH; ++j) {
+                        const unsigned w2 = *reinterpret_cast<const unsigned*>(xp + j * ROW);
+                        acc[kk][2 * j] = fhfma(acc[kk][2 * j], vh, (unsigned short)(w2 & 0xffffu));
+                        acc[kk][2 * j + 1] = fhfma(acc[kk][2 * j + 1], vh, (unsigned short)(w2 >> 16));
+                    }
+                } else if constexpr (VX == 1) {
 #pragma unroll
                     for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * ROW]);
                 } else {
@@ -231,7 +259,7 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
         if (k >= p.k) break;
         if (!pool) {
             if (n < p.n && lx < p.f) {
-                float* yp = static_cast<float*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * p.f + lx;
+                TIO* yp = static_cast<TIO*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * p.f + lx;
 #pragma unroll
                 for (int j = 0; j < TH; ++j) {
                     if (oy0 + j >= p.e) break;
@@ -242,7 +270,10 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
                     } else {
                         float o1 = acc[kk][j * VX + 1];
                         if (relu && o1 < 0.f) o1 = 0.f;
-                        *reinterpret_cast<float2*>(yp + (int64_t)j * p.f) = make_float2(o0, o1);
+                        if constexpr (F16IO)
+                            *reinterpret_cast<__half2*>(yp + (int64_t)j * p.f) = __floats2half2_rn(o0, o1);
+                        else
+                            *reinterpret_cast<float2*>(yp + (int64_t)j * p.f) = make_float2(o0, o1);
                     }
                 }
             }
@@ -260,15 +291,15 @@ __global__ void __launch_bounds__(256, 2) k_direct(const __grid_constant__ Direc
                 if (relu && o < 0.f) o = 0.f;
                 const int py = (oy0 + j) >> 1;
                 if (n < p.n && !(lx & 1) && lx < p.f && py < pe)
-                    static_cast<float*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + (lx >> 1)] = o;
+                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + (lx >> 1)] = (TIO)o;
             }
         }
     }
 }
 
-template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX>
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false>
 cudaError_t launch_direct_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX>;
+    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX, MINB, F16IO>;
     static int max_dyn = -1;  // benign race: idempotent
     if (max_dyn < 0) {
         cudaFuncAttributes fa;

@@ -370,6 +370,11 @@ DIRECTS = [(3, 3, 1, th, lw, kw, 1) for lw in (32, 16, 8) for th in (4, 8) for k
           [(3, 3, 1, th, lw, kw, 2) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)] + \
           [(3, 3, 1, 4, 4, 4, 1), (3, 3, 1, 4, 4, 8, 1),
            (5, 5, 2, 4, 32, 4, 1), (5, 5, 2, 4, 16, 4, 1), (5, 5, 2, 8, 8, 4, 1), (5, 5, 2, 4, 16, 4, 2)]
+DIRECTS = [d + (2,) for d in DIRECTS] + \
+          [(3, 3, 1, th, lw, kw, vx, 4) for lw in (32, 16, 8) for th, kw, vx in
+           ((8, 4, 1), (4, 4, 1), (4, 8, 1), (8, 2, 2), (4, 4, 2))]  # + min CTAs/SM (4: <= 64 registers)
+# f16-storage direct variants (FHFMA, column pairs): (R, S, PAD, TH, LW, KW)
+DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)]
 
 
 N_PARTS = 10
@@ -400,9 +405,11 @@ def main():
             loops.append(("plane", H, W, R, S, PAD, KT, NBT, wf, mode, f16))
             variants.append(("plane", H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb))
         groups[("plane", H, W, R, S, PAD, KT, NBT)] = (loops, variants)
-    for R, S, PAD, TH, LW, KW, VX in DIRECTS:
-        groups[("direct", R, S, PAD, TH, LW, KW, VX)] = (
-            [], [("direct", R, S, PAD, TH, LW, KW, VX, mode) for mode in (EXACT, FMA)])
+    for R, S, PAD, TH, LW, KW, VX, MB in DIRECTS:
+        groups[("direct", R, S, PAD, TH, LW, KW, VX, MB)] = (
+            [], [("direct", R, S, PAD, TH, LW, KW, VX, MB, mode) for mode in (EXACT, FMA)])
+    for R, S, PAD, TH, LW, KW in DIRECTS_F16:
+        groups[("direct16", R, S, PAD, TH, LW, KW)] = ([], [("direct16", R, S, PAD, TH, LW, KW)])
     for H, KW in DIMGS:
         groups[("dimg", H, KW)] = ([], [("dimg", H, KW, mode) for mode in (EXACT, FMA)])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
@@ -425,16 +432,22 @@ def main():
                 R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
                 src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
+                if v[0] == "direct16":
+                    _, R, S, PAD, TH, LW, KW = v
+                    ents.append(f"    {{{{{R}, {S}, {KW}, 2, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, {PAD}, "
+                                f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
+                                f"{FMA}, 2, 2, true>}},\n")
+                    continue
                 if v[0] == "dimg":
                     _, H, KW, mode = v
                     ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
                                 f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {mode}>}},\n")
                     continue
                 if v[0] == "direct":
-                    _, R, S, PAD, TH, LW, KW, VX, mode = v
+                    _, R, S, PAD, TH, LW, KW, VX, MB, mode = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, {VX}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
-                                f"{mode}, {VX}>}},\n")
+                                f"{mode}, {VX}, {MB}>}},\n")
                     continue
                 if v[0] == "plane":
                     _, H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb = v

@@ -77,7 +77,8 @@ struct scb_layer {
     std::mutex mu;
     // direct-kernel tables, built on first use: taps per (PLANE, ROW) layout, stage pointers per cc
     std::vector<int32_t> h_colidx, h_rowptr;
-    std::vector<float> h_vals;  // values as f32 (exact for f16/f32 storage)
+    std::vector<float> h_vals;     // values as f32 (exact for f16/f32 storage)
+    std::vector<uint32_t> h_pay;   // device payload bits (f32 bits, or f16 bits in the low half)
     std::map<std::vector<int>, DirectTap*> d_dtaps;  // key (plane, row, column of each s)
     std::map<int, int32_t*> d_sptr;
     std::map<int, int> sptr_maxseg;  // cc -> longest (channel, stage) tap segment
@@ -92,9 +93,9 @@ struct scb_layer {
         for (auto& kv : d_sptr) cudaFree(kv.second);
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
-    DirectTap* direct_taps(int plane, int row, const std::vector<int>& col) {
+    DirectTap* direct_taps(int plane, int row, const std::vector<int>& col, int es = 4) {
         std::lock_guard<std::mutex> lk(mu);
-        std::vector<int> key{plane, row};
+        std::vector<int> key{plane, row, es};
         key.insert(key.end(), col.begin(), col.end());
         auto it = d_dtaps.find(key);
         if (it != d_dtaps.end()) return it->second;
@@ -102,8 +103,9 @@ struct scb_layer {
         std::vector<DirectTap> t(std::max<int64_t>(nnz, 1));
         for (int64_t i = 0; i < nnz; ++i) {
             const int64_t c = h_colidx[i] / pp, rem = h_colidx[i] % pp;
-            t[i].v = h_vals[i];
-            t[i].off = (int32_t)(4 * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
+            uint32_t vb = h_pay[i];
+            std::memcpy(&t[i].v, &vb, 4);
+            t[i].off = (int32_t)(es * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
         }
         DirectTap* d = nullptr;
         if (cudaMalloc(&d, t.size() * sizeof(DirectTap)) != cudaSuccess) return nullptr;
@@ -330,6 +332,8 @@ int wf_of(const scb_layer* L) {
     return L->dt == SCB_F16 ? WF_F16 : WF_F32;
 }
 
+int elem_bytes(const scb_variant_info& v) { return v.io == SCB_F16 ? 2 : 4; }
+
 bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t flags) {
     const Geom& g = L->g;
     if (L->dt == SCB_F64) return false;
@@ -343,7 +347,7 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         return true;
     }
     if (v.kind == KIND_DIRECT) {
-        if (g.f != v.tw || (g.w % 4) != 0 || g.w > 32) return false;
+        if (g.f != v.tw || (g.w * elem_bytes(v)) % 16 != 0 || g.w > 32) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
         return true;
     }
@@ -356,7 +360,6 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     return true;
 }
 
-int elem_bytes(const scb_variant_info& v) { return v.io == SCB_F16 ? 2 : 4; }
 
 // smem row pitch (elements) of a zero-halo window row: XOFF (16 bytes) +
 // block columns + right halo + one copy chunk of rounding slack, 16-byte rows.
@@ -407,10 +410,11 @@ scb_status derive_plane(scb_layer* L, const scb_launch& c, int n, uint32_t flags
 }
 
 // Direct variants (direct.cuh): 32/tw images per CTA, th output rows, warps_k warps.
-// = direct.cuh DirectRow<S, PAD, LW = tw, VX = nbt>
+// = direct.cuh DirectRow<S, PAD, LW = tw, VX = nbt, ES>
 int direct_qw(const scb_variant_info& v) {
+    const int q = v.io == SCB_F16 ? 8 : 4;  // elements per 16 bytes (= XO)
     const int right = v.s - 1 - v.pad > 0 ? v.s - 1 - v.pad : 0;
-    return v.nbt == 1 ? (4 + v.tw + right + 3) / 4 * 4 : (4 + v.tw + v.s + 3) / 4 * 4;
+    return v.nbt == 1 ? (q + v.tw + right + q - 1) / q * q : (q + v.tw + v.s + q - 1) / q * q;
 }
 int direct_row(const scb_variant_info& v) { return v.nbt * direct_qw(v); }
 std::vector<int> direct_cols(const scb_variant_info& v) {
@@ -418,7 +422,8 @@ std::vector<int> direct_cols(const scb_variant_info& v) {
     const int qw = direct_qw(v);
     for (int s = 0; s < v.s; ++s) {
         const int t = s - v.pad;
-        col[s] = v.nbt == 1 ? 4 - v.pad + s : ((t % 2 == 0) ? 4 + t : qw + 4 + t + 1);
+        const int xo = v.io == SCB_F16 ? 8 : 4;
+        col[s] = v.nbt == 1 ? xo - v.pad + s : ((t % 2 == 0) ? xo + t : qw + xo + t + 1);
     }
     return col;
 }
@@ -432,14 +437,13 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     d->threads = 32 * c.warps_k;
     d->row = direct_row(v);
     const int plane = (v.th + v.r - 1) * d->row;
-    int ip = c.cc * plane;
-    if (G > 1) {
-        ip = (ip + 3) & ~3;
-        while (ip % 32 != v.tw % 32) ip += 4;
-    }
+    const int es = elem_bytes(v), q16 = 16 / es;
+    int ip = (c.cc * plane + q16 - 1) / q16 * q16;
+    if (G > 1)  // word pitch of an image = its row width in words (mod 32): conflict-free lanes
+        while ((ip * es / 4) % 32 != (v.tw * es / 4) % 32) ip += q16;
     d->chunk = ip;  // image pitch (elements) travels in `chunk`
-    const size_t stage_bytes = ((size_t)G * ip * 4 + 127) & ~(size_t)127;
-    d->stage_el = (int)(stage_bytes / 4);
+    const size_t stage_bytes = ((size_t)G * ip * es + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
     const int rows = G * c.cc * (v.th + v.r - 1);
     if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
@@ -448,7 +452,7 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     d->smem = 2 * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
               (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap);
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
-    if (2 * stage_bytes >= (1u << 24) * 4ull) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
+    if (2 * stage_bytes >= (1u << 24) * (size_t)es) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
     d->n_ey = (g.e + v.th - 1) / v.th;
     d->n_fx = 1;
     d->kblocks = (g.k + c.warps_k * v.kt - 1) / (c.warps_k * v.kt);
@@ -694,6 +698,7 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
     L->h_colidx.assign(colidx, colidx + nnz);
     L->h_rowptr.assign(rowptr, rowptr + g.k + 1);
     L->h_vals = as_f32;
+    L->h_pay = pay;
 
     // tiled tap programs for every KT a compiled variant of this (R, S) uses
     if (dt != SCB_F64 && g.stride == 1) {
@@ -795,7 +800,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
             for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * ve.info.th);
         else
             col = direct_cols(ve.info);
-        q.taps = L->direct_taps(d.tap_cap, d.row, col);
+        q.taps = L->direct_taps(d.tap_cap, d.row, col, elem_bytes(ve.info));
         q.sptr = L->stage_ptr(c.cc);
         if (!q.taps || !q.sptr) return fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed");
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;

@@ -445,3 +445,33 @@ def test_image_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     for cfg in pc[:: max(1, len(pc) // 6)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
         assert beq(o, want), cfg
+
+
+@pytest.mark.parametrize("c,hw,k,sp,n", [(64, 32, 64, 0.9, 3), (64, 16, 72, 0.9, 5), (256, 8, 256, 0.9, 9),
+                                         (96, 8, 40, 0.5, 7)])
+def test_direct_f16_kernels_bitwise(sc, orc, c, hw, k, sp, n):
+    """f16 storage, f32 accumulation with FHFMA: bit-identical to the reference's
+    f16 profile (f32 compute, one final round to f16)."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, sp), seed=0).astype(np.float16)
+    x, b = bench_inputs(sh, n)
+    x, b = x.astype(np.float16), b.astype(np.float16)
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+    xd = torch.from_numpy(x).cuda()
+    layer = device_layer(kern, 0, np.float16)
+    vs = _abi.variants()
+    cands = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 2]
+    assert cands, "no f16 direct variant"
+    for cfg in cands[:: max(1, len(cands) // 20)]:
+        o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
+        assert beq(o, ref), cfg
+    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref.astype(np.float32))), 2).numpy()
+    pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 2]
+    for cfg in pc[:: max(1, len(pc) // 6)]:
+        o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
+        assert beq(o, want.astype(np.float16)), cfg
