@@ -15,6 +15,7 @@ pk = {names.raw[16*i:16*i+16].split(b'\0')[0].decode(): vals[i] for i in range(c
 print("PEAKS_GMACS", json.dumps({k: round(v/1e9,1) for k,v in pk.items()}), flush=True)
 N = 256
 DT = np.float16 if '--f16' in sys.argv else np.float32
+FL = 2 if '--fast' in sys.argv else 0
 tot = 0
 for spec, pool in vgg16_cifar(0.9):
     sh = spec.shape.with_batch(N)
@@ -22,13 +23,13 @@ for spec, pool in vgg16_cifar(0.9):
     kern = sc.build_csr(w.astype(DT), sh)
     xd = torch.from_numpy(x.astype(DT)).cuda(); bd = torch.from_numpy(b).cuda()
     layer = device_layer(kern, 0, DT)
-    cands = layer.candidates(N)
+    cands = layer.candidates(N, FL)
     y = torch.empty((N, sh.k, sh.e, sh.f), device='cuda', dtype=xd.dtype)
     st = torch.cuda.current_stream().cuda_stream
     best = None
     res = []
     for c in cands:
-        t = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), N, 0, c, st), 3, 1)
+        t = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), N, FL, c, st), 3, 1)
         res.append((t, c))
     res.sort()
     tg = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), N, 8, None, st), 3, 1)

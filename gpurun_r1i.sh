@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -p no:cacheprovider -k "f16 or direct" > gpurun_out/pytest_direct.log 2>&1
-timeout 900 python gpurun_probe.py --f16 > gpurun_out/probe_f16.log 2>&1
+SCB_LIB=paper_2011_06295_b200/_lib/lib_u4.so timeout 900 python gpurun_probe.py > gpurun_out/probe_u4.log 2>&1
 echo done

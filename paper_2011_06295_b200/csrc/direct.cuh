@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
             if (k >= p.k) break;
             const int nt = __ldg(p.sptr + (size_t)k * np1 + st + 1) - __ldg(p.sptr + (size_t)k * np1 + st);
             const DirectTap* seg = tb + kk * p.segcap;
-#pragma unroll 2
+#pragma unroll 4
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
                 const TIO* xp = reinterpret_cast<const TIO*>(reinterpret_cast<const char*>(xl) + tp.off);
