@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline time budget")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-f16", action="store_true", help="skip the fp16 (config 4) secondary measurement")
     return ap.parse_args()
 
 
@@ -278,6 +279,57 @@ def dense_cudnn(specs, kernels, biases, batch: int, dev, reps: int = 10):
         torch.backends.cudnn.allow_tf32 = old
 
 
+def measure_f16(specs, args, dev, local_rank, reps: int = 10):
+    """BASELINE config 4 (secondary): the same stack with f16 weights and
+    activations (f16 storage, FHFMA f32 accumulation -- bit-identical to the
+    reference's f16 profile), vs dense cuDNN fp16 tensor-core convolutions."""
+    import torch
+    from paper_2011_06295_b200.network import build_net
+    net = build_net(specs, seed=0, dtype=np.float16, device=local_rank)
+    net.plan(args.batch, tune=not args.no_tune)
+    x = torch.randn((args.batch, 3, 32, 32), device=dev).half()
+    for _ in range(3):
+        net.forward_device(x)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ts = []
+    for _ in range(reps):
+        ev[0].record()
+        net.forward_device(x)
+        ev[1].record()
+        ev[1].synchronize()
+        ts.append(ev[0].elapsed_time(ev[1]))
+    ms = statistics.median(ts)
+    # dense fp16 comparator: channels_last tensor-core convolutions
+    torch.backends.cudnn.benchmark = True
+    ws = [torch.from_numpy(__import__("paper_2011_06295_b200").decompress(L.kernel).astype(np.float16)).to(dev)
+          .to(memory_format=torch.channels_last) for L in net.layers]
+    bs = [torch.from_numpy(L.bias.astype(np.float16)).to(dev) for L in net.layers]
+    xc = x.to(memory_format=torch.channels_last)
+
+    def dense():
+        a = xc
+        for (spec, pool), w, b in zip(specs, ws, bs):
+            a = torch.relu(torch.nn.functional.conv2d(a, w, b, padding=spec.shape.padding))
+            if pool:
+                a = torch.nn.functional.max_pool2d(a, 2)
+        return a
+    for _ in range(3):
+        dense()
+    torch.cuda.synchronize()
+    td = []
+    for _ in range(reps):
+        ev[0].record()
+        dense()
+        ev[1].record()
+        ev[1].synchronize()
+        td.append(ev[0].elapsed_time(ev[1]))
+    return {"images_per_s": round(args.batch / (ms * 1e-3), 1), "ms_per_step": round(ms, 4),
+            "dense_cudnn_fp16_ms": round(statistics.median(td), 4),
+            "arith": "f16 storage, FHFMA (f16 x f16 + f32) accumulation, bit-identical to the reference f16 profile",
+            "launches": [None if l is None else list(l) for l in net.launches]}
+
+
 def load_traffic():
     """Per-layer DRAM traffic (dram__bytes_read.sum + write.sum) from the
     committed ncu --set full capture summary, if any."""
@@ -413,6 +465,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "layers": layers,
         "fma_peaks_tflops": {k: round(v, 2) for k, v in peaks.items()},
     }
+    if not args.no_f16:
+        line["f16"] = measure_f16(specs, args, dev, local_rank)
     if not args.no_dense:
         line["dense_cudnn"] = dense_cudnn(specs, [L.kernel for L in net.layers], [L.bias for L in net.layers],
                                           args.batch, dev)

@@ -20,7 +20,7 @@ using namespace scb;
 
 namespace {
 
-constexpr int kSmemLimit = 227 * 1024;
+constexpr int kSmemLimit = 227 * 1024 - 1024;  // dynamic limit: 227 KB minus the kernels' static shared memory
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
 constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3;
