@@ -52,6 +52,15 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
     const int rows = 32 * p.cc * H;  // input rows per stage
     DirectTap* tsm = reinterpret_cast<DirectTap*>(smem + (size_t)2 * p.stage_el * 4);
     const int np1 = p.nst + 1;
+    // stage pointers of this CTA's output channels, after the tap segments: [warp*KW + kk][np1]
+    int* sps = reinterpret_cast<int*>(tsm + (size_t)2 * p.wk * KW * p.segcap);
+    {
+        const int kc0 = kb * p.wk * KW;
+        for (int i = tid; i < p.wk * KW * np1; i += nthreads) {
+            const int k = kc0 + i / np1;
+            sps[i] = k < p.k ? __ldg(p.sptr + (size_t)k * np1 + i % np1) : 0;
+        }
+    }
 
     {  // zero both stages: padding rows and the halo ends of copies 0 / 2 stay zero
         float4* z = reinterpret_cast<float4*>(smem);
@@ -78,8 +87,8 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
             if (k >= p.k) break;
-            const int t0 = __ldg(p.sptr + (size_t)k * np1 + st);
-            const int t1 = __ldg(p.sptr + (size_t)k * np1 + st + 1);
+            const int t0 = sps[(warp * KW + kk) * np1 + st];
+            const int t1 = sps[(warp * KW + kk) * np1 + st + 1];
             for (int i = lane; i < t1 - t0; i += 32) cp_async<8>(tb + kk * p.segcap + i, p.taps + t0 + i);
         }
     };
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
             if (k >= p.k) break;
-            const int nt = __ldg(p.sptr + (size_t)k * np1 + st + 1) - __ldg(p.sptr + (size_t)k * np1 + st);
+            const int nt = sps[(warp * KW + kk) * np1 + st + 1] - sps[(warp * KW + kk) * np1 + st];
             const DirectTap* seg = tb + kk * p.segcap;
 #pragma unroll 2
             for (int t = 0; t < nt; ++t) {

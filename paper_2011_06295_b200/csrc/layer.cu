@@ -450,7 +450,8 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     const int segcap = L->sptr_maxseg[c.cc];
     d->wp = segcap;  // tap segment slot travels in `wp`
     d->smem = 2 * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
-              (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap);
+              (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
+              (size_t)c.warps_k * v.kt * ((g.c + c.cc - 1) / c.cc + 1) * 4;  // stage pointers
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     if (2 * stage_bytes >= (1u << 24) * (size_t)es) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
     d->n_ey = (g.e + v.th - 1) / v.th;
@@ -483,7 +484,8 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
     const int segcap = L->sptr_maxseg[c.cc];
     d->wp = segcap;
-    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap);
+    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
+              (size_t)c.warps_k * v.kt * ((g.c + c.cc - 1) / c.cc + 1) * 4;  // stage pointers
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     d->n_ey = 1;
     d->n_fx = 1;
