@@ -71,6 +71,8 @@ typedef struct {
     int32_t imgs;      /* images per CTA                                          */
     int32_t bh, bw;    /* output block per CTA                                    */
     int32_t cc;        /* input channels staged per pipeline stage                */
+    int32_t stages;    /* shared-memory stage buffers in flight (direct kinds: 2 or 3;
+                          0 = 2; ignored by the tiled / plane kernels)            */
 } scb_launch;
 
 /* Static description of a compiled tiled variant (for the tuner). */

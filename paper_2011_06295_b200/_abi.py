@@ -41,10 +41,10 @@ class Shape(ctypes.Structure):
 
 
 class Launch(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int32) for n in ("variant", "warps_k", "imgs", "bh", "bw", "cc")]
+    _fields_ = [(n, ctypes.c_int32) for n in ("variant", "warps_k", "imgs", "bh", "bw", "cc", "stages")]
 
     def as_tuple(self):
-        return (self.variant, self.warps_k, self.imgs, self.bh, self.bw, self.cc)
+        return (self.variant, self.warps_k, self.imgs, self.bh, self.bw, self.cc, self.stages)
 
     @classmethod
     def from_tuple(cls, t):

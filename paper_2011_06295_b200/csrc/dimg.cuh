@@ -50,10 +50,10 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
     const int C = p.c;
     float* xs = reinterpret_cast<float*>(smem);
     const int rows = 32 * p.cc * H;  // input rows per stage
-    DirectTap* tsm = reinterpret_cast<DirectTap*>(smem + (size_t)2 * p.stage_el * 4);
+    DirectTap* tsm = reinterpret_cast<DirectTap*>(smem + (size_t)p.nbuf * p.stage_el * 4);
     const int np1 = p.nst + 1;
     // stage pointers of this CTA's output channels, after the tap segments: [warp*KW + kk][np1]
-    int* sps = reinterpret_cast<int*>(tsm + (size_t)2 * p.wk * KW * p.segcap);
+    int* sps = reinterpret_cast<int*>(tsm + (size_t)p.nbuf * p.wk * KW * p.segcap);
     {
         const int kc0 = kb * p.wk * KW;
         for (int i = tid; i < p.wk * KW * np1; i += nthreads) {
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
 
     {  // zero both stages: padding rows and the halo ends of copies 0 / 2 stay zero
         float4* z = reinterpret_cast<float4*>(smem);
-        const int n16 = (2 * p.stage_el * 4) / 16;
+        const int n16 = (p.nbuf * p.stage_el * 4) / 16;
         for (int i = tid; i < n16; i += nthreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
@@ -121,17 +121,15 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
         for (int j = 0; j < HW; ++j) acc[kk][j] = b;
     }
 
-    stage(0, 0);
-    cp_async_commit();
+    for (int s0 = 0; s0 < p.nbuf - 1; ++s0) {  // prologue: nbuf-1 stages in flight
+        if (s0 < p.nst) stage(s0, s0);
+        cp_async_commit();
+    }
     for (int st = 0; st < p.nst; ++st) {
-        const int buf = st & 1;
-        if (st + 1 < p.nst) {
-            stage(st + 1, buf ^ 1);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        const int buf = st % p.nbuf;
+        if (st + p.nbuf - 1 < p.nst) stage(st + p.nbuf - 1, (st + p.nbuf - 1) % p.nbuf);
+        cp_async_commit();  // possibly empty: keeps one group per iteration
+        cp_async_wait_nb(p.nbuf);
         __syncthreads();
         shift(st, buf);
         __syncthreads();

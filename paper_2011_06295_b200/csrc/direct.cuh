@@ -55,8 +55,15 @@ struct DirectParams {
     int stage_el;             // elements per stage (128-byte multiple)
     int kblocks, n_ey, nb;
     int segcap;               // taps per (output channel, stage) segment slot in shared memory
+    int nbuf;                 // stage buffers in flight (2 or 3)
     uint32_t flags;
 };
+
+// wait until at most NB-1 committed cp.async groups are pending
+__device__ __forceinline__ void cp_async_wait_nb(int nbuf) {
+    if (nbuf >= 3) cp_async_wait<2>();
+    else cp_async_wait<1>();
+}
 
 // Shared row geometry of a direct variant (host and device agree on it).
 template <int S, int PAD, int LW, int VX, int ES = 4>
@@ -112,12 +119,12 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     // zero both stages once: halo positions are never written again
     {
         float4* z = reinterpret_cast<float4*>(smem);
-        const int n16 = (2 * p.stage_el * ES) / 16;
+        const int n16 = (p.nbuf * p.stage_el * ES) / 16;
         for (int i = tid; i < n16; i += nthreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     // row descriptors after the stages: {src element offset from (n0, channel 0), dst | cl << 24}
     const int rows = G * p.cc * RT;
-    uint2* rdesc = reinterpret_cast<uint2*>(smem + (size_t)2 * p.stage_el * ES);
+    uint2* rdesc = reinterpret_cast<uint2*>(smem + (size_t)p.nbuf * p.stage_el * ES);
     const int hw = p.h * p.w;
     for (int rr = tid; rr < rows; rr += nthreads) {
         const int yy = rr % RT, q = rr / RT;
@@ -131,10 +138,10 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
 
     // tap segments after the row descriptors: [buf][warp][kk][segcap] (8-byte taps)
     DirectTap* tsm = reinterpret_cast<DirectTap*>(
-        smem + (size_t)2 * p.stage_el * ES + (((size_t)rows * 8 + 15) & ~(size_t)15));
+        smem + (size_t)p.nbuf * p.stage_el * ES + (((size_t)rows * 8 + 15) & ~(size_t)15));
     const int np1 = p.nst + 1;
     // stage pointers of this CTA's output channels, after the tap segments: [warp*KW + kk][np1]
-    int* sps = reinterpret_cast<int*>(tsm + (size_t)2 * p.wk * KW * p.segcap);
+    int* sps = reinterpret_cast<int*>(tsm + (size_t)p.nbuf * p.wk * KW * p.segcap);
     {
         const int kc0 = kb * p.wk * KW;
         for (int i = tid; i < p.wk * KW * np1; i += nthreads) {
@@ -206,18 +213,16 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
         for (int j = 0; j < TH * VX; ++j) acc[kk][j] = b;
     }
 
-    stage(0, 0);
-    cp_async_commit();
+    for (int s0 = 0; s0 < p.nbuf - 1; ++s0) {  // prologue: nbuf-1 stages in flight
+        if (s0 < p.nst) stage(s0, s0);
+        cp_async_commit();
+    }
     const int lane_off = lg * p.ip + lx;  // + tap off - c0*PLANE
     for (int st = 0; st < p.nst; ++st) {
-        const int buf = st & 1;
-        if (st + 1 < p.nst) {
-            stage(st + 1, buf ^ 1);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        const int buf = st % p.nbuf;
+        if (st + p.nbuf - 1 < p.nst) stage(st + p.nbuf - 1, (st + p.nbuf - 1) % p.nbuf);
+        cp_async_commit();  // possibly empty: keeps one group per iteration
+        cp_async_wait_nb(p.nbuf);
         __syncthreads();
         if constexpr (VX == 2) {
             shift(st, buf);

@@ -363,7 +363,7 @@ PLANES = [
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
 KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG = 0, 1, 2, 3
 # image-lane direct variants (dimg.cuh): (H, KW)
-DIMGS = [(4, 2), (4, 4), (2, 2), (2, 4), (2, 8)]
+DIMGS = [(4, 1), (4, 2), (4, 4), (2, 1), (2, 2), (2, 4), (2, 8)]
 
 # dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW, VX)
 DIRECTS = [(3, 3, 1, th, lw, kw, 1) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \

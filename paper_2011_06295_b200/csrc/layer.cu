@@ -434,6 +434,8 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     const int G = 32 * v.nbt / v.tw;
     if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
         return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32*vx/tw, bh = th, bw = tw, 1..8 warps");
+    const int nbuf = c.stages == 0 ? 2 : c.stages;
+    if (nbuf < 2 || nbuf > 3) return fail(SCB_ERR_SHAPE, "direct launch: stages must be 2 or 3");
     d->threads = 32 * c.warps_k;
     d->row = direct_row(v);
     const int plane = (v.th + v.r - 1) * d->row;
@@ -449,8 +451,8 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
     const int segcap = L->sptr_maxseg[c.cc];
     d->wp = segcap;  // tap segment slot travels in `wp`
-    d->smem = 2 * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
-              (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
+    d->smem = nbuf * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
+              (size_t)nbuf * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
               (size_t)c.warps_k * v.kt * ((g.c + c.cc - 1) / c.cc + 1) * 4;  // stage pointers
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     if (2 * stage_bytes >= (1u << 24) * (size_t)es) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
@@ -471,6 +473,8 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const int H = v.th;
     if (c.imgs != 32 || c.bh != H || c.bw != H || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
         return fail(SCB_ERR_SHAPE, "image-lane launch: imgs = 32, bh = bw = plane, 1..8 warps");
+    const int nbuf = c.stages == 0 ? 2 : c.stages;
+    if (nbuf < 2 || nbuf > 3) return fail(SCB_ERR_SHAPE, "image-lane launch: stages must be 2 or 3");
     d->threads = 32 * c.warps_k;
     d->row = 3 * H;
     const int blk = (H + 2) * 3 * H;
@@ -484,7 +488,7 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
     const int segcap = L->sptr_maxseg[c.cc];
     d->wp = segcap;
-    d->smem = 2 * stage_bytes + (size_t)2 * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
+    d->smem = nbuf * stage_bytes + (size_t)nbuf * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
               (size_t)c.warps_k * v.kt * ((g.c + c.cc - 1) / c.cc + 1) * 4;  // stage pointers
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     d->n_ey = 1;
@@ -554,22 +558,24 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         if (!variant_matches(L, v, flags)) continue;
         if (v.kind == KIND_DIMG) {
             for (int wk : {1, 2, 4, 8})
-                for (int cc : {2, 4, 8, 16, 32}) {
-                    scb_launch c{vi, wk, 32, v.th, v.tw, cc};
-                    Derived d;
-                    if (derive(L, c, n, flags, &d) != SCB_OK) continue;
-                    out.push_back(c);
-                }
+                for (int cc : {2, 4, 8, 16, 32})
+                    for (int ns : {2, 3}) {
+                        scb_launch c{vi, wk, 32, v.th, v.tw, cc, ns};
+                        Derived d;
+                        if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                        out.push_back(c);
+                    }
             continue;
         }
         if (v.kind == KIND_DIRECT) {
             for (int wk : {1, 2, 4, 8})
-                for (int cc : {4, 8, 16, 32, 64}) {
-                    scb_launch c{vi, wk, 32 * v.nbt / v.tw, v.th, v.tw, cc};
-                    Derived d;
-                    if (derive(L, c, n, flags, &d) != SCB_OK) continue;
-                    out.push_back(c);
-                }
+                for (int cc : {4, 8, 16, 32, 64})
+                    for (int ns : {2, 3}) {
+                        scb_launch c{vi, wk, 32 * v.nbt / v.tw, v.th, v.tw, cc, ns};
+                        Derived d;
+                        if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                        out.push_back(c);
+                    }
             continue;
         }
         if (v.kind == KIND_PLANE) {
@@ -758,7 +764,7 @@ SCB_API scb_status scb_default_launch(const scb_layer* layer, int32_t n, uint32_
     if (!layer || !out) return fail(SCB_ERR_ARG, "NULL");
     if ((flags & SCB_FLAG_GENERIC) ||
         !pick_default(const_cast<scb_layer*>(layer), std::max(n, 1), flags, prefer_imgs, out)) {
-        *out = scb_launch{-1, 0, 0, 0, 0, 0};
+        *out = scb_launch{-1, 0, 0, 0, 0, 0, 0};
     }
     return SCB_OK;
 }
@@ -809,6 +815,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
         q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
+        q.nbuf = c.stages == 0 ? 2 : c.stages;
         cudaError_t e = ve.dlaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
         return e == cudaSuccess ? SCB_OK : cuda_fail(e, "direct kernel launch");
     }

@@ -32,9 +32,13 @@ def test_library_exports_every_declared_symbol():
 def test_variant_table():
     vs = _abi.variants()
     assert len(vs) >= 10
+    kinds = set()
     for v in vs:
-        assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (2, 4, 8)
+        assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (1, 2, 4, 8)
         assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["dispatch"] in (0, 1)
+        assert v["kind"] in (0, 1, 2, 3) and v["io"] in (0, 2)
+        kinds.add(v["kind"])
+    assert kinds == {0, 1, 2, 3}  # tiled, whole-plane, direct, image-lane direct
 
 
 def test_sm100a_cubin_only():
@@ -55,10 +59,13 @@ def test_exact_kernels_never_fuse():
         name = body.split("\n", 1)[0].strip()
         m = re.match(r"_ZN3scb7k_tiledILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi(\d)ELi0ELi\dELi\dEE", name)
         g = re.match(r"_ZN3scb9k_genericI([fd])Li0EE", name)
-        if not (m or g):
+        d = re.match(r"_ZN3scb8k_directILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi0ELi\d+ELi\d+ELb0EE", name)
+        i = re.match(r"_ZN3scb6k_dimgILi\d+ELi\d+ELi0EE", name)
+        pl = re.match(r"_ZN3scb7k_planeILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi0ELi0ELi\dEE", name)
+        if not (m or g or d or i or pl):
             continue
         ops = re.findall(r"\b(FFMA2?|DFMA|FMUL2?|FADD2?|DMUL|DADD)\b", body)
         assert "FFMA" not in ops and "FFMA2" not in ops and "DFMA" not in ops, name
         assert any(o.startswith(("FMUL", "DMUL")) for o in ops), name
         checked += 1
-    assert checked >= 8
+    assert checked >= 40
