@@ -475,3 +475,33 @@ def test_direct_f16_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     for cfg in pc[:: max(1, len(pc) // 6)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
         assert beq(o, want.astype(np.float16)), cfg
+
+
+@pytest.mark.parametrize("c,hw,k,n", [(32, 16, 24, 5), (64, 8, 40, 9), (48, 4, 32, 33)])
+def test_ragged_csr_all_kinds_bitwise(sc, orc, c, hw, k, n):
+    """Non-unified CSR (build_csr(unify=False), csr.py:120-126): per-channel nnz
+    differ; every kernel kind walks its own row (rowptr) and stays bitwise."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    rng = np.random.default_rng(11)
+    w = random_sparse_weights(rng, k, c, 3, 3, 0.85)
+    x = rng.standard_normal((n, c, hw, hw)).astype(np.float32)
+    b = rng.standard_normal(k).astype(np.float32)
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    kern = sc.build_csr(w, sh, unify=False)
+    assert not kern.unified and len(set(np.diff(kern.rowptr))) > 1
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+    xd = torch.from_numpy(x).cuda()
+    layer = device_layer(kern, 0, np.float32)
+    vs = _abi.variants()
+    cands = layer.candidates(n)
+    seen = set()
+    for cfg in cands:
+        kind = vs[cfg[0]]["kind"]
+        if kind in seen and len(seen) < 4:
+            continue
+        seen.add(kind)
+        o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
+        assert beq(o, ref), cfg
+    assert seen >= ({0, 2} if hw >= 8 else {1, 3})
