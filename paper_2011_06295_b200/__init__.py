@@ -10,6 +10,7 @@ there is no CPU fallback.
 from .engine import (SUB_BATCH_CANDIDATES, EnginePlan, conv_sparse, conv_sparse_1d,
                      conv_sparse_reference, dense_mac_count, sparse_mac_count,
                      tune_sub_batch)
+from .configure import NetworkConfig, configure_network
 from .errors import FormatError, IntegrityError, ShapeError, SparseConvError, TrainingError
 from .geometry import ConvShape, check_nchw, compute_dtype, output_shape, pad_input
 from .weights import (CsrKernel, SparsityReport, analyze_sparsity, build_csr, decompress,
@@ -18,7 +19,7 @@ from .weights import (CsrKernel, SparsityReport, analyze_sparsity, build_csr, de
 __version__ = "0.1.0"
 
 __all__ = [
-    "ConvShape", "CsrKernel", "EnginePlan", "FormatError", "IntegrityError", "ShapeError",
+    "ConvShape", "CsrKernel", "EnginePlan", "NetworkConfig", "configure_network", "FormatError", "IntegrityError", "ShapeError",
     "SparseConvError", "SparsityReport", "SUB_BATCH_CANDIDATES", "TrainingError",
     "analyze_sparsity", "build_csr", "check_nchw", "compute_dtype", "conv_sparse",
     "conv_sparse_1d", "conv_sparse_reference", "decompress", "dense_mac_count",

@@ -91,6 +91,8 @@ class SparseConvNet:
                     raise ShapeError(f"{L.name}: bias must have shape ({L.kernel.shape.k},)")
                 self.biases.append(torch.from_numpy(b).to(self.tdev))
         self.launches = [None] * len(self.layers)
+        self.algorithms = ["sparse-direct"] * len(self.layers)
+        self._dense = [None] * len(self.layers)
 
     # ---- shapes ---------------------------------------------------------
     def flags(self, i: int) -> int:
@@ -167,9 +169,57 @@ class SparseConvNet:
                          y_dev, self.batch, self.flags(i), self.launches[i], stream,
                          scratch=self.scratch[i])
 
+    def dense_layer(self, i: int):
+        """Dense cuDNN equivalent of layer i (IEEE fp32 / fp16, TF32 off):
+        conv2d + bias, ReLU, 2x2 max-pool; the "dense-cudnn" algorithm of a
+        NetworkConfig (configure.py)."""
+        if self._dense[i] is None:
+            import torch
+            from .weights import decompress
+            L = self.layers[i]
+            sh = L.kernel.shape
+            w = torch.from_numpy(decompress(L.kernel).astype(self.dtype)).to(self.tdev)
+            b = None if L.bias is None else torch.from_numpy(
+                np.asarray(L.bias, dtype=self.dtype)).to(self.tdev)
+
+            def run(x, out=None):
+                old = torch.backends.cudnn.allow_tf32
+                torch.backends.cudnn.allow_tf32 = False
+                try:
+                    a = torch.nn.functional.conv2d(x, w, b, stride=sh.stride, padding=sh.padding)
+                finally:
+                    torch.backends.cudnn.allow_tf32 = old
+                if L.relu:
+                    a = torch.relu(a)
+                if L.pool:
+                    a = torch.nn.functional.max_pool2d(a, 2)
+                if out is not None:
+                    out.copy_(a)
+                    return out
+                return a
+            self._dense[i] = run
+        return self._dense[i]
+
+    def apply_config(self, config) -> None:
+        """Install a NetworkConfig (configure.py): per-layer algorithm and, for
+        sparse layers, the recorded launch."""
+        if self.batch is None or config.batch != self.batch:
+            self.plan(config.batch, tune=False)
+        launches = list(self.launches)
+        for i, L in enumerate(self.layers):
+            ch = config.choices.get(L.name, {})
+            algo = ch.get("algorithm", "sparse-direct")
+            if algo not in ("sparse-direct", "dense-cudnn"):
+                raise ShapeError(f"unknown algorithm {algo!r} for layer {L.name}")
+            self.algorithms[i] = algo
+            if algo == "sparse-direct" and "launch" in ch:
+                launches[i] = None if ch["launch"] is None else tuple(ch["launch"])
+        self.set_launches(launches)
+
     def kernels_per_step(self) -> int:
         """Kernel launches of one forward (a generic layer with a pool is two)."""
-        return sum(2 if (l is None and L.pool) else 1 for l, L in zip(self.launches, self.layers))
+        return sum(0 if a == "dense-cudnn" else (2 if (l is None and L.pool) else 1)
+                   for l, L, a in zip(self.launches, self.layers, self.algorithms))
 
     def forward_device(self, x_dev=None, events=None):
         """Run the stack on the current stream of the device; returns the last
@@ -190,7 +240,10 @@ class SparseConvNet:
             if events is not None:
                 events[0].record(stream)
             for i in range(len(self.layers)):
-                self.launch_layer(i, cur, self.acts[i], s)
+                if self.algorithms[i] == "dense-cudnn":
+                    self.dense_layer(i)(cur, self.acts[i])
+                else:
+                    self.launch_layer(i, cur, self.acts[i], s)
                 if events is not None:
                     events[i + 1].record(stream)
                 cur = self.acts[i]

@@ -100,3 +100,28 @@ def test_generic_pool_through_conv_sparse(torch):
         engine.TUNED.pop((layer.signature(), 4, flags), None)
     want = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, b, relu=True, pool=True).cpu().numpy()
     assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_configure_network_and_apply(torch, vgg_small):
+    """configure_network (bench.py:306-342 semantics) times sparse vs dense per
+    layer; an applied config mixing both stays within the reference tolerance,
+    an all-sparse config stays bitwise."""
+    import paper_2011_06295_b200 as sc
+    net, x, ref = vgg_small
+    net.plan(3, tune=False)
+    cfg = sc.configure_network(net, repetitions=2, warmups=1)
+    assert set(cfg.choices) == {L.name for L in net.layers}
+    for ch in cfg.choices.values():
+        assert ch["algorithm"] in ("sparse-direct", "dense-cudnn")
+        assert set(ch["median_ms"]) == {"sparse-direct", "dense-cudnn"}
+    back = sc.NetworkConfig.from_json(cfg.to_json())
+    assert back.choices == cfg.choices
+    mixed = sc.NetworkConfig(batch=3, choices={L.name: {"algorithm": "dense-cudnn" if i % 2 else "sparse-direct"}
+                                              for i, L in enumerate(net.layers)})
+    net.apply_config(mixed)
+    out = net.forward(x)
+    # dense cuDNN sums in its own order: 13 layers of N(0,1) weights amplify
+    # per-layer rounding, so compare globally (relative L2) rather than per element
+    assert np.linalg.norm(out.astype(np.float64) - ref) <= 1e-4 * np.linalg.norm(ref.astype(np.float64))
+    net.apply_config(sc.NetworkConfig(batch=3, choices={}))
+    assert np.array_equal(_bits(net.forward(x)), _bits(ref))
