@@ -71,8 +71,8 @@ typedef struct {
     int32_t imgs;      /* images per CTA                                          */
     int32_t bh, bw;    /* output block per CTA                                    */
     int32_t cc;        /* input channels staged per pipeline stage                */
-    int32_t stages;    /* shared-memory stage buffers in flight (direct kinds: 2 or 3;
-                          0 = 2; ignored by the tiled / plane kernels)            */
+    int32_t stages;    /* shared-memory stage buffers in flight (direct kinds 2/3: 2 or 3,
+                          kind 4: 2..4; 0 = default; ignored by tiled / plane)    */
 } scb_launch;
 
 /* Static description of a compiled tiled variant (for the tuner). */
@@ -89,7 +89,8 @@ typedef struct {
                             input plane a lane holds; small spatial extents); 2 direct
                             (dispatch-free: th rows x tw columns per lane group, kt = output
                             channels per warp); 3 image-lane direct (lane = image, whole
-                            th x tw plane, shifted-copy vector loads) */
+                            th x tw plane, shifted-copy vector loads); 4 warp-specialised
+                            direct (producer warp + mbarrier ring, bulk copies) */
 } scb_variant_info;
 
 /* ---------------------------------------------------------------------- */

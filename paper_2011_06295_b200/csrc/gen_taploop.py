@@ -361,7 +361,9 @@ PLANES = [
     (4, 4, 3, 3, 1, 2, 1, 2),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
-KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG = 0, 1, 2, 3
+KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS = 0, 1, 2, 3, 4
+# warp-specialised direct variants (ws.cuh): (R, S, PAD, TH, LW, KW)
+DWS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)]
 # image-lane direct variants (dimg.cuh): (H, KW)
 DIMGS = [(4, 1), (4, 2), (4, 4), (2, 1), (2, 2), (2, 4), (2, 8)]
 
@@ -408,6 +410,8 @@ def main():
     for R, S, PAD, TH, LW, KW, VX, MB in DIRECTS:
         groups[("direct", R, S, PAD, TH, LW, KW, VX, MB)] = (
             [], [("direct", R, S, PAD, TH, LW, KW, VX, MB, mode) for mode in (EXACT, FMA)])
+    for R, S, PAD, TH, LW, KW in DWS:
+        groups[("dws", R, S, PAD, TH, LW, KW)] = ([], [("dws", R, S, PAD, TH, LW, KW, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DIRECTS_F16:
         groups[("direct16", R, S, PAD, TH, LW, KW)] = ([], [("direct16", R, S, PAD, TH, LW, KW)])
     for H, KW in DIMGS:
@@ -421,7 +425,7 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
@@ -432,6 +436,11 @@ def main():
                 R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
                 src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
+                if v[0] == "dws":
+                    _, R, S, PAD, TH, LW, KW, mode = v
+                    ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
+                                f"{KIND_DWS}}}, nullptr, &launch_dws_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, {mode}>}},\n")
+                    continue
                 if v[0] == "direct16":
                     _, R, S, PAD, TH, LW, KW = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, 2, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, {PAD}, "

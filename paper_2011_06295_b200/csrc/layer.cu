@@ -23,7 +23,7 @@ namespace {
 constexpr int kSmemLimit = 227 * 1024 - 1024;  // dynamic limit: 227 KB minus the kernels' static shared memory
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
-constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3;
+constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4;
 
 scb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -100,10 +100,10 @@ struct scb_layer {
         auto it = d_dtaps.find(key);
         if (it != d_dtaps.end()) return it->second;
         const int64_t pp = (int64_t)g.hp * g.wp;
-        std::vector<DirectTap> t(std::max<int64_t>(nnz, 1));
+        std::vector<DirectTap> t(nnz + 2);  // +2: bulk copies read up to the next 16-byte boundary
         for (int64_t i = 0; i < nnz; ++i) {
             const int64_t c = h_colidx[i] / pp, rem = h_colidx[i] % pp;
-            uint32_t vb = h_pay[i];
+            uint32_t vb = h_pay[i];  // (slack entries stay zero)
             std::memcpy(&t[i].v, &vb, 4);
             t[i].off = (int32_t)(es * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
         }
@@ -341,12 +341,12 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     if (v.io != L->dt || v.wf != L->wf) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
-    if (v.kind != KIND_DIRECT && v.kind != KIND_DIMG && !L->prog(v.kt)) return false;
+    if (v.kind < KIND_DIRECT && !L->prog(v.kt)) return false;
     if (v.kind == KIND_DIMG) {
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
         return true;
     }
-    if (v.kind == KIND_DIRECT) {
+    if (v.kind == KIND_DIRECT || v.kind == KIND_DWS) {
         if (g.f != v.tw || (g.w * elem_bytes(v)) % 16 != 0 || g.w > 32) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
         return true;
@@ -501,6 +501,44 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     return SCB_OK;
 }
 
+// Warp-specialised direct variants (ws.cuh): warps_k consumer warps + 1 producer warp.
+scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const int G = 32 / v.tw;
+    const int nbuf = c.stages == 0 ? 3 : c.stages;
+    if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8 || nbuf < 2 ||
+        nbuf > 4)
+        return fail(SCB_ERR_SHAPE, "ws launch: imgs = 32/tw, bh = th, bw = tw, 1..8 warps, 2..4 stages");
+    d->threads = 32 * (c.warps_k + 1);
+    d->row = direct_row(v);
+    const int plane = (v.th + v.r - 1) * d->row;
+    int ip = (c.cc * plane + 3) / 4 * 4;
+    if (G > 1)
+        while (ip % 32 != v.tw % 32) ip += 4;
+    d->chunk = ip;
+    const size_t stage_bytes = ((size_t)G * ip * 4 + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / 4);
+    d->tap_cap = plane;
+    if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
+    const int segcap = L->sptr_maxseg[c.cc];
+    d->wp = segcap;
+    const int slot = (segcap + 3) & ~1;
+    const int np1 = (g.c + c.cc - 1) / c.cc + 1;
+    d->smem = nbuf * stage_bytes + (size_t)nbuf * c.warps_k * v.kt * slot * sizeof(DirectTap) +
+              (size_t)c.warps_k * v.kt * np1 * 4 + 8 + 2 * nbuf * 8;
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    if ((g.w * 4) % 16) return fail(SCB_ERR_SHAPE, "ws launch: input rows must be 16-byte multiples");
+    d->n_ey = (g.e + v.th - 1) / v.th;
+    d->n_fx = 1;
+    d->kblocks = (g.k + c.warps_k * v.kt - 1) / (c.warps_k * v.kt);
+    d->nb = (n + G - 1) / G;
+    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
 scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     if (c.variant < 0 || c.variant >= num_variants()) return fail(SCB_ERR_SHAPE, "bad variant index");
     const scb_variant_info& v = variant(c.variant).info;
@@ -508,6 +546,7 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     if (v.kind == KIND_PLANE) return derive_plane(L, c, n, flags, d);
     if (v.kind == KIND_DIRECT) return derive_direct(L, c, n, flags, d);
     if (v.kind == KIND_DIMG) return derive_dimg(L, c, n, flags, d);
+    if (v.kind == KIND_DWS) return derive_dws(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -556,6 +595,17 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_DWS) {
+            for (int wk : {2, 4, 8})
+                for (int cc : {4, 8, 16, 32})
+                    for (int ns : {3, 4}) {
+                        scb_launch c{vi, wk, 32 / v.tw, v.th, v.tw, cc, ns};
+                        Derived d;
+                        if (derive(L, c, n, flags, &d) != SCB_OK) continue;
+                        out.push_back(c);
+                    }
+            continue;
+        }
         if (v.kind == KIND_DIMG) {
             for (int wk : {1, 2, 4, 8})
                 for (int cc : {2, 4, 8, 16, 32})
@@ -738,7 +788,7 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
         return SCB_OK;
     }
     if (variant >= num_variants()) return fail(SCB_ERR_ARG, "bad variant");
-    if (scb::variant(variant).info.kind == KIND_DIRECT || scb::variant(variant).info.kind == KIND_DIMG) {
+    if (scb::variant(variant).info.kind >= KIND_DIRECT) {
         *bytes = L->nnz * (int64_t)sizeof(DirectTap) + (int64_t)(L->g.k + 1) * 4;
         return SCB_OK;
     }
@@ -799,7 +849,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
     if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
-    if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
+    if (ve.info.kind >= KIND_DIRECT) {
         DirectParams q;
         std::memset(&q, 0, sizeof(q));
         q.x = x; q.bias = static_cast<const float*>(bias); q.y = y;
@@ -815,7 +865,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
         q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
-        q.nbuf = c.stages == 0 ? 2 : c.stages;
+        q.nbuf = c.stages == 0 ? (ve.info.kind == KIND_DWS ? 3 : 2) : c.stages;
         cudaError_t e = ve.dlaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
         return e == cudaSuccess ? SCB_OK : cuda_fail(e, "direct kernel launch");
     }

@@ -410,12 +410,14 @@ def test_direct_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     vs = _abi.variants()
     cands = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 2]
     assert cands, "no direct variant"
-    for cfg in cands[:: max(1, len(cands) // 30)]:
+    ws = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 4]
+    assert ws or hw < 8, "no warp-specialised variant"
+    for cfg in cands[:: max(1, len(cands) // 30)] + ws[:: max(1, len(ws) // 20)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
     want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref)), 2).numpy()
-    pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 2]
-    for cfg in pc[:: max(1, len(pc) // 6)]:
+    pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] in (2, 4)]
+    for cfg in pc[:: max(1, len(pc) // 8)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
         assert beq(o, want), cfg
 
