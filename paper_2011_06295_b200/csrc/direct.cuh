@@ -70,9 +70,12 @@ template <int S, int PAD, int LW, int VX, int ES = 4>
 struct DirectRow {
     static constexpr int Q16 = 16 / ES;  // elements per 16 bytes
     static constexpr int XO = Q16;       // shared column of input column 0 (16-byte aligned)
-    // one copy of a row: left halo, LW columns, right halo, rounded to 16 bytes
-    static constexpr int QW = VX == 1 ? ((XO + LW + (S - 1 - PAD > 0 ? S - 1 - PAD : 0)) + Q16 - 1) / Q16 * Q16
+    // one copy of a row: left padding (XO >= the right halo), LW columns, rounded to 16 bytes.
+    // VX = 1: the right halo reads the NEXT row's never-written left padding (zero), so
+    // no right-halo columns are stored (the host leaves 16 zero bytes after each stage).
+    static constexpr int QW = VX == 1 ? ((XO + LW) + Q16 - 1) / Q16 * Q16
                                       : ((XO + LW + S) + Q16 - 1) / Q16 * Q16;
+    static_assert(XO >= S - 1 - PAD, "right halo must fit in the next row's left padding");
     static constexpr int ROW = VX * QW;
     // shared column (relative to the lane's first output column) of tap column s
     static constexpr int col(int s) {

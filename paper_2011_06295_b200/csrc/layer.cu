@@ -414,7 +414,8 @@ scb_status derive_plane(scb_layer* L, const scb_launch& c, int n, uint32_t flags
 int direct_qw(const scb_variant_info& v) {
     const int q = v.io == SCB_F16 ? 8 : 4;  // elements per 16 bytes (= XO)
     const int right = v.s - 1 - v.pad > 0 ? v.s - 1 - v.pad : 0;
-    return v.nbt == 1 ? (q + v.tw + right + q - 1) / q * q : (q + v.tw + v.s + q - 1) / q * q;
+    (void)right;  // VX = 1 rows alias the right halo onto the next row's left padding
+    return v.nbt == 1 ? (q + v.tw + q - 1) / q * q : (q + v.tw + v.s + q - 1) / q * q;
 }
 int direct_row(const scb_variant_info& v) { return v.nbt * direct_qw(v); }
 std::vector<int> direct_cols(const scb_variant_info& v) {
@@ -444,7 +445,7 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     if (G > 1)  // word pitch of an image = its row width in words (mod 32): conflict-free lanes
         while ((ip * es / 4) % 32 != (v.tw * es / 4) % 32) ip += q16;
     d->chunk = ip;  // image pitch (elements) travels in `chunk`
-    const size_t stage_bytes = ((size_t)G * ip * es + 127) & ~(size_t)127;
+    const size_t stage_bytes = ((size_t)G * ip * es + 16 + 127) & ~(size_t)127;  // +16: zero tail
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
     const int rows = G * c.cc * (v.th + v.r - 1);
@@ -517,7 +518,7 @@ scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     if (G > 1)
         while (ip % 32 != v.tw % 32) ip += 4;
     d->chunk = ip;
-    const size_t stage_bytes = ((size_t)G * ip * 4 + 127) & ~(size_t)127;
+    const size_t stage_bytes = ((size_t)G * ip * 4 + 16 + 127) & ~(size_t)127;  // +16: zero tail
     d->stage_el = (int)(stage_bytes / 4);
     d->tap_cap = plane;
     if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
