@@ -411,9 +411,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e_s = e_ev[0].elapsed_time(e_ev[1]) * 1e-3
 
     # max over ranks
-    t = torch.tensor([total_s, e2e_s], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_s, e2e_s], dtype=torch.float64,
+                     device=dev if (world > 1 and dist.get_backend() == "nccl") else "cpu")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # device time: max over ranks
     total_s, e2e_s = float(t[0]), float(t[1])
     if rank != 0:
         return
@@ -492,8 +493,13 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ndev = torch.cuda.device_count()
+        if ndev >= world:  # one process per GPU: NCCL over NVLink
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # oversubscribed test launch (more ranks than GPUs): CPU collectives
+            local_rank %= max(ndev, 1)
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
