@@ -674,6 +674,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
 // Heuristic default (used when the tuner has not run): favour large
 // accumulator tiles and enough resident warps, then plane (bulk) staging.
 bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_launch* out) {
+    const Geom& g = L->g;
     std::vector<scb_launch> cands;
     enumerate(L, n, flags, cands);
     if (cands.empty()) return false;
@@ -687,12 +688,32 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
         Derived d;
         if (derive(L, c, n, flags, &d) != SCB_OK) continue;
         const scb_variant_info& v = variant(c.variant).info;
-        const double acc = (double)v.kt * v.nbt * v.th * v.tw;  // MACs per tap dispatch
         const double warps = (double)d.grid * d.threads / 32.0;
         const double fill = std::min(1.0, warps / (148.0 * 8.0));
-        const double restage = 1.0 / (c.warps_k * v.kt);        // input re-reads per channel
-        double score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * restage;
-        if (c.cc == 8) score += 0.05;
+        double score;
+        if (v.kind >= KIND_DIRECT) {
+            // measured on B200 (profiles/r01_probe_*): the dispatch-free kernels win wherever
+            // they apply; prefer their tuned shapes -- 8 warps, 16-32 channels per stage,
+            // 8 rows x 4-8 channels per warp (direct), 4 channels per warp (image-lane)
+            score = 100.0 + 3.0 * std::log(fill + 1e-3);
+            if (v.kind == KIND_DWS) score -= 1.0;
+            if (c.warps_k == 8) score += 1.0;
+            if (v.kind == KIND_DIRECT) {
+                score += (v.th == 8 ? 1.0 : 0.0) + (v.kt >= 4 ? 0.5 : 0.0) + (v.nbt == 1 ? 0.3 : 0.0);
+                score += (c.cc == 16 ? 0.5 : 0.0);
+            } else if (v.kind == KIND_DIMG) {
+                score += (v.kt == 4 ? 0.5 : 0.0) + (c.cc == 32 ? 0.5 : 0.0) - (g.h == 4 ? 2.0 : 0.0);
+            }
+            if (c.stages == 2 || c.stages == 0) score += 0.2;
+        } else {
+            const double acc = (double)v.kt * v.nbt * v.th * v.tw;  // MACs per tap dispatch
+            const double restage = 1.0 / (c.warps_k * v.kt);        // input re-reads per channel
+            score = std::log(acc) + 3.0 * std::log(fill + 1e-3) - 2.0 * restage;
+            if (c.cc == 8) score += 0.05;
+            if (v.kind == KIND_PLANE && g.h * g.w <= 16) {  // 4x4: the measured winner
+                score += 50.0 + (v.kt == 2 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0) + (c.cc == 16 ? 0.5 : 0.0);
+            }
+        }
         if (score > best) { best = score; *out = c; }
     }
     set_error("");
