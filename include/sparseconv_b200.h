@@ -124,6 +124,10 @@ SCB_API scb_status scb_decompress(const scb_shape* shape, scb_dtype dt, const vo
                                   const int32_t* colidx, const int32_t* rowptr,
                                   int64_t nnz, void* dense_out);
 
+/* 64-bit FNV-1a of a byte range: the model-store blob checksum
+ * (store.py:46-51 fnv1a64, pkg/docs/format.md "checksum"). */
+SCB_API scb_status scb_fnv1a64(const void* data, int64_t size, uint64_t* out);
+
 /* ---------------------------------------------------------------------- */
 /* device layer: the uploaded, kernel-ready weights of one CsrKernel      */
 /* ---------------------------------------------------------------------- */

@@ -32,7 +32,7 @@ EXPORTS = (
     "scb_validate_csr", "scb_decompress", "scb_layer_create", "scb_layer_destroy",
     "scb_layer_weight_bytes", "scb_conv_sparse", "scb_launch_candidates",
     "scb_default_launch", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
-    "scb_fma_peaks", "scb_last_error", "scb_version",
+    "scb_fma_peaks", "scb_fnv1a64", "scb_last_error", "scb_version",
 )
 
 
@@ -97,6 +97,7 @@ def lib():
             "scb_variant_get": [i32, P(VariantInfo)],
             "scb_maxpool2": [i32, vp, vp, i64, i32, i32, vp],
             "scb_fma_peaks": [i32, vp, vp, i32, P(i32)],
+            "scb_fnv1a64": [vp, i64, P(ctypes.c_uint64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

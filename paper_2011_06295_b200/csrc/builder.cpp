@@ -243,3 +243,12 @@ SCB_API const char* scb_last_error(void) { return g_last_error.c_str(); }
 SCB_API const char* scb_version(void) { return "sparseconv_b200 0.1.0 (sm_100a)"; }
 
 }  // extern "C"
+
+extern "C" SCB_API scb_status scb_fnv1a64(const void* data, int64_t size, uint64_t* out) {
+    if (!out || size < 0 || (size > 0 && !data)) return scb::fail(SCB_ERR_ARG, "fnv1a64: bad arguments");
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (int64_t i = 0; i < size; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+    *out = h;
+    return SCB_OK;
+}
