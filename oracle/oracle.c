@@ -99,9 +99,16 @@ void orc_conv_sparse_kernel_##SUF(const T* xf, long long row_len,               
                 for (int e = 0; e < e_out; ++e) {                               \
                     const T* xr = x + base + (long long)e * stride * wp;        \
                     T* orow = o + (long long)e * f_out;                         \
-                    for (int f = 0; f < f_out; ++f) {                           \
-                        T prod = v * xr[(long long)f * stride];                 \
-                        orow[f] = orow[f] + prod;                               \
+                    if (stride == 1) { /* _kernels.py:80-82 contiguous axpy */  \
+                        for (int f = 0; f < f_out; ++f) {                       \
+                            T prod = v * xr[f];                                 \
+                            orow[f] = orow[f] + prod;                           \
+                        }                                                       \
+                    } else {                                                    \
+                        for (int f = 0; f < f_out; ++f) {                       \
+                            T prod = v * xr[(long long)f * stride];             \
+                            orow[f] = orow[f] + prod;                           \
+                        }                                                       \
                     }                                                           \
                 }                                                               \
             }                                                                   \

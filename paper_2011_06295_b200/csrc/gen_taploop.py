@@ -359,6 +359,7 @@ PLANES = [
     (2, 2, 3, 3, 1, 2, 2, 2),
     (4, 4, 3, 3, 1, 2, 2, 2), (4, 4, 3, 3, 1, 4, 1, 2), (4, 4, 3, 3, 1, 4, 2, 2), (4, 4, 3, 3, 1, 8, 1, 2),
     (4, 4, 3, 3, 1, 2, 1, 2),
+    (4, 4, 3, 3, 1, 2, 1, 3), (2, 2, 3, 3, 1, 2, 2, 3), (2, 2, 3, 3, 1, 2, 4, 3),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
 KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS = 0, 1, 2, 3, 4
@@ -409,7 +410,7 @@ def main():
         for f16, wf, mode in PLANE_MODES:
             loops.append(("plane", H, W, R, S, PAD, KT, NBT, wf, mode, f16))
             variants.append(("plane", H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb))
-        groups[("plane", H, W, R, S, PAD, KT, NBT)] = (loops, variants)
+        groups[("plane", H, W, R, S, PAD, KT, NBT, minb)] = (loops, variants)
     for R, S, PAD, TH, LW, KW, VX, MB in DIRECTS:
         groups[("direct", R, S, PAD, TH, LW, KW, VX, MB)] = (
             [], [("direct", R, S, PAD, TH, LW, KW, VX, MB, mode) for mode in (EXACT, FMA)])
