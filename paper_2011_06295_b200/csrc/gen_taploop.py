@@ -378,7 +378,8 @@ DIRECTS = [d + (2,) for d in DIRECTS] + \
            ((8, 4, 1), (4, 4, 1), (4, 8, 1), (8, 2, 2), (4, 4, 2))] + \
           [(3, 3, 1, 8, lw, 4, 1, 3) for lw in (32, 16, 8)] + \
           [(3, 3, 1, 8, lw, 2, 1, 4) for lw in (32, 16, 8)] + \
-          [(3, 3, 1, 8, lw, 2, 2, 3) for lw in (32, 16, 8)]  # + min CTAs/SM (4: <= 64 registers)
+          [(3, 3, 1, 8, lw, 2, 2, 3) for lw in (32, 16, 8)] + \
+          [(3, 3, 1, 16, lw, kw, 1, 2) for lw in (32, 16) for kw in (2, 4)]  # + min CTAs/SM (4: <= 64 regs)
 # f16-storage direct variants (FHFMA, column pairs): (R, S, PAD, TH, LW, KW)
 DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)]
 
