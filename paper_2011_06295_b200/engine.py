@@ -199,8 +199,36 @@ def _choose_launch(layer, n, flags, plan: EnginePlan):
     key = (layer.signature(), n, flags)
     if key in TUNED:
         return TUNED[key]
+    hit = _builtin().get(_builtin_key(layer.signature(), flags))
+    if hit is not None:
+        return hit
     d = layer.default_launch(n, flags, plan.sub_batch_size if plan.sub_batch_size > 1 else 0)
     return None if d[0] < 0 else d
+
+
+_BUILTIN = None
+
+
+def _builtin_key(sig, flags):
+    s = list(sig)
+    return (tuple(s[:8] + s[9:]), int(flags))  # geometry + dtype + format, not the sparse level
+
+
+def _builtin() -> dict:
+    """Launch table measured on B200 for the VGG-16/CIFAR geometries
+    (tools/tune_table.py -> tuned/b200_vgg_cifar.json); the fallback when the
+    tuner has not run in this process.  The C library re-validates every
+    launch, so a stale entry fails loudly rather than computing wrongly."""
+    global _BUILTIN
+    if _BUILTIN is None:
+        import json
+        from pathlib import Path
+        _BUILTIN = {}
+        p = Path(__file__).resolve().parent / "tuned" / "b200_vgg_cifar.json"
+        if p.exists():
+            for r in json.loads(p.read_text())["rows"]:
+                _BUILTIN[(tuple(r["sig"]), int(r["flags"]))] = None if r["launch"] is None else tuple(r["launch"])
+    return _BUILTIN
 
 
 def conv_sparse(x, kernel: CsrKernel, bias=None, plan: EnginePlan = EnginePlan(), *,

@@ -507,3 +507,25 @@ def test_ragged_csr_all_kinds_bitwise(sc, orc, c, hw, k, n):
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
     assert seen >= ({0, 2} if hw >= 8 else {1, 3})
+
+
+def test_builtin_launch_table_used_and_exact(sc, orc):
+    """conv_sparse on a VGG-CIFAR geometry without in-process tuning takes the
+    shipped B200 launch table (engine._builtin) and stays bitwise."""
+    import torch
+    from paper_2011_06295_b200 import engine
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import bench_inputs, make_layer_weights, vgg16_cifar
+    spec = [s for s, _ in vgg16_cifar(0.95) if s.name == "conv3_2"][0]  # other sparsity: table is L-free
+    sh = spec.shape.with_batch(20)
+    w = make_layer_weights(spec, 3)
+    x, b = bench_inputs(sh, 20)
+    kern = sc.build_csr(w, sh)
+    layer = device_layer(kern, 0, np.float32)
+    flags = engine._flags(sc.EnginePlan(), True, False, False)
+    engine.TUNED.pop((layer.signature(), 20, flags), None)
+    chosen = engine._choose_launch(layer, 20, flags, sc.EnginePlan())
+    assert chosen == engine._builtin()[engine._builtin_key(layer.signature(), flags)]
+    got = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, b, relu=True).cpu().numpy()
+    ref = np.maximum(orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, sh.k, 3, 3, 1, 1, b), 0)
+    assert beq(got, ref)
