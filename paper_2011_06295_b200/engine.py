@@ -226,8 +226,16 @@ def _builtin() -> dict:
         _BUILTIN = {}
         p = Path(__file__).resolve().parent / "tuned" / "b200_vgg_cifar.json"
         if p.exists():
+            # launches name their kernel by its description, not the compiled-table index
+            index = {tuple(sorted(v.items())): i for i, v in reversed(list(enumerate(_abi.variants())))}
             for r in json.loads(p.read_text())["rows"]:
-                _BUILTIN[(tuple(r["sig"]), int(r["flags"]))] = None if r["launch"] is None else tuple(r["launch"])
+                launch = r["launch"]
+                if launch is not None:
+                    vi = index.get(tuple(sorted(r["variant"].items())))
+                    if vi is None:
+                        continue  # kernel no longer compiled: fall back to the heuristic
+                    launch = (vi, *launch[1:])
+                _BUILTIN[(tuple(r["sig"]), int(r["flags"]))] = None if launch is None else tuple(launch)
     return _BUILTIN
 
 

@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2011_06295_b200 as sc  # noqa: E402
-from paper_2011_06295_b200 import engine  # noqa: E402
+from paper_2011_06295_b200 import _abi, engine  # noqa: E402
 from paper_2011_06295_b200.synth import bench_inputs, make_layer_weights, vgg16_cifar  # noqa: E402
 from paper_2011_06295_b200.tuner import tune_launch  # noqa: E402
 
@@ -31,7 +31,10 @@ for dt in (np.float32, np.float16):
             sig = list(engine.device_layer(kern, 0, engine._io_dtype(xd.numpy().dtype if False else np.dtype(dt), kern)).signature())
             sig = [s if not isinstance(s, (np.integer,)) else int(s) for s in sig]
             # the table is keyed without the sparse level: the best launch depends on geometry and dtype
-            rows.append({"sig": sig[:8] + sig[9:], "flags": flags, "launch": None if best is None else list(best)})
+            row = {"sig": sig[:8] + sig[9:], "flags": flags, "launch": None if best is None else list(best)}
+            if best is not None:
+                row["variant"] = _abi.variants()[best[0]]
+            rows.append(row)
             print(spec.name, str(np.dtype(dt)), flags, best, flush=True)
 out = ROOT / "paper_2011_06295_b200" / "tuned" / "b200_vgg_cifar.json"
 out.parent.mkdir(exist_ok=True)
