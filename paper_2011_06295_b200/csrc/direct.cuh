@@ -56,6 +56,7 @@ struct DirectParams {
     int kblocks, n_ey, nb;
     int segcap;               // taps per (output channel, stage) segment slot in shared memory
     int nbuf;                 // stage buffers in flight (2 or 3)
+    const int32_t* blkoff;    // k_direct: [group*nst + st] 16-byte-chunk offset of each tap block (+ end)
     uint32_t flags;
 };
 
@@ -139,20 +140,13 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     }
     __syncthreads();
 
-    // tap segments after the row descriptors: [buf][warp][kk][segcap] (8-byte taps)
-    DirectTap* tsm = reinterpret_cast<DirectTap*>(
+    // tap blocks after the row descriptors: [buf][warp] slots of segcap 16-byte chunks; a
+    // block is [KW int32 counts, padded to 16 B][taps of the KW channels, kk-major]
+    int4* tsm = reinterpret_cast<int4*>(
         smem + (size_t)p.nbuf * p.stage_el * ES + (((size_t)rows * 8 + 15) & ~(size_t)15));
-    const int np1 = p.nst + 1;
-    // stage pointers of this CTA's output channels, after the tap segments: [warp*KW + kk][np1]
-    int* sps = reinterpret_cast<int*>(tsm + (size_t)p.nbuf * p.wk * KW * p.segcap);
-    {
-        const int kc0 = kb * p.wk * KW;
-        for (int i = tid; i < p.wk * KW * np1; i += nthreads) {
-            const int k = kc0 + i / np1;
-            sps[i] = k < p.k ? __ldg(p.sptr + (size_t)k * np1 + i % np1) : 0;
-        }
-        __syncthreads();
-    }
+    constexpr int HDR = (KW * 4 + 15) / 16;  // header chunks
+    const int grp = kb * p.wk + warp;        // this warp's channel group
+    const int groups = (p.k + KW - 1) / KW;
 
     const TIO* xg = static_cast<const TIO*>(p.x) + (size_t)n0 * C * hw;
     constexpr int Q16 = 16 / ES;
@@ -170,15 +164,14 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
                 for (int q = 0; q < nchunk; ++q) cp_async<16>(d + Q16 * q, s + Q16 * q);
             }
         }
-        // this warp's KW tap segments of the stage (each lane copies every 32nd tap)
-        DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
-#pragma unroll
-        for (int kk = 0; kk < KW; ++kk) {
-            const int k = k0 + kk;
-            if (k >= p.k) break;
-            const int t0 = sps[(warp * KW + kk) * np1 + st];
-            const int t1 = sps[(warp * KW + kk) * np1 + st + 1];
-            for (int i = lane; i < t1 - t0; i += 32) cp_async<8>(tb + kk * p.segcap + i, p.taps + t0 + i);
+        // this warp's contiguous tap block of the stage: 16-byte chunks, one per lane
+        if (grp < groups) {
+            const int o0 = __ldg(p.blkoff + (size_t)grp * p.nst + st);
+            const int o1 = __ldg(p.blkoff + (size_t)grp * p.nst + st + 1);  // blocks are consecutive
+            const int4* src = reinterpret_cast<const int4*>(p.taps) + o0;
+            int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
+            const int nch = min(o1 - o0, p.segcap);
+            for (int i = lane; i < nch; i += 32) cp_async<16>(tb + i, src + i);
         }
     };
 
@@ -232,13 +225,14 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
             __syncthreads();
         }
         const TIO* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
-        const DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
+        const int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
+        const int* cnt = reinterpret_cast<const int*>(tb);
+        const DirectTap* seg = reinterpret_cast<const DirectTap*>(tb + HDR);
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
             if (k >= p.k) break;
-            const int nt = sps[(warp * KW + kk) * np1 + st + 1] - sps[(warp * KW + kk) * np1 + st];
-            const DirectTap* seg = tb + kk * p.segcap;
+            const int nt = cnt[kk];
 #pragma unroll 4
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
@@ -263,6 +257,7 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
                     }
                 }
             }
+            seg += nt;
         }
         __syncthreads();
     }

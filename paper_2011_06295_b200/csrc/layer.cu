@@ -82,6 +82,83 @@ struct scb_layer {
     std::map<std::vector<int>, DirectTap*> d_dtaps;  // key (plane, row, column of each s)
     std::map<int, int32_t*> d_sptr;
     std::map<int, int> sptr_maxseg;  // cc -> longest (channel, stage) tap segment
+    std::map<int, std::vector<int32_t>> h_sptr;  // cc -> host copy of the stage pointers
+    // stage-major tap blocks of the direct kernel, key (layout..., es, cc, kw):
+    // per (channel group g of kw, stage st) one contiguous 16-byte-aligned block
+    // [kw int32 counts, padded to 16 B][taps of the kw channels in that stage, kk-major]
+    struct Blocks { DirectTap* taps = nullptr; int32_t* off = nullptr; };
+    std::map<std::vector<int>, Blocks> d_blocks;
+    std::map<std::pair<int, int>, int> blk_cap;  // (cc, kw) -> largest block in 16-byte units
+
+    // largest block (16-byte units) for (cc, kw), from the host stage pointers
+    int block_cap(int cc, int kw) {
+        if (!stage_ptr(cc)) return -1;
+        std::lock_guard<std::mutex> lk(mu);
+        auto key = std::make_pair(cc, kw);
+        auto it = blk_cap.find(key);
+        if (it != blk_cap.end()) return it->second;
+        const std::vector<int32_t>& sp = h_sptr[cc];
+        const int nst = (g.c + cc - 1) / cc, groups = (g.k + kw - 1) / kw;
+        const int hdr = (kw * 4 + 15) / 16;  // header chunks
+        int mx = 1;
+        for (int gg = 0; gg < groups; ++gg)
+            for (int st = 0; st < nst; ++st) {
+                int n = 0;
+                for (int kk = 0; kk < kw; ++kk) {
+                    const int k = gg * kw + kk;
+                    if (k < g.k) n += sp[(size_t)k * (nst + 1) + st + 1] - sp[(size_t)k * (nst + 1) + st];
+                }
+                mx = std::max(mx, hdr + (n + 1) / 2);
+            }
+        blk_cap[key] = mx;
+        return mx;
+    }
+    // device tables: taps (as 16-byte chunks) and per-(g, st) chunk offsets
+    Blocks direct_blocks(int plane, int row, const std::vector<int>& col, int es, int cc, int kw) {
+        if (!stage_ptr(cc)) return Blocks{};
+        std::lock_guard<std::mutex> lk(mu);
+        std::vector<int> key{plane, row, es, cc, kw};
+        key.insert(key.end(), col.begin(), col.end());
+        auto it = d_blocks.find(key);
+        if (it != d_blocks.end()) return it->second;
+        const std::vector<int32_t>& sp = h_sptr[cc];
+        const int64_t pp = (int64_t)g.hp * g.wp;
+        const int nst = (g.c + cc - 1) / cc, groups = (g.k + kw - 1) / kw;
+        const int hdr = (kw * 4 + 15) / 16;
+        std::vector<DirectTap> out;
+        std::vector<int32_t> off((size_t)groups * nst + 1);
+        for (int gg = 0; gg < groups; ++gg)
+            for (int st = 0; st < nst; ++st) {
+                off[(size_t)gg * nst + st] = (int32_t)(out.size() / 2);  // in 16-byte chunks
+                const size_t h0 = out.size();
+                out.resize(h0 + 2 * hdr);
+                int32_t* cnt = reinterpret_cast<int32_t*>(&out[h0]);
+                for (int kk = 0; kk < kw; ++kk) {
+                    const int k = gg * kw + kk;
+                    const int t0 = k < g.k ? sp[(size_t)k * (nst + 1) + st] : 0;
+                    const int t1 = k < g.k ? sp[(size_t)k * (nst + 1) + st + 1] : 0;
+                    cnt = reinterpret_cast<int32_t*>(&out[h0]);
+                    cnt[kk] = t1 - t0;
+                    for (int t = t0; t < t1; ++t) {
+                        const int64_t c = h_colidx[t] / pp, rem = h_colidx[t] % pp;
+                        DirectTap d;
+                        uint32_t vb = h_pay[t];
+                        std::memcpy(&d.v, &vb, 4);
+                        d.off = (int32_t)(es * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
+                        out.push_back(d);
+                    }
+                }
+                if (out.size() & 1) out.push_back(DirectTap{0.f, 0});
+            }
+        off[(size_t)groups * nst] = (int32_t)(out.size() / 2);  // end of the last block
+        Blocks b;
+        if (cudaMalloc(&b.taps, std::max<size_t>(out.size(), 2) * sizeof(DirectTap)) != cudaSuccess) return Blocks{};
+        if (cudaMalloc(&b.off, off.size() * 4) != cudaSuccess) { cudaFree(b.taps); return Blocks{}; }
+        cudaMemcpy(b.taps, out.data(), out.size() * sizeof(DirectTap), cudaMemcpyHostToDevice);
+        cudaMemcpy(b.off, off.data(), off.size() * 4, cudaMemcpyHostToDevice);
+        d_blocks[key] = b;
+        return b;
+    }
 
     ~scb_layer() {
         DeviceGuard dg(device);
@@ -91,6 +168,7 @@ struct scb_layer {
         for (auto& p : progs) { cudaFree(p.d_ptr); cudaFree(p.d_taps); cudaFree(p.d_ptr_m); cudaFree(p.d_taps_m); cudaFree(p.d_masks); }
         for (auto& kv : d_dtaps) cudaFree(kv.second);
         for (auto& kv : d_sptr) cudaFree(kv.second);
+        for (auto& kv : d_blocks) { cudaFree(kv.second.taps); cudaFree(kv.second.off); }
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
     DirectTap* direct_taps(int plane, int row, const std::vector<int>& col, int es = 4) {
@@ -137,6 +215,7 @@ struct scb_layer {
             for (int st = 0; st < nst; ++st)
                 mx = std::max(mx, sp[(size_t)k * (nst + 1) + st + 1] - sp[(size_t)k * (nst + 1) + st]);
         sptr_maxseg[cc] = mx;
+        h_sptr[cc] = sp;
         int32_t* d = nullptr;
         if (cudaMalloc(&d, sp.size() * 4) != cudaSuccess) return nullptr;
         if (cudaMemcpy(d, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -449,12 +528,11 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
     const int rows = G * c.cc * (v.th + v.r - 1);
-    if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
-    const int segcap = L->sptr_maxseg[c.cc];
-    d->wp = segcap;  // tap segment slot travels in `wp`
+    const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
+    if (cap < 0) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
+    d->wp = cap;  // tap block slot (16-byte units) travels in `wp`
     d->smem = nbuf * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
-              (size_t)nbuf * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
-              (size_t)c.warps_k * v.kt * ((g.c + c.cc - 1) / c.cc + 1) * 4;  // stage pointers
+              (size_t)nbuf * c.warps_k * cap * 16;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     if (2 * stage_bytes >= (1u << 24) * (size_t)es) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
     d->n_ey = (g.e + v.th - 1) / v.th;
@@ -880,8 +958,16 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
             for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * ve.info.th);
         else
             col = direct_cols(ve.info);
-        q.taps = L->direct_taps(d.tap_cap, d.row, col, elem_bytes(ve.info));
-        q.sptr = L->stage_ptr(c.cc);
+        if (ve.info.kind == KIND_DIRECT) {
+            auto blk = L->direct_blocks(d.tap_cap, d.row, col, elem_bytes(ve.info), c.cc, ve.info.kt);
+            q.taps = blk.taps;
+            q.blkoff = blk.off;
+            q.sptr = L->stage_ptr(c.cc);
+            if (!q.taps || !q.blkoff) return fail(SCB_ERR_CUDA, "direct tap blocks: device allocation failed");
+        } else {
+            q.taps = L->direct_taps(d.tap_cap, d.row, col, elem_bytes(ve.info));
+            q.sptr = L->stage_ptr(c.cc);
+        }
         if (!q.taps || !q.sptr) return fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed");
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
