@@ -50,17 +50,11 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
     const int C = p.c;
     float* xs = reinterpret_cast<float*>(smem);
     const int rows = 32 * p.cc * H;  // input rows per stage
-    DirectTap* tsm = reinterpret_cast<DirectTap*>(smem + (size_t)p.nbuf * p.stage_el * 4);
-    const int np1 = p.nst + 1;
-    // stage pointers of this CTA's output channels, after the tap segments: [warp*KW + kk][np1]
-    int* sps = reinterpret_cast<int*>(tsm + (size_t)p.nbuf * p.wk * KW * p.segcap);
-    {
-        const int kc0 = kb * p.wk * KW;
-        for (int i = tid; i < p.wk * KW * np1; i += nthreads) {
-            const int k = kc0 + i / np1;
-            sps[i] = k < p.k ? __ldg(p.sptr + (size_t)k * np1 + i % np1) : 0;
-        }
-    }
+    // tap blocks after the stages: [buf][warp] slots of segcap 16-byte chunks (direct.cuh layout)
+    int4* tsm = reinterpret_cast<int4*>(smem + (size_t)p.nbuf * p.stage_el * 4);
+    constexpr int HDR = (KW * 4 + 15) / 16;
+    const int grp = kb * p.wk + warp;
+    const int groups = (p.k + KW - 1) / KW;
 
     {  // zero both stages: padding rows and the halo ends of copies 0 / 2 stay zero
         float4* z = reinterpret_cast<float4*>(smem);
@@ -82,14 +76,13 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
                 cp_async<H * 4>(dst + img * p.ip + cl * BLK + (y + 1) * RW + H,
                                 xg + ((size_t)img * C + c0 + cl) * HW + y * H);
         }
-        DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
-#pragma unroll
-        for (int kk = 0; kk < KW; ++kk) {
-            const int k = k0 + kk;
-            if (k >= p.k) break;
-            const int t0 = sps[(warp * KW + kk) * np1 + st];
-            const int t1 = sps[(warp * KW + kk) * np1 + st + 1];
-            for (int i = lane; i < t1 - t0; i += 32) cp_async<8>(tb + kk * p.segcap + i, p.taps + t0 + i);
+        if (grp < groups) {  // this warp's contiguous tap block of the stage
+            const int o0 = __ldg(p.blkoff + (size_t)grp * p.nst + st);
+            const int o1 = __ldg(p.blkoff + (size_t)grp * p.nst + st + 1);
+            const int4* src = reinterpret_cast<const int4*>(p.taps) + o0;
+            int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
+            const int nch = min(o1 - o0, p.segcap);
+            for (int i = lane; i < nch; i += 32) cp_async<16>(tb + i, src + i);
         }
     };
     // copy_0 = (0, x0 .. x_{H-2}), copy_2 = (x1 .. x_{H-1}, 0) from copy_1
@@ -136,14 +129,15 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
         // lane's image block, minus the stage's first channel (tap offsets are absolute)
         const char* xl = reinterpret_cast<const char*>(xs + (size_t)buf * p.stage_el + lane * p.ip) -
                          (size_t)st * p.cc * BLK * 4;
-        const DirectTap* tb = tsm + ((size_t)buf * p.wk + warp) * KW * p.segcap;
+        const int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
+        const int* cnt = reinterpret_cast<const int*>(tb);
+        const DirectTap* seg = reinterpret_cast<const DirectTap*>(tb + HDR);
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
             if (k >= p.k) break;
-            const int nt = sps[(warp * KW + kk) * np1 + st + 1] - sps[(warp * KW + kk) * np1 + st];
-            const DirectTap* seg = tb + kk * p.segcap;
-#pragma unroll 2
+            const int nt = cnt[kk];
+#pragma unroll 4
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
                 const float* xp = reinterpret_cast<const float*>(xl + tp.off);
@@ -155,6 +149,7 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
                     for (int x = 0; x < H; ++x) acc[kk][y * H + x] = mac1<MODE>(acc[kk][y * H + x], tp.v, vf[x]);
                 }
             }
+            seg += nt;
         }
         __syncthreads();
     }

@@ -564,11 +564,10 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const size_t stage_bytes = ((size_t)32 * ip * 4 + 127) & ~(size_t)127;
     d->stage_el = (int)(stage_bytes / 4);
     d->tap_cap = blk;
-    if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
-    const int segcap = L->sptr_maxseg[c.cc];
-    d->wp = segcap;
-    d->smem = nbuf * stage_bytes + (size_t)nbuf * c.warps_k * v.kt * segcap * sizeof(DirectTap) +
-              (size_t)c.warps_k * v.kt * ((g.c + c.cc - 1) / c.cc + 1) * 4;  // stage pointers
+    const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
+    if (cap < 0) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
+    d->wp = cap;
+    d->smem = nbuf * stage_bytes + (size_t)nbuf * c.warps_k * cap * 16;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     d->n_ey = 1;
     d->n_fx = 1;
@@ -958,7 +957,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
             for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * ve.info.th);
         else
             col = direct_cols(ve.info);
-        if (ve.info.kind == KIND_DIRECT) {
+        if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
             auto blk = L->direct_blocks(d.tap_cap, d.row, col, elem_bytes(ve.info), c.cc, ve.info.kt);
             q.taps = blk.taps;
             q.blkoff = blk.off;
