@@ -120,12 +120,12 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
     }
     for (int st = 0; st < p.nst; ++st) {
         const int buf = st % p.nbuf;
-        if (st + p.nbuf - 1 < p.nst) stage(st + p.nbuf - 1, (st + p.nbuf - 1) % p.nbuf);
-        cp_async_commit();  // possibly empty: keeps one group per iteration
-        cp_async_wait_nb(p.nbuf);
-        __syncthreads();
+        cp_async_wait_nb2(p.nbuf);
+        __syncthreads();  // stage st landed; every warp has left stage st-1
         shift(st, buf);
         __syncthreads();
+        if (st + p.nbuf - 1 < p.nst) stage(st + p.nbuf - 1, (st + p.nbuf - 1) % p.nbuf);
+        cp_async_commit();  // possibly empty: keeps one group per iteration
         // lane's image block, minus the stage's first channel (tap offsets are absolute)
         const char* xl = reinterpret_cast<const char*>(xs + (size_t)buf * p.stage_el + lane * p.ip) -
                          (size_t)st * p.cc * BLK * 4;
@@ -151,7 +151,6 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
             }
             seg += nt;
         }
-        __syncthreads();
     }
 
     // ---- epilogue: lane's image plane per output channel is contiguous

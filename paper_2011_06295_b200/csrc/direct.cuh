@@ -65,6 +65,12 @@ __device__ __forceinline__ void cp_async_wait_nb(int nbuf) {
     if (nbuf >= 3) cp_async_wait<2>();
     else cp_async_wait<1>();
 }
+// wait until at most NB-2 committed cp.async groups are pending (the stage
+// about to be consumed has landed; the next one may still be in flight)
+__device__ __forceinline__ void cp_async_wait_nb2(int nbuf) {
+    if (nbuf >= 3) cp_async_wait<1>();
+    else cp_async_wait<0>();
+}
 
 // Shared row geometry of a direct variant (host and device agree on it).
 template <int S, int PAD, int LW, int VX, int ES = 4>
@@ -216,14 +222,16 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     const int lane_off = lg * p.ip + lx;  // + tap off - c0*PLANE
     for (int st = 0; st < p.nst; ++st) {
         const int buf = st % p.nbuf;
-        if (st + p.nbuf - 1 < p.nst) stage(st + p.nbuf - 1, (st + p.nbuf - 1) % p.nbuf);
-        cp_async_commit();  // possibly empty: keeps one group per iteration
-        cp_async_wait_nb(p.nbuf);
+        // one barrier per stage: it publishes stage st AND proves every warp has left
+        // stage st-1, whose buffer the refill below then overwrites
+        cp_async_wait_nb2(p.nbuf);
         __syncthreads();
         if constexpr (VX == 2) {
             shift(st, buf);
             __syncthreads();
         }
+        if (st + p.nbuf - 1 < p.nst) stage(st + p.nbuf - 1, (st + p.nbuf - 1) % p.nbuf);
+        cp_async_commit();  // possibly empty: keeps one group per iteration
         const TIO* xl = xs + (size_t)buf * p.stage_el + lane_off - st * p.cc * PLANE;
         const int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
         const int* cnt = reinterpret_cast<const int*>(tb);
@@ -259,7 +267,6 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
             }
             seg += nt;
         }
-        __syncthreads();
     }
 
     // ---- epilogue: lane holds rows oy0..oy0+TH-1 of columns lx..lx+VX-1 of image n0+lg
