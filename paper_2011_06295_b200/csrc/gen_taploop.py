@@ -379,7 +379,8 @@ DIRECTS = [d + (2,) for d in DIRECTS] + \
           [(3, 3, 1, 8, lw, 4, 1, 3) for lw in (32, 16, 8)] + \
           [(3, 3, 1, 8, lw, 2, 1, 4) for lw in (32, 16, 8)] + \
           [(3, 3, 1, 8, lw, 2, 2, 3) for lw in (32, 16, 8)] + \
-          [(3, 3, 1, 16, lw, kw, 1, 2) for lw in (32, 16) for kw in (2, 4)]  # + min CTAs/SM (4: <= 64 regs)
+          [(3, 3, 1, 16, lw, kw, 1, 2) for lw in (32, 16) for kw in (2, 4)] + \
+          [(3, 3, 1, 4, 4, kw, 2, 2) for kw in (4, 8)]  # + min CTAs/SM (4: <= 64 regs)
 # f16-storage direct variants (FHFMA, column pairs): (R, S, PAD, TH, LW, KW)
 DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)]
 
