@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f16", action="store_true", help="skip the fp16 (config 4) secondary measurement")
+    ap.add_argument("--no-alexnet", action="store_true", help="skip the AlexNet-style (config 2) secondary line")
     return ap.parse_args()
 
 
@@ -330,6 +331,35 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
             "launches": [None if l is None else list(l) for l in net.launches]}
 
 
+def measure_alexnet(args, dev, local_rank, reps: int = 10):
+    """BASELINE config 2 (secondary): the AlexNet-style CIFAR-10 stack (5x5 and
+    3x3 convs) at 90 % unified sparsity, batch 128, exact fp32."""
+    import torch
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import alexnet_cifar
+    net = build_net(alexnet_cifar(args.sparsity), seed=0, device=local_rank)
+    batch = 128
+    net.plan(batch, tune=not args.no_tune)
+    x = torch.randn((batch, 3, 32, 32), device=dev)
+    for _ in range(3):
+        net.forward_device(x)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ts = []
+    for _ in range(reps):
+        ev[0].record()
+        net.forward_device(x)
+        ev[1].record()
+        ev[1].synchronize()
+        ts.append(ev[0].elapsed_time(ev[1]))
+    ms = statistics.median(ts)
+    macs = sum(batch * L.kernel.shape.k * L.kernel.shape.e * L.kernel.shape.f * L.kernel.sparse_level
+               for L in net.layers)
+    return {"images_per_s": round(batch / (ms * 1e-3), 1), "ms_per_step": round(ms, 4), "batch": batch,
+            "tflops": round(2 * macs / (ms * 1e-3) / 1e12, 3),
+            "launches": [None if l is None else list(l) for l in net.launches]}
+
+
 def load_traffic():
     """Per-layer DRAM traffic (dram__bytes_read.sum + write.sum) from the
     committed ncu --set full capture summary, if any."""
@@ -468,6 +498,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     }
     if not args.no_f16:
         line["f16"] = measure_f16(specs, args, dev, local_rank)
+    if not args.no_alexnet:
+        line["alexnet"] = measure_alexnet(args, dev, local_rank)
     if not args.no_dense:
         line["dense_cudnn"] = dense_cudnn(specs, [L.kernel for L in net.layers], [L.bias for L in net.layers],
                                           args.batch, dev)
