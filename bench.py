@@ -412,18 +412,29 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.barrier()
     torch.cuda.synchronize()
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
+    # timed steps: events only around each step, so consecutive layer kernels keep their
+    # programmatic-dependent-launch overlap (an event between kernels would serialise them)
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with Clocks(local_rank) as clk:
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
-            step(ev[k])
+            sev[k][0].record(stream)
+            step()
+            sev[k][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms = [ev[k][0].elapsed_time(ev[k][nl]) for k in range(args.steps)]
-    layer_ms = [[ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(args.steps)] for i in range(nl)]
+    step_ms = [a.elapsed_time(b) for a, b in sev]
     total_s = sum(step_ms) * 1e-3
+    # per-layer breakdown: separate (untimed for `value`) steps with events between layers
+    nlay = max(5, args.steps // 5)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(nlay)]
+    for k in range(nlay):
+        flush.zero_()
+        step(ev[k])
+    torch.cuda.synchronize()
+    layer_ms = [[ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(nlay)] for i in range(nl)]
 
     # e2e: the host-facing call, H2D + 13 kernels + D2H every step
     out_host = torch.empty(net.out_shape(nl - 1, args.batch), dtype=torch.float32, pin_memory=True)

@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
         for (int j = 0; j < HW; ++j) acc[kk][j] = b;
     }
 
+    // programmatic dependent launch: everything above overlapped the previous layer's tail;
+    // its output (our input) is visible after this wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int s0 = 0; s0 < p.nbuf - 1; ++s0) {  // prologue: nbuf-1 stages in flight
         if (s0 < p.nst) stage(s0, s0);
         cp_async_commit();
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
         }
     }
 
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next layer may start its prologue
     // ---- epilogue: lane's image plane per output channel is contiguous
     const int n = n0 + lane;
     if (n >= p.n) return;
@@ -196,8 +200,7 @@ cudaError_t launch_dimg_t(const DirectParams& p, unsigned grid, unsigned threads
         max_dyn = lim;
     }
     if ((int)smem > max_dyn) return cudaErrorInvalidValue;
-    kern<<<grid, threads, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(kern, p, grid, threads, smem, st);
 }
 
 }  // namespace scb

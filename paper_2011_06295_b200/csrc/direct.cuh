@@ -72,6 +72,25 @@ __device__ __forceinline__ void cp_async_wait_nb2(int nbuf) {
     else cp_async_wait<0>();
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel's prologue
+// (shared-memory zeroing, descriptors) overlaps the previous kernel's tail and
+// `griddepcontrol.wait` orders the first read of its input.
+template <typename K, typename P>
+cudaError_t launch_pdl(K kern, const P& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // Shared row geometry of a direct variant (host and device agree on it).
 template <int S, int PAD, int LW, int VX, int ES = 4>
 struct DirectRow {
@@ -215,6 +234,9 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
         for (int j = 0; j < TH * VX; ++j) acc[kk][j] = b;
     }
 
+    // programmatic dependent launch: everything above overlapped the previous layer's tail;
+    // its output (our input) is visible after this wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int s0 = 0; s0 < p.nbuf - 1; ++s0) {  // prologue: nbuf-1 stages in flight
         if (s0 < p.nst) stage(s0, s0);
         cp_async_commit();
@@ -269,6 +291,7 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
         }
     }
 
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next layer may start its prologue
     // ---- epilogue: lane holds rows oy0..oy0+TH-1 of columns lx..lx+VX-1 of image n0+lg
     const int n = n0 + lg;
     const bool relu = p.flags & SCB_FLAG_RELU;
@@ -331,8 +354,7 @@ cudaError_t launch_direct_t(const DirectParams& p, unsigned grid, unsigned threa
         max_dyn = lim;
     }
     if ((int)smem > max_dyn) return cudaErrorInvalidValue;
-    kern<<<grid, threads, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(kern, p, grid, threads, smem, st);
 }
 
 }  // namespace scb
