@@ -281,6 +281,55 @@ class SparseConvNet:
             torch.cuda.current_stream(self.device).synchronize()
         return out_host if isinstance(x_host, torch.Tensor) else out_host.numpy()
 
+    def forward_stream(self, x_hosts, out_hosts) -> None:
+        """Streaming inference over many pinned host batches: the H2D copy of
+        batch i+1 and the D2H copy of batch i-1 run on a copy stream while the
+        stack computes batch i (two device input buffers).  Synchronous on return;
+        every batch's copies and compute happen inside the call."""
+        torch = self.torch
+        if len(x_hosts) != len(out_hosts):
+            raise ShapeError("one output buffer per input batch")
+        with torch.cuda.device(self.device):
+            comp = torch.cuda.current_stream(self.device)
+            copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream(self.device)
+            self._copy_stream = copy
+            if getattr(self, "_x2", None) is None or self._x2.shape != self.x_in.shape:
+                self._x2 = torch.empty_like(self.x_in)
+            bufs = (self.x_in, self._x2)
+            loaded = [torch.cuda.Event() for _ in x_hosts]
+            done = [torch.cuda.Event() for _ in x_hosts]
+            freed = [torch.cuda.Event() for _ in x_hosts]
+            with torch.cuda.stream(copy):
+                bufs[0].copy_(x_hosts[0], non_blocking=True)
+                loaded[0].record(copy)
+            for i in range(len(x_hosts)):
+                xb = bufs[i % 2]
+                if i + 1 < len(x_hosts):
+                    with torch.cuda.stream(copy):
+                        if i >= 1:
+                            copy.wait_event(freed[i - 1])  # batch i-1 no longer reads that buffer
+                        bufs[(i + 1) % 2].copy_(x_hosts[i + 1], non_blocking=True)
+                        loaded[i + 1].record(copy)
+                comp.wait_event(loaded[i])
+                s = comp.cuda_stream
+                cur = xb
+                for li in range(len(self.layers)):
+                    if self.algorithms[li] == "dense-cudnn":
+                        self.dense_layer(li)(cur, self.acts[li])
+                    else:
+                        self.launch_layer(li, cur, self.acts[li], s)
+                    if li == 0:
+                        freed[i].record(comp)
+                    cur = self.acts[li]
+                done[i].record(comp)
+                with torch.cuda.stream(copy):
+                    copy.wait_event(done[i])
+                    out_hosts[i].copy_(cur, non_blocking=True)
+                # the next batch overwrites the activations only after this D2H read them
+                comp.wait_stream(copy)
+            copy.synchronize()
+            comp.synchronize()
+
 
 def build_net(specs_pools, seed: int = 0, dtype=np.float32, device: int = 0,
               weight_format: str = "native", fast_math: bool = False):

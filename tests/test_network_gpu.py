@@ -125,3 +125,17 @@ def test_configure_network_and_apply(torch, vgg_small):
     assert np.linalg.norm(out.astype(np.float64) - ref) <= 1e-4 * np.linalg.norm(ref.astype(np.float64))
     net.apply_config(sc.NetworkConfig(batch=3, choices={}))
     assert np.array_equal(_bits(net.forward(x)), _bits(ref))
+
+
+def test_forward_stream_bitwise(torch, vgg_small):
+    """Streaming host->device->host inference (copies overlapped) equals the
+    oracle for every batch."""
+    net, x, ref = vgg_small
+    net.plan(3, tune=False)
+    x2 = np.random.default_rng(9).standard_normal(x.shape).astype(np.float32)
+    ref2 = oracle_stack(net, x2)
+    xs = [torch.from_numpy(a).pin_memory() for a in (x, x2, x, x2, x)]
+    outs = [torch.empty((3, 512, 1, 1)).pin_memory() for _ in xs]
+    net.forward_stream(xs, outs)
+    for i, o in enumerate(outs):
+        assert np.array_equal(_bits(o.numpy()), _bits(ref if i % 2 == 0 else ref2)), i
