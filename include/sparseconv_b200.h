@@ -90,7 +90,9 @@ typedef struct {
                             (dispatch-free: th rows x tw columns per lane group, kt = output
                             channels per warp); 3 image-lane direct (lane = image, whole
                             th x tw plane, shifted-copy vector loads); 4 warp-specialised
-                            direct (producer warp + mbarrier ring, bulk copies) */
+                            direct (producer warp + mbarrier ring, bulk copies); 5 direct with
+                            tensor-memory operands (tcgen05.ld of a lane's tap inputs; nbt =
+                            warps per TMEM lane quarter) */
 } scb_variant_info;
 
 /* ---------------------------------------------------------------------- */

@@ -362,7 +362,9 @@ PLANES = [
     (4, 4, 3, 3, 1, 2, 1, 3), (2, 2, 3, 3, 1, 2, 2, 3), (2, 2, 3, 3, 1, 2, 4, 3),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
-KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS = 0, 1, 2, 3, 4
+KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS, KIND_DTM = 0, 1, 2, 3, 4, 5
+# TMEM-operand direct variants (tm.cuh): (TH, LW, KW, M warps per lane quarter)
+DTMS = [(8, lw, kw, m) for lw in (32, 16, 8) for kw in (4, 8) for m in (2, 4)] + [(4, 4, kw, m) for kw in (4, 8) for m in (2, 4)]
 # warp-specialised direct variants (ws.cuh): (R, S, PAD, TH, LW, KW)
 DWS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)]
 # image-lane direct variants (dimg.cuh): (H, KW)
@@ -416,6 +418,8 @@ def main():
     for R, S, PAD, TH, LW, KW, VX, MB in DIRECTS:
         groups[("direct", R, S, PAD, TH, LW, KW, VX, MB)] = (
             [], [("direct", R, S, PAD, TH, LW, KW, VX, MB, mode) for mode in (EXACT, FMA)])
+    for TH, LW, KW, M in DTMS:
+        groups[("dtm", TH, LW, KW, M)] = ([], [("dtm", TH, LW, KW, M, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DWS:
         groups[("dws", R, S, PAD, TH, LW, KW)] = ([], [("dws", R, S, PAD, TH, LW, KW, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DIRECTS_F16:
@@ -431,7 +435,7 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n#include \"tm.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
@@ -442,6 +446,11 @@ def main():
                 R, S, PAD, KT, NBT, TH, TW, wf, mode, d, f16 = key
                 src.append((gen_jump if d == JUMP else gen_mask)(R, S, PAD, KT, NBT, TH, TW, wf, mode, f16))
             for v in variants:
+                if v[0] == "dtm":
+                    _, TH, LW, KW, M, mode = v
+                    ents.append(f"    {{{{3, 3, {KW}, {M}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
+                                f"{KIND_DTM}}}, nullptr, &launch_dtm_t<3, 3, 1, {TH}, {LW}, {KW}, {M}, {mode}>}},\n")
+                    continue
                 if v[0] == "dws":
                     _, R, S, PAD, TH, LW, KW, mode = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "

@@ -23,7 +23,7 @@ namespace {
 constexpr int kSmemLimit = 227 * 1024 - 1024;  // dynamic limit: 227 KB minus the kernels' static shared memory
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
-constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4;
+constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4, KIND_DTM = 5;
 
 scb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -425,6 +425,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
         return true;
     }
+    if (v.kind == KIND_DTM) {
+        if (g.f != v.tw || (g.w * 4) % 16 != 0 || g.w > 32 || g.r != 3 || g.s != 3 || g.pad != 1) return false;
+        if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
+        return true;
+    }
     if (v.kind == KIND_DIRECT || v.kind == KIND_DWS) {
         if (g.f != v.tw || (g.w * elem_bytes(v)) % 16 != 0 || g.w > 32) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
@@ -579,6 +584,41 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     return SCB_OK;
 }
 
+// TMEM-operand direct variants (tm.cuh): 4 lane quarters x nbt warps, 8 channels per stage.
+scb_status derive_dtm(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const int M = v.nbt, G = 4 * (32 / v.tw), CC = 8;
+    if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc != CC || c.warps_k != M)
+        return fail(SCB_ERR_SHAPE, "tmem launch: imgs = 4*32/tw, bh = th, bw = tw, cc = 8, warps_k = nbt");
+    d->threads = 128 * M;
+    scb_variant_info v1 = v;
+    v1.nbt = 1;                // nbt means warps per quarter here; the window rows are direct.cuh VX = 1 rows
+    d->row = direct_row(v1);
+    const int plane = (v.th + v.r - 1) * d->row;
+    int ip = (CC * plane + 3) / 4 * 4;
+    if (32 / v.tw > 1)
+        while (ip % 32 != v.tw % 32) ip += 4;
+    d->chunk = ip;
+    const size_t stage_bytes = ((size_t)G * ip * 4 + 16 + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / 4);
+    d->tap_cap = 32;  // TMEM columns per channel slot
+    const int cap = L->block_cap(CC, v.kt);
+    if (cap < 0) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
+    d->wp = cap;
+    const int rows = G * CC * (v.th + v.r - 1);
+    d->smem = 2 * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) + (size_t)2 * M * cap * 16;
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    d->n_ey = (g.e + v.th - 1) / v.th;
+    d->n_fx = 1;
+    d->kblocks = (g.k + M * v.kt - 1) / (M * v.kt);
+    d->nb = (n + G - 1) / G;
+    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
 // Warp-specialised direct variants (ws.cuh): warps_k consumer warps + 1 producer warp.
 scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     const scb_variant_info& v = variant(c.variant).info;
@@ -625,6 +665,7 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     if (v.kind == KIND_DIRECT) return derive_direct(L, c, n, flags, d);
     if (v.kind == KIND_DIMG) return derive_dimg(L, c, n, flags, d);
     if (v.kind == KIND_DWS) return derive_dws(L, c, n, flags, d);
+    if (v.kind == KIND_DTM) return derive_dtm(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -673,6 +714,12 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_DTM) {
+            scb_launch c{vi, v.nbt, 4 * (32 / v.tw), v.th, v.tw, 8, 2};
+            Derived d;
+            if (derive(L, c, n, flags, &d) == SCB_OK) out.push_back(c);
+            continue;
+        }
         if (v.kind == KIND_DWS) {
             for (int wk : {2, 4, 8})
                 for (int cc : {4, 8, 16, 32})
@@ -957,7 +1004,15 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
             for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * ve.info.th);
         else
             col = direct_cols(ve.info);
-        if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
+        if (ve.info.kind == KIND_DTM) {  // tap offsets in TMEM columns: slot(c) + s*RT + r
+            col.clear();
+            for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * (ve.info.th + g.r - 1));
+            auto blk = L->direct_blocks(32, 1, col, 1, c.cc, ve.info.kt);
+            q.taps = blk.taps;
+            q.blkoff = blk.off;
+            q.sptr = L->stage_ptr(c.cc);
+            if (!q.taps || !q.blkoff) return fail(SCB_ERR_CUDA, "tmem tap blocks: device allocation failed");
+        } else if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
             auto blk = L->direct_blocks(d.tap_cap, d.row, col, elem_bytes(ve.info), c.cc, ve.info.kt);
             q.taps = blk.taps;
             q.blkoff = blk.off;

@@ -36,9 +36,9 @@ def test_variant_table():
     for v in vs:
         assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (1, 2, 4, 8)
         assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["dispatch"] in (0, 1)
-        assert v["kind"] in (0, 1, 2, 3, 4) and v["io"] in (0, 2)
+        assert v["kind"] in (0, 1, 2, 3, 4, 5) and v["io"] in (0, 2)
         kinds.add(v["kind"])
-    assert kinds == {0, 1, 2, 3, 4}  # tiled, whole-plane, direct, image-lane direct, warp-specialised
+    assert kinds == {0, 1, 2, 3, 4, 5}  # tiled, plane, direct, image-lane, warp-specialised, TMEM
 
 
 def test_sm100a_cubin_only():
@@ -60,7 +60,8 @@ def test_exact_kernels_never_fuse():
         m = re.match(r"_ZN3scb7k_tiledILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi(\d)ELi0ELi\dELi\dEE", name)
         g = re.match(r"_ZN3scb9k_genericI([fd])Li0EE", name)
         d = re.match(r"_ZN3scb8k_directILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi0ELi\d+ELi\d+ELb0EE", name) or \
-            re.match(r"_ZN3scb5k_dwsILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi0EE", name)
+            re.match(r"_ZN3scb5k_dwsILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi0EE", name) or \
+            re.match(r"_ZN3scb5k_dtmILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi0EE", name)
         i = re.match(r"_ZN3scb6k_dimgILi\d+ELi\d+ELi0EE", name)
         pl = re.match(r"_ZN3scb7k_planeILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi0ELi0ELi\dEE", name)
         if not (m or g or d or i or pl):

@@ -412,11 +412,13 @@ def test_direct_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     assert cands, "no direct variant"
     ws = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 4]
     assert ws or hw < 8, "no warp-specialised variant"
-    for cfg in cands[:: max(1, len(cands) // 30)] + ws[:: max(1, len(ws) // 20)]:
+    tm = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 5]
+    assert tm or hw not in (32, 16, 8, 4), "no TMEM-operand variant"
+    for cfg in cands[:: max(1, len(cands) // 30)] + ws[:: max(1, len(ws) // 20)] + tm:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
     want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref)), 2).numpy()
-    pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] in (2, 4)]
+    pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] in (2, 4, 5)]
     for cfg in pc[:: max(1, len(pc) // 8)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
         assert beq(o, want), cfg
