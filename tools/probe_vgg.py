@@ -1,5 +1,5 @@
 import sys, time, json
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.join(__import__('os').path.dirname(__file__), '..'))
 import numpy as np, torch, ctypes
 import paper_2011_06295_b200 as sc
 from paper_2011_06295_b200 import _abi
