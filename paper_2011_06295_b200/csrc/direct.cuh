@@ -302,21 +302,23 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
         if (k >= p.k) break;
         if (!pool) {
             if (n < p.n && lx < p.f) {
-                TIO* yp = static_cast<TIO*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * p.f + lx;
+                // F == LW for every direct variant (derive), so row offsets are immediates
+                TIO* yp = static_cast<TIO*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * LW + lx;
+                const int jmax = min(TH, p.e - oy0);
 #pragma unroll
                 for (int j = 0; j < TH; ++j) {
-                    if (oy0 + j >= p.e) break;
+                    if (j >= jmax) break;
                     float o0 = acc[kk][j * VX];
                     if (relu && o0 < 0.f) o0 = 0.f;
                     if constexpr (VX == 1) {
-                        yp[(int64_t)j * p.f] = o0;
+                        yp[j * LW] = o0;
                     } else {
                         float o1 = acc[kk][j * VX + 1];
                         if (relu && o1 < 0.f) o1 = 0.f;
                         if constexpr (F16IO)
-                            *reinterpret_cast<__half2*>(yp + (int64_t)j * p.f) = __floats2half2_rn(o0, o1);
+                            *reinterpret_cast<__half2*>(yp + j * LW) = __floats2half2_rn(o0, o1);
                         else
-                            *reinterpret_cast<float2*>(yp + (int64_t)j * p.f) = make_float2(o0, o1);
+                            *reinterpret_cast<float2*>(yp + j * LW) = make_float2(o0, o1);
                     }
                 }
             }
