@@ -83,7 +83,9 @@ typedef struct {
     int32_t io;          /* scb_dtype of activations */
     int32_t wf;          /* payload: 0 f32, 1 f16, 2 codebook-4bit, 3 int16 fixed-point */
     int32_t mode;        /* 0 exact mul+add, 1 fma */
-    int32_t dispatch;    /* tap dispatch: 0 brx.idx jump table, 1 per-channel mask walk */
+    int32_t dispatch;    /* tap dispatch: 0 brx.idx jump table, 1 per-channel mask walk;
+                            direct kind: 2 = column tiles of tw for any output row width,
+                            3 = 1D rows (H = R = 1) in tiles of th*tw columns */
     int32_t pad;         /* padding the variant is specialised for */
     int32_t kind;        /* 0 tiled (output blocks, halo patches); 1 whole plane (th x tw = the
                             input plane a lane holds; small spatial extents); 2 direct

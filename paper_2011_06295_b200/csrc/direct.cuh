@@ -56,6 +56,7 @@ struct DirectParams {
     int kblocks, n_ey, nb;
     int segcap;               // taps per (output channel, stage) segment slot in shared memory
     int nbuf;                 // stage buffers in flight (2 or 3)
+    int nfx;                  // k_direct WIDE: column tiles of LW per output row
     const int32_t* blkoff;    // k_direct: [group*nst + st] 16-byte-chunk offset of each tap block (+ end)
     uint32_t flags;
 };
@@ -92,15 +93,17 @@ cudaError_t launch_pdl(K kern, const P& p, unsigned grid, unsigned threads, size
 }
 
 // Shared row geometry of a direct variant (host and device agree on it).
-template <int S, int PAD, int LW, int VX, int ES = 4>
+template <int S, int PAD, int LW, int VX, int ES = 4, bool WIDE = false>
 struct DirectRow {
     static constexpr int Q16 = 16 / ES;  // elements per 16 bytes
     static constexpr int XO = Q16;       // shared column of input column 0 (16-byte aligned)
     // one copy of a row: left padding (XO >= the right halo), LW columns, rounded to 16 bytes.
     // VX = 1: the right halo reads the NEXT row's never-written left padding (zero), so
     // no right-halo columns are stored (the host leaves 16 zero bytes after each stage).
-    static constexpr int QW = VX == 1 ? ((XO + LW) + Q16 - 1) / Q16 * Q16
-                                      : ((XO + LW + S) + Q16 - 1) / Q16 * Q16;
+    // WIDE (column tiles of a wider row): the row also holds a real right halo.
+    static constexpr int QW = WIDE ? XO + LW + Q16
+                                   : (VX == 1 ? ((XO + LW) + Q16 - 1) / Q16 * Q16
+                                              : ((XO + LW + S) + Q16 - 1) / Q16 * Q16);
     static_assert(XO >= S - 1 - PAD, "right halo must fit in the next row's left padding");
     static constexpr int ROW = VX * QW;
     // shared column (relative to the lane's first output column) of tap column s
@@ -119,15 +122,24 @@ __device__ __forceinline__ float fhfma(float acc, unsigned short v, unsigned sho
 
 // LW: output columns per lane group (= F when F <= 32), TH: output rows per
 // lane, VX: adjacent output columns per lane (1 or 2; f16 storage needs 2).
-template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false>
+// WIDE: output rows wider than LW are cut into column tiles (grid dimension
+// nfx); each staged row then carries its real left/right halo columns.
+// ONED (1D convolution, H = R = 1): a lane's TH outputs are columns lx + j*LW of
+// one tile of TH*LW columns, staged as one contiguous row per (image, channel).
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false,
+          bool WIDE = false, bool ONED = false>
 __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ DirectParams p) {
     static_assert(!F16IO || VX == 2, "f16 storage reads column pairs");
+    static_assert(!WIDE || (VX == 1 && !F16IO), "wide tiles: f32, one column per lane");
+    static_assert(!ONED || (WIDE && R == 1), "1D tiles are wide tiles of one input row");
     using TIO = typename std::conditional<F16IO, __half, float>::type;
     constexpr int ES = (int)sizeof(TIO);
-    using RG = DirectRow<S, PAD, LW, VX, ES>;
+    using RG = DirectRow<S, PAD, LW, VX, ES, WIDE>;
     constexpr int XO = RG::XO, QW = RG::QW, ROW = RG::ROW;
-    constexpr int RT = TH + R - 1;
-    constexpr int PLANE = RT * ROW;
+    constexpr int RT = ONED ? 1 : TH + R - 1;                        // staged rows per channel
+    constexpr int PLANE = ONED ? XO + TH * LW + RG::Q16 : RT * ROW;  // elements per channel
+    constexpr int JS = ONED ? LW : ROW;                              // smem stride of a lane's outputs
+    constexpr int TC = ONED ? TH * LW : LW;                          // output columns per CTA tile
     constexpr int LPI = LW / VX;   // lanes per image row
     constexpr int G = 32 / LPI;    // images per CTA
     extern __shared__ __align__(128) unsigned char smem[];
@@ -139,8 +151,10 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     const int kb = bid % p.kblocks;
     bid /= p.kblocks;
     const int ey = bid % p.n_ey;
-    const int nbk = bid / p.n_ey;
-    const int n0 = nbk * G, oy0 = ey * TH;
+    bid /= p.n_ey;
+    const int fx = WIDE ? bid % p.nfx : 0;
+    const int nbk = WIDE ? bid / p.nfx : bid;
+    const int n0 = nbk * G, oy0 = ONED ? 0 : ey * TH, ox0 = fx * TC;
     const int k0 = (kb * p.wk + warp) * KW;
     const int C = p.c;
     TIO* xs = reinterpret_cast<TIO*>(smem);
@@ -161,7 +175,8 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
         const int gy = oy0 - PAD + yy;
         const bool ok = n0 + g < p.n && (unsigned)gy < (unsigned)p.h;
         rdesc[rr] = make_uint2((unsigned)((g * C + cl) * hw + gy * p.w),
-                               (unsigned)(g * p.ip + cl * PLANE + yy * ROW + XO) | ((unsigned)(ok ? cl : 255) << 24));
+                               (unsigned)(g * p.ip + cl * PLANE + yy * ROW + (WIDE ? 0 : XO)) |
+                                   ((unsigned)(ok ? cl : 255) << 24));
     }
     __syncthreads();
 
@@ -173,9 +188,14 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     const int grp = kb * p.wk + warp;        // this warp's channel group
     const int groups = (p.k + KW - 1) / KW;
 
-    const TIO* xg = static_cast<const TIO*>(p.x) + (size_t)n0 * C * hw;
     constexpr int Q16 = 16 / ES;
-    const int nchunk = p.w / Q16;  // 16-byte chunks per input row (derive() requires it exact)
+    // WIDE: a staged row is global columns ox0-XO .. ox0+ROW-XO-1, elements e_lo..e_hi of it
+    // (in copies of ce elements: 16, 8 or 4 bytes as the row width's alignment allows)
+    const TIO* xg = static_cast<const TIO*>(p.x) + (size_t)n0 * C * hw + (WIDE ? ox0 - XO : 0);
+    const int e_lo = WIDE ? (ox0 == 0 ? XO : 0) : 0;
+    const int e_hi = WIDE ? min(ONED ? PLANE : ROW, p.w - (ox0 - XO)) : 0;
+    const int ce = (p.w % Q16 == 0) ? Q16 : (p.w % 2 == 0 ? 2 : 1);
+    const int nchunk = p.w / Q16;  // narrow: 16-byte chunks per input row (derive() requires it exact)
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;
         const unsigned ncl = (unsigned)min(p.cc, C - c0);
@@ -186,7 +206,16 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
             if ((rd.y >> 24) < ncl) {
                 const TIO* s = src + rd.x;
                 TIO* d = dst + (rd.y & 0xffffffu);
-                for (int q = 0; q < nchunk; ++q) cp_async<16>(d + Q16 * q, s + Q16 * q);
+                if constexpr (WIDE) {
+                    if (ce == Q16)
+                        for (int q = e_lo; q < e_hi; q += Q16) cp_async<16>(d + q, s + q);
+                    else if (ce == 2)
+                        for (int q = e_lo; q < e_hi; q += 2) cp_async<8>(d + q, s + q);
+                    else
+                        for (int q = e_lo; q < e_hi; ++q) cp_async<4>(d + q, s + q);
+                } else {
+                    for (int q = 0; q < nchunk; ++q) cp_async<16>(d + Q16 * q, s + Q16 * q);
+                }
             }
         }
         // this warp's contiguous tap block of the stage: 16-byte chunks, one per lane
@@ -277,7 +306,7 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
                     }
                 } else if constexpr (VX == 1) {
 #pragma unroll
-                    for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * ROW]);
+                    for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * JS]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < TH; ++j) {
@@ -300,10 +329,22 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
         if (k >= p.k) break;
-        if (!pool) {
-            if (n < p.n && lx < p.f) {
-                // F == LW for every direct variant (derive), so row offsets are immediates
-                TIO* yp = static_cast<TIO*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * LW + lx;
+        if constexpr (ONED) {  // E = 1: outputs (n, k, 0, ox0 + lx + j*LW)
+            if (n < p.n) {
+                TIO* yp = static_cast<TIO*>(p.y) + ((int64_t)n * p.k + k) * p.f + ox0 + lx;
+#pragma unroll
+                for (int j = 0; j < TH; ++j) {
+                    float o0 = acc[kk][j];
+                    if (relu && o0 < 0.f) o0 = 0.f;
+                    if (ox0 + lx + j * LW < p.f) yp[j * LW] = o0;
+                }
+            }
+        } else if (!pool) {
+            if (n < p.n && ox0 + lx < p.f) {
+                // narrow variants have F == LW (derive), so row offsets are immediates
+                constexpr int FP = WIDE ? 1 : LW;
+                const int fpitch = WIDE ? p.f : 1;
+                TIO* yp = static_cast<TIO*>(p.y) + (((int64_t)n * p.k + k) * p.e + oy0) * (WIDE ? p.f : LW) + ox0 + lx;
                 const int jmax = min(TH, p.e - oy0);
 #pragma unroll
                 for (int j = 0; j < TH; ++j) {
@@ -311,7 +352,7 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
                     float o0 = acc[kk][j * VX];
                     if (relu && o0 < 0.f) o0 = 0.f;
                     if constexpr (VX == 1) {
-                        yp[j * LW] = o0;
+                        yp[j * FP * fpitch] = o0;
                     } else {
                         float o1 = acc[kk][j * VX + 1];
                         if (relu && o1 < 0.f) o1 = 0.f;
@@ -335,16 +376,17 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
                 }
                 if (relu && o < 0.f) o = 0.f;
                 const int py = (oy0 + j) >> 1;
-                if (n < p.n && !(lx & 1) && lx < p.f && py < pe)
-                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + (lx >> 1)] = (TIO)o;
+                if (n < p.n && !(lx & 1) && ox0 + lx < p.f && py < pe)
+                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] = (TIO)o;
             }
         }
     }
 }
 
-template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false>
+template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false,
+          bool WIDE = false, bool ONED = false>
 cudaError_t launch_direct_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX, MINB, F16IO>;
+    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX, MINB, F16IO, WIDE, ONED>;
     static int max_dyn = -1;  // benign race: idempotent
     if (max_dyn < 0) {
         cudaFuncAttributes fa;

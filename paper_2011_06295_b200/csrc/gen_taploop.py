@@ -383,6 +383,14 @@ DIRECTS = [d + (2,) for d in DIRECTS] + \
           [(3, 3, 1, 8, lw, 2, 2, 3) for lw in (32, 16, 8)] + \
           [(3, 3, 1, 16, lw, kw, 1, 2) for lw in (32, 16) for kw in (2, 4)] + \
           [(3, 3, 1, 4, 4, kw, 2, 2) for kw in (4, 8)]  # + min CTAs/SM (4: <= 64 regs)
+# wide direct variants (column tiles of 32 for output rows wider than 32, e.g. the
+# ImageNet shapes; also rows whose width is no tile width, 28/14/7): (R, S, PAD, TH, LW, KW, min CTAs/SM)
+DIRECTS_WIDE = [(3, 3, 1, th, lw, kw, 2) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
+               [(3, 3, 1, 16, 32, 4, 2), (3, 3, 1, 8, 32, 2, 4), (5, 5, 2, 4, 32, 4, 2), (5, 5, 2, 4, 16, 4, 2)] + \
+               [(1, 1, 0, 8, lw, kw, 2) for lw in (32, 16, 8) for kw in (4, 8)] + [(1, 1, 0, 16, 32, 4, 2)]
+WIDE, ONED = 2, 3                                # kernels.cuh DISPATCH_WIDE / DISPATCH_ONED
+# 1D direct variants (H = R = 1, e.g. the reference's cnn-non-static presets): (S, TH, KW)
+DIRECTS_1D = [(s, th, kw) for s in (2, 3, 4, 5) for th in (4, 8) for kw in (4, 8)]
 # f16-storage direct variants (FHFMA, column pairs): (R, S, PAD, TH, LW, KW)
 DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)]
 
@@ -418,6 +426,11 @@ def main():
     for R, S, PAD, TH, LW, KW, VX, MB in DIRECTS:
         groups[("direct", R, S, PAD, TH, LW, KW, VX, MB)] = (
             [], [("direct", R, S, PAD, TH, LW, KW, VX, MB, mode) for mode in (EXACT, FMA)])
+    for R, S, PAD, TH, LW, KW, MB in DIRECTS_WIDE:
+        groups[("wide", R, S, PAD, TH, LW, KW, MB)] = (
+            [], [("wide", R, S, PAD, TH, LW, KW, MB, mode) for mode in (EXACT, FMA)])
+    for S, TH, KW in DIRECTS_1D:
+        groups[("oned", S, TH, KW)] = ([], [("oned", S, TH, KW, mode) for mode in (EXACT, FMA)])
     for TH, LW, KW, M in DTMS:
         groups[("dtm", TH, LW, KW, M)] = ([], [("dtm", TH, LW, KW, M, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DWS:
@@ -466,6 +479,18 @@ def main():
                     _, H, KW, mode = v
                     ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
                                 f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {mode}>}},\n")
+                    continue
+                if v[0] == "oned":
+                    _, S, TH, KW, mode = v
+                    ents.append(f"    {{{{1, {S}, {KW}, 1, {TH}, 32, SCB_F32, {WF_F32}, {mode}, {ONED}, 0, "
+                                f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<1, {S}, 0, {TH}, 32, {KW}, "
+                                f"{mode}, 1, 2, false, true, true>}},\n")
+                    continue
+                if v[0] == "wide":
+                    _, R, S, PAD, TH, LW, KW, MB, mode = v
+                    ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {WIDE}, {PAD}, "
+                                f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
+                                f"{mode}, 1, {MB}, false, true>}},\n")
                     continue
                 if v[0] == "direct":
                     _, R, S, PAD, TH, LW, KW, VX, MB, mode = v

@@ -18,7 +18,9 @@ enum { MODE_EXACT = 0, MODE_FMA = 1 };
 enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3 };
 // how the tiled kernel dispatches a tap to its unrolled MAC block (gen_taploop.py)
 enum { DISPATCH_JUMP = 0,   // brx.idx jump table, one indirect branch per tap
-       DISPATCH_MASK = 1 }; // per-channel KT x 16-bit masks walked in order
+       DISPATCH_MASK = 1,   // per-channel KT x 16-bit masks walked in order
+       DISPATCH_WIDE = 2,   // (direct kind) column tiles of tw for any row width
+       DISPATCH_ONED = 3 }; // (direct kind) 1D rows: tiles of th*tw columns, H = R = 1
 
 template <int MODE>
 __device__ __forceinline__ float mac1(float acc, float v, float x) {

@@ -430,6 +430,13 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
         return true;
     }
+    if (v.kind == KIND_DIRECT && v.dispatch == DISPATCH_ONED)  // 1D rows
+        return g.h == 1 && g.e == 1 && !(flags & SCB_FLAG_POOL2);
+    if (v.kind == KIND_DIRECT && v.dispatch == DISPATCH_WIDE) {  // column tiles: any row width
+        if (v.tw > 8 && g.f <= v.tw / 2) return false;          // a narrower tile fits better
+        if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
+        return true;
+    }
     if (v.kind == KIND_DIRECT || v.kind == KIND_DWS) {
         if (g.f != v.tw || (g.w * elem_bytes(v)) % 16 != 0 || g.w > 32) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
@@ -499,6 +506,7 @@ int direct_qw(const scb_variant_info& v) {
     const int q = v.io == SCB_F16 ? 8 : 4;  // elements per 16 bytes (= XO)
     const int right = v.s - 1 - v.pad > 0 ? v.s - 1 - v.pad : 0;
     (void)right;  // VX = 1 rows alias the right halo onto the next row's left padding
+    if (v.kind == KIND_DIRECT && v.dispatch == DISPATCH_WIDE) return q + v.tw + q;  // real right halo
     return v.nbt == 1 ? (q + v.tw + q - 1) / q * q : (q + v.tw + v.s + q - 1) / q * q;
 }
 int direct_row(const scb_variant_info& v) { return v.nbt * direct_qw(v); }
@@ -523,8 +531,9 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     if (nbuf < 2 || nbuf > 3) return fail(SCB_ERR_SHAPE, "direct launch: stages must be 2 or 3");
     d->threads = 32 * c.warps_k;
     d->row = direct_row(v);
-    const int plane = (v.th + v.r - 1) * d->row;
+    const bool oned = v.dispatch == DISPATCH_ONED;
     const int es = elem_bytes(v), q16 = 16 / es;
+    const int plane = oned ? q16 + v.th * v.tw + q16 : (v.th + v.r - 1) * d->row;  // = direct.cuh PLANE
     int ip = (c.cc * plane + q16 - 1) / q16 * q16;
     if (G > 1)  // word pitch of an image = its row width in words (mod 32): conflict-free lanes
         while ((ip * es / 4) % 32 != (v.tw * es / 4) % 32) ip += q16;
@@ -532,7 +541,7 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     const size_t stage_bytes = ((size_t)G * ip * es + 16 + 127) & ~(size_t)127;  // +16: zero tail
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
-    const int rows = G * c.cc * (v.th + v.r - 1);
+    const int rows = G * c.cc * (oned ? 1 : v.th + v.r - 1);
     const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
     if (cap < 0) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
     d->wp = cap;  // tap block slot (16-byte units) travels in `wp`
@@ -540,11 +549,12 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
               (size_t)nbuf * c.warps_k * cap * 16;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     if (2 * stage_bytes >= (1u << 24) * (size_t)es) return fail(SCB_ERR_SHAPE, "stage too large for row descriptors");
-    d->n_ey = (g.e + v.th - 1) / v.th;
-    d->n_fx = 1;
+    d->n_ey = oned ? 1 : (g.e + v.th - 1) / v.th;
+    d->n_fx = v.dispatch == DISPATCH_WIDE ? (g.f + v.tw - 1) / v.tw
+              : oned                      ? (g.f + v.th * v.tw - 1) / (v.th * v.tw) : 1;
     d->kblocks = (g.k + c.warps_k * v.kt - 1) / (c.warps_k * v.kt);
     d->nb = (n + G - 1) / G;
-    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->nb;
+    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->n_fx * d->nb;
     if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
     d->grid = (unsigned)grid;
     return SCB_OK;
@@ -651,7 +661,7 @@ scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     d->n_fx = 1;
     d->kblocks = (g.k + c.warps_k * v.kt - 1) / (c.warps_k * v.kt);
     d->nb = (n + G - 1) / G;
-    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->nb;
+    const int64_t grid = (int64_t)d->kblocks * d->n_ey * d->n_fx * d->nb;
     if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
     d->grid = (unsigned)grid;
     return SCB_OK;
@@ -824,6 +834,8 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
             if (c.warps_k == 8) score += 1.0;
             if (v.kind == KIND_DIRECT) {
                 score += (v.th == 8 ? 1.0 : 0.0) + (v.kt >= 4 ? 0.5 : 0.0) + (v.nbt == 1 ? 0.3 : 0.0);
+                if (v.dispatch == DISPATCH_WIDE)  // exact-fit rows first, then the fewest idle lanes
+                    score -= 0.4 + 2.0 * (1.0 - (double)g.f / (d.n_fx * v.tw));
                 score += (c.cc == 16 ? 0.5 : 0.0);
             } else if (v.kind == KIND_DIMG) {
                 score += (v.kt == 4 ? 0.5 : 0.0) + (c.cc == 32 ? 0.5 : 0.0) - (g.h == 4 ? 2.0 : 0.0);
@@ -1026,7 +1038,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
-        q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
+        q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nfx = d.n_fx; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
         q.nbuf = c.stages == 0 ? (ve.info.kind == KIND_DWS ? 3 : 2) : c.stages;
         cudaError_t e = ve.dlaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
         return e == cudaSuccess ? SCB_OK : cuda_fail(e, "direct kernel launch");

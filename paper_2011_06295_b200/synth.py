@@ -94,3 +94,26 @@ SWEEP_SPARSITIES = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.97, 0.98, 0.99)
 def sweep_layer(sparsity: float) -> LayerSpec:
     """BASELINE config 5: 256->256, 3x3, 32x32."""
     return LayerSpec(f"sweep256_s{sparsity:g}", _vgg(256, 32, 256), sparsity)
+
+
+def _shape(c, h, w, k, r, s, padding=0):
+    return ConvShape(n=1, c=c, h=h, w=w, k=k, r=r, s=s, stride=1, padding=padding)
+
+
+# The reference's named layer presets (pkg/src/sparseconv/bench.py:74-102),
+# timed at its DEFAULT_BATCH = 128 (bench.py:29) by tools/bench_presets.py.
+PRESET_BATCH = 128
+PRESETS = {
+    "vgg16": [LayerSpec(f"{c}x{hw}x{hw}x{k}", _vgg(c, hw, k), 0.90)
+              for c, hw, k in [(3, 224, 64), (64, 224, 64), (64, 112, 128), (128, 112, 128), (128, 56, 256),
+                               (256, 56, 256), (256, 28, 512), (512, 28, 512), (512, 14, 512)]],
+    "vgg16-mini": [LayerSpec("64x28x28x64", _vgg(64, 28, 64), 0.90)],
+    "resnet-1x1": [LayerSpec("256-filters-1x1x64", _shape(64, 56, 56, 256, 1, 1), 0.90),
+                   LayerSpec("64-filters-1x1x256", _shape(256, 56, 56, 64, 1, 1), 0.90)],
+    "densenet-1x1": [LayerSpec("densenet121-block3-layer24", _shape(992, 14, 14, 128, 1, 1), 0.875),
+                     LayerSpec("densenet121-block3-layer24-r91", _shape(992, 14, 14, 128, 1, 1), 0.91),
+                     LayerSpec("densenet161-block4-layer16", _shape(1776, 7, 7, 192, 1, 1), 0.91),
+                     LayerSpec("densenet161-block3-layer16", _shape(1104, 14, 14, 192, 1, 1), 0.93)],
+    "cnn-non-static": [LayerSpec(f"300x64-kernel{s}-s{sp * 100:g}", _shape(64, 1, 300, 100, 1, s), sp)
+                       for s in (2, 3) for sp in (0.77, 0.83, 0.875)],
+}

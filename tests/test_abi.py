@@ -35,7 +35,8 @@ def test_variant_table():
     kinds = set()
     for v in vs:
         assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (1, 2, 4, 8)
-        assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["dispatch"] in (0, 1)
+        assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1) and v["dispatch"] in (0, 1, 2, 3)
+        assert v["dispatch"] < 2 or v["kind"] == 2  # column-tiled (wide) / 1D direct
         assert v["kind"] in (0, 1, 2, 3, 4, 5) and v["io"] in (0, 2)
         kinds.add(v["kind"])
     assert kinds == {0, 1, 2, 3, 4, 5}  # tiled, plane, direct, image-lane, warp-specialised, TMEM

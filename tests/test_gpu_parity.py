@@ -424,6 +424,73 @@ def test_direct_kernels_bitwise(sc, orc, c, hw, k, sp, n):
         assert beq(o, want), cfg
 
 
+@pytest.mark.parametrize("c,h,w,k,r,pad,sp,n", [(64, 56, 56, 64, 3, 1, 0.9, 2), (32, 40, 36, 24, 3, 1, 0.7, 3),
+                                                 (48, 28, 100, 40, 1, 0, 0.9, 2), (16, 20, 68, 16, 5, 2, 0.8, 2),
+                                                 (3, 64, 64, 16, 3, 1, 0.5, 1), (64, 28, 28, 64, 3, 1, 0.9, 3),
+                                                 (40, 14, 14, 48, 3, 1, 0.8, 5), (32, 7, 7, 40, 3, 1, 0.8, 9),
+                                                 (96, 14, 14, 64, 1, 0, 0.875, 4), (64, 7, 7, 48, 1, 0, 0.9, 6)])
+def test_wide_direct_kernels_bitwise(sc, orc, c, h, w, k, r, pad, sp, n):
+    """Direct kernel on column tiles (DISPATCH_WIDE): output rows wider than
+    32 or of no tile width (28, 14, 7; 8- and 4-byte row copies), the
+    reference's ImageNet-size presets (pkg/src/sparseconv/bench.py:74-102)."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=n, c=c, h=h, w=w, k=k, r=r, s=r, padding=pad)
+    wt = make_layer_weights(LayerSpec("l", sh, sp), seed=1)
+    x, b = bench_inputs(sh, n)
+    kern = sc.build_csr(wt, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, r, r, 1, pad, b)
+    xd = torch.from_numpy(x).cuda()
+    layer = device_layer(kern, 0, np.float32)
+    vs = _abi.variants()
+    cands = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 2 and vs[cf[0]]["dispatch"] == 2]
+    assert cands, "no wide direct variant"
+    for cfg in cands[:: max(1, len(cands) // 24)]:
+        o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
+        assert beq(o, ref), cfg
+    # the default launch picks a wide direct variant too
+    o = sc.conv_sparse(xd, kern, b).cpu().numpy()
+    assert beq(o, ref)
+    if sh.e % 2 == 0 and sh.f % 2 == 0:
+        want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref)), 2).numpy()
+        pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 2 and vs[cf[0]]["dispatch"] == 2]
+        assert pc
+        for cfg in pc[:: max(1, len(pc) // 6)]:
+            o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
+            assert beq(o, want), cfg
+
+
+@pytest.mark.parametrize("c,w,k,s,sp,n", [(64, 300, 100, 2, 0.77, 5), (64, 300, 100, 3, 0.875, 3),
+                                          (16, 37, 24, 5, 0.5, 7), (8, 1030, 12, 4, 0.6, 2)])
+def test_oned_direct_kernels_bitwise(sc, orc, c, w, k, s, sp, n):
+    """1D direct kernel (DISPATCH_ONED, H = R = 1): the reference's
+    conv_sparse_1d (sc/engine.py:90-106) on the cnn-non-static presets
+    (pkg/src/sparseconv/bench.py:94-101) plus odd widths (4-byte row copies)."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=n, c=c, h=1, w=w, k=k, r=1, s=s)
+    wt = make_layer_weights(LayerSpec("l", sh, sp), seed=2)
+    x, b = bench_inputs(sh, n)
+    kern = sc.build_csr(wt, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 1, s, 1, 0, b)
+    xd = torch.from_numpy(x).cuda()
+    layer = device_layer(kern, 0, np.float32)
+    vs = _abi.variants()
+    cands = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 2 and vs[cf[0]]["dispatch"] == 3]
+    assert cands, "no 1D direct variant"
+    for cfg in cands[:: max(1, len(cands) // 24)]:
+        o = sc.conv_sparse_1d(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
+        assert beq(o, ref), cfg
+    o = sc.conv_sparse_1d(xd, kern, b).cpu().numpy()
+    assert beq(o, ref)
+    o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cands[0]), relu=True).cpu().numpy()
+    assert beq(o, np.maximum(ref, 0))
+
+
 @pytest.mark.parametrize("c,hw,k,sp,n", [(512, 4, 512, 0.9, 40), (96, 4, 40, 0.5, 7), (512, 2, 512, 0.9, 70),
                                          (64, 2, 72, 0.8, 33), (24, 4, 16, 0.9, 3)])
 def test_image_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n):

@@ -1,0 +1,112 @@
+"""Time the reference's named layer presets (pkg/src/sparseconv/bench.py:74-102)
+on one B200: the sparse engine (exact fp32, fastest launch of a bounded
+candidate sample per kind) against cuDNN dense fp32 (TF32 off) and the
+generic kernel, at the reference's DEFAULT_BATCH = 128.  Every sparse output
+is checked bitwise against the generic (thread-per-output) kernel, which the
+GPU parity tests pin to the oracle.
+
+python tools/bench_presets.py [preset ...] [--out profiles/r01_presets.jsonl]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2011_06295_b200 as sc  # noqa: E402
+from paper_2011_06295_b200 import _abi  # noqa: E402
+from paper_2011_06295_b200.device import device_layer  # noqa: E402
+from paper_2011_06295_b200.synth import PRESET_BATCH, PRESETS, make_layer_weights  # noqa: E402
+from paper_2011_06295_b200.tuner import time_call  # noqa: E402
+
+KIND = {0: "tiled", 1: "plane", 2: "direct", 3: "image-lane", 4: "ws", 5: "tmem"}
+
+
+def sample(cands, vs, per_kind):
+    by = {}
+    for c in cands:
+        v = vs[c[0]]
+        by.setdefault((v["kind"], v["dispatch"]), []).append(c)
+    out = []
+    for lst in by.values():
+        out += lst[:: max(1, len(lst) // per_kind)]
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("presets", nargs="*", default=list(PRESETS))
+    ap.add_argument("--batch", type=int, default=PRESET_BATCH)
+    ap.add_argument("--per-kind", type=int, default=24)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.benchmark = True
+    vs = _abi.variants()
+    st = torch.cuda.current_stream().cuda_stream
+    recs = []
+    for pname in a.presets:
+        for spec in PRESETS[pname]:
+            n = a.batch
+            sh = spec.shape.with_batch(n)
+            w = make_layer_weights(spec, 0)
+            kern = sc.build_csr(w, sh)
+            g = torch.Generator().manual_seed(1)
+            xd = torch.randn((n, sh.c, sh.h, sh.w), generator=g).cuda()
+            bd = torch.randn(sh.k, generator=g).cuda()
+            layer = device_layer(kern, 0, np.float32)
+            y = torch.empty((n, sh.k, sh.e, sh.f), device="cuda")
+            yg = torch.empty_like(y)
+            macs = sc.sparse_mac_count(kern, n)
+            dense_macs = n * sh.k * sh.c * sh.r * sh.s * sh.e * sh.f
+            t_gen = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), yg.data_ptr(), n,
+                                                   _abi.FLAG_GENERIC, None, st), 3, 1)
+            cands = layer.candidates(n)
+            timed = {}
+
+            def run(cs):
+                for c in cs:
+                    if c in timed:
+                        continue
+                    try:
+                        timed[c] = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), n,
+                                                                  0, c, st), 3, 1)
+                    except Exception:  # noqa: BLE001 -- a launch the device rejects is skipped
+                        pass
+            # sampled pass over every (kind, dispatch), then every launch of the 3 best variants
+            run(sample(cands, vs, a.per_kind))
+            top = {c[0] for c in sorted(timed, key=timed.get)[:3]}
+            run([c for c in cands if c[0] in top])
+            best = min(timed, key=timed.get)
+            t_best = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), n, 0, best, st),
+                               10, 2)
+            layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), n, 0, best, st)
+            torch.cuda.synchronize()
+            exact = bool(torch.equal(y.view(torch.int32), yg.view(torch.int32)))
+            wt = torch.from_numpy(w).cuda()
+            t_cudnn = time_call(lambda: torch.nn.functional.conv2d(xd, wt, bd, padding=sh.padding), 10, 3)
+            v = vs[best[0]]
+            rec = {"preset": pname, "layer": spec.name, "sparsity": spec.sparsity, "batch": n,
+                   "sparse_us": t_best * 1e6, "generic_us": t_gen * 1e6, "cudnn_fp32_us": t_cudnn * 1e6,
+                   "speedup_vs_cudnn": t_cudnn / t_best, "sparse_tmacs": macs / t_best / 1e12,
+                   "cudnn_tflops": 2 * dense_macs / t_cudnn / 1e12, "kind": KIND[v["kind"]],
+                   "tile": {2: "wide", 3: "1d"}.get(v["dispatch"], "") if v["kind"] == 2 else "",
+                   "launch": list(best),
+                   "bitwise_vs_generic": exact}
+            recs.append(rec)
+            print(f"{pname:15s} {spec.name:32s} sparse {t_best * 1e6:9.1f}us ({rec['sparse_tmacs']:5.2f} TMAC/s, "
+                  f"{rec['kind']}{'/' + rec['tile'] if rec['tile'] else ''})  cuDNN {t_cudnn * 1e6:9.1f}us  "
+                  f"x{rec['speedup_vs_cudnn']:.2f}  generic {t_gen * 1e6:9.1f}us  exact={exact}", flush=True)
+            del xd, y, yg, layer
+            torch.cuda.empty_cache()
+    if a.out:
+        Path(a.out).parent.mkdir(parents=True, exist_ok=True)
+        Path(a.out).write_text("".join(json.dumps(r) + "\n" for r in recs))
+
+
+if __name__ == "__main__":
+    main()
