@@ -192,9 +192,10 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     // WIDE: a staged row is global columns ox0-XO .. ox0+ROW-XO-1, elements e_lo..e_hi of it
     // (in copies of ce elements: 16, 8 or 4 bytes as the row width's alignment allows)
     const TIO* xg = static_cast<const TIO*>(p.x) + (size_t)n0 * C * hw + (WIDE ? ox0 - XO : 0);
-    const int e_lo = WIDE ? (ox0 == 0 ? XO : 0) : 0;
+    const int e_lo = WIDE ? max(0, XO - ox0) : 0;  // first element at global column >= 0
     const int e_hi = WIDE ? min(ONED ? PLANE : ROW, p.w - (ox0 - XO)) : 0;
-    const int ce = (p.w % Q16 == 0) ? Q16 : (p.w % 2 == 0 ? 2 : 1);
+    // = layer.cu direct_copy_elems: the widest copy both the global and the shared row allow
+    const int ce = (p.w % Q16 == 0 && ROW % Q16 == 0) ? Q16 : ((p.w % 2 == 0 && ROW % 2 == 0) ? 2 : 1);
     const int nchunk = p.w / Q16;  // narrow: 16-byte chunks per input row (derive() requires it exact)
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;

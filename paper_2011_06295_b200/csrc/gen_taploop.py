@@ -387,7 +387,10 @@ DIRECTS = [d + (2,) for d in DIRECTS] + \
 # ImageNet shapes; also rows whose width is no tile width, 28/14/7): (R, S, PAD, TH, LW, KW, min CTAs/SM)
 DIRECTS_WIDE = [(3, 3, 1, th, lw, kw, 2) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
                [(3, 3, 1, 16, 32, 4, 2), (3, 3, 1, 8, 32, 2, 4), (5, 5, 2, 4, 32, 4, 2), (5, 5, 2, 4, 16, 4, 2)] + \
-               [(1, 1, 0, 8, lw, kw, 2) for lw in (32, 16, 8) for kw in (4, 8)] + [(1, 1, 0, 16, 32, 4, 2)]
+               [(1, 1, 0, 8, lw, kw, 2) for lw in (32, 16, 8) for kw in (4, 8)] + [(1, 1, 0, 16, 32, 4, 2)] + \
+               [(3, 3, 1, 2, 2, 4, 2), (3, 3, 1, 4, 4, 8, 2)]
+# (2x2 / 4x4 planes as WIDE tiles of 2 / 4 columns, 16 / 8 images per warp: correct, measured
+# 110 us vs the image-lane kernel's 92 us on conv5 and 221 vs 217 us on conv4 -- one each kept)
 WIDE, ONED = 2, 3                                # kernels.cuh DISPATCH_WIDE / DISPATCH_ONED
 # 1D direct variants (H = R = 1, e.g. the reference's cnn-non-static presets): (S, TH, KW)
 DIRECTS_1D = [(s, th, kw) for s in (2, 3, 4, 5) for th in (4, 8) for kw in (4, 8)]

@@ -434,6 +434,7 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         return g.h == 1 && g.e == 1 && !(flags & SCB_FLAG_POOL2);
     if (v.kind == KIND_DIRECT && v.dispatch == DISPATCH_WIDE) {  // column tiles: any row width
         if (v.tw > 8 && g.f <= v.tw / 2) return false;          // a narrower tile fits better
+        if (v.tw < 8 && g.f > 2 * v.tw) return false;           // tiny tiles: small planes only
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
         return true;
     }
@@ -521,6 +522,14 @@ std::vector<int> direct_cols(const scb_variant_info& v) {
     return col;
 }
 
+// elements per staging copy of a WIDE/ONED direct row (= direct.cuh `ce`): 16, 8 or 4 bytes
+int direct_copy_elems(const scb_variant_info& v, int w, int row) {
+    const int q = 16 / elem_bytes(v);
+    if (v.dispatch != DISPATCH_WIDE && v.dispatch != DISPATCH_ONED) return q;
+    if (w % q == 0 && row % q == 0) return q;
+    return (w % 2 == 0 && row % 2 == 0) ? 2 : 1;
+}
+
 scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
@@ -534,9 +543,13 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     const bool oned = v.dispatch == DISPATCH_ONED;
     const int es = elem_bytes(v), q16 = 16 / es;
     const int plane = oned ? q16 + v.th * v.tw + q16 : (v.th + v.r - 1) * d->row;  // = direct.cuh PLANE
-    int ip = (c.cc * plane + q16 - 1) / q16 * q16;
-    if (G > 1)  // word pitch of an image = its row width in words (mod 32): conflict-free lanes
-        while ((ip * es / 4) % 32 != (v.tw * es / 4) % 32) ip += q16;
+    const int ce = direct_copy_elems(v, g.w, d->row);  // image pitch granule (copy alignment)
+    int ip = (c.cc * plane + ce - 1) / ce * ce;
+    if (G > 1) {  // word pitch of an image = its row width in words (mod 32): conflict-free lanes
+        int t = ip;
+        for (int i = 0; i < 64 && (t * es / 4) % 32 != (v.tw * es / 4) % 32; ++i) t += ce;
+        if ((t * es / 4) % 32 == (v.tw * es / 4) % 32) ip = t;
+    }
     d->chunk = ip;  // image pitch (elements) travels in `chunk`
     const size_t stage_bytes = ((size_t)G * ip * es + 16 + 127) & ~(size_t)127;  // +16: zero tail
     d->stage_el = (int)(stage_bytes / es);

@@ -93,6 +93,8 @@ class SparseConvNet:
         self.launches = [None] * len(self.layers)
         self.algorithms = ["sparse-direct"] * len(self.layers)
         self._dense = [None] * len(self.layers)
+        self.chains = 1
+        self._side_streams = []
 
     # ---- shapes ---------------------------------------------------------
     def flags(self, i: int) -> int:
@@ -162,12 +164,61 @@ class SparseConvNet:
                 self.scratch[i] = self.torch.empty((self.batch, sh.k, sh.e, sh.f), dtype=self.tdtype,
                                                    device=self.tdev)
 
+    def set_chains(self, chains: int) -> None:
+        """Run the batch as `chains` independent sub-batch chains on their own
+        streams (images are independent, so this changes no result bit): the
+        last partial wave of one chain's layer kernel overlaps the other
+        chains' kernels instead of leaving SMs idle.  1 = one stream."""
+        chains = int(chains)
+        if chains < 1 or (self.batch is not None and chains > self.batch):
+            raise ShapeError(f"chains must be in [1, batch], got {chains}")
+        self.chains = chains
+        self.graph = None
+
+    def _chain_bounds(self):
+        from .runner import shard_range
+        return [shard_range(self.batch, self.chains, j) for j in range(self.chains)]
+
     # ---- execution ------------------------------------------------------
-    def launch_layer(self, i: int, x_dev, y_dev, stream: int) -> None:
+    def launch_layer(self, i: int, x_dev, y_dev, stream: int, rows: tuple | None = None) -> None:
+        """Layer i on images rows[0]:rows[1] (default: the whole batch)."""
         b = self.biases[i]
-        engine.run_layer(self.dlayers[i], x_dev.data_ptr(), b.data_ptr() if b is not None else 0,
-                         y_dev, self.batch, self.flags(i), self.launches[i], stream,
-                         scratch=self.scratch[i])
+        a, e = rows if rows is not None else (0, self.batch)
+        sc = self.scratch[i]
+        engine.run_layer(self.dlayers[i], x_dev[a:e].data_ptr(), b.data_ptr() if b is not None else 0,
+                         y_dev[a:e], e - a, self.flags(i), self.launches[i], stream,
+                         scratch=None if sc is None else sc[a:e])
+
+    def _run_chain(self, x, stream, rows, on_first=None) -> None:
+        cur = x
+        a, e = rows
+        for i in range(len(self.layers)):
+            if self.algorithms[i] == "dense-cudnn":
+                with self.torch.cuda.stream(stream):
+                    self.dense_layer(i)(cur[a:e], self.acts[i][a:e])
+            else:
+                self.launch_layer(i, cur, self.acts[i], stream.cuda_stream, rows)
+            if i == 0 and on_first is not None:
+                on_first(stream)
+            cur = self.acts[i]
+
+    def _run_stack(self, x, stream, on_first=None) -> None:
+        """The whole stack on `stream`, forked over the sub-batch chains."""
+        torch = self.torch
+        if self.chains == 1:
+            self._run_chain(x, stream, (0, self.batch), on_first)
+            return
+        while len(self._side_streams) < self.chains - 1:
+            self._side_streams.append(torch.cuda.Stream(self.device))
+        streams = [stream] + self._side_streams[:self.chains - 1]
+        for s in streams[1:]:
+            s.wait_stream(stream)
+        for s, rows in zip(streams, self._chain_bounds()):
+            self._run_chain(x, s, rows)
+        for s in streams[1:]:
+            stream.wait_stream(s)
+        if on_first is not None:
+            on_first(stream)  # (joined: every chain is past its first layer)
 
     def dense_layer(self, i: int):
         """Dense cuDNN equivalent of layer i (IEEE fp32 / fp16, TF32 off):
@@ -235,17 +286,19 @@ class SparseConvNet:
             if self.graph is not None and events is None:
                 self.graph.replay()
                 return self.acts[-1]
+            if events is None:
+                self._run_stack(self.x_in, stream)
+                return self.acts[-1]
+            # per-layer events: one chain, an event between layers
             s = stream.cuda_stream
             cur = self.x_in
-            if events is not None:
-                events[0].record(stream)
+            events[0].record(stream)
             for i in range(len(self.layers)):
                 if self.algorithms[i] == "dense-cudnn":
                     self.dense_layer(i)(cur, self.acts[i])
                 else:
                     self.launch_layer(i, cur, self.acts[i], s)
-                if events is not None:
-                    events[i + 1].record(stream)
+                events[i + 1].record(stream)
                 cur = self.acts[i]
         return self.acts[-1]
 
@@ -311,16 +364,8 @@ class SparseConvNet:
                         bufs[(i + 1) % 2].copy_(x_hosts[i + 1], non_blocking=True)
                         loaded[i + 1].record(copy)
                 comp.wait_event(loaded[i])
-                s = comp.cuda_stream
-                cur = xb
-                for li in range(len(self.layers)):
-                    if self.algorithms[li] == "dense-cudnn":
-                        self.dense_layer(li)(cur, self.acts[li])
-                    else:
-                        self.launch_layer(li, cur, self.acts[li], s)
-                    if li == 0:
-                        freed[i].record(comp)
-                    cur = self.acts[li]
+                self._run_stack(xb, comp, on_first=lambda st, ev=freed[i]: ev.record(st))
+                cur = self.acts[-1]
                 done[i].record(comp)
                 with torch.cuda.stream(copy):
                     copy.wait_event(done[i])

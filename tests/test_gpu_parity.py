@@ -428,7 +428,9 @@ def test_direct_kernels_bitwise(sc, orc, c, hw, k, sp, n):
                                                  (48, 28, 100, 40, 1, 0, 0.9, 2), (16, 20, 68, 16, 5, 2, 0.8, 2),
                                                  (3, 64, 64, 16, 3, 1, 0.5, 1), (64, 28, 28, 64, 3, 1, 0.9, 3),
                                                  (40, 14, 14, 48, 3, 1, 0.8, 5), (32, 7, 7, 40, 3, 1, 0.8, 9),
-                                                 (96, 14, 14, 64, 1, 0, 0.875, 4), (64, 7, 7, 48, 1, 0, 0.9, 6)])
+                                                 (96, 14, 14, 64, 1, 0, 0.875, 4), (64, 7, 7, 48, 1, 0, 0.9, 6),
+                                                 (512, 2, 2, 512, 3, 1, 0.9, 37), (256, 4, 4, 96, 3, 1, 0.9, 19),
+                                                 (64, 3, 3, 40, 3, 1, 0.6, 21)])
 def test_wide_direct_kernels_bitwise(sc, orc, c, h, w, k, r, pad, sp, n):
     """Direct kernel on column tiles (DISPATCH_WIDE): output rows wider than
     32 or of no tile width (28, 14, 7; 8- and 4-byte row copies), the

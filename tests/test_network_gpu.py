@@ -139,3 +139,24 @@ def test_forward_stream_bitwise(torch, vgg_small):
     net.forward_stream(xs, outs)
     for i, o in enumerate(outs):
         assert np.array_equal(_bits(o.numpy()), _bits(ref if i % 2 == 0 else ref2)), i
+
+
+@pytest.mark.parametrize("chains", [2, 3])
+def test_subbatch_chains_bitwise(torch, vgg_small, chains):
+    """Sub-batch chains on separate streams (set_chains): same bits as one
+    stream, eager, graph-replayed and streamed."""
+    net, x, ref = vgg_small
+    net.plan(3, tune=False)
+    net.set_chains(chains)
+    try:
+        assert np.array_equal(_bits(net.forward(x)), _bits(ref))
+        net.capture()
+        x2 = np.random.default_rng(11).standard_normal(x.shape).astype(np.float32)
+        assert np.array_equal(_bits(net.forward(x2)), _bits(oracle_stack(net, x2)))
+        xs = [torch.from_numpy(a).pin_memory() for a in (x, x2, x)]
+        outs = [torch.empty((3, 512, 1, 1)).pin_memory() for _ in xs]
+        net.forward_stream(xs, outs)
+        for i, o in enumerate(outs):
+            assert np.array_equal(_bits(o.numpy()), _bits(ref if i % 2 == 0 else oracle_stack(net, x2))), i
+    finally:
+        net.set_chains(1)

@@ -34,6 +34,6 @@ for spec, _ in vgg16_cifar(0.9):
             continue
         t = time_call(lambda: layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), N, 0, c, st), 3, 1)
         v = vs[c[0]]
-        res.append((t, c, (v["th"], v["tw"], v["kt"], v["nbt"])))
+        res.append((t, c, (v["th"], v["tw"], v["kt"], v["nbt"], v["dispatch"])))
     for t, c, v in sorted(res)[:8]:
-        print(f"{spec.name} {t * 1e6:8.1f}us {macs / t / 1e12:5.2f}TMAC/s {c} th,tw,kt,nbt={v}", flush=True)
+        print(f"{spec.name} {t * 1e6:8.1f}us {macs / t / 1e12:5.2f}TMAC/s {c} th,tw,kt,nbt,disp={v}", flush=True)
