@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-images", type=int, default=8, help="images per CPU-baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline time budget")
     ap.add_argument("--chains", type=int, default=2, help="sub-batch chains on separate streams per GPU")
+    ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch between layers")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f16", action="store_true", help="skip the fp16 (config 4) secondary measurement")
@@ -394,6 +395,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     launches = list(net.launches)
     tune_s = time.perf_counter() - t0
     net.set_chains(args.chains)
+    net.pdl = not args.no_pdl
 
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
     x_host = torch.randn((args.batch, 3, 32, 32), generator=g).pin_memory()
@@ -503,7 +505,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "parallelism": f"batch-sharded x{world} (weak, no collective)",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
                    "tuned": not args.no_tune, "tune_seconds": round(tune_s, 1),
-                   "streams_per_gpu": args.chains},
+                   "streams_per_gpu": args.chains, "pdl": not args.no_pdl},
         "e2e": {"value": round(args.batch * args.steps * world / e2e_s, 1), "unit": "images/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
                 "api": "SparseConvNet.forward_stream (pinned host in/out, copies overlapped across steps)"},

@@ -62,6 +62,7 @@ typedef struct {
 #define SCB_FLAG_FAST      0x2u   /* f32: single-rounding FFMA instead of mul+add   */
 #define SCB_FLAG_POOL2     0x4u   /* fused 2x2/2 max-pool epilogue (VGG stage glue) */
 #define SCB_FLAG_GENERIC   0x8u   /* force the generic (any-geometry) kernel        */
+#define SCB_FLAG_NO_PDL    0x10u  /* launch without programmatic dependent launch   */
 
 /* Launch configuration: replaces EnginePlan.sub_batch_size (engine.py:28-39)
  * and the timed tune_sub_batch (engine.py:143-166). variant < 0 = generic. */

@@ -24,7 +24,7 @@ SCB_ERR_CUDA, SCB_ERR_ARG, SCB_ERR_UNSUPPORTED = 4, 5, 6
 SCB_F32, SCB_F64, SCB_F16 = 0, 1, 2
 SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16 = 0, 1, 2
 
-FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC = 0x1, 0x2, 0x4, 0x8
+FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC, FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8, 0x10
 
 # every symbol include/sparseconv_b200.h declares
 EXPORTS = (

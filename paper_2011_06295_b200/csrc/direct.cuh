@@ -87,7 +87,7 @@ cudaError_t launch_pdl(K kern, const P& p, unsigned grid, unsigned threads, size
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = (p.flags & SCB_FLAG_NO_PDL) ? 0 : 1;  // without it griddepcontrol.* are no-ops
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     return e != cudaSuccess ? e : cudaGetLastError();
 }

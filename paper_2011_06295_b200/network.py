@@ -94,6 +94,7 @@ class SparseConvNet:
         self.algorithms = ["sparse-direct"] * len(self.layers)
         self._dense = [None] * len(self.layers)
         self.chains = 1
+        self.pdl = True  # programmatic dependent launch between consecutive layer kernels
         self._side_streams = []
 
     # ---- shapes ---------------------------------------------------------
@@ -186,7 +187,8 @@ class SparseConvNet:
         a, e = rows if rows is not None else (0, self.batch)
         sc = self.scratch[i]
         engine.run_layer(self.dlayers[i], x_dev[a:e].data_ptr(), b.data_ptr() if b is not None else 0,
-                         y_dev[a:e], e - a, self.flags(i), self.launches[i], stream,
+                         y_dev[a:e], e - a, self.flags(i) | (0 if self.pdl else _abi.FLAG_NO_PDL),
+                         self.launches[i], stream,
                          scratch=None if sc is None else sc[a:e])
 
     def _run_chain(self, x, stream, rows, on_first=None) -> None:

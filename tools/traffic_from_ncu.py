@@ -1,7 +1,7 @@
 """Per-layer DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum, bytes
 per launch) of one profiled forward pass of the VGG-CIFAR stack -> JSON
 {layer: bytes} for bench.py's roofline.traffic.  Usage:
-  python tools/traffic_from_ncu.py <report.ncu-rep> <launches.json> > profiles/traffic.json
+  python tools/traffic_from_ncu.py <report.ncu-rep | raw-page.csv> <launches.json> > profiles/traffic.json
 Conv launches are matched to layers in order; a generic layer with a fused
 pool contributes its conv launch plus the following k_maxpool2 launch."""
 import csv
@@ -15,7 +15,8 @@ from paper_2011_06295_b200.synth import vgg16_cifar  # noqa: E402
 
 rep, lf = sys.argv[1], sys.argv[2]
 launches = json.load(open(lf))
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = open(rep).read() if rep.endswith(".csv") else \
+    subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 h = r[0]
 iN, iR, iW = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
