@@ -196,27 +196,34 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     const int e_hi = WIDE ? min(ONED ? PLANE : ROW, p.w - (ox0 - XO)) : 0;
     // = layer.cu direct_copy_elems: the widest copy both the global and the shared row allow
     const int ce = (p.w % Q16 == 0 && ROW % Q16 == 0) ? Q16 : ((p.w % 2 == 0 && ROW % 2 == 0) ? 2 : 1);
-    const int nchunk = p.w / Q16;  // narrow: 16-byte chunks per input row (derive() requires it exact)
+    // narrow: 16-byte chunks per input row (rows have W == F == LW; derive() requires 16-byte rows)
+    constexpr int NCH = (LW * ES) / 16 > 0 ? (LW * ES) / 16 : 1;
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;
         const unsigned ncl = (unsigned)min(p.cc, C - c0);
         TIO* dst = xs + (size_t)buf * p.stage_el;
         const TIO* src = xg + (size_t)c0 * hw;
-        for (int rr = tid; rr < rows; rr += nthreads) {
-            const uint2 rd = rdesc[rr];
-            if ((rd.y >> 24) < ncl) {
-                const TIO* s = src + rd.x;
-                TIO* d = dst + (rd.y & 0xffffffu);
-                if constexpr (WIDE) {
+        if constexpr (WIDE) {
+            for (int rr = tid; rr < rows; rr += nthreads) {
+                const uint2 rd = rdesc[rr];
+                if ((rd.y >> 24) < ncl) {
+                    const TIO* s = src + rd.x;
+                    TIO* d = dst + (rd.y & 0xffffffu);
                     if (ce == Q16)
                         for (int q = e_lo; q < e_hi; q += Q16) cp_async<16>(d + q, s + q);
                     else if (ce == 2)
                         for (int q = e_lo; q < e_hi; q += 2) cp_async<8>(d + q, s + q);
                     else
                         for (int q = e_lo; q < e_hi; ++q) cp_async<4>(d + q, s + q);
-                } else {
-                    for (int q = 0; q < nchunk; ++q) cp_async<16>(d + Q16 * q, s + Q16 * q);
                 }
+            }
+        } else {
+            // thread = (row, 16-byte chunk), chunk fastest: a warp's copies land in a few
+            // contiguous shared-memory runs (one thread per row costs ~1 wavefront per thread)
+            for (int it = tid; it < rows * NCH; it += nthreads) {
+                const int rr = it / NCH, q = it % NCH;
+                const uint2 rd = rdesc[rr];
+                if ((rd.y >> 24) < ncl) cp_async<16>(dst + (rd.y & 0xffffffu) + Q16 * q, src + rd.x + Q16 * q);
             }
         }
         // this warp's contiguous tap block of the stage: 16-byte chunks, one per lane
@@ -234,24 +241,24 @@ __global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ Di
     auto shift = [&](int st, int buf) {
         const unsigned ncl = (unsigned)min(p.cc, C - st * p.cc);
         TIO* base = xs + (size_t)buf * p.stage_el;
-        for (int rr = tid; rr < rows; rr += nthreads) {
+        // thread = (row, chunk i in 0..NCH), chunk fastest (conflict-free 16-byte accesses)
+        for (int it = tid; it < rows * (NCH + 1); it += nthreads) {
+            const int rr = it / (NCH + 1), i = it % (NCH + 1);
             const uint2 rd = rdesc[rr];
             if ((rd.y >> 24) >= ncl) continue;
             const TIO* q = base + (rd.y & 0xffffffu);  // Q[XO]
             TIO* pr = const_cast<TIO*>(q) + QW;         // P[XO]
-            uint4 prev = *reinterpret_cast<const uint4*>(q - Q16);
-            for (int i = 0; i <= nchunk; ++i) {
-                const uint4 cur = *reinterpret_cast<const uint4*>(q + Q16 * i);
-                uint4 o;
-                if constexpr (ES == 4) {
-                    o = make_uint4(prev.w, cur.x, cur.y, cur.z);
-                } else {  // shift by one half: word w = (cur[w] << 16) | (prev word >> 16)
-                    o = make_uint4(__funnelshift_l(prev.w, cur.x, 16), __funnelshift_l(cur.x, cur.y, 16),
-                                   __funnelshift_l(cur.y, cur.z, 16), __funnelshift_l(cur.z, cur.w, 16));
-                }
-                *reinterpret_cast<uint4*>(pr + Q16 * i) = o;
-                prev = cur;
+            // last 32-bit word of the previous chunk (chunk -1 = the zero left padding)
+            const unsigned prevw = *reinterpret_cast<const unsigned*>(q + Q16 * i - 4 / ES);
+            const uint4 cur = *reinterpret_cast<const uint4*>(q + Q16 * i);
+            uint4 o;
+            if constexpr (ES == 4) {
+                o = make_uint4(prevw, cur.x, cur.y, cur.z);
+            } else {  // shift by one half: word w = (cur[w] << 16) | (prev word >> 16)
+                o = make_uint4(__funnelshift_l(prevw, cur.x, 16), __funnelshift_l(cur.x, cur.y, 16),
+                               __funnelshift_l(cur.y, cur.z, 16), __funnelshift_l(cur.z, cur.w, 16));
             }
+            *reinterpret_cast<uint4*>(pr + Q16 * i) = o;
         }
     };
 

@@ -1,5 +1,5 @@
 """Launch one VGG-CIFAR layer with an explicit launch a few times (for ncu):
-python tools/profile_one.py <layer> <v,wk,imgs,bh,bw,cc,stages>"""
+python tools/profile_one.py <layer> <v,wk,imgs,bh,bw,cc,stages> [f16]"""
 import sys
 from pathlib import Path
 
@@ -15,11 +15,12 @@ name, launch = sys.argv[1], tuple(int(v) for v in sys.argv[2].split(","))
 spec = [s for s, _ in vgg16_cifar(0.9) if s.name == name][0]
 N = 256
 sh = spec.shape.with_batch(N)
-kern = sc.build_csr(make_layer_weights(spec, 0), sh)
+dt = np.float16 if sys.argv[3:] == ["f16"] else np.float32
+kern = sc.build_csr(make_layer_weights(spec, 0).astype(dt), sh)
 x, b = bench_inputs(sh, N)
-xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
-layer = device_layer(kern, 0, np.float32)
-y = torch.empty((N, sh.k, sh.e, sh.f), device="cuda")
+xd, bd = torch.from_numpy(x.astype(dt)).cuda(), torch.from_numpy(b).cuda()
+layer = device_layer(kern, 0, dt)
+y = torch.empty((N, sh.k, sh.e, sh.f), device="cuda", dtype=xd.dtype)
 for _ in range(3):
     layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), N, 0, launch, torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
