@@ -7,15 +7,18 @@
 // and walked in the reference's colidx order per output channel
 // (_kernels.py:73-84), so exact mode is bit-identical to the reference.
 //
-// Shared layout per (image, channel): H+2 rows (top/bottom zero-padding rows
-// never written) x 3 column-shifted copies of each padded input row,
-// copy_s = padded_row[s .. s+H), each one H-float vector.  A tap (c, r, s)
-// then reads output row y's inputs as ONE aligned vector load
-// (ld.shared.v4 for H=4, .v2 for H=2) at c*BLK + (y+r)*3H + s*H: 4 B per MAC
-// but one instruction per H MACs.  Images sit at a pitch whose vector index
-// is odd, so the 8 (v4) / 16 (v2) lanes of a shared-memory wavefront hit
-// distinct banks.  copy_1 is the input row itself (one 16/8-byte cp.async);
-// copy_0 / copy_2 are built from it in shared memory after it lands.
+// Shared layout per (image, channel): 3H+4 rows of H floats holding the three
+// column-shifted copies of the H input rows, copy_s = padded_row[s .. s+H), with
+// the four zero padding rows shared between neighbouring copies:
+//   pos 0: 0 | 1..H: copy_1 (the input plane itself) | H+1: 0 | H+2..2H+1: copy_0 |
+//   2H+2: 0 | 2H+3..3H+2: copy_2 | 3H+3: 0
+// so padded row r (0..H+1) of copy s sits at pos START_s + r, START = {H+1, 0, 2H+2}.
+// A tap (c, r, s) then reads output row y's inputs as ONE aligned vector load
+// (ld.shared.v4 for H=4, .v2 for H=2) at c*BLK + BASE + (START_s + y + r)*H:
+// 4 B per MAC but one instruction per H MACs.  copy_1 is the image plane
+// contiguous, so a stage lands with one 16-byte cp.async per thread per chunk;
+// copy_0 / copy_2 are built from it in shared memory.  Images sit at a pitch whose
+// vector index is odd, so the 8 (v4) / 16 (v2) lanes of a wavefront hit distinct banks.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -35,11 +38,15 @@ template <>
 struct VecT<2> { using T = float2; };
 
 template <int H, int KW, int MODE>
-__global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectParams p) {
+__global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectParams p) {
     using V = typename VecT<H>::T;
-    constexpr int RW = 3 * H;            // one padded row: 3 shifted copies
-    constexpr int BLK = (H + 2) * RW;    // floats per (image, channel)
+    constexpr int RW = H;                    // row stride inside a copy
+    constexpr int BLK = (3 * H + 4) * H;     // floats per (image, channel)
+    constexpr int BASE = (H == 2) ? 2 : 0;   // copy_1's plane 16-byte aligned: (BASE + H) % 4 == 0
     constexpr int HW = H * H;
+    constexpr int C1 = BASE + H;                  // copy_1 rows 1..H (the plane)
+    constexpr int C0 = BASE + (H + 2) * H;        // copy_0 rows 1..H
+    constexpr int C2 = BASE + (2 * H + 3) * H;    // copy_2 rows 1..H
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int tid = threadIdx.x, nthreads = blockDim.x;
@@ -49,7 +56,7 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
     const int k0 = (kb * p.wk + warp) * KW;
     const int C = p.c;
     float* xs = reinterpret_cast<float*>(smem);
-    const int rows = 32 * p.cc * H;  // input rows per stage
+    const int planes = 32 * p.cc;  // (image, channel) planes per stage
     // tap blocks after the stages: [buf][warp] slots of segcap 16-byte chunks (direct.cuh layout)
     int4* tsm = reinterpret_cast<int4*>(smem + (size_t)p.nbuf * p.stage_el * 4);
     constexpr int HDR = (KW * 4 + 15) / 16;
@@ -63,18 +70,26 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
     }
     __syncthreads();
 
-    // row q of a stage: image q / (cc*H), channel slot (q / H) % cc, row q % H
+    // plane t of a stage: image t / cc, channel slot t % cc; 16-byte chunks, chunk fastest
+    constexpr int PQ = HW / 4;
     const float* xg = static_cast<const float*>(p.x) + (size_t)n0 * C * HW;
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;
         const int ncl = min(p.cc, C - c0);
         float* dst = xs + (size_t)buf * p.stage_el;
-        for (int q = tid; q < rows; q += nthreads) {
-            const int y = q % H, t = q / H;
+        for (int it = tid; it < planes * PQ; it += nthreads) {
+            const int q = it % PQ, t = it / PQ;
             const int cl = t % p.cc, img = t / p.cc;
-            if (cl < ncl && n0 + img < p.n)
-                cp_async<H * 4>(dst + img * p.ip + cl * BLK + (y + 1) * RW + H,
-                                xg + ((size_t)img * C + c0 + cl) * HW + y * H);
+            if (cl < ncl && n0 + img < p.n) {
+                float* d = dst + img * p.ip + cl * BLK + C1 + 4 * q;
+                const float* g = xg + ((size_t)img * C + c0 + cl) * HW + 4 * q;
+                if (H == 4 || !(img & 1)) {
+                    cp_async<16>(d, g);
+                } else {  // H = 2: odd images sit 8 bytes off (odd float2 image pitch)
+                    cp_async<8>(d, g);
+                    cp_async<8>(d + 2, g + 2);
+                }
+            }
         }
         if (grp < groups) {  // this warp's contiguous tap block of the stage
             const int o0 = __ldg(p.blkoff + (size_t)grp * p.nst + st);
@@ -85,22 +100,31 @@ __global__ void __launch_bounds__(256, 2) k_dimg(const __grid_constant__ DirectP
             for (int i = lane; i < nch; i += 32) cp_async<16>(tb + i, src + i);
         }
     };
-    // copy_0 = (0, x0 .. x_{H-2}), copy_2 = (x1 .. x_{H-1}, 0) from copy_1
+    // copy_0 row = (0, x0 .. x_{H-2}), copy_2 row = (x1 .. x_{H-1}, 0), from copy_1
     auto shift = [&](int st, int buf) {
         const int ncl = min(p.cc, C - st * p.cc);
         float* base = xs + (size_t)buf * p.stage_el;
-        for (int q = tid; q < rows; q += nthreads) {
-            const int y = q % H, t = q / H;
-            const int cl = t % p.cc, img = t / p.cc;
-            if (cl >= ncl) continue;
-            float* r = base + img * p.ip + cl * BLK + (y + 1) * RW;
-            const V m = *reinterpret_cast<const V*>(r + H);
-            if constexpr (H == 4) {
-                *reinterpret_cast<float4*>(r) = make_float4(0.f, m.x, m.y, m.z);
-                *reinterpret_cast<float4*>(r + 2 * H) = make_float4(m.y, m.z, m.w, 0.f);
-            } else {
-                *reinterpret_cast<float2*>(r) = make_float2(0.f, m.x);
-                *reinterpret_cast<float2*>(r + 2 * H) = make_float2(m.y, 0.f);
+        if constexpr (H == 2) {  // thread = plane (8-byte accesses: odd images are 8-byte aligned)
+            for (int t = tid; t < planes; t += nthreads) {
+                const int cl = t % p.cc, img = t / p.cc;
+                if (cl >= ncl) continue;
+                float* b = base + img * p.ip + cl * BLK;
+                const float2 r0 = *reinterpret_cast<const float2*>(b + C1);
+                const float2 r1 = *reinterpret_cast<const float2*>(b + C1 + 2);
+                *reinterpret_cast<float2*>(b + C0) = make_float2(0.f, r0.x);
+                *reinterpret_cast<float2*>(b + C0 + 2) = make_float2(0.f, r1.x);
+                *reinterpret_cast<float2*>(b + C2) = make_float2(r0.y, 0.f);
+                *reinterpret_cast<float2*>(b + C2 + 2) = make_float2(r1.y, 0.f);
+            }
+        } else {  // thread = (plane, row)
+            for (int it = tid; it < planes * H; it += nthreads) {
+                const int y = it % H, t = it / H;
+                const int cl = t % p.cc, img = t / p.cc;
+                if (cl >= ncl) continue;
+                float* b = base + img * p.ip + cl * BLK + y * H;
+                const float4 m = *reinterpret_cast<const float4*>(b + C1);
+                *reinterpret_cast<float4*>(b + C0) = make_float4(0.f, m.x, m.y, m.z);
+                *reinterpret_cast<float4*>(b + C2) = make_float4(m.y, m.z, m.w, 0.f);
             }
         }
     };

@@ -578,14 +578,14 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
     const int H = v.th;
-    if (c.imgs != 32 || c.bh != H || c.bw != H || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
-        return fail(SCB_ERR_SHAPE, "image-lane launch: imgs = 32, bh = bw = plane, 1..8 warps");
+    if (c.imgs != 32 || c.bh != H || c.bw != H || c.cc < 1 || c.warps_k < 1 || c.warps_k > 16)
+        return fail(SCB_ERR_SHAPE, "image-lane launch: imgs = 32, bh = bw = plane, 1..16 warps");
     const int nbuf = c.stages == 0 ? 2 : c.stages;
     if (nbuf < 2 || nbuf > 3) return fail(SCB_ERR_SHAPE, "image-lane launch: stages must be 2 or 3");
     d->threads = 32 * c.warps_k;
-    d->row = 3 * H;
-    const int blk = (H + 2) * 3 * H;
-    int ip = c.cc * blk;
+    d->row = H;                             // = dimg.cuh RW / BLK / BASE
+    const int blk = (3 * H + 4) * H;
+    int ip = c.cc * blk + (H == 2 ? 2 : 0);
     const int vec = H;                      // floats per vector load
     while ((ip / vec) % 2 == 0 || ip % vec) ++ip;  // odd vector index: conflict-free lanes
     d->chunk = ip;
@@ -755,7 +755,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
             continue;
         }
         if (v.kind == KIND_DIMG) {
-            for (int wk : {1, 2, 4, 8})
+            for (int wk : {1, 2, 4, 8, 16})
                 for (int cc : {2, 4, 8, 16, 32})
                     for (int ns : {2, 3}) {
                         scb_launch c{vi, wk, 32, v.th, v.tw, cc, ns};
@@ -1025,8 +1025,10 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         std::memset(&q, 0, sizeof(q));
         q.x = x; q.bias = static_cast<const float*>(bias); q.y = y;
         std::vector<int> col;
-        if (ve.info.kind == KIND_DIMG)
-            for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * ve.info.th);
+        if (ve.info.kind == KIND_DIMG) {  // = dimg.cuh: BASE + START_s * H, START = {H+1, 0, 2H+2}
+            const int H = ve.info.th, start[3] = {H + 1, 0, 2 * H + 2};
+            for (int s2 = 0; s2 < g.s; ++s2) col.push_back((H == 2 ? 2 : 0) + start[s2] * H);
+        }
         else
             col = direct_cols(ve.info);
         if (ve.info.kind == KIND_DTM) {  // tap offsets in TMEM columns: slot(c) + s*RT + r
