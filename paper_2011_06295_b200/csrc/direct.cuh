@@ -128,7 +128,8 @@ __device__ __forceinline__ float fhfma(float acc, unsigned short v, unsigned sho
 // one tile of TH*LW columns, staged as one contiguous row per (image, channel).
 template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false,
           bool WIDE = false, bool ONED = false>
-__global__ void __launch_bounds__(256, MINB) k_direct(const __grid_constant__ DirectParams p) {
+// (MINB = 2 variants may run 16 warps per CTA: 512 threads, one CTA per SM, same 128 registers)
+__global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k_direct(const __grid_constant__ DirectParams p) {
     static_assert(!F16IO || VX == 2, "f16 storage reads column pairs");
     static_assert(!WIDE || (VX == 1 && !F16IO), "wide tiles: f32, one column per lane");
     static_assert(!ONED || (WIDE && R == 1), "1D tiles are wide tiles of one input row");

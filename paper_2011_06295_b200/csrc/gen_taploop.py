@@ -476,30 +476,30 @@ def main():
                     _, R, S, PAD, TH, LW, KW = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, 2, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
-                                f"{FMA}, 2, 2, true>}},\n")
+                                f"{FMA}, 2, 2, true>, 512}},\n")
                     continue
                 if v[0] == "dimg":
                     _, H, KW, mode = v
                     ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
-                                f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {mode}>}},\n")
+                                f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {mode}>, 512}},\n")
                     continue
                 if v[0] == "oned":
                     _, S, TH, KW, mode = v
                     ents.append(f"    {{{{1, {S}, {KW}, 1, {TH}, 32, SCB_F32, {WF_F32}, {mode}, {ONED}, 0, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<1, {S}, 0, {TH}, 32, {KW}, "
-                                f"{mode}, 1, 2, false, true, true>}},\n")
+                                f"{mode}, 1, 2, false, true, true>, 512}},\n")
                     continue
                 if v[0] == "wide":
                     _, R, S, PAD, TH, LW, KW, MB, mode = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {WIDE}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
-                                f"{mode}, 1, {MB}, false, true>}},\n")
+                                f"{mode}, 1, {MB}, false, true>, {512 if MB == 2 else 256}}},\n")
                     continue
                 if v[0] == "direct":
                     _, R, S, PAD, TH, LW, KW, VX, MB, mode = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, {VX}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
-                                f"{mode}, {VX}, {MB}>}},\n")
+                                f"{mode}, {VX}, {MB}>, {512 if MB == 2 else 256}}},\n")
                     continue
                 if v[0] == "plane":
                     _, H, W, R, S, PAD, KT, NBT, f16, wf, mode, minb = v

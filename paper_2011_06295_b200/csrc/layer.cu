@@ -534,8 +534,9 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
     const int G = 32 * v.nbt / v.tw;
-    if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 || c.warps_k > 8)
-        return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32*vx/tw, bh = th, bw = tw, 1..8 warps");
+    if (c.imgs != G || c.bh != v.th || c.bw != v.tw || c.cc < 1 || c.warps_k < 1 ||
+        32 * c.warps_k > variant(c.variant).max_threads)
+        return fail(SCB_ERR_SHAPE, "direct launch: imgs = 32*vx/tw, bh = th, bw = tw, warps within the kernel's bound");
     const int nbuf = c.stages == 0 ? 2 : c.stages;
     if (nbuf < 2 || nbuf > 3) return fail(SCB_ERR_SHAPE, "direct launch: stages must be 2 or 3");
     d->threads = 32 * c.warps_k;
@@ -766,7 +767,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
             continue;
         }
         if (v.kind == KIND_DIRECT) {
-            for (int wk : {1, 2, 4, 8})
+            for (int wk : {1, 2, 4, 8, 16})
                 for (int cc : {4, 8, 16, 32, 64})
                     for (int ns : {2, 3}) {
                         scb_launch c{vi, wk, 32 * v.nbt / v.tw, v.th, v.tw, cc, ns};
