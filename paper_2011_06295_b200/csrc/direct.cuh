@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
     // = layer.cu direct_copy_elems: the widest copy both the global and the shared row allow
     const int ce = (p.w % Q16 == 0 && ROW % Q16 == 0) ? Q16 : ((p.w % 2 == 0 && ROW % 2 == 0) ? 2 : 1);
     // narrow: 16-byte chunks per input row (rows have W == F == LW; derive() requires 16-byte rows)
-    constexpr int NCH = (LW * ES) / 16 > 0 ? (LW * ES) / 16 : 1;
+    constexpr int CB = LW * ES >= 16 ? 16 : LW * ES;  // bytes per staged chunk (rows under 16 B: one)
+    constexpr int QC = CB / ES;                        // elements per chunk
+    constexpr int NCH = (LW * ES) / CB;
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;
         const unsigned ncl = (unsigned)min(p.cc, C - c0);
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
             for (int it = tid; it < rows * NCH; it += nthreads) {
                 const int rr = it / NCH, q = it % NCH;
                 const uint2 rd = rdesc[rr];
-                if ((rd.y >> 24) < ncl) cp_async<16>(dst + (rd.y & 0xffffffu) + Q16 * q, src + rd.x + Q16 * q);
+                if ((rd.y >> 24) < ncl) cp_async<CB>(dst + (rd.y & 0xffffffu) + QC * q, src + rd.x + QC * q);
             }
         }
         // this warp's contiguous tap block of the stage: 16-byte chunks, one per lane
@@ -242,24 +244,32 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
     auto shift = [&](int st, int buf) {
         const unsigned ncl = (unsigned)min(p.cc, C - st * p.cc);
         TIO* base = xs + (size_t)buf * p.stage_el;
-        // thread = (row, chunk i in 0..NCH), chunk fastest (conflict-free 16-byte accesses)
-        for (int it = tid; it < rows * (NCH + 1); it += nthreads) {
-            const int rr = it / (NCH + 1), i = it % (NCH + 1);
+        // thread = (row, chunk i of CB bytes), chunk fastest (conflict-free accesses); the
+        // chunks cover the columns the odd taps read, XO .. XO+LW+S-1
+        constexpr int NSH = (LW + S + QC - 1) / QC;
+        for (int it = tid; it < rows * NSH; it += nthreads) {
+            const int rr = it / NSH, i = it % NSH;
             const uint2 rd = rdesc[rr];
             if ((rd.y >> 24) >= ncl) continue;
             const TIO* q = base + (rd.y & 0xffffffu);  // Q[XO]
             TIO* pr = const_cast<TIO*>(q) + QW;         // P[XO]
             // last 32-bit word of the previous chunk (chunk -1 = the zero left padding)
-            const unsigned prevw = *reinterpret_cast<const unsigned*>(q + Q16 * i - 4 / ES);
-            const uint4 cur = *reinterpret_cast<const uint4*>(q + Q16 * i);
-            uint4 o;
-            if constexpr (ES == 4) {
-                o = make_uint4(prevw, cur.x, cur.y, cur.z);
-            } else {  // shift by one half: word w = (cur[w] << 16) | (prev word >> 16)
-                o = make_uint4(__funnelshift_l(prevw, cur.x, 16), __funnelshift_l(cur.x, cur.y, 16),
-                               __funnelshift_l(cur.y, cur.z, 16), __funnelshift_l(cur.z, cur.w, 16));
+            const unsigned prevw = *reinterpret_cast<const unsigned*>(q + QC * i - 4 / ES);
+            if constexpr (CB == 16) {
+                const uint4 cur = *reinterpret_cast<const uint4*>(q + QC * i);
+                uint4 o;
+                if constexpr (ES == 4) {
+                    o = make_uint4(prevw, cur.x, cur.y, cur.z);
+                } else {  // shift by one half: word w = (cur[w] << 16) | (prev word >> 16)
+                    o = make_uint4(__funnelshift_l(prevw, cur.x, 16), __funnelshift_l(cur.x, cur.y, 16),
+                                   __funnelshift_l(cur.y, cur.z, 16), __funnelshift_l(cur.z, cur.w, 16));
+                }
+                *reinterpret_cast<uint4*>(pr + QC * i) = o;
+            } else if constexpr (CB == 8 && ES == 2) {  // f16 rows of 4: only 8-byte aligned
+                const uint2 cur = *reinterpret_cast<const uint2*>(q + QC * i);
+                *reinterpret_cast<uint2*>(pr + QC * i) =
+                    make_uint2(__funnelshift_l(prevw, cur.x, 16), __funnelshift_l(cur.x, cur.y, 16));
             }
-            *reinterpret_cast<uint4*>(pr + Q16 * i) = o;
         }
     };
 

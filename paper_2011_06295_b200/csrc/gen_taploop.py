@@ -395,7 +395,8 @@ WIDE, ONED = 2, 3                                # kernels.cuh DISPATCH_WIDE / D
 # 1D direct variants (H = R = 1, e.g. the reference's cnn-non-static presets): (S, TH, KW)
 DIRECTS_1D = [(s, th, kw) for s in (2, 3, 4, 5) for th in (4, 8) for kw in (4, 8)]
 # f16-storage direct variants (FHFMA, column pairs): (R, S, PAD, TH, LW, KW)
-DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)]
+DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)] + \
+              [(3, 3, 1, 4, 4, kw) for kw in (4, 8)]  # 4x4 planes: 8-byte rows, 16 images per warp
 
 
 N_PARTS = 10

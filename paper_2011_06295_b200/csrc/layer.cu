@@ -439,7 +439,9 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         return true;
     }
     if (v.kind == KIND_DIRECT || v.kind == KIND_DWS) {
-        if (g.f != v.tw || (g.w * elem_bytes(v)) % 16 != 0 || g.w > 32) return false;
+        // rows are staged in 16-byte chunks (one chunk when a row is shorter: direct.cuh CB)
+        const int cb = v.kind == KIND_DIRECT ? std::min(16, v.tw * elem_bytes(v)) : 16;
+        if (g.f != v.tw || (g.w * elem_bytes(v)) % cb != 0 || g.w > 32) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.e & 1) || (g.f & 1) || (v.th & 1))) return false;
         return true;
     }
@@ -525,7 +527,8 @@ std::vector<int> direct_cols(const scb_variant_info& v) {
 // elements per staging copy of a WIDE/ONED direct row (= direct.cuh `ce`): 16, 8 or 4 bytes
 int direct_copy_elems(const scb_variant_info& v, int w, int row) {
     const int q = 16 / elem_bytes(v);
-    if (v.dispatch != DISPATCH_WIDE && v.dispatch != DISPATCH_ONED) return q;
+    if (v.dispatch != DISPATCH_WIDE && v.dispatch != DISPATCH_ONED)  // = direct.cuh QC
+        return std::min(16, v.tw * elem_bytes(v)) / elem_bytes(v);
     if (w % q == 0 && row % q == 0) return q;
     return (w % 2 == 0 && row % 2 == 0) ? 2 : 1;
 }

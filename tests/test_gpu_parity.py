@@ -521,7 +521,7 @@ def test_image_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n):
 
 
 @pytest.mark.parametrize("c,hw,k,sp,n", [(64, 32, 64, 0.9, 3), (64, 16, 72, 0.9, 5), (256, 8, 256, 0.9, 9),
-                                         (96, 8, 40, 0.5, 7)])
+                                         (96, 8, 40, 0.5, 7), (512, 4, 512, 0.9, 37), (48, 4, 40, 0.6, 19)])
 def test_direct_f16_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     """f16 storage, f32 accumulation with FHFMA: bit-identical to the reference's
     f16 profile (f32 compute, one final round to f16)."""
