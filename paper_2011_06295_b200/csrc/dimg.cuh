@@ -30,19 +30,35 @@
 
 namespace scb {
 
-template <int H>
-struct VecT;
-template <>
-struct VecT<4> { using T = float4; };
-template <>
-struct VecT<2> { using T = float2; };
+// element type traits: f32 storage (V = H floats) or f16 storage (V = H halves;
+// FHFMA accumulation in f32, one final round -- the reference's f16 profile)
+template <int H, bool F16>
+struct DimgT;
+template <> struct DimgT<4, false> { using E = float; using V = float4; };
+template <> struct DimgT<2, false> { using E = float; using V = float2; };
+template <> struct DimgT<4, true> { using E = __half; using V = uint2; };
+template <> struct DimgT<2, true> { using E = __half; using V = unsigned; };
 
-template <int H, int KW, int MODE>
+template <int H, bool F16>
+__device__ __forceinline__ float dimg_elem(const typename DimgT<H, F16>::V& v, int x) {
+    if constexpr (!F16) return reinterpret_cast<const float*>(&v)[x];
+    else return 0.f;  // (f16 reads go through dimg_half)
+}
+template <int H>
+__device__ __forceinline__ unsigned short dimg_half(const typename DimgT<H, true>::V& v, int x) {
+    const unsigned w = reinterpret_cast<const unsigned*>(&v)[x >> 1];
+    return (unsigned short)((x & 1) ? (w >> 16) : (w & 0xffffu));
+}
+
+template <int H, int KW, int MODE, bool F16 = false>
 __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectParams p) {
-    using V = typename VecT<H>::T;
-    constexpr int RW = H;                    // row stride inside a copy
-    constexpr int BLK = (3 * H + 4) * H;     // floats per (image, channel)
-    constexpr int BASE = (H == 2) ? 2 : 0;   // copy_1's plane 16-byte aligned: (BASE + H) % 4 == 0
+    using E = typename DimgT<H, F16>::E;
+    using V = typename DimgT<H, F16>::V;
+    constexpr int ES = (int)sizeof(E);
+    constexpr int RW = H;                    // row stride inside a copy (elements)
+    constexpr int BLK = (3 * H + 4) * H;     // elements per (image, channel)
+    // BASE puts copy_1's plane on its copy alignment: f32 16 B, f16 8 B (H=2) / 16 B (H=4)
+    constexpr int BASE = F16 ? (H == 2 ? 2 : 4) : (H == 2 ? 2 : 0);
     constexpr int HW = H * H;
     constexpr int C1 = BASE + H;                  // copy_1 rows 1..H (the plane)
     constexpr int C0 = BASE + (H + 2) * H;        // copy_0 rows 1..H
@@ -55,39 +71,43 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
     const int n0 = (blockIdx.x / p.kblocks) * 32;
     const int k0 = (kb * p.wk + warp) * KW;
     const int C = p.c;
-    float* xs = reinterpret_cast<float*>(smem);
+    E* xs = reinterpret_cast<E*>(smem);
     const int planes = 32 * p.cc;  // (image, channel) planes per stage
     // tap blocks after the stages: [buf][warp] slots of segcap 16-byte chunks (direct.cuh layout)
-    int4* tsm = reinterpret_cast<int4*>(smem + (size_t)p.nbuf * p.stage_el * 4);
+    int4* tsm = reinterpret_cast<int4*>(smem + (size_t)p.nbuf * p.stage_el * ES);
     constexpr int HDR = (KW * 4 + 15) / 16;
     const int grp = kb * p.wk + warp;
     const int groups = (p.k + KW - 1) / KW;
 
     {  // zero both stages: padding rows and the halo ends of copies 0 / 2 stay zero
         float4* z = reinterpret_cast<float4*>(smem);
-        const int n16 = (p.nbuf * p.stage_el * 4) / 16;
+        const int n16 = (p.nbuf * p.stage_el * ES) / 16;
         for (int i = tid; i < n16; i += nthreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
 
-    // plane t of a stage: image t / cc, channel slot t % cc; 16-byte chunks, chunk fastest
-    constexpr int PQ = HW / 4;
-    const float* xg = static_cast<const float*>(p.x) + (size_t)n0 * C * HW;
+    // plane t of a stage: image t / cc, channel slot t % cc; chunks of CH bytes, chunk fastest.
+    // Odd images sit at half the copy alignment (odd vector image pitch): two half copies.
+    constexpr int PB = HW * ES;               // plane bytes
+    constexpr int CH = PB >= 16 ? 16 : PB;    // copy chunk
+    constexpr int PQ = PB / CH, QE = CH / ES;
+    const E* xg = static_cast<const E*>(p.x) + (size_t)n0 * C * HW;
     auto stage = [&](int st, int buf) {
         const int c0 = st * p.cc;
         const int ncl = min(p.cc, C - c0);
-        float* dst = xs + (size_t)buf * p.stage_el;
+        E* dst = xs + (size_t)buf * p.stage_el;
         for (int it = tid; it < planes * PQ; it += nthreads) {
             const int q = it % PQ, t = it / PQ;
             const int cl = t % p.cc, img = t / p.cc;
             if (cl < ncl && n0 + img < p.n) {
-                float* d = dst + img * p.ip + cl * BLK + C1 + 4 * q;
-                const float* g = xg + ((size_t)img * C + c0 + cl) * HW + 4 * q;
-                if (H == 4 || !(img & 1)) {
-                    cp_async<16>(d, g);
-                } else {  // H = 2: odd images sit 8 bytes off (odd float2 image pitch)
-                    cp_async<8>(d, g);
-                    cp_async<8>(d + 2, g + 2);
+                const int off = img * p.ip + cl * BLK + C1 + QE * q;
+                E* d = dst + off;
+                const E* g = xg + ((size_t)img * C + c0 + cl) * HW + QE * q;
+                if ((off * ES) % CH == 0) {
+                    cp_async<CH>(d, g);
+                } else {
+                    cp_async<CH / 2>(d, g);
+                    cp_async<CH / 2>(d + QE / 2, g + QE / 2);
                 }
             }
         }
@@ -103,8 +123,24 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
     // copy_0 row = (0, x0 .. x_{H-2}), copy_2 row = (x1 .. x_{H-1}, 0), from copy_1
     auto shift = [&](int st, int buf) {
         const int ncl = min(p.cc, C - st * p.cc);
-        float* base = xs + (size_t)buf * p.stage_el;
-        if constexpr (H == 2) {  // thread = plane (8-byte accesses: odd images are 8-byte aligned)
+        E* base = xs + (size_t)buf * p.stage_el;
+        if constexpr (F16) {  // thread = (plane, row); 32-bit words of halves
+            for (int it = tid; it < planes * H; it += nthreads) {
+                const int y = it % H, t = it / H;
+                const int cl = t % p.cc, img = t / p.cc;
+                if (cl >= ncl) continue;
+                E* b = base + img * p.ip + cl * BLK + y * H;
+                if constexpr (H == 2) {
+                    const unsigned w = *reinterpret_cast<const unsigned*>(b + C1);
+                    *reinterpret_cast<unsigned*>(b + C0) = w << 16;   // (0, x0)
+                    *reinterpret_cast<unsigned*>(b + C2) = w >> 16;   // (x1, 0)
+                } else {
+                    const uint2 w = *reinterpret_cast<const uint2*>(b + C1);
+                    *reinterpret_cast<uint2*>(b + C0) = make_uint2(w.x << 16, __funnelshift_l(w.x, w.y, 16));
+                    *reinterpret_cast<uint2*>(b + C2) = make_uint2(__funnelshift_r(w.x, w.y, 16), w.y >> 16);
+                }
+            }
+        } else if constexpr (H == 2) {  // thread = plane (8-byte accesses: odd images are 8-byte aligned)
             for (int t = tid; t < planes; t += nthreads) {
                 const int cl = t % p.cc, img = t / p.cc;
                 if (cl >= ncl) continue;
@@ -155,7 +191,7 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
         cp_async_commit();  // possibly empty: keeps one group per iteration
         // lane's image block, minus the stage's first channel (tap offsets are absolute)
         const char* xl = reinterpret_cast<const char*>(xs + (size_t)buf * p.stage_el + lane * p.ip) -
-                         (size_t)st * p.cc * BLK * 4;
+                         (size_t)st * p.cc * BLK * ES;
         const int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
         const int* cnt = reinterpret_cast<const int*>(tb);
         const DirectTap* seg = reinterpret_cast<const DirectTap*>(tb + HDR);
@@ -167,13 +203,19 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
 #pragma unroll 4
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
-                const float* xp = reinterpret_cast<const float*>(xl + tp.off);
+                const E* xp = reinterpret_cast<const E*>(xl + tp.off);
 #pragma unroll
                 for (int y = 0; y < H; ++y) {
                     const V v = *reinterpret_cast<const V*>(xp + y * RW);
-                    const float* vf = reinterpret_cast<const float*>(&v);
+                    if constexpr (F16) {
+                        const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
 #pragma unroll
-                    for (int x = 0; x < H; ++x) acc[kk][y * H + x] = mac1<MODE>(acc[kk][y * H + x], tp.v, vf[x]);
+                        for (int x = 0; x < H; ++x) acc[kk][y * H + x] = fhfma(acc[kk][y * H + x], vh, dimg_half<H>(v, x));
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < H; ++x)
+                            acc[kk][y * H + x] = mac1<MODE>(acc[kk][y * H + x], tp.v, dimg_elem<H, F16>(v, x));
+                    }
                 }
             }
             seg += nt;
@@ -194,25 +236,31 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
 #pragma unroll
         for (int j = 0; j < HW; ++j) o[j] = (relu && acc[kk][j] < 0.f) ? 0.f : acc[kk][j];
         if (!pool) {
-            float* yp = static_cast<float*>(p.y) + ((int64_t)n * p.k + k) * HW;
+            E* yp = static_cast<E*>(p.y) + ((int64_t)n * p.k + k) * HW;
+            if constexpr (F16) {
 #pragma unroll
-            for (int j = 0; j < HW; j += H) *reinterpret_cast<V*>(yp + j) = *reinterpret_cast<const V*>(&o[j]);
+                for (int j = 0; j < HW; j += 2)
+                    *reinterpret_cast<__half2*>(yp + j) = __floats2half2_rn(o[j], o[j + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < HW; j += H) *reinterpret_cast<V*>(yp + j) = *reinterpret_cast<const V*>(&o[j]);
+            }
         } else {
             constexpr int PH = H / 2;
-            float* yp = static_cast<float*>(p.y) + ((int64_t)n * p.k + k) * PH * PH;
+            E* yp = static_cast<E*>(p.y) + ((int64_t)n * p.k + k) * PH * PH;
 #pragma unroll
             for (int yy = 0; yy < PH; ++yy)
 #pragma unroll
                 for (int xx = 0; xx < PH; ++xx)
-                    yp[yy * PH + xx] = fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
-                                             fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1]));
+                    yp[yy * PH + xx] = (E)fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
+                                                fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1]));
         }
     }
 }
 
-template <int H, int KW, int MODE>
+template <int H, int KW, int MODE, bool F16 = false>
 cudaError_t launch_dimg_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_dimg<H, KW, MODE>;
+    auto kern = k_dimg<H, KW, MODE, F16>;
     static int max_dyn = -1;  // benign race: idempotent
     if (max_dyn < 0) {
         cudaFuncAttributes fa;

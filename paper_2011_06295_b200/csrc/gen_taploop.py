@@ -369,6 +369,7 @@ DTMS = [(8, lw, kw, m) for lw in (32, 16, 8) for kw in (4, 8) for m in (2, 4)] +
 DWS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)]
 # image-lane direct variants (dimg.cuh): (H, KW)
 DIMGS = [(4, 1), (4, 2), (4, 4), (2, 1), (2, 2), (2, 4), (2, 8)]
+DIMGS_F16 = [(2, 2), (2, 4), (2, 8), (4, 2), (4, 4)]  # f16 storage, FHFMA
 
 # dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW, VX)
 DIRECTS = [(3, 3, 1, th, lw, kw, 1) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \
@@ -443,6 +444,8 @@ def main():
         groups[("direct16", R, S, PAD, TH, LW, KW)] = ([], [("direct16", R, S, PAD, TH, LW, KW)])
     for H, KW in DIMGS:
         groups[("dimg", H, KW)] = ([], [("dimg", H, KW, mode) for mode in (EXACT, FMA)])
+    for H, KW in DIMGS_F16:
+        groups[("dimg16", H, KW)] = ([], [("dimg16", H, KW)])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -478,6 +481,11 @@ def main():
                     ents.append(f"    {{{{{R}, {S}, {KW}, 2, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
                                 f"{FMA}, 2, 2, true>, 512}},\n")
+                    continue
+                if v[0] == "dimg16":
+                    _, H, KW = v
+                    ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, 1, "
+                                f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {FMA}, true>, 512}},\n")
                     continue
                 if v[0] == "dimg":
                     _, H, KW, mode = v

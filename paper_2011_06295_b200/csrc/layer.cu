@@ -578,6 +578,11 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
 }
 
 // Image-lane direct variants (dimg.cuh): 32 images per CTA, (H+2) x 3H floats per (image, channel).
+// = dimg.cuh BASE (elements before copy_1's padded row 0 in an (image, channel) block)
+int dimg_base(const scb_variant_info& v) {
+    return v.io == SCB_F16 ? (v.th == 2 ? 2 : 4) : (v.th == 2 ? 2 : 0);
+}
+
 scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
@@ -587,14 +592,15 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const int nbuf = c.stages == 0 ? 2 : c.stages;
     if (nbuf < 2 || nbuf > 3) return fail(SCB_ERR_SHAPE, "image-lane launch: stages must be 2 or 3");
     d->threads = 32 * c.warps_k;
+    const int es = elem_bytes(v);
     d->row = H;                             // = dimg.cuh RW / BLK / BASE
     const int blk = (3 * H + 4) * H;
-    int ip = c.cc * blk + (H == 2 ? 2 : 0);
-    const int vec = H;                      // floats per vector load
+    int ip = c.cc * blk + dimg_base(v);
+    const int vec = H;                      // elements per vector load
     while ((ip / vec) % 2 == 0 || ip % vec) ++ip;  // odd vector index: conflict-free lanes
     d->chunk = ip;
-    const size_t stage_bytes = ((size_t)32 * ip * 4 + 127) & ~(size_t)127;
-    d->stage_el = (int)(stage_bytes / 4);
+    const size_t stage_bytes = ((size_t)32 * ip * es + 127) & ~(size_t)127;
+    d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = blk;
     const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
     if (cap < 0) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
@@ -1031,7 +1037,7 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         std::vector<int> col;
         if (ve.info.kind == KIND_DIMG) {  // = dimg.cuh: BASE + START_s * H, START = {H+1, 0, 2H+2}
             const int H = ve.info.th, start[3] = {H + 1, 0, 2 * H + 2};
-            for (int s2 = 0; s2 < g.s; ++s2) col.push_back((H == 2 ? 2 : 0) + start[s2] * H);
+            for (int s2 = 0; s2 < g.s; ++s2) col.push_back(dimg_base(ve.info) + start[s2] * H);
         }
         else
             col = direct_cols(ve.info);

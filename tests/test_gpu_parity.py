@@ -493,31 +493,34 @@ def test_oned_direct_kernels_bitwise(sc, orc, c, w, k, s, sp, n):
     assert beq(o, np.maximum(ref, 0))
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float16])
 @pytest.mark.parametrize("c,hw,k,sp,n", [(512, 4, 512, 0.9, 40), (96, 4, 40, 0.5, 7), (512, 2, 512, 0.9, 70),
                                          (64, 2, 72, 0.8, 33), (24, 4, 16, 0.9, 3)])
-def test_image_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n):
+def test_image_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n, dt):
+    """Image-lane kernel, f32 exact and f16 storage (FHFMA, one final round)."""
     import torch
     from paper_2011_06295_b200 import _abi
     from paper_2011_06295_b200.device import device_layer
     from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
     sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
-    w = make_layer_weights(LayerSpec("l", sh, sp), seed=0)
+    w = make_layer_weights(LayerSpec("l", sh, sp), seed=0).astype(dt)
     x, b = bench_inputs(sh, n)
+    x, b = x.astype(dt), b.astype(dt)
     kern = sc.build_csr(w, sh)
     ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
     xd = torch.from_numpy(x).cuda()
-    layer = device_layer(kern, 0, np.float32)
+    layer = device_layer(kern, 0, dt)
     vs = _abi.variants()
     cands = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] == 3]
     assert cands, "no image-lane variant"
     for cfg in cands[:: max(1, len(cands) // 30)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
-    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref)), 2).numpy()
+    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref.astype(np.float32))), 2).numpy()
     pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 3]
     for cfg in pc[:: max(1, len(pc) // 6)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
-        assert beq(o, want), cfg
+        assert beq(o, want.astype(dt)), cfg
 
 
 @pytest.mark.parametrize("c,hw,k,sp,n", [(64, 32, 64, 0.9, 3), (64, 16, 72, 0.9, 5), (256, 8, 256, 0.9, 9),
