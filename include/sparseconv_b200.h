@@ -63,6 +63,8 @@ typedef struct {
 #define SCB_FLAG_POOL2     0x4u   /* fused 2x2/2 max-pool epilogue (VGG stage glue) */
 #define SCB_FLAG_GENERIC   0x8u   /* force the generic (any-geometry) kernel        */
 #define SCB_FLAG_NO_PDL    0x10u  /* launch without programmatic dependent launch   */
+#define SCB_FLAG_ACT_QUANT 0x20u  /* fused activation fake-quant epilogue with the
+                                     layer's scb_act_quant (store.py:285-286)      */
 
 /* Launch configuration: replaces EnginePlan.sub_batch_size (engine.py:28-39)
  * and the timed tune_sub_batch (engine.py:143-166). variant < 0 = generic. */
@@ -183,6 +185,27 @@ SCB_API scb_status scb_variant_get(int32_t idx, scb_variant_info* out);
 /* 2x2 stride-2 max pool over (n*c) planes of h x w (h, w even). */
 SCB_API scb_status scb_maxpool2(scb_dtype dt, const void* x, void* y, int64_t planes,
                                 int32_t h, int32_t w, void* stream);
+
+/* Activation fake-quant parameters (the reference's layer.act_quant dict,
+ * quantize.py:324-326; applied by fake_quant_activation, quantize.py:332-338):
+ * a -> clip(a, clip_lo, clip_hi) in the activation dtype, code = clamp(rint((c - mu) / step))
+ * in f64 over [0, 2^bits-1] (asymmetric) or [-(2^(bits-1)-1), 2^(bits-1)-1] (symmetric),
+ * a' = (dtype)(mu + code * step).  Bit-identical to the reference. */
+typedef struct {
+    int32_t bits;
+    int32_t symmetric;   /* 0: "asymmetric", 1: "symmetric" */
+    double clip_lo, clip_hi, mu, step;
+} scb_act_quant;
+
+/* In-place fake-quant of `count` activations of dtype dt on `stream`
+ * (replaces fake_quant_activation, quantize.py:332-338). */
+SCB_API scb_status scb_fake_quant(scb_dtype dt, void* y, int64_t count, const scb_act_quant* q,
+                                  void* stream);
+
+/* Attach (q != NULL) or clear (NULL) a layer's activation quantizer; conv calls with
+ * SCB_FLAG_ACT_QUANT apply it to the layer output (fused into the direct and
+ * image-lane epilogues, a following scb_fake_quant pass for the other kernels). */
+SCB_API scb_status scb_layer_set_act_quant(scb_layer* layer, const scb_act_quant* q);
 
 /* ---------------------------------------------------------------------- */
 /* measurement                                                            */

@@ -25,6 +25,7 @@ SCB_F32, SCB_F64, SCB_F16 = 0, 1, 2
 SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16 = 0, 1, 2
 
 FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC, FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8, 0x10
+FLAG_ACT_QUANT = 0x20
 
 # every symbol include/sparseconv_b200.h declares
 EXPORTS = (
@@ -32,7 +33,8 @@ EXPORTS = (
     "scb_validate_csr", "scb_decompress", "scb_layer_create", "scb_layer_destroy",
     "scb_layer_weight_bytes", "scb_conv_sparse", "scb_launch_candidates",
     "scb_default_launch", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
-    "scb_fma_peaks", "scb_fnv1a64", "scb_last_error", "scb_version",
+    "scb_fma_peaks", "scb_fnv1a64", "scb_last_error", "scb_version", "scb_fake_quant",
+    "scb_layer_set_act_quant",
 )
 
 
@@ -49,6 +51,20 @@ class Launch(ctypes.Structure):
     @classmethod
     def from_tuple(cls, t):
         return cls(*[int(v) for v in t])
+
+
+class ActQuant(ctypes.Structure):
+    """scb_act_quant: the reference's layer.act_quant dict (quantize.py:324-326)."""
+    _fields_ = [("bits", ctypes.c_int32), ("symmetric", ctypes.c_int32), ("clip_lo", ctypes.c_double),
+                ("clip_hi", ctypes.c_double), ("mu", ctypes.c_double), ("step", ctypes.c_double)]
+
+    @classmethod
+    def from_dict(cls, aq: dict):
+        mode = aq.get("mode", "asymmetric")
+        if mode not in ("asymmetric", "symmetric"):
+            raise ValueError(f"unknown activation quantization mode {mode!r}")
+        return cls(int(aq["bits"]), 1 if mode == "symmetric" else 0, float(aq["clip_lo"]),
+                   float(aq["clip_hi"]), float(aq["mu"]), float(aq["step"]))
 
 
 class VariantInfo(ctypes.Structure):
@@ -98,6 +114,8 @@ def lib():
             "scb_maxpool2": [i32, vp, vp, i64, i32, i32, vp],
             "scb_fma_peaks": [i32, vp, vp, i32, P(i32)],
             "scb_fnv1a64": [vp, i64, P(ctypes.c_uint64)],
+            "scb_fake_quant": [i32, vp, i64, P(ActQuant), vp],
+            "scb_layer_set_act_quant": [vp, P(ActQuant)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -145,6 +163,15 @@ def variants():
 
 
 _DT_CODE = {"float32": SCB_F32, "float64": SCB_F64, "float16": SCB_F16}
+
+
+def fake_quant(dtype, y_ptr: int, count: int, aq: dict, stream: int = 0) -> None:
+    """In-place activation fake-quant of `count` device values (scb_fake_quant,
+    the reference's fake_quant_activation, quantize.py:332-338)."""
+    import numpy as np
+    q = ActQuant.from_dict(aq)
+    check(lib().scb_fake_quant(_DT_CODE[str(np.dtype(dtype))], ctypes.c_void_p(y_ptr), int(count),
+                               ctypes.byref(q), ctypes.c_void_p(stream)), "scb_fake_quant")
 
 
 def maxpool2(dtype, x_ptr: int, y_ptr: int, planes: int, h: int, w: int, stream: int = 0) -> None:

@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
     if (n >= p.n) return;
     const bool relu = p.flags & SCB_FLAG_RELU;
     const bool pool = p.flags & SCB_FLAG_POOL2;
+    const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -240,8 +241,13 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
             if constexpr (F16) {
 #pragma unroll
                 for (int j = 0; j < HW; j += 2)
-                    *reinterpret_cast<__half2*>(yp + j) = __floats2half2_rn(o[j], o[j + 1]);
+                    *reinterpret_cast<__half2*>(yp + j) =
+                        __halves2half2(out_val<__half>(o[j], aq, p.aq), out_val<__half>(o[j + 1], aq, p.aq));
             } else {
+                if (aq) {
+#pragma unroll
+                    for (int j = 0; j < HW; ++j) o[j] = fq_f32(o[j], p.aq);
+                }
 #pragma unroll
                 for (int j = 0; j < HW; j += H) *reinterpret_cast<V*>(yp + j) = *reinterpret_cast<const V*>(&o[j]);
             }
@@ -252,8 +258,9 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
             for (int yy = 0; yy < PH; ++yy)
 #pragma unroll
                 for (int xx = 0; xx < PH; ++xx)
-                    yp[yy * PH + xx] = (E)fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
-                                                fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1]));
+                    yp[yy * PH + xx] = out_val<E>(fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
+                                                        fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1])),
+                                                  aq, p.aq);
         }
     }
 }

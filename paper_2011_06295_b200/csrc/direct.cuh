@@ -57,6 +57,7 @@ struct DirectParams {
     int segcap;               // taps per (output channel, stage) segment slot in shared memory
     int nbuf;                 // stage buffers in flight (2 or 3)
     int nfx;                  // k_direct WIDE: column tiles of LW per output row
+    ActQuant aq;              // activation fake-quant (flags & SCB_FLAG_ACT_QUANT)
     const int32_t* blkoff;    // k_direct: [group*nst + st] 16-byte-chunk offset of each tap block (+ end)
     uint32_t flags;
 };
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
     const int n = n0 + lg;
     const bool relu = p.flags & SCB_FLAG_RELU;
     const bool pool = p.flags & SCB_FLAG_POOL2;
+    const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 for (int j = 0; j < TH; ++j) {
                     float o0 = acc[kk][j];
                     if (relu && o0 < 0.f) o0 = 0.f;
-                    if (ox0 + lx + j * LW < p.f) yp[j * LW] = o0;
+                    if (ox0 + lx + j * LW < p.f) yp[j * LW] = out_val<TIO>(o0, aq, p.aq);
                 }
             }
         } else if (!pool) {
@@ -371,14 +373,16 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                     float o0 = acc[kk][j * VX];
                     if (relu && o0 < 0.f) o0 = 0.f;
                     if constexpr (VX == 1) {
-                        yp[j * FP * fpitch] = o0;
+                        yp[j * FP * fpitch] = out_val<TIO>(o0, aq, p.aq);
                     } else {
                         float o1 = acc[kk][j * VX + 1];
                         if (relu && o1 < 0.f) o1 = 0.f;
                         if constexpr (F16IO)
-                            *reinterpret_cast<__half2*>(yp + j * LW) = __floats2half2_rn(o0, o1);
+                            *reinterpret_cast<__half2*>(yp + j * LW) =
+                                __halves2half2(out_val<__half>(o0, aq, p.aq), out_val<__half>(o1, aq, p.aq));
                         else
-                            *reinterpret_cast<float2*>(yp + j * LW) = make_float2(o0, o1);
+                            *reinterpret_cast<float2*>(yp + j * LW) =
+                                make_float2(out_val<float>(o0, aq, p.aq), out_val<float>(o1, aq, p.aq));
                     }
                 }
             }
@@ -396,7 +400,8 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 if (relu && o < 0.f) o = 0.f;
                 const int py = (oy0 + j) >> 1;
                 if (n < p.n && !(lx & 1) && ox0 + lx < p.f && py < pe)
-                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] = (TIO)o;
+                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] =
+                        out_val<TIO>(o, aq, p.aq);
             }
         }
     }

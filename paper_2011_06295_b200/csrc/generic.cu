@@ -108,6 +108,29 @@ __global__ void k_maxpool2(const T* __restrict__ x, T* __restrict__ y, int64_t p
     }
 }
 
+// Activation fake-quant pass (quantize.py:332-338) over `count` activations in place.
+template <typename T>
+__global__ void k_fake_quant(T* y, int64_t count, const ActQuant q) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        if constexpr (std::is_same<T, __half>::value) y[i] = fq_f16(y[i], q);
+        else if constexpr (std::is_same<T, double>::value) y[i] = fq_f64(y[i], q);
+        else y[i] = fq_f32(y[i], q);
+    }
+}
+
+cudaError_t launch_fake_quant(int dtype, void* y, int64_t count, const ActQuant& q, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (dtype == SCB_F16)
+        k_fake_quant<__half><<<(unsigned)blocks, 256, 0, st>>>((__half*)y, count, q);
+    else if (dtype == SCB_F64)
+        k_fake_quant<double><<<(unsigned)blocks, 256, 0, st>>>((double*)y, count, q);
+    else
+        k_fake_quant<float><<<(unsigned)blocks, 256, 0, st>>>((float*)y, count, q);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_maxpool2(int dtype, const void* x, void* y, int64_t planes, int h, int w, cudaStream_t st) {
     const int64_t total = planes * (h >> 1) * (w >> 1);
     if (total == 0) return cudaSuccess;

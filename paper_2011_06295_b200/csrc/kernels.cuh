@@ -22,6 +22,46 @@ enum { DISPATCH_JUMP = 0,   // brx.idx jump table, one indirect branch per tap
        DISPATCH_WIDE = 2,   // (direct kind) column tiles of tw for any row width
        DISPATCH_ONED = 3 }; // (direct kind) 1D rows: tiles of th*tw columns, H = R = 1
 
+// Activation fake-quant (quantize.py:332-338, affine int quantize.py:122-138): clip in
+// the activation dtype, code = clamp(rint((c - mu) / step)) in f64, mu + code*step in
+// f64, one round to the activation dtype.  Separate IEEE roundings as numpy does.
+struct ActQuant {
+    float lo, hi;         // clip bounds rounded to the activation dtype (f32 / f16 values)
+    double dlo, dhi;      // ... as f64 (f64 activations)
+    double mu, step, clo, chi;
+};
+__device__ __forceinline__ double fq_code(double c, const ActQuant& q) {
+    double r = rint(__ddiv_rn(__dsub_rn(c, q.mu), q.step));
+    return fmin(fmax(r, q.clo), q.chi);
+}
+__device__ __forceinline__ double fq_value(double code, const ActQuant& q) {
+    return __dadd_rn(q.mu, __dmul_rn(code, q.step));
+}
+__device__ __forceinline__ float fq_f32(float a, const ActQuant& q) {
+    const float c = fminf(fmaxf(a, q.lo), q.hi);
+    return __double2float_rn(fq_value(fq_code((double)c, q), q));
+}
+__device__ __forceinline__ __half fq_f16(__half a, const ActQuant& q) {
+    const float c = fminf(fmaxf(__half2float(a), q.lo), q.hi);  // exact: f16 values in f32
+    return __double2half(fq_value(fq_code((double)c, q), q));
+}
+__device__ __forceinline__ double fq_f64(double a, const ActQuant& q) {
+    return fq_value(fq_code(fmin(fmax(a, q.dlo), q.dhi), q), q);
+}
+
+// epilogue store value: one round to the storage type, then the optional fake-quant
+template <typename T>
+__device__ __forceinline__ T out_val(float o, bool aq, const ActQuant& q);
+template <>
+__device__ __forceinline__ float out_val<float>(float o, bool aq, const ActQuant& q) {
+    return aq ? fq_f32(o, q) : o;
+}
+template <>
+__device__ __forceinline__ __half out_val<__half>(float o, bool aq, const ActQuant& q) {
+    const __half h = __float2half_rn(o);
+    return aq ? fq_f16(h, q) : h;
+}
+
 template <int MODE>
 __device__ __forceinline__ float mac1(float acc, float v, float x) {
     if constexpr (MODE == MODE_EXACT) return __fadd_rn(acc, __fmul_rn(v, x));

@@ -62,6 +62,8 @@ struct Program {
 
 struct scb_layer {
     Geom g{};
+    bool has_aq = false;  // activation fake-quant attached (scb_layer_set_act_quant)
+    ActQuant aq{};
     scb_dtype dt = SCB_F32;
     scb_wfmt wfmt = SCB_W_NATIVE;
     int wf = WF_F32;
@@ -1000,9 +1002,28 @@ SCB_API scb_status scb_default_launch(const scb_layer* layer, int32_t n, uint32_
     return SCB_OK;
 }
 
+static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const void* bias, void* y, int32_t n,
+                                   uint32_t flags, const scb_launch* cfg, void* stream, bool* fused_aq);
+
 SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
                                    void* y, int32_t n, uint32_t flags,
                                    const scb_launch* cfg, void* stream) {
+    if (layer && (flags & SCB_FLAG_ACT_QUANT) && !layer->has_aq)
+        return fail(SCB_ERR_ARG, "SCB_FLAG_ACT_QUANT on a layer without an activation quantizer");
+    bool fused = false;
+    scb_status s = conv_sparse_impl(layer, x, bias, y, n, flags, cfg, stream, &fused);
+    if (s != SCB_OK || !(flags & SCB_FLAG_ACT_QUANT) || fused || n == 0) return s;
+    // kernels without the fused epilogue: one in-place pass over the layer output
+    const Geom& g = layer->g;
+    const bool pool = flags & SCB_FLAG_POOL2;
+    const int64_t count = (int64_t)n * g.k * (pool ? g.e / 2 : g.e) * (pool ? g.f / 2 : g.f);
+    DeviceGuard dg(layer->device);
+    cudaError_t e = launch_fake_quant(layer->dt, y, count, layer->aq, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SCB_OK : cuda_fail(e, "fake-quant launch");
+}
+
+static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const void* bias, void* y, int32_t n,
+                                   uint32_t flags, const scb_launch* cfg, void* stream, bool* fused_aq) {
     if (!layer) return fail(SCB_ERR_ARG, "layer is NULL");
     auto* L = const_cast<scb_layer*>(layer);
     if (n < 0) return fail(SCB_ERR_SHAPE, "negative batch");
@@ -1064,6 +1085,12 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
         q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nfx = d.n_fx; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
+        if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {  // fused fake-quant epilogue
+            q.aq = L->aq;
+            *fused_aq = true;
+        } else {
+            q.flags &= ~SCB_FLAG_ACT_QUANT;
+        }
         q.nbuf = c.stages == 0 ? (ve.info.kind == KIND_DWS ? 3 : 2) : c.stages;
         cudaError_t e = ve.dlaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
         return e == cudaSuccess ? SCB_OK : cuda_fail(e, "direct kernel launch");
@@ -1091,6 +1118,58 @@ SCB_API scb_status scb_variant_get(int32_t idx, scb_variant_info* out) {
     if (idx < 0 || idx >= num_variants() || !out) return fail(SCB_ERR_ARG, "bad variant index");
     *out = variant(idx).info;
     return SCB_OK;
+}
+
+static scb_status make_act_quant(const scb_act_quant* q, scb_dtype dt, ActQuant* out) {
+    if (!q) return fail(SCB_ERR_ARG, "act quant is NULL");
+    if (q->bits < 1 || q->bits > 31 || !(q->step > 0.0) || (q->symmetric != 0 && q->symmetric != 1))
+        return fail(SCB_ERR_ARG, "act quant: bits in 1..31, step > 0, symmetric 0/1");
+    ActQuant a{};
+    if (dt == SCB_F16) {  // bounds rounded to the activation dtype (numpy's weak python scalars)
+        a.lo = __half2float(__double2half(q->clip_lo));
+        a.hi = __half2float(__double2half(q->clip_hi));
+    } else {
+        a.lo = (float)q->clip_lo;
+        a.hi = (float)q->clip_hi;
+    }
+    a.dlo = q->clip_lo;
+    a.dhi = q->clip_hi;
+    a.mu = q->mu;
+    a.step = q->step;
+    if (q->symmetric) {
+        a.chi = std::ldexp(1.0, q->bits - 1) - 1.0;
+        a.clo = -a.chi;
+    } else {
+        a.clo = 0.0;
+        a.chi = std::ldexp(1.0, q->bits) - 1.0;
+    }
+    *out = a;
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_layer_set_act_quant(scb_layer* layer, const scb_act_quant* q) {
+    if (!layer) return fail(SCB_ERR_ARG, "layer is NULL");
+    if (!q) {
+        layer->has_aq = false;
+        return SCB_OK;
+    }
+    ActQuant a;
+    scb_status s = make_act_quant(q, layer->dt, &a);
+    if (s != SCB_OK) return s;
+    layer->aq = a;
+    layer->has_aq = true;
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_fake_quant(scb_dtype dt, void* y, int64_t count, const scb_act_quant* q, void* stream) {
+    if (count < 0) return fail(SCB_ERR_ARG, "negative count");
+    if (count > 0 && !y) return fail(SCB_ERR_ARG, "y is NULL");
+    if (dtype_size(dt) == 0) return fail(SCB_ERR_ARG, "bad dtype");
+    ActQuant a;
+    scb_status s = make_act_quant(q, dt, &a);
+    if (s != SCB_OK) return s;
+    cudaError_t e = launch_fake_quant(dt, y, count, a, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SCB_OK : cuda_fail(e, "fake-quant launch");
 }
 
 SCB_API scb_status scb_maxpool2(scb_dtype dt, const void* x, void* y, int64_t planes, int32_t h,

@@ -85,6 +85,13 @@ class DeviceLayer:
                                                      ctypes.byref(b)))
         return int(b.value)
 
+    def set_act_quant(self, aq: dict | None) -> None:
+        """Attach (dict as in the reference's layer.act_quant, quantize.py:324-326)
+        or clear (None) the activation fake-quant applied under FLAG_ACT_QUANT."""
+        q = None if aq is None else ctypes.byref(_abi.ActQuant.from_dict(aq))
+        _abi.check(_abi.lib().scb_layer_set_act_quant(ctypes.c_void_p(self.handle), q),
+                   "scb_layer_set_act_quant")
+
     def signature(self):
         """Key of the tuner cache: everything the best launch depends on."""
         sh = self.shape

@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi, engine
-from .device import device_layer
+from .device import DeviceLayer, device_layer
 from .errors import ShapeError
 from .weights import CsrKernel
 
@@ -43,6 +43,7 @@ class NetLayer:
     bias: np.ndarray | None = None
     relu: bool = True
     pool: bool = False  # fused 2x2 stride-2 max-pool after the activation
+    act_quant: dict | None = None  # activation fake-quant after the ReLU (store.py:285-286)
 
 
 class SparseConvNet:
@@ -82,7 +83,12 @@ class SparseConvNet:
         for L in self.layers:
             if self.dtype == np.float16 and L.kernel.values.dtype != np.float16:
                 raise ShapeError(f"{L.name}: f16 activations need f16 weights")
-            self.dlayers.append(device_layer(L.kernel, self.device, self.dtype, weight_format))
+            if L.act_quant is None:
+                self.dlayers.append(device_layer(L.kernel, self.device, self.dtype, weight_format))
+            else:  # a private device layer: the quantizer is attached to it
+                dl = DeviceLayer(L.kernel, self.device, self.dtype, weight_format)
+                dl.set_act_quant(L.act_quant)
+                self.dlayers.append(dl)
             if L.bias is None:
                 self.biases.append(None)
             else:
@@ -107,6 +113,8 @@ class SparseConvNet:
             f |= _abi.FLAG_POOL2
         if self.fast_math:
             f |= _abi.FLAG_FAST
+        if L.act_quant is not None:
+            f |= _abi.FLAG_ACT_QUANT
         return f
 
     def out_shape(self, i: int, n: int):
@@ -198,6 +206,7 @@ class SparseConvNet:
             if self.algorithms[i] == "dense-cudnn":
                 with self.torch.cuda.stream(stream):
                     self.dense_layer(i)(cur[a:e], self.acts[i][a:e])
+                self._dense_quant(i, self.acts[i][a:e], stream.cuda_stream)
             else:
                 self.launch_layer(i, cur, self.acts[i], stream.cuda_stream, rows)
             if i == 0 and on_first is not None:
@@ -269,10 +278,27 @@ class SparseConvNet:
                 launches[i] = None if ch["launch"] is None else tuple(ch["launch"])
         self.set_launches(launches)
 
+    def _dense_quant(self, i: int, out, stream: int) -> None:
+        """Activation fake-quant after a dense (cuDNN) layer (store.py:285-286)."""
+        aq = self.layers[i].act_quant
+        if aq is not None:
+            _abi.fake_quant(self.dtype, out.data_ptr(), out.numel(), aq, stream)
+
     def kernels_per_step(self) -> int:
-        """Kernel launches of one forward (a generic layer with a pool is two)."""
-        return sum(0 if a == "dense-cudnn" else (2 if (l is None and L.pool) else 1)
-                   for l, L, a in zip(self.launches, self.layers, self.algorithms))
+        """Our kernel launches in one forward: one per sparse layer, +1 for a generic
+        layer's separate pool, +1 for a fake-quant pass the layer's kernel does not fuse
+        (only the direct and image-lane epilogues do), +1 after a dense layer with one."""
+        vs = _abi.variants()
+        n = 0
+        for l, L, a in zip(self.launches, self.layers, self.algorithms):
+            aq = L.act_quant is not None
+            if a == "dense-cudnn":
+                n += 1 if aq else 0
+                continue
+            n += 2 if (l is None and L.pool) else 1
+            if aq and (l is None or vs[l[0]]["kind"] not in (2, 3)):
+                n += 1
+        return n
 
     def forward_device(self, x_dev=None, events=None):
         """Run the stack on the current stream of the device; returns the last
@@ -298,6 +324,7 @@ class SparseConvNet:
             for i in range(len(self.layers)):
                 if self.algorithms[i] == "dense-cudnn":
                     self.dense_layer(i)(cur, self.acts[i])
+                    self._dense_quant(i, self.acts[i], s)
                 else:
                     self.launch_layer(i, cur, self.acts[i], s)
                 events[i + 1].record(stream)

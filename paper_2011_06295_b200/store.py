@@ -12,7 +12,10 @@ for the input geometry propagated from the recorded architecture -- the
 reference rebuilds them on every forward (store.py:178-182).  Codebook
 layers need nothing extra: the reference stores their dequantized values
 (quantize.py:275-288), which the device layer can also re-encode as 4-bit
-codes (weight_format="cb4").  The fully connected head is out of scope.
+codes (weight_format="cb4").  Layers with an activation quantizer (the
+manifest's act_quant, fitted by apply_quantization) get the fused fake-quant
+epilogue (quantize.py:332-338; store.py:285-286).  The fully connected head is
+out of scope.
 """
 from __future__ import annotations
 
@@ -122,7 +125,8 @@ def load_conv_layers(path, input_chw: tuple | None = None):
             kern = build_csr(w, sh)
         else:
             raise FormatError(f"unknown storage {rec['storage']!r}")
-        layers.append(NetLayer(rec["name"], kern, bias, relu=rec.get("activation", "relu") == "relu", pool=False))
+        layers.append(NetLayer(rec["name"], kern, bias, relu=rec.get("activation", "relu") == "relu", pool=False,
+                               act_quant=rec.get("act_quant")))
         chw = (kern.shape.k, kern.shape.e, kern.shape.f)
     if not layers:
         raise FormatError("model has no conv layers")

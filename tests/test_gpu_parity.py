@@ -603,3 +603,66 @@ def test_builtin_launch_table_used_and_exact(sc, orc):
     got = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, b, relu=True).cpu().numpy()
     ref = np.maximum(orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, sh.k, 3, 3, 1, 1, b), 0)
     assert beq(got, ref)
+
+
+# ---------------------------------------------------------------------------
+# activation fake-quant (quantize.py:332-338): standalone pass and fused epilogues
+# ---------------------------------------------------------------------------
+
+def test_fake_quant_kernel_bitwise(sc):
+    import torch
+    from paper_2011_06295_b200 import _abi
+    z = np.load(GOLDEN / "fake_quant_cases.npz")
+    meta = json.loads(str(z["meta"]))
+    for i, m in enumerate(meta):
+        y = torch.from_numpy(z[f"x{i}"].copy()).cuda()
+        _abi.fake_quant(z[f"x{i}"].dtype, y.data_ptr(), y.numel(), m["params"],
+                        torch.cuda.current_stream().cuda_stream)
+        assert beq(y.cpu().numpy(), z[f"y{i}"]), (i, m)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float16])
+@pytest.mark.parametrize("c,hw,k,n", [(64, 16, 48, 5), (128, 4, 96, 19), (96, 2, 64, 33), (32, 40, 24, 2)])
+def test_fused_act_quant_all_kinds_bitwise(sc, orc, c, hw, k, n, dt):
+    """conv -> ReLU -> fake-quant (-> pool) through every launch kind: fused in the
+    direct / image-lane epilogues, a separate pass after the others."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import DeviceLayer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    aq = {"bits": 8, "clip_lo": 0.0, "clip_hi": 6.0, "mu": 0.0, "step": 6.0 / 255, "mode": "asymmetric"}
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("l", sh, 0.85), seed=3).astype(dt)
+    x, b = bench_inputs(sh, n)
+    x, b = x.astype(dt), b.astype(dt)
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+    want = orc.fake_quant(np.maximum(ref, 0), aq)
+    wantp = orc.fake_quant(torch.nn.functional.max_pool2d(
+        torch.from_numpy(np.maximum(ref, 0).astype(np.float32)), 2).numpy().astype(dt), aq) if hw % 2 == 0 else None
+    layer = DeviceLayer(kern, 0, dt)
+    layer.set_act_quant(aq)
+    xd = torch.from_numpy(x).cuda()
+    bd = torch.from_numpy(b.astype(np.float32)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    vs = _abi.variants()
+    for flags, exp in ((_abi.FLAG_RELU | _abi.FLAG_ACT_QUANT, want),
+                       (_abi.FLAG_RELU | _abi.FLAG_POOL2 | _abi.FLAG_ACT_QUANT, wantp)):
+        if exp is None:
+            continue
+        cands = layer.candidates(n, flags)
+        by_kind = {}
+        for cf in cands:
+            by_kind.setdefault(vs[cf[0]]["kind"], []).append(cf)
+        picks = [cf for lst in by_kind.values() for cf in lst[:: max(1, len(lst) // 4)]]
+        if not flags & _abi.FLAG_POOL2:
+            picks.append(None)  # generic kernel + fake-quant pass
+        for cf in picks:
+            y = torch.empty(exp.shape, dtype=xd.dtype, device="cuda")
+            layer.launch(xd.data_ptr(), bd.data_ptr(), y.data_ptr(), n,
+                         flags | (_abi.FLAG_GENERIC if cf is None else 0), cf, st)
+            assert beq(y.cpu().numpy(), exp), (cf, flags)
+    # the flag without an attached quantizer is refused
+    layer.set_act_quant(None)
+    with pytest.raises(Exception):
+        layer.launch(xd.data_ptr(), bd.data_ptr(), xd.data_ptr(), n, _abi.FLAG_ACT_QUANT, None, st)

@@ -76,3 +76,14 @@ def test_c1_digests():
             o16 = orc.conv_sparse(x.astype(np.float16), v16, c16, r16, sh["k"], sh["r"], sh["s"],
                                   sh["stride"], sh["padding"], bias.astype(np.float16))
             assert sha256(o16) == rec["out16_sha"], sh
+
+
+def test_fake_quant_matches_reference():
+    """oracle.fake_quant == the reference's fake_quant_activation (quantize.py:332-338)
+    on f32 / f16 / f64 arrays, asymmetric and symmetric, incl. exact code ties."""
+    z = np.load(GOLDEN / "fake_quant_cases.npz")
+    meta = json.loads(str(z["meta"]))
+    assert len(meta) == 12
+    for i, m in enumerate(meta):
+        y = orc.fake_quant(z[f"x{i}"], m["params"])
+        assert y.dtype == z[f"y{i}"].dtype and np.array_equal(_bits(y), _bits(z[f"y{i}"])), (i, m)

@@ -66,3 +66,32 @@ def test_loaded_net_forward_bitwise():
     net16 = load_net(STORE, weight_format="cb4")
     net16.plan(exp["x"].shape[0], tune=False)
     assert np.array_equal(net16.forward(exp["x"]).view(np.uint32), exp["conv_out"].view(np.uint32))
+
+
+STORE_AQ = GOLDEN / "store_aq"
+
+
+def test_act_quant_loaded_from_manifest():
+    """Layers carry the manifest's act_quant (quantize.py:324-326, store.py:339,411)."""
+    from paper_2011_06295_b200.store import load_conv_layers
+    layers = load_conv_layers(STORE_AQ)
+    m = json.loads((STORE_AQ / "manifest.json").read_text())
+    want = {r["name"]: r.get("act_quant") for r in m["layers"] if r["type"] == "conv"}
+    assert [L.name for L in layers] == list(want)
+    for L in layers:
+        assert L.act_quant == want[L.name] and L.act_quant["bits"] == 8
+
+
+@pytest.mark.gpu
+def test_act_quant_net_forward_bitwise():
+    """Model.forward with activation quantizers (conv -> ReLU -> fake_quant per layer,
+    store.py:276-286): fused epilogue, generic kernel + fake-quant pass, bit-identical
+    to the reference's own output."""
+    from paper_2011_06295_b200.store import load_net
+    exp = np.load(GOLDEN / "store_aq_expected.npz")
+    net = load_net(STORE_AQ)
+    net.plan(exp["x"].shape[0], tune=False)
+    out = net.forward(exp["x"])
+    assert np.array_equal(out.view(np.uint32), exp["conv_out"].view(np.uint32))
+    net.set_launches([None] * len(net.layers))  # generic kernels: separate fake-quant pass
+    assert np.array_equal(net.forward(exp["x"]).view(np.uint32), exp["conv_out"].view(np.uint32))
