@@ -862,12 +862,12 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                 // CTAs with 32 channels per stage win wherever the input is re-staged for few
                 // output-channel work (small planes, 1x1, 1D, wide rows); the dense 32x32 / 16x16
                 // layers prefer 8 warps x 16 channels
-                const bool few_taps = g.r * g.s <= 3 || g.h * g.w <= 64 || v.dispatch != DISPATCH_JUMP;
+                const bool few_taps = g.r * g.s <= 3 || g.h * g.w <= 64 || g.f > 32;  // a layer property
                 if (c.warps_k == 16) score += few_taps ? 1.3 : 0.8;
                 score += few_taps ? (c.cc >= 32 ? 0.8 : 0.0) : (c.cc == 16 ? 0.5 : 0.0);
                 score += (v.th == 8 && v.dispatch != DISPATCH_ONED ? 1.0 : 0.0) + (v.kt >= 4 ? 0.5 : 0.0) +
                          (v.nbt == 1 ? 0.3 : 0.0);
-                if (v.dispatch == DISPATCH_WIDE && fill >= 1.0 && v.tw == 32) score += 0.3;
+                if (v.dispatch == DISPATCH_WIDE && g.f > 32 && fill >= 1.0 && v.tw == 32) score += 0.3;
                 if (v.dispatch == DISPATCH_WIDE)  // exact-fit rows first, then the fewest idle lanes
                     score -= 0.4 + 2.0 * (1.0 - (double)g.f / (d.n_fx * v.tw));
                 if (v.dispatch == DISPATCH_ONED)  // idle columns of the last tile
