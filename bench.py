@@ -327,7 +327,28 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
         ev[1].record()
         ev[1].synchronize()
         td.append(ev[0].elapsed_time(ev[1]))
+    # the config-4 weight formats: 4-bit codebook and linear 16-bit weights (decoded into the
+    # direct kernels' tap blocks on upload; same f16 activations and FHFMA arithmetic)
+    from paper_2011_06295_b200.synth import codebook16, linear16
+    fmts = {}
+    for fmt, fn in (("cb4", codebook16), ("lin16", linear16)):
+        qn = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_format=fmt, weight_fn=fn)
+        qn.plan(args.batch, tune=not args.no_tune)
+        for _ in range(3):
+            qn.forward_device(x)
+        torch.cuda.synchronize()
+        tq = []
+        for _ in range(reps):
+            ev[0].record()
+            qn.forward_device(x)
+            ev[1].record()
+            ev[1].synchronize()
+            tq.append(ev[0].elapsed_time(ev[1]))
+        fmts[fmt] = {"ms_per_step": round(statistics.median(tq), 4),
+                     "images_per_s": round(args.batch / (statistics.median(tq) * 1e-3), 1)}
+        del qn
     return {"images_per_s": round(args.batch / (ms * 1e-3), 1), "ms_per_step": round(ms, 4),
+            "weight_formats": fmts,
             "dense_cudnn_fp16_ms": round(statistics.median(td), 4),
             "arith": "f16 storage, FHFMA (f16 x f16 + f32) accumulation, bit-identical to the reference f16 profile",
             "launches": [None if l is None else list(l) for l in net.launches]}

@@ -115,6 +115,18 @@ struct scb_layer {
         blk_cap[key] = mx;
         return mx;
     }
+    // native value bits of nonzero t (f32 bits, or f16 bits in the low half) whatever the
+    // stored weight format: quantized payloads are decoded here, exactly
+    uint32_t native_bits(int64_t t) const {
+        if (wfmt == SCB_W_NATIVE) return h_pay[t];
+        if (dt == SCB_F16) {
+            const __half h = __float2half_rn(h_vals[t]);  // exact: the value came from f16
+            return (uint32_t)__half_as_ushort(h);
+        }
+        uint32_t b;
+        std::memcpy(&b, &h_vals[t], 4);
+        return b;
+    }
     // device tables: taps (as 16-byte chunks) and per-(g, st) chunk offsets
     Blocks direct_blocks(int plane, int row, const std::vector<int>& col, int es, int cc, int kw) {
         if (!stage_ptr(cc)) return Blocks{};
@@ -144,7 +156,7 @@ struct scb_layer {
                     for (int t = t0; t < t1; ++t) {
                         const int64_t c = h_colidx[t] / pp, rem = h_colidx[t] % pp;
                         DirectTap d;
-                        uint32_t vb = h_pay[t];
+                        const uint32_t vb = native_bits(t);
                         std::memcpy(&d.v, &vb, 4);
                         d.off = (int32_t)(es * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
                         out.push_back(d);
@@ -419,7 +431,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     const Geom& g = L->g;
     if (L->dt == SCB_F64) return false;
     if (g.stride != 1 || v.r != g.r || v.s != g.s || v.pad != g.pad) return false;
-    if (v.io != L->dt || v.wf != L->wf) return false;
+    // direct / image-lane kernels take any weight format: their tap blocks carry the
+    // decoded native value (decoded once on upload, direct_blocks)
+    const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG) &&
+                         v.wf == (L->dt == SCB_F16 ? WF_F16 : WF_F32);
+    if (v.io != L->dt || (v.wf != L->wf && !decoded)) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
     if (v.kind < KIND_DIRECT && !L->prog(v.kt)) return false;

@@ -406,14 +406,17 @@ class SparseConvNet:
 
 
 def build_net(specs_pools, seed: int = 0, dtype=np.float32, device: int = 0,
-              weight_format: str = "native", fast_math: bool = False):
+              weight_format: str = "native", fast_math: bool = False, weight_fn=None):
     """SparseConvNet of synthetic unified-sparsity layers
-    (synth.make_layer_weights / bench_inputs, bench.py:105-116,175-177)."""
+    (synth.make_layer_weights / bench_inputs, bench.py:105-116,175-177).
+    `weight_fn(w) -> w` post-processes each layer's weights (e.g. synth.codebook16)."""
     from .synth import bench_inputs, make_layer_weights
     from .weights import build_csr
     layers = []
     for spec, pool in specs_pools:
         w = make_layer_weights(spec, seed).astype(dtype)
+        if weight_fn is not None:
+            w = weight_fn(w)
         _, b = bench_inputs(spec.shape, 1, seed)
         layers.append(NetLayer(spec.name, build_csr(w, spec.shape), b, relu=True, pool=pool))
     return SparseConvNet(layers, device=device, dtype=dtype, weight_format=weight_format,

@@ -117,3 +117,28 @@ PRESETS = {
     "cnn-non-static": [LayerSpec(f"300x64-kernel{s}-s{sp * 100:g}", _shape(64, 1, 300, 100, 1, s), sp)
                        for s in (2, 3) for sp in (0.77, 0.83, 0.875)],
 }
+
+
+def codebook16(w: np.ndarray) -> np.ndarray:
+    """Synthetic 4-bit-codebook weights (config 4, the paper's "4b/16b"): every nonzero
+    mapped to the nearest of 14 f16 centroids spread over [-max|w|, max|w|] (zero excluded),
+    so a layer holds <= 16 distinct values with the +-0.0 of promoted zeros -- what
+    quantize_weights_array("codebook", 16) produces in form (quantize.py:284-288)."""
+    w = np.asarray(w)
+    m = float(np.abs(w).max()) or 1.0
+    cent = np.concatenate([-np.geomspace(m, m / 16, 7), np.geomspace(m / 16, m, 7)]).astype(np.float16)
+    out = w.astype(np.float32).copy()
+    nz = out != 0
+    idx = np.abs(out[nz][:, None] - cent.astype(np.float32)[None, :]).argmin(axis=1)
+    out[nz] = cent[idx].astype(np.float32)
+    return out.astype(w.dtype)
+
+
+def linear16(w: np.ndarray, frac: int = 8) -> np.ndarray:
+    """Synthetic linear 16-bit weights (config 4, quantize_fixed's sigma * code with
+    sigma = 2^-frac, quantize.py:48-71): multiples of 2^-frac, |w| < 2^(15-frac)."""
+    w = np.asarray(w)
+    s = 2.0 ** frac
+    q = np.clip(np.round(w.astype(np.float64) * s), -(2 ** 15 - 1), 2 ** 15 - 1) / s
+    q[(w != 0) & (q == 0)] = 1.0 / s  # keep the sparsity pattern
+    return q.astype(w.dtype)

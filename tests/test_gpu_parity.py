@@ -275,6 +275,23 @@ def test_quantized_formats_bitwise(sc, orc, key, fmt):
     native = sc.conv_sparse(x, kern, b)
     quant = sc.conv_sparse(x, kern, b, sc.EnginePlan(weight_format=fmt))
     assert beq(native, ref) and beq(quant, ref)
+    # direct kernels take the quantized formats decoded on upload: every kind, bitwise
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    sh16 = sc.ConvShape(n=n, c=6, h=16, w=16, k=8, r=3, s=3, padding=1)
+    x16 = rng.standard_normal((n, 6, 16, 16)).astype(wq.dtype)
+    k16 = sc.build_csr(wq, sh16)
+    ref16 = orc.conv_sparse(x16, k16.values, k16.colidx, k16.rowptr, 8, 3, 3, 1, 1, b)
+    layer = device_layer(k16, 0, wq.dtype, fmt)
+    vs = _abi.variants()
+    cands = layer.candidates(n)
+    kinds = {vs[cf[0]]["kind"] for cf in cands}
+    assert 2 in kinds, kinds
+    xd = torch.from_numpy(x16).cuda()
+    for cf in [cf for cf in cands if vs[cf[0]]["kind"] == 2][::7]:
+        o = sc.conv_sparse(xd, k16, b, sc.EnginePlan(weight_format=fmt, launch=cf)).cpu().numpy()
+        assert beq(o, ref16), cf
 
 
 def test_affine_weights_rejected_by_lin16(sc):
