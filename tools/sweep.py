@@ -47,20 +47,28 @@ def ev_time(fn, reps=10, warm=3):
     return statistics.median(ts)
 
 
-def tune(layer, x64, y64, bptr, kinds, max_c=160):
+def tune(layer, x64, y64, bptr, kinds, per_kind=40):
+    """Sampled pass over every (kind, dispatch) group, then every launch of the 3 best variants."""
     vs = _abi.variants()
     st = torch.cuda.current_stream().cuda_stream
-    cands = [c for c in layer.candidates(64) if vs[c[0]]["kind"] in kinds][:max_c]
-    best, bt = None, 1e30
+    cands = [c for c in layer.candidates(64) if vs[c[0]]["kind"] in kinds]
+    timed = {}
+
+    def run(cs):
+        for c in cs:
+            if c in timed:
+                continue
+            try:
+                timed[c] = time_call(lambda: layer.launch(x64.data_ptr(), bptr, y64.data_ptr(), 64, 0, c, st), 2, 1)
+            except Exception as e:  # a candidate the device cannot launch is skipped, not fatal
+                print("skip", c, e, file=sys.stderr)
+    groups = {}
     for c in cands:
-        try:
-            t = time_call(lambda: layer.launch(x64.data_ptr(), bptr, y64.data_ptr(), 64, 0, c, st), 2, 1)
-        except Exception as e:  # a candidate the device cannot launch is skipped, not fatal
-            print("skip", c, e, file=sys.stderr)
-            continue
-        if t < bt:
-            best, bt = c, t
-    return best
+        groups.setdefault((vs[c[0]]["kind"], vs[c[0]]["dispatch"]), []).append(c)
+    run([c for lst in groups.values() for c in lst[:: max(1, len(lst) // per_kind)]])
+    top = {c[0] for c in sorted(timed, key=timed.get)[:3]}
+    run([c for c in cands if c[0] in top])
+    return min(timed, key=timed.get)
 
 
 def crossover(sps, sparse, dense):
@@ -98,7 +106,7 @@ def main():
             layer = device_layer(kern, 0, dt)
             y = torch.empty((n, 256, 32, 32), device=dev, dtype=x.dtype)
             y64 = torch.empty((64, 256, 32, 32), device=dev, dtype=x.dtype)
-            best = tune(layer, x[:64], y64, bias.data_ptr(), kinds=(0, 2))
+            best = tune(layer, x[:64], y64, bias.data_ptr(), kinds=(0, 1, 2, 3))
             # integrity gate: tuned launch == generic kernel, bitwise (64 images)
             ref = torch.empty_like(y64)
             layer.launch(x[:64].data_ptr(), bias.data_ptr(), y64.data_ptr(), 64, 0, best, st)
@@ -110,6 +118,9 @@ def main():
             macs = sc.sparse_mac_count(kern, n)
             row[f"sparse_{name}_us"] = round(t * 1e6, 1)
             row[f"sparse_{name}_tmacs"] = round(macs / t / 1e12, 3)
+            es = np.dtype(dt).itemsize  # algorithmic bytes: x + y once, taps {value, index}
+            nbytes = 2 * n * 256 * 32 * 32 * es + kern.nnz * (es + 4) + 4 * 257 + 4 * 256
+            row[f"sparse_{name}_hbm_gbs"] = round(nbytes / t / 1e9, 1)
             row[f"launch_{name}"] = list(best)
             row["L"] = int(kern.sparse_level)
             del layer
