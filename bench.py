@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-images", type=int, default=8, help="images per CPU-baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline time budget")
     ap.add_argument("--chains", type=int, default=2, help="sub-batch chains on separate streams per GPU")
+    ap.add_argument("--graph", type=int, default=0, help="1: replay the stack as one CUDA graph per step")
     ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch between layers")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -422,6 +423,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     x_host = torch.randn((args.batch, 3, 32, 32), generator=g).pin_memory()
     x_dev = x_host.to(dev)
     integrity_gate(net, x_dev)
+    if args.graph:
+        net.x_in.copy_(x_dev)
+        net.capture()  # forward_device replays it (per-layer event passes stay eager)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     nl = len(net.layers)
@@ -526,7 +530,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "parallelism": f"batch-sharded x{world} (weak, no collective)",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
                    "tuned": not args.no_tune, "tune_seconds": round(tune_s, 1),
-                   "streams_per_gpu": args.chains, "pdl": not args.no_pdl},
+                   "streams_per_gpu": args.chains, "pdl": not args.no_pdl, "cuda_graph": bool(args.graph)},
         "e2e": {"value": round(args.batch * args.steps * world / e2e_s, 1), "unit": "images/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
                 "api": "SparseConvNet.forward_stream (pinned host in/out, copies overlapped across steps)"},
