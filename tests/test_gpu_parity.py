@@ -411,7 +411,8 @@ def test_plane_kernels_bitwise(sc, orc, c, hw, k, sp, n, dtype):
 # ---------------------------------------------------------------------------
 
 @pytest.mark.parametrize("c,hw,k,sp,n", [(64, 32, 64, 0.9, 3), (64, 16, 72, 0.9, 5), (256, 8, 256, 0.9, 9),
-                                         (96, 8, 40, 0.5, 7), (512, 4, 512, 0.95, 17), (3, 32, 64, 0.9, 2)])
+                                         (96, 8, 40, 0.5, 7), (512, 4, 512, 0.95, 17), (3, 32, 64, 0.9, 2),
+                                         (64, 2, 72, 0.8, 33), (40, 4, 24, 0.6, 11)])
 def test_direct_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     import torch
     from paper_2011_06295_b200 import _abi
