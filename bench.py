@@ -141,10 +141,12 @@ class Clocks:
 # CPU legs (the oracle: reference algorithm restated in C, OpenMP threads)
 # ---------------------------------------------------------------------------
 
-def cpu_stack_time(specs, kernels, biases, images: int, budget_s: float, seed: int = 7):
+def cpu_stack_time(specs, kernels, biases, images: int, budget_s: float, seed: int = 7,
+                   steps: int | None = None, warmup: int = 1):
     """Run the reference algorithm over the conv stack on `images` images
-    (conv_sparse -> ReLU -> 2x2 max-pool, store.py:276-284) until `budget_s`
-    is spent; returns (seconds per pass, passes, threads)."""
+    (conv_sparse -> ReLU -> 2x2 max-pool, store.py:276-284): `warmup` untimed
+    passes, then exactly `steps` timed passes, or (steps None) passes until
+    `budget_s` is spent; returns (seconds per pass, passes, threads)."""
     from oracle import oracle as orc
     rng = np.random.default_rng(seed)
     x0 = rng.standard_normal((images, specs[0][0].shape.c, 32, 32)).astype(np.float32)
@@ -161,14 +163,18 @@ def cpu_stack_time(specs, kernels, biases, images: int, budget_s: float, seed: i
                 a = a.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
         return a
 
-    one_pass()  # warm (threads, page faults)
+    for _ in range(max(1, warmup)):
+        one_pass()  # warm (threads, page faults)
     t0 = time.perf_counter()
     passes = 0
     while True:
         one_pass()
         passes += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or passes >= 1000:
+        if steps is not None:
+            if passes >= steps:
+                break
+        elif el >= budget_s or passes >= 1000:
             break
     return el / passes, passes, orc.max_threads()
 
@@ -188,12 +194,16 @@ def run_reference(args, rank: int, world: int):
         return
     specs = workload(args.sparsity)
     kernels, biases = build_kernels(specs)
+    # a step = one pass of the stack over a bounded sample of cpu_images images;
+    # W untimed warm-up passes, then exactly K timed passes
     per_pass, passes, threads = cpu_stack_time(specs, kernels, biases, args.cpu_images,
-                                               max(args.cpu_seconds, 1.0))
+                                               max(args.cpu_seconds, 1.0), steps=args.steps,
+                                               warmup=args.warmup)
     ips = args.cpu_images / per_pass
     line = {
         "impl": "reference", "metric": METRIC, "value": round(ips, 3), "unit": "images/s",
-        "n_gpus": args.gpus, "steps": passes, "warmup": 1, "ms_per_step": round(per_pass * 1e3, 3),
+        "n_gpus": args.gpus, "steps": passes, "warmup": max(1, args.warmup),
+        "ms_per_step": round(per_pass * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (make_layer_weights bench.py:105-116 restated; N(0,1) inputs)",
         "config": {"workload": f"VGG-16 CIFAR-10 13-conv stack, {args.sparsity:g} unified sparsity, "
