@@ -226,9 +226,16 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
     // ---- epilogue: lane's image plane per output channel is contiguous
     const int n = n0 + lane;
     if (n >= p.n) return;
-    const bool relu = p.flags & SCB_FLAG_RELU;
-    const bool pool = p.flags & SCB_FLAG_POOL2;
     const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
+    if (aq) {  // ReLU + fake-quant in place (monotone: commutes with the max-pool)
+        const bool r0 = p.flags & SCB_FLAG_RELU;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk)
+#pragma unroll
+            for (int j = 0; j < HW; ++j) acc[kk][j] = fq_store<E>(r0 && acc[kk][j] < 0.f ? 0.f : acc[kk][j], p.aq);
+    }
+    const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
+    const bool pool = p.flags & SCB_FLAG_POOL2;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -241,13 +248,8 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
             if constexpr (F16) {
 #pragma unroll
                 for (int j = 0; j < HW; j += 2)
-                    *reinterpret_cast<__half2*>(yp + j) =
-                        __halves2half2(out_val<__half>(o[j], aq, p.aq), out_val<__half>(o[j + 1], aq, p.aq));
+                    *reinterpret_cast<__half2*>(yp + j) = __floats2half2_rn(o[j], o[j + 1]);
             } else {
-                if (aq) {
-#pragma unroll
-                    for (int j = 0; j < HW; ++j) o[j] = fq_f32(o[j], p.aq);
-                }
 #pragma unroll
                 for (int j = 0; j < HW; j += H) *reinterpret_cast<V*>(yp + j) = *reinterpret_cast<const V*>(&o[j]);
             }
@@ -258,9 +260,8 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
             for (int yy = 0; yy < PH; ++yy)
 #pragma unroll
                 for (int xx = 0; xx < PH; ++xx)
-                    yp[yy * PH + xx] = out_val<E>(fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
-                                                        fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1])),
-                                                  aq, p.aq);
+                    yp[yy * PH + xx] = (E)fmaxf(fmaxf(o[(2 * yy) * H + 2 * xx], o[(2 * yy) * H + 2 * xx + 1]),
+                                                fmaxf(o[(2 * yy + 1) * H + 2 * xx], o[(2 * yy + 1) * H + 2 * xx + 1]));
         }
     }
 }

@@ -343,9 +343,18 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // next layer may start its prologue
     // ---- epilogue: lane holds rows oy0..oy0+TH-1 of columns lx..lx+VX-1 of image n0+lg
     const int n = n0 + lg;
-    const bool relu = p.flags & SCB_FLAG_RELU;
-    const bool pool = p.flags & SCB_FLAG_POOL2;
     const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
+    // activation fake-quant in place, ahead of the stores: ReLU then the quantizer (store.py:
+    // 284-286); the quantizer is monotone, so it commutes with the 2x2 max-pool below
+    if (aq) {
+        const bool r0 = p.flags & SCB_FLAG_RELU;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk)
+#pragma unroll
+            for (int j = 0; j < TH * VX; ++j) acc[kk][j] = fq_store<TIO>(r0 && acc[kk][j] < 0.f ? 0.f : acc[kk][j], p.aq);
+    }
+    const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;  // (already applied with the quantizer)
+    const bool pool = p.flags & SCB_FLAG_POOL2;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 for (int j = 0; j < TH; ++j) {
                     float o0 = acc[kk][j];
                     if (relu && o0 < 0.f) o0 = 0.f;
-                    if (ox0 + lx + j * LW < p.f) yp[j * LW] = out_val<TIO>(o0, aq, p.aq);
+                    if (ox0 + lx + j * LW < p.f) yp[j * LW] = o0;
                 }
             }
         } else if (!pool) {
@@ -373,16 +382,14 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                     float o0 = acc[kk][j * VX];
                     if (relu && o0 < 0.f) o0 = 0.f;
                     if constexpr (VX == 1) {
-                        yp[j * FP * fpitch] = out_val<TIO>(o0, aq, p.aq);
+                        yp[j * FP * fpitch] = o0;
                     } else {
                         float o1 = acc[kk][j * VX + 1];
                         if (relu && o1 < 0.f) o1 = 0.f;
                         if constexpr (F16IO)
-                            *reinterpret_cast<__half2*>(yp + j * LW) =
-                                __halves2half2(out_val<__half>(o0, aq, p.aq), out_val<__half>(o1, aq, p.aq));
+                            *reinterpret_cast<__half2*>(yp + j * LW) = __floats2half2_rn(o0, o1);
                         else
-                            *reinterpret_cast<float2*>(yp + j * LW) =
-                                make_float2(out_val<float>(o0, aq, p.aq), out_val<float>(o1, aq, p.aq));
+                            *reinterpret_cast<float2*>(yp + j * LW) = make_float2(o0, o1);
                     }
                 }
             }
@@ -400,8 +407,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 if (relu && o < 0.f) o = 0.f;
                 const int py = (oy0 + j) >> 1;
                 if (n < p.n && !(lx & 1) && ox0 + lx < p.f && py < pe)
-                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] =
-                        out_val<TIO>(o, aq, p.aq);
+                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] = (TIO)o;
             }
         }
     }

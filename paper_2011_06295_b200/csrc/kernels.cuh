@@ -49,17 +49,15 @@ __device__ __forceinline__ double fq_f64(double a, const ActQuant& q) {
     return fq_value(fq_code(fmin(fmax(a, q.dlo), q.dhi), q), q);
 }
 
-// epilogue store value: one round to the storage type, then the optional fake-quant
+// fake-quant of an epilogue value in its storage type, returned as the (exact) float of the
+// stored value: f32 directly, f16 via one round to half first (the reference's f16 profile)
 template <typename T>
-__device__ __forceinline__ T out_val(float o, bool aq, const ActQuant& q);
+__device__ __forceinline__ float fq_store(float o, const ActQuant& q);
 template <>
-__device__ __forceinline__ float out_val<float>(float o, bool aq, const ActQuant& q) {
-    return aq ? fq_f32(o, q) : o;
-}
+__device__ __forceinline__ float fq_store<float>(float o, const ActQuant& q) { return fq_f32(o, q); }
 template <>
-__device__ __forceinline__ __half out_val<__half>(float o, bool aq, const ActQuant& q) {
-    const __half h = __float2half_rn(o);
-    return aq ? fq_f16(h, q) : h;
+__device__ __forceinline__ float fq_store<__half>(float o, const ActQuant& q) {
+    return __half2float(fq_f16(__float2half_rn(o), q));
 }
 
 template <int MODE>
