@@ -131,7 +131,7 @@ template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int M
           bool WIDE = false, bool ONED = false>
 // (MINB = 2 variants may run 16 warps per CTA: 512 threads, one CTA per SM, same 128 registers)
 __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k_direct(const __grid_constant__ DirectParams p) {
-    static_assert(!F16IO || VX == 2, "f16 storage reads column pairs");
+    static_assert(!F16IO || !WIDE, "f16 storage: narrow rows");
     static_assert(!WIDE || (VX == 1 && !F16IO), "wide tiles: f32, one column per lane");
     static_assert(!ONED || (WIDE && R == 1), "1D tiles are wide tiles of one input row");
     using TIO = typename std::conditional<F16IO, __half, float>::type;
@@ -316,7 +316,12 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
             for (int t = 0; t < nt; ++t) {
                 const DirectTap tp = seg[t];
                 const TIO* xp = reinterpret_cast<const TIO*>(reinterpret_cast<const char*>(xl) + tp.off);
-                if constexpr (F16IO) {
+                if constexpr (F16IO && VX == 1) {  // one half per MAC: no shifted copy needed
+                    const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
+#pragma unroll
+                    for (int j = 0; j < TH; ++j)
+                        acc[kk][j] = fhfma(acc[kk][j], vh, *reinterpret_cast<const unsigned short*>(xp + j * JS));
+                } else if constexpr (F16IO) {
                     const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
 #pragma unroll
                     for (int j = 0; j < TH; ++j) {
@@ -382,7 +387,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                     float o0 = acc[kk][j * VX];
                     if (relu && o0 < 0.f) o0 = 0.f;
                     if constexpr (VX == 1) {
-                        yp[j * FP * fpitch] = o0;
+                        yp[j * FP * fpitch] = (TIO)o0;
                     } else {
                         float o1 = acc[kk][j * VX + 1];
                         if (relu && o1 < 0.f) o1 = 0.f;

@@ -398,6 +398,8 @@ DIRECTS_1D = [(s, th, kw) for s in (2, 3, 4, 5) for th in (4, 8) for kw in (4, 8
 # f16-storage direct variants (FHFMA, column pairs): (R, S, PAD, TH, LW, KW)
 DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (2, 4)] + \
               [(3, 3, 1, 4, 4, kw) for kw in (4, 8)]  # 4x4 planes: 8-byte rows, 16 images per warp
+# f16 storage, one column per lane (VX = 1: no shifted row copy): (TH, LW, KW)
+DIRECTS_F16_VX1 = [(8, 32, 4), (16, 32, 4), (8, 32, 8), (8, 16, 4), (8, 16, 8), (8, 8, 8)]
 
 
 N_PARTS = 10
@@ -442,6 +444,8 @@ def main():
         groups[("dws", R, S, PAD, TH, LW, KW)] = ([], [("dws", R, S, PAD, TH, LW, KW, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DIRECTS_F16:
         groups[("direct16", R, S, PAD, TH, LW, KW)] = ([], [("direct16", R, S, PAD, TH, LW, KW)])
+    for TH, LW, KW in DIRECTS_F16_VX1:
+        groups[("direct16v1", TH, LW, KW)] = ([], [("direct16v1", TH, LW, KW)])
     for H, KW in DIMGS:
         groups[("dimg", H, KW)] = ([], [("dimg", H, KW, mode) for mode in (EXACT, FMA)])
     for H, KW in DIMGS_F16:
@@ -475,6 +479,12 @@ def main():
                     _, R, S, PAD, TH, LW, KW, mode = v
                     ents.append(f"    {{{{{R}, {S}, {KW}, 1, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, {PAD}, "
                                 f"{KIND_DWS}}}, nullptr, &launch_dws_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, {mode}>}},\n")
+                    continue
+                if v[0] == "direct16v1":
+                    _, TH, LW, KW = v
+                    ents.append(f"    {{{{3, 3, {KW}, 1, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, 1, "
+                                f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<3, 3, 1, {TH}, {LW}, {KW}, "
+                                f"{FMA}, 1, 2, true>, 512}},\n")
                     continue
                 if v[0] == "direct16":
                     _, R, S, PAD, TH, LW, KW = v
