@@ -5,8 +5,7 @@
 linear interpolation where sparse time == dense time).
 
 Per sparsity: L = 2304 - round(sp*2304) (make_layer_weights), sparse time with
-a launch tuned on a 64-image slice (launch parameters do not depend on the
-batch), dense fp32 (cuDNN, TF32 off), dense TF32 and dense fp16
+a launch tuned at the full batch, dense fp32 (cuDNN, TF32 off), dense TF32 and dense fp16
 (channels_last, tensor cores) for reference.  Every sparse result is checked
 bit-for-bit against the engine's independent generic kernel before timing.
 
@@ -48,10 +47,12 @@ def ev_time(fn, reps=10, warm=3):
 
 
 def tune(layer, x64, y64, bptr, kinds, per_kind=40):
-    """Sampled pass over every (kind, dispatch) group, then every launch of the 3 best variants."""
+    """Sampled pass over every (kind, dispatch) group, then every launch of the 3 best variants,
+    timed at the batch of x64 (the full sweep batch: a 64-image slice misranks launches)."""
     vs = _abi.variants()
     st = torch.cuda.current_stream().cuda_stream
-    cands = [c for c in layer.candidates(64) if vs[c[0]]["kind"] in kinds]
+    nb = x64.shape[0]
+    cands = [c for c in layer.candidates(nb) if vs[c[0]]["kind"] in kinds]
     timed = {}
 
     def run(cs):
@@ -59,7 +60,7 @@ def tune(layer, x64, y64, bptr, kinds, per_kind=40):
             if c in timed:
                 continue
             try:
-                timed[c] = time_call(lambda: layer.launch(x64.data_ptr(), bptr, y64.data_ptr(), 64, 0, c, st), 2, 1)
+                timed[c] = time_call(lambda: layer.launch(x64.data_ptr(), bptr, y64.data_ptr(), nb, 0, c, st), 2, 1)
             except Exception as e:  # a candidate the device cannot launch is skipped, not fatal
                 print("skip", c, e, file=sys.stderr)
     groups = {}
@@ -106,7 +107,7 @@ def main():
             layer = device_layer(kern, 0, dt)
             y = torch.empty((n, 256, 32, 32), device=dev, dtype=x.dtype)
             y64 = torch.empty((64, 256, 32, 32), device=dev, dtype=x.dtype)
-            best = tune(layer, x[:64], y64, bias.data_ptr(), kinds=(0, 1, 2, 3))
+            best = tune(layer, x, y, bias.data_ptr(), kinds=(0, 1, 2, 3))
             # integrity gate: tuned launch == generic kernel, bitwise (64 images)
             ref = torch.empty_like(y64)
             layer.launch(x[:64].data_ptr(), bias.data_ptr(), y64.data_ptr(), 64, 0, best, st)
