@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
     using V = typename DimgT<H, F16>::V;
     constexpr int ES = (int)sizeof(E);
     constexpr int RW = H;                    // row stride inside a copy (elements)
-    constexpr int BLK = (3 * H + 4) * H;     // elements per (image, channel)
+    // elements per (image, channel); 4x4 planes add 32 bytes so consecutive planes land on
+    // different bank groups in the per-(plane, row) copy pass (= layer.cu dimg_blk)
+    constexpr int BLK = (3 * H + 4) * H + (H == 4 ? 32 / ES : 0);
     // BASE puts copy_1's plane on its copy alignment: f32 16 B, f16 8 B (H=2) / 16 B (H=4)
     constexpr int BASE = F16 ? (H == 2 ? 2 : 4) : (H == 2 ? 2 : 0);
     constexpr int HW = H * H;

@@ -612,7 +612,7 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     d->threads = 32 * c.warps_k;
     const int es = elem_bytes(v);
     d->row = H;                             // = dimg.cuh RW / BLK / BASE
-    const int blk = (3 * H + 4) * H;
+    const int blk = (3 * H + 4) * H + (H == 4 ? 32 / elem_bytes(v) : 0);  // = dimg.cuh BLK
     int ip = c.cc * blk + dimg_base(v);
     const int vec = H;                      // elements per vector load
     while ((ip / vec) % 2 == 0 || ip % vec) ++ip;  // odd vector index: conflict-free lanes
