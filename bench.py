@@ -406,6 +406,25 @@ def load_traffic():
     return {}
 
 
+def load_smem_pipe():
+    """Per-layer shared-memory pipe utilisation (l1tex throughput % of peak, the kernels'
+    real ceiling) from the committed ncu --set full stack summary, layers in order."""
+    import csv
+    caps = sorted((ROOT / "profiles").glob("r01_ncu_full_stack_v*.csv"),
+                  key=lambda q: int(q.stem.rsplit("_v", 1)[1]))
+    if not caps:
+        return {}, None
+    rows = list(csv.reader(caps[-1].open()))
+    h = rows[0]
+    col = "l1tex__throughput.avg.pct_of_peak_sustained_active"
+    if col not in h:
+        return {}, None
+    vals = [float(r[h.index(col)]) for r in rows[2:] if len(r) > h.index(col)]
+    from paper_2011_06295_b200.synth import VGG16_CIFAR_LAYERS
+    names = [n for n, *_ in VGG16_CIFAR_LAYERS]
+    return dict(zip(names, vals)), f"profiles/{caps[-1].name}"
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
@@ -509,6 +528,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     hbm_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     traffic = load_traffic()
+    smem, smem_src = load_smem_pipe()
     layers = []
     for i, ((spec, pool), kern) in enumerate(zip(specs, [L.kernel for L in net.layers])):
         us = statistics.median(layer_ms[i]) * 1e3
@@ -528,7 +548,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "ffma_peak_tflops": round(peaks.get("ffma", 0), 2),
             "algorithmic_flops": fl, "algorithmic_bytes": by,
             "hbm_achieved_gbs": round(by / (mean_us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
-            "traffic": traffic.get(specs[top][0].name)}
+            "traffic": traffic.get(specs[top][0].name),
+            "smem_pipe_pct": smem.get(specs[top][0].name), "smem_pipe_source": smem_src}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(total_s / args.steps * 1e3, 4),
