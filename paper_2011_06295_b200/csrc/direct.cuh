@@ -102,9 +102,12 @@ struct DirectRow {
     // VX = 1: the right halo reads the NEXT row's never-written left padding (zero), so
     // no right-halo columns are stored (the host leaves 16 zero bytes after each stage).
     // WIDE (column tiles of a wider row): the row also holds a real right halo.
-    static constexpr int QW = WIDE ? XO + LW + Q16
-                                   : (VX == 1 ? ((XO + LW) + Q16 - 1) / Q16 * Q16
-                                              : ((XO + LW + S) + Q16 - 1) / Q16 * Q16);
+    static constexpr int QW0 = WIDE ? XO + LW + Q16
+                                    : (VX == 1 ? ((XO + LW) + Q16 - 1) / Q16 * Q16
+                                               : ((XO + LW + S) + Q16 - 1) / Q16 * Q16);
+    // VX = 2: rows (two copies) a multiple of 128 bytes apart would put every row's chunk i in
+    // the same bank group during the shifted-copy pass; one more 16-byte chunk staggers them
+    static constexpr int QW = (VX == 2 && !WIDE && (2 * QW0 * ES) % 128 == 0) ? QW0 + Q16 : QW0;
     static_assert(XO >= S - 1 - PAD, "right halo must fit in the next row's left padding");
     static constexpr int ROW = VX * QW;
     // shared column (relative to the lane's first output column) of tap column s

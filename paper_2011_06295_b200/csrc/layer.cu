@@ -528,7 +528,9 @@ int direct_qw(const scb_variant_info& v) {
     const int right = v.s - 1 - v.pad > 0 ? v.s - 1 - v.pad : 0;
     (void)right;  // VX = 1 rows alias the right halo onto the next row's left padding
     if (v.kind == KIND_DIRECT && v.dispatch == DISPATCH_WIDE) return q + v.tw + q;  // real right halo
-    return v.nbt == 1 ? (q + v.tw + q - 1) / q * q : (q + v.tw + v.s + q - 1) / q * q;
+    if (v.nbt == 1) return (q + v.tw + q - 1) / q * q;
+    const int qw = (q + v.tw + v.s + q - 1) / q * q;  // VX = 2: = direct.cuh DirectRow::QW
+    return (2 * qw * elem_bytes(v)) % 128 == 0 ? qw + q : qw;
 }
 int direct_row(const scb_variant_info& v) { return v.nbt * direct_qw(v); }
 std::vector<int> direct_cols(const scb_variant_info& v) {
