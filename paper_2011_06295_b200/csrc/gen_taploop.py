@@ -362,7 +362,10 @@ PLANES = [
     (4, 4, 3, 3, 1, 2, 1, 3), (2, 2, 3, 3, 1, 2, 2, 3), (2, 2, 3, 3, 1, 2, 4, 3),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
-KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS, KIND_DTM = 0, 1, 2, 3, 4, 5
+KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS, KIND_DTM, KIND_TMI = 0, 1, 2, 3, 4, 5, 6
+# TMEM image-lane variants (tmi.cuh): (W plane, TE rows per lane unit, J images per lane, KW, WQ warps per quarter)
+TMIS = [(w, te, j, kw, wq) for (w, te, j) in ((4, 4, 1), (2, 2, 4), (2, 2, 2), (8, 2, 1))
+        for kw, wq in ((2, 3), (3, 3), (2, 4), (4, 2))] + [(16, 1, 1, 2, 3), (16, 1, 1, 3, 3), (8, 4, 1, 1, 3), (8, 4, 1, 2, 3)]
 # TMEM-operand direct variants (tm.cuh): (TH, LW, KW, M warps per lane quarter)
 DTMS = [(8, lw, kw, m) for lw in (32, 16, 8) for kw in (4, 8) for m in (2, 4)] + [(4, 4, kw, m) for kw in (4, 8) for m in (2, 4)]
 # warp-specialised direct variants (ws.cuh): (R, S, PAD, TH, LW, KW)
@@ -440,6 +443,8 @@ def main():
         groups[("oned", S, TH, KW)] = ([], [("oned", S, TH, KW, mode) for mode in (EXACT, FMA)])
     for TH, LW, KW, M in DTMS:
         groups[("dtm", TH, LW, KW, M)] = ([], [("dtm", TH, LW, KW, M, m) for m in (EXACT, FMA)])
+    for W, TE, J, KW, WQ in TMIS:
+        groups[("tmi", W, TE, J, KW, WQ)] = ([], [("tmi", W, TE, J, KW, WQ, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DWS:
         groups[("dws", R, S, PAD, TH, LW, KW)] = ([], [("dws", R, S, PAD, TH, LW, KW, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DIRECTS_F16:
@@ -459,7 +464,7 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n#include \"tm.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n#include \"tm.cuh\"\n#include \"tmi.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
@@ -474,6 +479,12 @@ def main():
                     _, TH, LW, KW, M, mode = v
                     ents.append(f"    {{{{3, 3, {KW}, {M}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
                                 f"{KIND_DTM}}}, nullptr, &launch_dtm_t<3, 3, 1, {TH}, {LW}, {KW}, {M}, {mode}>}},\n")
+                    continue
+                if v[0] == "tmi":  # info: kt = KW, nbt = J, th = TE, tw = W, dispatch = WQ
+                    _, W, TE, J, KW, WQ, mode = v
+                    ents.append(f"    {{{{3, 3, {KW}, {J}, {TE}, {W}, SCB_F32, {WF_F32}, {mode}, {WQ}, 1, "
+                                f"{KIND_TMI}}}, nullptr, nullptr, {32 * (4 + 4 * WQ)}, "
+                                f"&launch_tmi_t<{W}, {TE}, {J}, {KW}, {WQ}, {mode}>}},\n")
                     continue
                 if v[0] == "dws":
                     _, R, S, PAD, TH, LW, KW, mode = v

@@ -23,7 +23,37 @@ namespace {
 constexpr int kSmemLimit = 227 * 1024 - 1024;  // dynamic limit: 227 KB minus the kernels' static shared memory
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
-constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4, KIND_DTM = 5;
+constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4, KIND_DTM = 5, KIND_TMI = 6;
+
+// SM count of a device (persistent grids), cached per device
+int sm_count(int dev) {
+    static int cnt[64];
+    if (dev < 0 || dev >= 64) return 148;
+    if (cnt[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cnt[dev] = v;
+    }
+    return cnt[dev];
+}
+
+// TMEM image-lane geometry (= tmi.cuh TmiGeom<W, TE, J>)
+struct TmiG {
+    int W, TE, J, UE, CPR, SROWS, RW, SW, WIN, NSLOT, CS, NSET, IMGS;
+    explicit TmiG(const scb_variant_info& v) : W(v.tw), TE(v.th), J(v.nbt) {
+        UE = W / TE;
+        const bool fullh = TE == W;
+        CPR = fullh ? TE + 1 : TE + 2;
+        SROWS = fullh ? 3 * CPR + 1 : 3 * CPR;
+        RW = J * W;
+        SW = SROWS * RW;
+        WIN = TE * RW;
+        NSLOT = 512 / SW;
+        CS = NSLOT >= 8 ? NSLOT / 4 : 1;
+        NSET = std::min(8, NSLOT / CS);
+        IMGS = 32 * J / UE;
+    }
+};
 
 scb_status cuda_fail(cudaError_t e, const char* where) {
     return fail(SCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -91,6 +121,55 @@ struct scb_layer {
     struct Blocks { DirectTap* taps = nullptr; int32_t* off = nullptr; };
     std::map<std::vector<int>, Blocks> d_blocks;
     std::map<std::pair<int, int>, int> blk_cap;  // (cc, kw) -> largest block in 16-byte units
+    // TMEM image-lane tables (tmi.cuh), key (SW, CPR, RW, CS): taps {v, TMEM column} per
+    // output channel in CSR order, each run padded to an even count (16-byte aligned)
+    struct TmiTables { TmiTap* taps = nullptr; int32_t* tbase = nullptr; int32_t* soff = nullptr; int tcap = 0; };
+    std::map<std::vector<int>, TmiTables> d_tmi;
+
+    TmiTables tmi_tables(int sw, int cpr, int rw, int cs, int nset) {
+        std::lock_guard<std::mutex> lk(mu);
+        std::vector<int> key{sw, cpr, rw, cs, nset};
+        auto it = d_tmi.find(key);
+        if (it != d_tmi.end()) return it->second;
+        const int64_t pp = (int64_t)g.hp * g.wp;
+        const int nst = (g.c + cs - 1) / cs;
+        std::vector<TmiTap> taps;
+        std::vector<int32_t> tb(g.k + 1), so((size_t)g.k * (nst + 1));
+        int tcap = 2;
+        for (int k = 0; k < g.k; ++k) {
+            tb[k] = (int32_t)taps.size();
+            int st = 0;
+            for (int t = h_rowptr[k]; t < h_rowptr[k + 1]; ++t) {
+                const int64_t c = h_colidx[t] / pp, rem = h_colidx[t] % pp;
+                const int r = (int)(rem / g.wp), s2 = (int)(rem % g.wp);
+                while (st <= nst && (int64_t)st * cs <= c) so[(size_t)k * (nst + 1) + st++] = t - h_rowptr[k];
+                TmiTap d;
+                const uint32_t vb = native_bits(t);
+                std::memcpy(&d.v, &vb, 4);
+                d.col = (uint32_t)((c % cs) * sw + (s2 * cpr + r) * rw);
+                taps.push_back(d);
+            }
+            const int cnt = h_rowptr[k + 1] - h_rowptr[k];
+            while (st <= nst) so[(size_t)k * (nst + 1) + st++] = cnt;
+            if (taps.size() & 1) taps.push_back(TmiTap{0.f, 0u});
+            tcap = std::max(tcap, (int)taps.size() - tb[k]);
+        }
+        tb[g.k] = (int32_t)taps.size();
+        TmiTables T;
+        T.tcap = tcap;
+        if (taps.empty()) taps.push_back(TmiTap{0.f, 0u});
+        if (cudaMalloc(&T.taps, taps.size() * sizeof(TmiTap)) != cudaSuccess) return TmiTables{};
+        if (cudaMalloc(&T.tbase, tb.size() * 4) != cudaSuccess) { cudaFree(T.taps); return TmiTables{}; }
+        if (cudaMalloc(&T.soff, so.size() * 4) != cudaSuccess) { cudaFree(T.taps); cudaFree(T.tbase); return TmiTables{}; }
+        if (cudaMemcpy(T.taps, taps.data(), taps.size() * sizeof(TmiTap), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(T.tbase, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(T.soff, so.data(), so.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(T.taps); cudaFree(T.tbase); cudaFree(T.soff);
+            return TmiTables{};
+        }
+        d_tmi[key] = T;
+        return T;
+    }
 
     // largest block (16-byte units) for (cc, kw), from the host stage pointers
     int block_cap(int cc, int kw) {
@@ -183,6 +262,7 @@ struct scb_layer {
         for (auto& kv : d_dtaps) cudaFree(kv.second);
         for (auto& kv : d_sptr) cudaFree(kv.second);
         for (auto& kv : d_blocks) { cudaFree(kv.second.taps); cudaFree(kv.second.off); }
+        for (auto& kv : d_tmi) { cudaFree(kv.second.taps); cudaFree(kv.second.tbase); cudaFree(kv.second.soff); }
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
     DirectTap* direct_taps(int plane, int row, const std::vector<int>& col, int es = 4) {
@@ -433,7 +513,7 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     if (g.stride != 1 || v.r != g.r || v.s != g.s || v.pad != g.pad) return false;
     // direct / image-lane kernels take any weight format: their tap blocks carry the
     // decoded native value (decoded once on upload, direct_blocks)
-    const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG) &&
+    const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG || v.kind == KIND_TMI) &&
                          v.wf == (L->dt == SCB_F16 ? WF_F16 : WF_F32);
     if (v.io != L->dt || (v.wf != L->wf && !decoded)) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
@@ -441,6 +521,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     if (v.kind < KIND_DIRECT && !L->prog(v.kt)) return false;
     if (v.kind == KIND_DIMG) {
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
+        return true;
+    }
+    if (v.kind == KIND_TMI) {  // square W x W planes, 3x3 "same" convolution
+        if (g.h != v.tw || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
+        if ((flags & SCB_FLAG_POOL2) && (v.th & 1)) return false;
         return true;
     }
     if (v.kind == KIND_DTM) {
@@ -672,6 +757,42 @@ scb_status derive_dtm(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     return SCB_OK;
 }
 
+// TMEM image-lane variants (tmi.cuh): persistent grid over (lane block, output channel) items.
+scb_status derive_tmi(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const TmiG t(v);
+    const int WQ = v.dispatch, KW = v.kt;
+    const int depth = c.stages == 0 ? 4 : c.stages;
+    if (c.warps_k != WQ || c.imgs != t.IMGS || c.bh != t.TE || c.bw != t.W || c.cc != t.CS)
+        return fail(SCB_ERR_SHAPE, "tmem image-lane launch: warps_k = WQ, imgs = lane block, bh = TE, bw = W, cc = CS");
+    if (depth < 2 || depth > 8) return fail(SCB_ERR_SHAPE, "tmem image-lane launch: stages (filler ring depth) 2..8");
+    int ip = (t.CS * g.h * g.w + 3) / 4 * 4;
+    while ((ip / 4) % 2 == 0) ip += 4;  // odd 16-byte pitch: a quarter-warp's row loads hit 8 bank groups
+    const int stage_fl = (t.IMGS * ip + 31) / 32 * 32;
+    auto T = L->tmi_tables(t.SW, t.CPR, t.RW, t.CS, t.NSET);
+    if (!T.taps) return fail(SCB_ERR_CUDA, "tmem image-lane tables: device allocation failed");
+    const int nst = (g.c + t.CS - 1) / t.CS;
+    const int cap = 4 * WQ * KW;
+    // four filler rings + the consumers' taps and stage offsets
+    d->smem = (size_t)4 * depth * stage_fl * 4 + (size_t)cap * T.tcap * sizeof(TmiTap) + (size_t)cap * (nst + 1) * 4;
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    d->threads = 32 * (4 + 4 * WQ);
+    d->chunk = ip;
+    d->stage_el = stage_fl;
+    d->tap_cap = T.tcap;
+    d->row = depth;
+    d->wp = nst;
+    d->n_ey = 1;
+    d->n_fx = 1;
+    d->nb = (n + t.IMGS - 1) / t.IMGS;
+    d->kblocks = 1;
+    const int64_t items = (int64_t)d->nb * g.k;
+    if (items > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "too many work items");
+    d->grid = (unsigned)std::min<int64_t>(items, sm_count(L->device));
+    return SCB_OK;
+}
+
 // Warp-specialised direct variants (ws.cuh): warps_k consumer warps + 1 producer warp.
 scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     const scb_variant_info& v = variant(c.variant).info;
@@ -719,6 +840,7 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     if (v.kind == KIND_DIMG) return derive_dimg(L, c, n, flags, d);
     if (v.kind == KIND_DWS) return derive_dws(L, c, n, flags, d);
     if (v.kind == KIND_DTM) return derive_dtm(L, c, n, flags, d);
+    if (v.kind == KIND_TMI) return derive_tmi(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -767,6 +889,15 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_TMI) {
+            const TmiG t(v);
+            for (int depth : {3, 5}) {
+                scb_launch c{vi, v.dispatch, t.IMGS, t.TE, t.W, t.CS, depth};
+                Derived d;
+                if (derive(L, c, n, flags, &d) == SCB_OK) out.push_back(c);
+            }
+            continue;
+        }
         if (v.kind == KIND_DTM) {
             scb_launch c{vi, v.nbt, 4 * (32 / v.tw), v.th, v.tw, 8, 2};
             Derived d;
@@ -895,6 +1026,9 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                          (g.h == 4 && v.io != SCB_F16 ? 2.0 : 0.0);
             }
             if (c.stages == 2 || c.stages == 0) score += 0.2;
+            // TMEM image-lane kernels: correct, measured slower than direct on VGG-CIFAR
+            // (profiles/r02_tmem_*): tuner candidates only, never the untuned default
+            if (v.kind == KIND_TMI) score = -100.0;
         } else {
             const double acc = (double)v.kt * v.nbt * v.th * v.tw;  // MACs per tap dispatch
             const double restage = 1.0 / (c.warps_k * v.kt);        // input re-reads per channel
@@ -1080,6 +1214,26 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
     if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
+    if (ve.info.kind == KIND_TMI) {
+        const TmiG t(ve.info);
+        auto T = L->tmi_tables(t.SW, t.CPR, t.RW, t.CS, t.NSET);
+        if (!T.taps) return fail(SCB_ERR_CUDA, "tmem image-lane tables: device allocation failed");
+        TmiParams q;
+        std::memset(&q, 0, sizeof(q));
+        q.x = static_cast<const float*>(x);
+        q.bias = static_cast<const float*>(bias);
+        q.y = static_cast<float*>(y);
+        q.taps = T.taps; q.tbase = T.tbase; q.soff = T.soff;
+        q.n = n; q.c = g.c; q.k = g.k;
+        q.nst = d.wp; q.nblk = d.nb; q.depth = d.row; q.ipitch = d.chunk; q.stage_fl = d.stage_el;
+        q.tcap = d.tap_cap; q.items = d.nb * g.k;
+        q.aq = L->aq;
+        q.flags = flags;
+        *fused_aq = true;
+        if (reinterpret_cast<uintptr_t>(y) & 7) return fail(SCB_ERR_UNSUPPORTED, "tmem image-lane kernel needs an 8-byte aligned output");
+        cudaError_t e = ve.tlaunch(q, d.grid, d.smem, st);
+        return e == cudaSuccess ? SCB_OK : cuda_fail(e, "tmem image-lane kernel launch");
+    }
     if (ve.info.kind >= KIND_DIRECT) {
         DirectParams q;
         std::memset(&q, 0, sizeof(q));

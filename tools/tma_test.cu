@@ -43,7 +43,7 @@ int main(int argc, char** argv) {
   CUresult r = enc(&p.m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dx, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   CUtensorMap* dm; cudaMalloc(&dm, sizeof(CUtensorMap)); cudaMemcpy(dm, &p.m, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
-  p.gm = dm; p.use_global = use_global; p.x0 = neg ? -1 : 0; p.y0 = neg ? -1 : 0;
+  p.gm = dm; p.use_global = use_global; p.x0 = (neg & 1) ? -1 : 0; p.y0 = (neg & 2) ? -1 : 0;
   p.n = bw*10*2*4; cudaMalloc(&dout, p.n*4); p.out = dout;
   k<<<1, 128, p.n*4>>>(p);
   cudaError_t e = cudaDeviceSynchronize();
