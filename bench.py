@@ -54,6 +54,8 @@ def parse():
                     "(tuner skipped), else written after tuning")
     ap.add_argument("--cpu-images", type=int, default=8, help="images per CPU-baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline time budget")
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="reference arm: time budget of warm-up + timed steps (bounds the per-step sample)")
     ap.add_argument("--chains", type=int, default=2, help="sub-batch chains on separate streams per GPU")
     ap.add_argument("--graph", type=int, default=0, help="1: replay the stack as one CUDA graph per step")
     ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch between layers")
@@ -141,6 +143,39 @@ class Clocks:
 # CPU legs (the oracle: reference algorithm restated in C, OpenMP threads)
 # ---------------------------------------------------------------------------
 
+def oracle_forward(x, specs, kernels, biases):
+    """The conv stack through the oracle (oracle/oracle.c, the reference's
+    conv_sparse_kernel restated, golden-pinned): conv_sparse -> ReLU -> 2x2
+    max-pool in the activation dtype, exactly the reference's Model.forward glue
+    (store.py:276-284).  Checker / CPU baseline only."""
+    from oracle import oracle as orc
+    a = x
+    for (spec, pool), kern, b in zip(specs, kernels, biases):
+        sh = spec.shape
+        z = orc.conv_sparse(a, kern.values, kern.colidx, kern.rowptr, sh.k, sh.r, sh.s, sh.stride,
+                            sh.padding, b)
+        a = np.maximum(z, z.dtype.type(0))
+        if pool:
+            n, k, e, f = a.shape
+            a = a.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
+    return a
+
+
+def parity_gate(name, got, want):
+    """Bit-for-bit gate of a timed configuration against the oracle (the reference
+    gates every timed result, bench.py:139-147)."""
+    from paper_2011_06295_b200.errors import IntegrityError
+    got = np.ascontiguousarray(got)
+    if got.shape != want.shape or got.dtype != want.dtype:
+        raise IntegrityError(f"{name}: output {got.shape}/{got.dtype} vs oracle {want.shape}/{want.dtype}")
+    iv = {2: np.uint16, 4: np.uint32}[want.dtype.itemsize]
+    bad = int(np.count_nonzero(got.view(iv) != want.view(iv)))
+    if bad:
+        raise IntegrityError(f"{name}: {bad} of {want.size} outputs differ from the oracle")
+    return {"vs": "oracle (oracle/oracle.c: reference conv_sparse_kernel restated, golden-pinned)",
+            "bitwise": True, "outputs": int(want.size)}
+
+
 def cpu_stack_time(specs, kernels, biases, images: int, budget_s: float, seed: int = 7,
                    steps: int | None = None, warmup: int = 1):
     """Run the reference algorithm over the conv stack on `images` images
@@ -152,16 +187,7 @@ def cpu_stack_time(specs, kernels, biases, images: int, budget_s: float, seed: i
     x0 = rng.standard_normal((images, specs[0][0].shape.c, 32, 32)).astype(np.float32)
 
     def one_pass():
-        a = x0
-        for (spec, pool), kern, b in zip(specs, kernels, biases):
-            sh = spec.shape
-            z = orc.conv_sparse(a, kern.values, kern.colidx, kern.rowptr, sh.k, sh.r, sh.s, sh.stride,
-                                sh.padding, b)
-            a = np.maximum(z, 0)
-            if pool:
-                n, k, e, f = a.shape
-                a = a.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
-        return a
+        return oracle_forward(x0, specs, kernels, biases)
 
     for _ in range(max(1, warmup)):
         one_pass()  # warm (threads, page faults)
@@ -189,30 +215,134 @@ def build_kernels(specs, seed: int = 0):
     return kernels, biases
 
 
+def repo_libs_loaded():
+    """Shared objects under this repo mapped into the process (evidence of which native code ran)."""
+    try:
+        maps = Path("/proc/self/maps").read_text()
+    except OSError:
+        return None
+    root = str(ROOT.resolve())
+    return sorted({ln.split()[-1][len(root) + 1:] for ln in maps.splitlines()
+                   if ln.split() and ln.split()[-1].startswith(root) and ".so" in ln.split()[-1]})
+
+
+def workload_name(sparsity: float) -> str:
+    return (f"VGG-16 CIFAR-10, 13 sparse 3x3 convs at {sparsity:g} unified sparsity, bias+ReLU, "
+            "2x2 max-pool per stage, exact fp32 (mul+add)")
+
+
+# VGG-16/CIFAR conv stack (name, C, H, K, pool) = synth.VGG16_CIFAR_LAYERS, restated here so
+# the reference arm imports nothing of this repo
+_VGG = [("conv1_1", 3, 32, 64, 0), ("conv1_2", 64, 32, 64, 1), ("conv2_1", 64, 16, 128, 0),
+        ("conv2_2", 128, 16, 128, 1), ("conv3_1", 128, 8, 256, 0), ("conv3_2", 256, 8, 256, 0),
+        ("conv3_3", 256, 8, 256, 1), ("conv4_1", 256, 4, 512, 0), ("conv4_2", 512, 4, 512, 0),
+        ("conv4_3", 512, 4, 512, 1), ("conv5_1", 512, 2, 512, 0), ("conv5_2", 512, 2, 512, 0),
+        ("conv5_3", 512, 2, 512, 1)]
+
+
+def _import_reference():
+    """The UNMODIFIED reference package, pip-installed into baseline/_ref (DESIGN.md
+    'reference arm'): its numba conv_sparse, build_csr and make_layer_weights."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_sparseconv_ref")
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "sparseconv").is_dir():
+        raise ImportError(f"reference not installed at {ref_dir}")
+    if str(ref_dir) not in sys.path:
+        sys.path.insert(0, str(ref_dir))
+    import sparseconv
+    if not str(Path(sparseconv.__file__).resolve()).startswith(str(ref_dir.resolve())):
+        raise ImportError(f"sparseconv resolved to {sparseconv.__file__}, not {ref_dir}")
+    return sparseconv
+
+
 def run_reference(args, rank: int, world: int):
+    """The reference's own CPU path for the same workload: sparseconv.conv_sparse (numba,
+    sc/engine.py:68-87) with EnginePlan(sub_batch_size=8, worker_count=os.cpu_count()),
+    CSR from sparseconv.build_csr, weights from sparseconv.bench.make_layer_weights, the
+    Model.forward glue (ReLU, 2x2 max-pool) in numpy.  One step = one pass over
+    `images` images of the 256-image batch (all 256 unless the steps would not fit the
+    time budget; then a bounded sample, stated in config)."""
     if rank != 0:
         return
-    specs = workload(args.sparsity)
-    kernels, biases = build_kernels(specs)
-    # a step = one pass of the stack over a bounded sample of cpu_images images;
-    # W untimed warm-up passes, then exactly K timed passes
-    per_pass, passes, threads = cpu_stack_time(specs, kernels, biases, args.cpu_images,
-                                               max(args.cpu_seconds, 1.0), steps=args.steps,
-                                               warmup=args.warmup)
-    ips = args.cpu_images / per_pass
+    ref = _import_reference()
+    import numba
+    specs = [(ref.LayerSpec(n, ref.ConvShape(n=1, c=c, h=h, w=h, k=k, r=3, s=3, stride=1, padding=1),
+                            args.sparsity), bool(pool)) for n, c, h, k, pool in _VGG]
+    kernels, biases = [], []
+    for spec, _ in specs:
+        kernels.append(ref.build_csr(ref.bench.make_layer_weights(spec, seed=0), spec.shape))
+        brng = np.random.default_rng(1)  # = bench inputs: x (1 image) then bias, default_rng(seed+1)
+        brng.standard_normal((1, spec.shape.c, spec.shape.h, spec.shape.w))
+        biases.append(brng.standard_normal(spec.shape.k).astype(np.float32))
+    cores = os.cpu_count() or 1
+    plan = ref.EnginePlan(sub_batch_size=8, worker_count=cores)
+    x_all = np.random.default_rng(7).standard_normal((args.batch, 3, 32, 32)).astype(np.float32)
+
+    def one_pass(x):
+        a = x
+        for (spec, pool), kern, b in zip(specs, kernels, biases):
+            a = np.maximum(ref.conv_sparse(a, kern, b, plan), 0)
+            if pool:
+                n, k, e, f = a.shape
+                a = a.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
+        return a
+
+    one_pass(x_all[:8])  # numba JIT compile (the reference's own first call), untimed
+    t0 = time.perf_counter()
+    one_pass(x_all)
+    t_full = time.perf_counter() - t0
+    images = args.batch
+    budget = max(60.0, args.ref_seconds)
+    if t_full * (args.steps + args.warmup) > budget:
+        images = max(8, int(args.batch * budget / (t_full * (args.steps + args.warmup))) // 8 * 8)
+    x = x_all[:images]
+    for _ in range(max(0, args.warmup - 1)):
+        one_pass(x)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        one_pass(x)
+        ts.append(time.perf_counter() - t0)
+    per_pass = sum(ts) / len(ts)
+    ips = images / per_pass
+    # second figure: the oracle's C restatement (oracle/, OpenMP) on the same sample, <= 3 passes
+    port = None
+    try:
+        from oracle import oracle as orc
+        okern = [orc.build_csr(w, spec.shape.h, spec.shape.w, spec.shape.padding)
+                 for (spec, _), w in zip(specs, [ref.bench.make_layer_weights(sp, seed=0) for sp, _ in specs])]
+
+        class _K:  # oracle CSR triple in the attribute form oracle_forward reads
+            def __init__(self, t):
+                self.values, self.colidx, self.rowptr = t[0], t[1], t[2]
+        ospecs = [(type("S", (), {"shape": spec.shape})(), pool) for spec, pool in specs]
+        oracle_forward(x, ospecs, [_K(t) for t in okern], biases)
+        tp = []
+        for _ in range(min(3, args.steps)):
+            t0 = time.perf_counter()
+            oracle_forward(x, ospecs, [_K(t) for t in okern], biases)
+            tp.append(time.perf_counter() - t0)
+        port = {"images_per_s": round(images / (sum(tp) / len(tp)), 3), "cores": orc.max_threads(),
+                "passes": len(tp), "what": "oracle/oracle.c restatement of conv_sparse_kernel (C, OpenMP)"}
+    except Exception as e:  # the port is a secondary figure only
+        port = {"unavailable": str(e)[:200]}
     line = {
         "impl": "reference", "metric": METRIC, "value": round(ips, 3), "unit": "images/s",
-        "n_gpus": args.gpus, "steps": passes, "warmup": max(1, args.warmup),
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(per_pass * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (make_layer_weights bench.py:105-116 restated; N(0,1) inputs)",
-        "config": {"workload": f"VGG-16 CIFAR-10 13-conv stack, {args.sparsity:g} unified sparsity, "
-                               f"fp32, conv+bias+ReLU(+2x2 max-pool)", "images_per_sample": args.cpu_images,
-                   "global_batch": args.cpu_images, "parallelism": "cpu"},
-        "cpu_baseline": {"value": round(ips, 3), "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{passes} passes of the 13-layer stack over {args.cpu_images} images "
-                                   f"(oracle/oracle.c conv_sparse restatement, OpenMP {threads} threads)"},
+        "data": "synthetic: sparseconv.bench.make_layer_weights (reference), N(0,1) activations",
+        "config": {"workload": workload_name(args.sparsity), "global_batch": args.batch,
+                   "images_per_step": images, "parallelism": "cpu",
+                   "normalisation": "images/s = images per step / step time (per-image work identical "
+                                    "to the 256-image batch)" if images != args.batch else "full batch per step"},
+        "cpu_baseline": {"value": round(ips, 3), "unit": "images/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} passes of the 13-layer stack over {images} images through "
+                                   f"the unmodified reference sparseconv.conv_sparse (numba "
+                                   f"{numba.__version__}, EnginePlan(sub_batch_size=8, worker_count={cores}))"},
         "e2e": {"value": round(ips, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "port": port,
+        "repo_native_libs_loaded": repo_libs_loaded(),
     }
     print(json.dumps(line), flush=True)
 
@@ -314,6 +444,9 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
         ev[1].synchronize()
         ts.append(ev[0].elapsed_time(ev[1]))
     ms = statistics.median(ts)
+    gates = {"f16": parity_gate("f16 stack", net.forward_device(x).cpu().numpy(),
+                                oracle_forward(x.cpu().numpy(), specs, [L.kernel for L in net.layers],
+                                               [L.bias for L in net.layers]))["bitwise"]}
     # dense fp16 comparator: channels_last tensor-core convolutions
     torch.backends.cudnn.benchmark = True
     ws = [torch.from_numpy(__import__("paper_2011_06295_b200").decompress(L.kernel).astype(np.float16)).to(dev)
@@ -338,12 +471,15 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
         ev[1].record()
         ev[1].synchronize()
         td.append(ev[0].elapsed_time(ev[1]))
-    # the config-4 weight formats: 4-bit codebook and linear 16-bit weights (decoded into the
-    # direct kernels' tap blocks on upload; same f16 activations and FHFMA arithmetic)
-    from paper_2011_06295_b200.synth import codebook16, linear16
+    # the config-4 weight formats with the REFERENCE's quantizers (quantize_weights_array
+    # codebook:16 -> 4-bit codes + f16 table, fixed:16 -> int16 codes x 2^-frac; restated
+    # bit-exactly by synth.reference_quantize, pinned by tests/golden/quant_vgg.json)
+    from paper_2011_06295_b200.synth import reference_quantized_values_fn
+    fixture = ROOT / "tests" / "golden" / "quant_vgg.json"
     fmts = {}
-    for fmt, fn in (("cb4", codebook16), ("lin16", linear16)):
-        qn = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_format=fmt, weight_fn=fn)
+    for fmt, kind in (("cb4", "codebook"), ("lin16", "fixed")):
+        qn = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_format=fmt,
+                       values_fn=reference_quantized_values_fn(kind, fixture))
         qn.plan(args.batch, tune=not args.no_tune)
         for _ in range(3):
             qn.forward_device(x)
@@ -357,9 +493,12 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
             tq.append(ev[0].elapsed_time(ev[1]))
         fmts[fmt] = {"ms_per_step": round(statistics.median(tq), 4),
                      "images_per_s": round(args.batch / (statistics.median(tq) * 1e-3), 1)}
+        gates[fmt] = parity_gate(f"f16 stack, {fmt} weights", qn.forward_device(x).cpu().numpy(),
+                                 oracle_forward(x.cpu().numpy(), specs, [L.kernel for L in qn.layers],
+                                                [L.bias for L in qn.layers]))["bitwise"]
         del qn
     return {"images_per_s": round(args.batch / (ms * 1e-3), 1), "ms_per_step": round(ms, 4),
-            "weight_formats": fmts,
+            "weight_formats": fmts, "parity_bitwise_vs_oracle": gates,
             "dense_cudnn_fp16_ms": round(statistics.median(td), 4),
             "arith": "f16 storage, FHFMA (f16 x f16 + f32) accumulation, bit-identical to the reference f16 profile",
             "launches": [None if l is None else list(l) for l in net.launches]}
@@ -387,9 +526,13 @@ def measure_alexnet(args, dev, local_rank, reps: int = 10):
         ev[1].synchronize()
         ts.append(ev[0].elapsed_time(ev[1]))
     ms = statistics.median(ts)
+    gate = parity_gate("AlexNet-style stack", net.forward_device(x).cpu().numpy(),
+                       oracle_forward(x.cpu().numpy(), alexnet_cifar(args.sparsity), [L.kernel for L in net.layers],
+                                      [L.bias for L in net.layers]))["bitwise"]
     macs = sum(batch * L.kernel.shape.k * L.kernel.shape.e * L.kernel.shape.f * L.kernel.sparse_level
                for L in net.layers)
     return {"images_per_s": round(batch / (ms * 1e-3), 1), "ms_per_step": round(ms, 4), "batch": batch,
+            "parity_bitwise_vs_oracle": gate,
             "tflops": round(2 * macs / (ms * 1e-3) / 1e12, 3),
             "launches": [None if l is None else list(l) for l in net.launches]}
 
@@ -452,6 +595,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     x_host = torch.randn((args.batch, 3, 32, 32), generator=g).pin_memory()
     x_dev = x_host.to(dev)
     integrity_gate(net, x_dev)
+    # the exact timed configuration (tuned launches, sub-batch chains, PDL) against the oracle,
+    # bit for bit, on this step's 256-image input
+    got = net.forward_device(x_dev).cpu().numpy()
+    parity = parity_gate("VGG-16/CIFAR fp32 stack (timed mode)", got,
+                         oracle_forward(x_host.numpy(), specs, [L.kernel for L in net.layers],
+                                        [L.bias for L in net.layers]))
+    parity.update({"images": args.batch, "mode": f"timed launches, {args.chains} sub-batch chain(s), "
+                                                  f"pdl={not args.no_pdl}"})
     if args.graph:
         net.x_in.copy_(x_dev)
         net.capture()  # forward_device replays it (per-layer event passes stay eager)
@@ -555,8 +706,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "warmup": max(args.warmup, 3), "ms_per_step": round(total_s / args.steps * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: make_layer_weights (bench.py:105-116 restated), N(0,1) activations",
-        "config": {"workload": f"VGG-16 CIFAR-10, 13 sparse 3x3 convs at {args.sparsity:g} unified sparsity, "
-                               "bias+ReLU fused, 2x2 max-pool fused per stage, exact fp32 (mul+add)",
+        "config": {"workload": workload_name(args.sparsity),
                    "batch_per_gpu": args.batch, "global_batch": args.batch * world,
                    "parallelism": f"batch-sharded x{world} (weak, no collective)",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
@@ -568,8 +718,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "gpu_launches": net.kernels_per_step() * args.steps,
         "clocks": clk.summary(),
         "roofline": roof,
+        "parity": parity,
         "layers": layers,
         "fma_peaks_tflops": {k: round(v, 2) for k, v in peaks.items()},
+        "repo_native_libs_loaded": repo_libs_loaded(),
     }
     if not args.no_f16:
         line["f16"] = measure_f16(specs, args, dev, local_rank)

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk)
 #pragma unroll
-            for (int j = 0; j < HW; ++j) acc[kk][j] = fq_store<E>(r0 && acc[kk][j] < 0.f ? 0.f : acc[kk][j], p.aq);
+            for (int j = 0; j < HW; ++j) acc[kk][j] = fq_store<E>(r0 ? relu_io<E>(acc[kk][j]) : acc[kk][j], p.aq);
     }
     const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
     const bool pool = p.flags & SCB_FLAG_POOL2;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
         if (k >= p.k) break;
         float o[HW];
 #pragma unroll
-        for (int j = 0; j < HW; ++j) o[j] = (relu && acc[kk][j] < 0.f) ? 0.f : acc[kk][j];
+        for (int j = 0; j < HW; ++j) o[j] = relu ? relu_io<E>(acc[kk][j]) : acc[kk][j];
         if (!pool) {
             E* yp = static_cast<E*>(p.y) + ((int64_t)n * p.k + k) * HW;
             if constexpr (F16) {

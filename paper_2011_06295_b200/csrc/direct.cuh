@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk)
 #pragma unroll
-            for (int j = 0; j < TH * VX; ++j) acc[kk][j] = fq_store<TIO>(r0 && acc[kk][j] < 0.f ? 0.f : acc[kk][j], p.aq);
+            for (int j = 0; j < TH * VX; ++j) acc[kk][j] = fq_store<TIO>(r0 ? relu_io<TIO>(acc[kk][j]) : acc[kk][j], p.aq);
     }
     const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;  // (already applied with the quantizer)
     const bool pool = p.flags & SCB_FLAG_POOL2;
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
 #pragma unroll
                 for (int j = 0; j < TH; ++j) {
                     float o0 = acc[kk][j];
-                    if (relu && o0 < 0.f) o0 = 0.f;
+                    if (relu) o0 = relu_io<TIO>(o0);
                     if (ox0 + lx + j * LW < p.f) yp[j * LW] = o0;
                 }
             }
@@ -388,12 +388,12 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 for (int j = 0; j < TH; ++j) {
                     if (j >= jmax) break;
                     float o0 = acc[kk][j * VX];
-                    if (relu && o0 < 0.f) o0 = 0.f;
+                    if (relu) o0 = relu_io<TIO>(o0);
                     if constexpr (VX == 1) {
                         yp[j * FP * fpitch] = (TIO)o0;
                     } else {
                         float o1 = acc[kk][j * VX + 1];
-                        if (relu && o1 < 0.f) o1 = 0.f;
+                        if (relu) o1 = relu_io<TIO>(o1);
                         if constexpr (F16IO)
                             *reinterpret_cast<__half2*>(yp + j * LW) = __floats2half2_rn(o0, o1);
                         else
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 } else {
                     o = fmaxf(fmaxf(acc[kk][2 * j], acc[kk][2 * j + 1]), fmaxf(acc[kk][2 * j + 2], acc[kk][2 * j + 3]));
                 }
-                if (relu && o < 0.f) o = 0.f;
+                if (relu) o = relu_io<TIO>(o);
                 const int py = (oy0 + j) >> 1;
                 if (n < p.n && !(lx & 1) && ox0 + lx < p.f && py < pe)
                     static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] = (TIO)o;

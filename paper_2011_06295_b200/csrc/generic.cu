@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ Generic
                     acc = mac1<MODE>(acc, v, xv);
                 }
             }
-            if ((p.flags & SCB_FLAG_RELU) && acc < 0.f) acc = 0.f;
+            if (p.flags & SCB_FLAG_RELU) acc = relu_io<T>(acc);  // f16: round, then max(., 0)
             if constexpr (std::is_same<T, __half>::value) y[idx] = __float2half_rn(acc);
             else y[idx] = acc;
         }

@@ -60,6 +60,19 @@ __device__ __forceinline__ float fq_store<__half>(float o, const ActQuant& q) {
     return __half2float(fq_f16(__float2half_rn(o), q));
 }
 
+// ReLU in the storage dtype (store.py:284 applies np.maximum(., 0) to the conv output AFTER
+// it was rounded to the activation dtype): for f16 a tiny negative sum rounds to -0.0 and
+// stays -0.0.  Returns the exact float of the value to store.
+template <typename T>
+__device__ __forceinline__ float relu_io(float o);
+template <>
+__device__ __forceinline__ float relu_io<float>(float o) { return o < 0.f ? 0.f : o; }
+template <>
+__device__ __forceinline__ float relu_io<__half>(float o) {
+    const float r = __half2float(__float2half_rn(o));
+    return r < 0.f ? 0.f : r;
+}
+
 template <int MODE>
 __device__ __forceinline__ float mac1(float acc, float v, float x) {
     if constexpr (MODE == MODE_EXACT) return __fadd_rn(acc, __fmul_rn(v, x));

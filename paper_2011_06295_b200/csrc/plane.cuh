@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256, MINB) k_plane(const __grid_constant__ Til
                 TIO* yp = static_cast<TIO*>(p.y) + ((int64_t)n * p.k + k) * EF;
                 float o[EF];
 #pragma unroll
-                for (int i = 0; i < EF; ++i) o[i] = (relu && a[i] < 0.f) ? 0.f : a[i];
+                for (int i = 0; i < EF; ++i) o[i] = relu ? relu_io<TIO>(a[i]) : a[i];
                 if constexpr (!F16IO && EF % 4 == 0) {
 #pragma unroll
                     for (int i = 0; i < EF; i += 4)
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256, MINB) k_plane(const __grid_constant__ Til
                     for (int xx = 0; xx < PF; ++xx) {
                         float o = fmaxf(fmaxf(a[(2 * yy) * F + 2 * xx], a[(2 * yy) * F + 2 * xx + 1]),
                                         fmaxf(a[(2 * yy + 1) * F + 2 * xx], a[(2 * yy + 1) * F + 2 * xx + 1]));
-                        if (relu && o < 0.f) o = 0.f;
+                        if (relu) o = relu_io<TIO>(o);
                         if constexpr (F16IO) yp[yy * PF + xx] = __float2half_rn(o);
                         else yp[yy * PF + xx] = o;
                     }

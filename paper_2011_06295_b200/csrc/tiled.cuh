@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
                     for (int xx = 0; xx < TW; ++xx) {
                         if (ox0t + xx >= p.f) continue;
                         float o = a[yy * TW + xx];
-                        if (relu && o < 0.f) o = 0.f;
+                        if (relu) o = relu_io<TIO>(o);
                         if constexpr (F16IO) yrow[xx] = __float2half_rn(o);
                         else yrow[xx] = o;
                     }
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(256, MINB) k_tiled(const __grid_constant__ Til
                         if (ox >= pf) continue;
                         float o = fmaxf(fmaxf(a[yy * TW + xx], a[yy * TW + xx + 1]),
                                         fmaxf(a[(yy + 1) * TW + xx], a[(yy + 1) * TW + xx + 1]));
-                        if (relu && o < 0.f) o = 0.f;
+                        if (relu) o = relu_io<TIO>(o);
                         TIO* yp = static_cast<TIO*>(p.y) + pbase + (int64_t)oy * pf + ox;
                         if constexpr (F16IO) *yp = __float2half_rn(o);
                         else *yp = o;

@@ -406,10 +406,12 @@ class SparseConvNet:
 
 
 def build_net(specs_pools, seed: int = 0, dtype=np.float32, device: int = 0,
-              weight_format: str = "native", fast_math: bool = False, weight_fn=None):
+              weight_format: str = "native", fast_math: bool = False, weight_fn=None, values_fn=None):
     """SparseConvNet of synthetic unified-sparsity layers
     (synth.make_layer_weights / bench_inputs, bench.py:105-116,175-177).
-    `weight_fn(w) -> w` post-processes each layer's weights (e.g. synth.codebook16)."""
+    `weight_fn(w) -> w` post-processes each layer's dense weights (e.g. synth.codebook16);
+    `values_fn(name, values) -> values` replaces each layer's CSR values (e.g. the
+    reference quantizer, synth.reference_quantized_values_fn)."""
     from .synth import bench_inputs, make_layer_weights
     from .weights import build_csr
     layers = []
@@ -418,6 +420,11 @@ def build_net(specs_pools, seed: int = 0, dtype=np.float32, device: int = 0,
         if weight_fn is not None:
             w = weight_fn(w)
         _, b = bench_inputs(spec.shape, 1, seed)
-        layers.append(NetLayer(spec.name, build_csr(w, spec.shape), b, relu=True, pool=pool))
+        kern = build_csr(w, spec.shape)
+        if values_fn is not None:
+            from dataclasses import replace
+            kern = replace(kern, values=np.ascontiguousarray(values_fn(spec.name, kern.values)),
+                           _device_cache={})
+        layers.append(NetLayer(spec.name, kern, b, relu=True, pool=pool))
     return SparseConvNet(layers, device=device, dtype=dtype, weight_format=weight_format,
                          fast_math=fast_math)

@@ -13,6 +13,7 @@ there is no network for datasets or checkpoints).
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -142,3 +143,61 @@ def linear16(w: np.ndarray, frac: int = 8) -> np.ndarray:
     q = np.clip(np.round(w.astype(np.float64) * s), -(2 ** 15 - 1), 2 ** 15 - 1) / s
     q[(w != 0) & (q == 0)] = 1.0 / s  # keep the sparsity pattern
     return q.astype(w.dtype)
+
+
+def reference_quantize(values: np.ndarray, kind: str, centers=None, pin_zero: bool = False,
+                       bits: int = 16) -> np.ndarray:
+    """Restates quantize_weights_array(values, kind, bits) (quantize.py:265-288) on a CSR
+    values array, bit for bit (pinned by tests/golden/quant_vgg.json digests):
+
+    * "fixed": fit_fixed_point (int_bits = ceil(log2 max|x|), clamped at 0) and
+      quantize_fixed (mu + sigma * round((x - mu) / sigma), saturated), quantize.py:48-71,
+      computed in float64, then cast to the storage dtype;
+    * "codebook": the decode of build_codebook (quantize.py:217-246): every value takes
+      the float64 k-means center nearest to it (squared distance, first on ties -- the
+      final assignment of _cluster.py:45-47), the table is stored as float16; with
+      pin_zero the zeros keep centroid 0 = 0.0.  `centers` are the reference's k-means
+      centers (they come from its seeded k-means++ run, recorded by
+      tests/golden/make_quant_vgg.py)."""
+    dtype = values.dtype
+    x = np.asarray(values, dtype=np.float64).ravel()
+    if kind == "fixed":
+        m = float(np.max(np.abs(x))) if x.size else 0.0
+        int_bits = 0 if m == 0 else max(0, math.ceil(math.log2(m)))
+        sigma = 2.0 ** (-(bits - int_bits - 1))
+        mu = 0.0
+        q = mu + sigma * np.round((x - mu) / sigma)
+        return np.clip(q, -(2.0 ** int_bits), 2.0 ** int_bits - sigma).astype(dtype).reshape(values.shape)
+    if kind != "codebook":
+        raise ShapeError(f"unknown quantizer {kind!r}")
+    c = np.asarray(centers, dtype=np.float64).ravel()
+    labels = np.zeros(x.size, dtype=np.int64)
+    sel = x != 0 if pin_zero else np.ones(x.size, bool)
+    pts = x[sel]
+    best = np.full(pts.size, np.inf)
+    lab = np.zeros(pts.size, dtype=np.int64)
+    for j, cj in enumerate(c):  # argmin over centers, first on ties
+        d = (pts - cj) ** 2
+        upd = d < best
+        best[upd] = d[upd]
+        lab[upd] = j
+    table = np.concatenate([[0.0], c]) if pin_zero else c
+    labels[sel] = lab + (1 if pin_zero else 0)
+    return table.astype(np.float16)[labels].astype(dtype).reshape(values.shape)
+
+
+def reference_quantized_values_fn(kind: str, fixture) -> "callable":
+    """values_fn for network.build_net: replaces each layer's CSR values by the
+    reference quantizer's output (config 4 with the reference's own "fixed:16" /
+    "codebook:16" weights), using the recorded k-means centers of `fixture`
+    (tests/golden/quant_vgg.json)."""
+    import json
+    from pathlib import Path
+    recs = {r["name"]: r for r in json.loads(Path(fixture).read_text())["layers"]}
+
+    def fn(name, values):
+        r = recs[name]
+        if kind == "fixed":
+            return reference_quantize(values, "fixed")
+        return reference_quantize(values, "codebook", r["codebook"]["centers"], r["codebook"]["pin_zero"])
+    return fn

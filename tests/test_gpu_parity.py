@@ -20,6 +20,14 @@ from golden_gen import c1_configs, make_case, random_sparse_weights, sha256
 pytestmark = pytest.mark.gpu
 
 
+
+def relu_pool_ref(ref):
+    """The reference's glue in its own dtype (store.py:284): np.maximum(conv, 0) on the
+    conv output as stored (f16 rounded first), then the 2x2 max-pool."""
+    r = np.maximum(ref, ref.dtype.type(0))
+    n, k, e, f = r.shape
+    return r.reshape(n, k, e // 2, 2, f // 2, 2).max(axis=(3, 5))
+
 def bits(a):
     a = np.ascontiguousarray(a)
     return a.view({2: np.uint16, 4: np.uint32, 8: np.uint64}[a.dtype.itemsize])
@@ -399,7 +407,7 @@ def test_plane_kernels_bitwise(sc, orc, c, hw, k, sp, n, dtype):
         o = sc.conv_sparse(xd, kern, bq, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
     # fused ReLU + 2x2 max-pool epilogue
-    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref.astype(np.float32))), 2).numpy()
+    want = relu_pool_ref(ref)
     flags = 0x1 | 0x4
     for cfg in _plane_cands(layer, n, flags)[:6]:
         o = sc.conv_sparse(xd, kern, bq, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
@@ -435,7 +443,7 @@ def test_direct_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     for cfg in cands[:: max(1, len(cands) // 30)] + ws[:: max(1, len(ws) // 20)] + tm:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
-    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref)), 2).numpy()
+    want = relu_pool_ref(ref)
     pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] in (2, 4, 5)]
     for cfg in pc[:: max(1, len(pc) // 8)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
@@ -474,7 +482,7 @@ def test_wide_direct_kernels_bitwise(sc, orc, c, h, w, k, r, pad, sp, n):
     o = sc.conv_sparse(xd, kern, b).cpu().numpy()
     assert beq(o, ref)
     if sh.e % 2 == 0 and sh.f % 2 == 0:
-        want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref)), 2).numpy()
+        want = relu_pool_ref(ref)
         pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 2 and vs[cf[0]]["dispatch"] == 2]
         assert pc
         for cfg in pc[:: max(1, len(pc) // 6)]:
@@ -534,7 +542,7 @@ def test_image_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n, dt):
     for cfg in cands[:: max(1, len(cands) // 30)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
-    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref.astype(np.float32))), 2).numpy()
+    want = relu_pool_ref(ref)
     pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 3]
     for cfg in pc[:: max(1, len(pc) // 6)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()
@@ -566,7 +574,7 @@ def test_direct_f16_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     for cfg in cands[:: max(1, len(cands) // 20)] + vx1[:: max(1, len(vx1) // 10)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
         assert beq(o, ref), cfg
-    want = torch.nn.functional.max_pool2d(torch.relu(torch.from_numpy(ref.astype(np.float32))), 2).numpy()
+    want = relu_pool_ref(ref)
     pc = [cf for cf in layer.candidates(n, 0x5) if vs[cf[0]]["kind"] == 2]
     for cfg in pc[:: max(1, len(pc) // 6)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg), relu=True, pool=True).cpu().numpy()

@@ -160,3 +160,77 @@ def test_subbatch_chains_bitwise(torch, vgg_small, chains):
             assert np.array_equal(_bits(o.numpy()), _bits(ref if i % 2 == 0 else oracle_stack(net, x2))), i
     finally:
         net.set_chains(1)
+
+
+# ---------------------------------------------------------------------------
+# The exact configurations bench.py times ("pin every timed
+# configuration to the oracle"): full batches, shipped launch table, sub-batch
+# chains and PDL as in the timed step.
+# ---------------------------------------------------------------------------
+
+def _bits16(a):
+    return np.ascontiguousarray(a).view(np.uint16)
+
+
+@pytest.mark.parametrize("sparsity,chains", [(0.9, 2), (0.9, 1), (0.95, 2)])
+def test_config3_vgg_batch256_timed_mode_bitwise(torch, sparsity, chains):
+    """BASELINE config 3: VGG-16/CIFAR, 256 images, the shipped (tuned-on-B200) launch
+    table, `chains` sub-batch chains on separate streams, PDL -- vs the oracle."""
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import vgg16_cifar
+    net = build_net(vgg16_cifar(sparsity), seed=0)
+    net.plan(256, tune=False)
+    net.set_chains(chains)
+    net.pdl = True
+    x = np.random.default_rng(11).standard_normal((256, 3, 32, 32)).astype(np.float32)
+    got = net.forward_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(oracle_stack(net, x)))
+
+
+@pytest.mark.parametrize("fmt", ["native", "cb4", "lin16"])
+def test_config4_vgg_f16_batch256_bitwise(torch, fmt):
+    """BASELINE config 4: the same stack with f16 activations and weights -- plain f16,
+    the REFERENCE's codebook:16 weights as 4-bit codes (cb4) and its fixed:16 weights as
+    int16 codes (lin16), restated bit-exactly (synth.reference_quantize, pinned by
+    tests/golden/quant_vgg.json) -- batch 256, in-kernel decode + FHFMA, vs the oracle."""
+    from pathlib import Path
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import reference_quantized_values_fn, vgg16_cifar
+    fixture = Path(__file__).resolve().parent / "golden" / "quant_vgg.json"
+    fn = {"native": None, "cb4": reference_quantized_values_fn("codebook", fixture),
+          "lin16": reference_quantized_values_fn("fixed", fixture)}[fmt]
+    net = build_net(vgg16_cifar(0.9), seed=0, dtype=np.float16, weight_format=fmt, values_fn=fn)
+    net.plan(256, tune=False)
+    x = np.random.default_rng(12).standard_normal((256, 3, 32, 32)).astype(np.float16)
+    got = net.forward_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(_bits16(got), _bits16(oracle_stack(net, x)))
+
+
+def test_config2_alexnet_batch128_bitwise(torch):
+    """BASELINE config 2: AlexNet-style CIFAR stack (5x5 and 3x3), batch 128."""
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import alexnet_cifar
+    net = build_net(alexnet_cifar(0.9), seed=0)
+    net.plan(128, tune=False)
+    x = np.random.default_rng(13).standard_normal((128, 3, 32, 32)).astype(np.float32)
+    got = net.forward_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(oracle_stack(net, x)))
+
+
+@pytest.mark.parametrize("sparsity", [0.9, 0.95, 0.99])
+@pytest.mark.parametrize("dt", [np.float32, np.float16])
+def test_config5_sweep_points_batch512_bitwise(torch, sparsity, dt):
+    """BASELINE config 5 sweep points: 256->256 3x3 @32x32, batch 512, the launch the
+    sweep times (shipped table / heuristic) -- vs the oracle."""
+    import paper_2011_06295_b200 as sc
+    from oracle import oracle as orc
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=512, c=256, h=32, w=32, k=256, r=3, s=3, padding=1)
+    w = make_layer_weights(LayerSpec("sweep", sh, sparsity), seed=0).astype(dt)
+    x, b = bench_inputs(sh, 512)
+    x = x.astype(dt)
+    kern = sc.build_csr(w, sh)
+    got = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, b).cpu().numpy()
+    want = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 256, 3, 3, 1, 1, b)
+    iv = np.uint16 if dt == np.float16 else np.uint32
+    assert np.array_equal(got.view(iv), want.view(iv))

@@ -87,3 +87,25 @@ def test_fake_quant_matches_reference():
     for i, m in enumerate(meta):
         y = orc.fake_quant(z[f"x{i}"], m["params"])
         assert y.dtype == z[f"y{i}"].dtype and np.array_equal(_bits(y), _bits(z[f"y{i}"])), (i, m)
+
+
+def test_reference_quantizers_restated_bitwise():
+    """synth.reference_quantize reproduces the reference's quantize_weights_array
+    ("fixed", 16) and ("codebook", 16, seed=0) on every VGG-16/CIFAR layer's f16 CSR
+    values bit for bit (digests recorded from the reference, make_quant_vgg.py)."""
+    import hashlib
+    import json
+
+    import paper_2011_06295_b200 as sc
+    from paper_2011_06295_b200.synth import LayerSpec, make_layer_weights, reference_quantize, vgg16_cifar
+    fx = json.loads((GOLDEN / "quant_vgg.json").read_text())
+    recs = {r["name"]: r for r in fx["layers"]}
+    for spec, _ in vgg16_cifar(0.9):
+        r = recs[spec.name]
+        vals = sc.build_csr(make_layer_weights(spec, 0).astype(np.float16), spec.shape).values
+        assert hashlib.sha256(vals.tobytes()).hexdigest() == r["values_sha"], spec.name
+        fixed = reference_quantize(vals, "fixed")
+        assert hashlib.sha256(fixed.tobytes()).hexdigest() == r["fixed"]["sha"], spec.name
+        cb = reference_quantize(vals, "codebook", r["codebook"]["centers"], r["codebook"]["pin_zero"])
+        assert hashlib.sha256(cb.tobytes()).hexdigest() == r["codebook"]["sha"], spec.name
+        assert len(np.unique(cb)) <= 16
