@@ -429,7 +429,8 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
     reference's f16 profile), vs dense cuDNN fp16 tensor-core convolutions."""
     import torch
     from paper_2011_06295_b200.network import build_net
-    net = build_net(specs, seed=0, dtype=np.float16, device=local_rank)
+    from paper_2011_06295_b200.synth import f16_scaled
+    net = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_fn=f16_scaled)
     net.plan(args.batch, tune=not args.no_tune)
     x = torch.randn((args.batch, 3, 32, 32), device=dev).half()
     for _ in range(3):
@@ -479,7 +480,7 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
     fmts = {}
     for fmt, kind in (("cb4", "codebook"), ("lin16", "fixed")):
         qn = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_format=fmt,
-                       values_fn=reference_quantized_values_fn(kind, fixture))
+                       weight_fn=f16_scaled, values_fn=reference_quantized_values_fn(kind, fixture))
         qn.plan(args.batch, tune=not args.no_tune)
         for _ in range(3):
             qn.forward_device(x)

@@ -145,6 +145,17 @@ def linear16(w: np.ndarray, frac: int = 8) -> np.ndarray:
     return q.astype(w.dtype)
 
 
+def f16_scaled(w: np.ndarray) -> np.ndarray:
+    """Config-4 weights in f16 storage: make_layer_weights' N(0,1) nonzeros scaled by
+    sqrt(2 / L) (L = nonzeros per output channel, He-style) in float32, then rounded to
+    f16.  Unscaled N(0,1) weights overflow f16 by conv3_3 of the VGG stack (inf, then
+    NaN), which no fp16 deployment would run; the f32 stack keeps the unscaled weights.
+    Restated identically by tests/golden/make_quant_vgg.py."""
+    w = np.asarray(w, dtype=np.float32)
+    L = int(np.count_nonzero(w.reshape(w.shape[0], -1)[0]))
+    return (w * np.float32(math.sqrt(2.0 / max(L, 1)))).astype(np.float16)
+
+
 def reference_quantize(values: np.ndarray, kind: str, centers=None, pin_zero: bool = False,
                        bits: int = 16) -> np.ndarray:
     """Restates quantize_weights_array(values, kind, bits) (quantize.py:265-288) on a CSR

@@ -6,7 +6,8 @@ Run in the build container (the reference is not on the GPU box):
         python tests/golden/make_quant_vgg.py
 
 For every VGG-16/CIFAR layer at 90 % unified sparsity (make_layer_weights,
-bench.py:105-116, seed 0) in f16 storage, the CSR values (build_csr) are passed
+bench.py:105-116, seed 0, scaled by sqrt(2/L) as synth.f16_scaled does) in f16
+storage, the CSR values (build_csr) are passed
 through quantize_weights_array(values, "fixed", 16) and ("codebook", 16, seed=0)
 (quantize.py:265-288).  Stored per layer: the sha256 of both reference outputs
 (bit patterns), the fixed-point split, and the codebook's float64 k-means centers
@@ -17,6 +18,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+import math
 from pathlib import Path
 
 import numpy as np
@@ -42,7 +44,10 @@ def main():
     recs = []
     for name, c, h, k in LAYERS:
         sh = ConvShape(n=1, c=c, h=h, w=h, k=k, r=3, s=3, stride=1, padding=1)
-        w16 = make_layer_weights(LayerSpec(name, sh, 0.9), seed=0).astype(np.float16)
+        w = make_layer_weights(LayerSpec(name, sh, 0.9), seed=0)
+        # = synth.f16_scaled: N(0,1) nonzeros x sqrt(2/L) in f32, rounded to f16
+        L = int(np.count_nonzero(w.reshape(w.shape[0], -1)[0]))
+        w16 = (w.astype(np.float32) * np.float32(math.sqrt(2.0 / max(L, 1)))).astype(np.float16)
         vals = build_csr(w16, sh).values
         fixed, fmeta, _ = quantize_weights_array(vals, "fixed", 16)
         cbv, cmeta, cb = quantize_weights_array(vals, "codebook", 16, seed=0)

@@ -195,15 +195,18 @@ def test_config4_vgg_f16_batch256_bitwise(torch, fmt):
     tests/golden/quant_vgg.json) -- batch 256, in-kernel decode + FHFMA, vs the oracle."""
     from pathlib import Path
     from paper_2011_06295_b200.network import build_net
-    from paper_2011_06295_b200.synth import reference_quantized_values_fn, vgg16_cifar
+    from paper_2011_06295_b200.synth import f16_scaled, reference_quantized_values_fn, vgg16_cifar
     fixture = Path(__file__).resolve().parent / "golden" / "quant_vgg.json"
     fn = {"native": None, "cb4": reference_quantized_values_fn("codebook", fixture),
           "lin16": reference_quantized_values_fn("fixed", fixture)}[fmt]
-    net = build_net(vgg16_cifar(0.9), seed=0, dtype=np.float16, weight_format=fmt, values_fn=fn)
+    net = build_net(vgg16_cifar(0.9), seed=0, dtype=np.float16, weight_format=fmt, weight_fn=f16_scaled,
+                    values_fn=fn)
     net.plan(256, tune=False)
     x = np.random.default_rng(12).standard_normal((256, 3, 32, 32)).astype(np.float16)
     got = net.forward_device(torch.from_numpy(x).cuda()).cpu().numpy()
-    assert np.array_equal(_bits16(got), _bits16(oracle_stack(net, x)))
+    want = oracle_stack(net, x)
+    assert np.isfinite(want).all()  # the scaled f16 stack stays in range
+    assert np.array_equal(_bits16(got), _bits16(want))
 
 
 def test_config2_alexnet_batch128_bitwise(torch):

@@ -97,12 +97,12 @@ def test_reference_quantizers_restated_bitwise():
     import json
 
     import paper_2011_06295_b200 as sc
-    from paper_2011_06295_b200.synth import LayerSpec, make_layer_weights, reference_quantize, vgg16_cifar
+    from paper_2011_06295_b200.synth import f16_scaled, make_layer_weights, reference_quantize, vgg16_cifar
     fx = json.loads((GOLDEN / "quant_vgg.json").read_text())
     recs = {r["name"]: r for r in fx["layers"]}
     for spec, _ in vgg16_cifar(0.9):
         r = recs[spec.name]
-        vals = sc.build_csr(make_layer_weights(spec, 0).astype(np.float16), spec.shape).values
+        vals = sc.build_csr(f16_scaled(make_layer_weights(spec, 0)), spec.shape).values
         assert hashlib.sha256(vals.tobytes()).hexdigest() == r["values_sha"], spec.name
         fixed = reference_quantize(vals, "fixed")
         assert hashlib.sha256(fixed.tobytes()).hexdigest() == r["fixed"]["sha"], spec.name
