@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--batch", type=int, default=256, help="images per GPU")
+    ap.add_argument("--batch", type=int, default=256,
+                    help="GLOBAL batch (BASELINE config 3: 256), split into contiguous per-GPU shards")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the batch-32 (8-GPU shard) proxy line")
     ap.add_argument("--sparsity", type=float, default=0.9)
     ap.add_argument("--no-tune", action="store_true", help="C heuristic launches instead of the tuner")
     ap.add_argument("--launches", default="", help="JSON of per-layer launches: loaded if present "
@@ -538,6 +540,35 @@ def measure_alexnet(args, dev, local_rank, reps: int = 10):
             "launches": [None if l is None else list(l) for l in net.launches]}
 
 
+def measure_shard_proxy(args, specs, local_rank, dev, rate_full: float, reps: int = 20):
+    """The 8-GPU strong-scaling shard on one GPU: the same stack re-planned (tuned) for
+    batch/8 = 32 images, timed like the main step.  Its per-image rate as a fraction of the
+    full batch's is what 8 GPUs can at best scale to (no collective on the compute path)."""
+    import torch
+    from paper_2011_06295_b200.network import build_net
+    nb = args.batch // 8
+    net = build_net(specs, seed=0, device=local_rank)
+    net.plan(nb, tune=not args.no_tune)
+    net.pdl = not args.no_pdl
+    x = torch.randn((nb, 3, 32, 32), device=dev)
+    for _ in range(5):
+        net.forward_device(x)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(reps):
+        net.forward_device(x)
+    ev[1].record()
+    ev[1].synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / reps
+    rate = nb / (ms * 1e-3)
+    return {"images_per_gpu": nb, "ms_per_step": round(ms, 4), "images_per_s": round(rate, 1),
+            "fraction_of_full_batch_rate": round(rate / rate_full, 4),
+            "implied_8gpu_images_per_s": round(8 * rate, 1),
+            "note": "back-to-back steps without L2 flush (the shard's working set is L2-resident on a real "
+                    "8-GPU run too); launches tuned at this batch"}
+
+
 def load_traffic():
     """Per-layer DRAM traffic (dram__bytes_read.sum + write.sum) from the
     committed ncu --set full capture summary, if any."""
@@ -575,15 +606,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2011_06295_b200.network import build_net
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    from paper_2011_06295_b200.runner import shard_range, shard_sizes
     specs = workload(args.sparsity)
     net = build_net(specs, seed=0, device=local_rank)
+    # strong scaling: the global batch is split into contiguous shards, one per rank
+    s0, s1 = shard_range(args.batch, world, rank)
+    nloc = s1 - s0
     t0 = time.perf_counter()
     lf = Path(args.launches) if args.launches else None
     if lf is not None and lf.exists():
-        net.plan(args.batch, tune=False)
+        net.plan(nloc, tune=False)
         net.set_launches([None if l is None else tuple(l) for l in json.loads(lf.read_text())])
     else:
-        net.plan(args.batch, tune=not args.no_tune)
+        net.plan(nloc, tune=not args.no_tune)
         if lf is not None and rank == 0:
             lf.parent.mkdir(parents=True, exist_ok=True)
             lf.write_text(json.dumps([None if l is None else list(l) for l in net.launches]))
@@ -592,18 +627,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     net.set_chains(args.chains)
     net.pdl = not args.no_pdl
 
-    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
-    x_host = torch.randn((args.batch, 3, 32, 32), generator=g).pin_memory()
+    g = torch.Generator(device="cpu").manual_seed(1234)
+    x_global = torch.randn((args.batch, 3, 32, 32), generator=g)  # identical on every rank
+    x_host = x_global[s0:s1].contiguous().pin_memory()
     x_dev = x_host.to(dev)
     integrity_gate(net, x_dev)
     # the exact timed configuration (tuned launches, sub-batch chains, PDL) against the oracle,
-    # bit for bit, on this step's 256-image input
+    # bit for bit, on this rank's shard of the step's input
     got = net.forward_device(x_dev).cpu().numpy()
     parity = parity_gate("VGG-16/CIFAR fp32 stack (timed mode)", got,
                          oracle_forward(x_host.numpy(), specs, [L.kernel for L in net.layers],
                                         [L.bias for L in net.layers]))
-    parity.update({"images": args.batch, "mode": f"timed launches, {args.chains} sub-batch chain(s), "
-                                                  f"pdl={not args.no_pdl}"})
+    parity.update({"images": nloc, "mode": f"timed launches, {args.chains} sub-batch chain(s), "
+                                           f"pdl={not args.no_pdl}"})
     if args.graph:
         net.x_in.copy_(x_dev)
         net.capture()  # forward_device replays it (per-layer event passes stay eager)
@@ -646,22 +682,49 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     layer_ms = [[ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(nlay)] for i in range(nl)]
 
-    # e2e: the host-facing streaming call (SparseConvNet.forward_stream): every step's input
-    # is copied from pinned host memory and its result read back to pinned host memory
-    # inside the timed region; copies of neighbouring steps overlap the compute
-    out_host = torch.empty(net.out_shape(nl - 1, args.batch), dtype=torch.float32, pin_memory=True)
-    xs_host = [x_host] * args.steps
-    outs_host = [torch.empty_like(out_host).pin_memory() for _ in range(2)]
-    outs_list = [outs_host[i % 2] for i in range(args.steps)]
-    net.forward_stream(xs_host[:2], outs_list[:2])
+    # e2e through the host-facing API, every step's host->device input copy and device->host
+    # result inside the timed region.  N = 1: SparseConvNet.forward_stream (pinned host in and
+    # out, copies of neighbouring steps overlapped with compute).  N > 1: per step each rank
+    # copies its shard in, runs the stack, the outputs are gathered to rank 0 with a collective
+    # (BatchShardedRunner, NCCL over NVLink) and rank 0 reads the global result back.
+    out_shape_loc = net.out_shape(nl - 1, nloc)
     e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    torch.cuda.synchronize()
-    if world > 1:
+    if world == 1:
+        out_host = torch.empty(out_shape_loc, dtype=torch.float32, pin_memory=True)
+        xs_host = [x_host] * args.steps
+        outs_host = [torch.empty_like(out_host).pin_memory() for _ in range(2)]
+        outs_list = [outs_host[i % 2] for i in range(args.steps)]
+        net.forward_stream(xs_host[:2], outs_list[:2])
+        torch.cuda.synchronize()
+        e_ev[0].record(stream)
+        net.forward_stream(xs_host, outs_list)
+        e_ev[1].record(stream)
+        e_ev[1].synchronize()
+        gather_api = "SparseConvNet.forward_stream (pinned host in/out, copies overlapped across steps)"
+    else:
+        from paper_2011_06295_b200.runner import BatchShardedRunner
+        x_step = torch.empty_like(x_dev)
+        out_host = torch.empty((args.batch, *out_shape_loc[1:]), dtype=torch.float32, pin_memory=True)
+
+        def fwd(xh):
+            x_step.copy_(xh, non_blocking=True)
+            return net.forward_device(x_step)
+        runner = BatchShardedRunner(fwd)
+
+        def e2e_step():
+            y = runner.run(x_host)  # x_host is this rank's shard; sizes exchanged by all_gather
+            if rank == 0:
+                out_host.copy_(y, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
         dist.barrier()
-    e_ev[0].record(stream)
-    net.forward_stream(xs_host, outs_list)
-    e_ev[1].record(stream)
-    e_ev[1].synchronize()
+        e_ev[0].record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e_ev[1].record(stream)
+        e_ev[1].synchronize()
+        gather_api = ("BatchShardedRunner.run: per-rank H2D of the shard, SparseConvNet.forward_device, "
+                      f"{dist.get_backend()} gather to rank 0, D2H of the global output on rank 0")
     e2e_s = e_ev[0].elapsed_time(e_ev[1]) * 1e-3
 
     # max over ranks
@@ -670,10 +733,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # device time: max over ranks
     total_s, e2e_s = float(t[0]), float(t[1])
+    proxy = None
+    if world == 1 and not args.no_proxy and args.batch >= 64:
+        proxy = measure_shard_proxy(args, specs, local_rank, dev, args.batch / (total_s / args.steps))
     if rank != 0:
         return
 
-    images = args.batch * args.steps * world
+    images = args.batch * args.steps  # the global batch per step (strong scaling)
     value = images / total_s
     peaks = fma_peak_tflops(local_rank)
     peak_exact = peaks.get("fmul_fadd")
@@ -684,13 +750,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     layers = []
     for i, ((spec, pool), kern) in enumerate(zip(specs, [L.kernel for L in net.layers])):
         us = statistics.median(layer_ms[i]) * 1e3
-        fl, by = layer_work(spec, kern.sparse_level, args.batch, pool)
+        fl, by = layer_work(spec, kern.sparse_level, nloc, pool)
         layers.append({"layer": spec.name, "L": int(kern.sparse_level), "us": round(us, 2),
                        "tflops": round(fl / (us * 1e-6) / 1e12, 3), "hbm_gbs": round(by / (us * 1e-6) / 1e9, 1),
                        "fma_frac": round(fl / (us * 1e-6) / 1e12 / peak_exact, 4) if peak_exact else None,
                        "launch": list(launches[i]) if launches[i] is not None else "generic"})
     top = max(range(nl), key=lambda i: layers[i]["us"])
-    fl, by = layer_work(specs[top][0], layers[top]["L"], args.batch, specs[top][1])
+    fl, by = layer_work(specs[top][0], layers[top]["L"], nloc, specs[top][1])
     mean_us = statistics.mean(layer_ms[top]) * 1e3
     ach = fl / (mean_us * 1e-6) / 1e12
     roof = {"bound": "fma", "kernel": specs[top][0].name, "achieved": round(ach, 3), "peak": round(peak_exact, 3),
@@ -705,17 +771,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(total_s / args.steps * 1e3, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: make_layer_weights (bench.py:105-116 restated), N(0,1) activations",
         "config": {"workload": workload_name(args.sparsity),
-                   "batch_per_gpu": args.batch, "global_batch": args.batch * world,
-                   "parallelism": f"batch-sharded x{world} (weak, no collective)",
+                   "batch_per_gpu": max(shard_sizes(args.batch, world)), "global_batch": args.batch,
+                   "parallelism": f"batch-sharded x{world} (strong: shards {shard_sizes(args.batch, world)}; "
+                                  "no collective on the compute path, final gather in e2e)",
                    "l2": "flushed between timed steps (256 MB write, untimed)",
                    "tuned": not args.no_tune, "tune_seconds": round(tune_s, 1),
                    "streams_per_gpu": args.chains, "pdl": not args.no_pdl, "cuda_graph": bool(args.graph)},
-        "e2e": {"value": round(args.batch * args.steps * world / e2e_s, 1), "unit": "images/s",
-                "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
-                "api": "SparseConvNet.forward_stream (pinned host in/out, copies overlapped across steps)"},
+        "e2e": {"value": round(args.batch * args.steps / e2e_s, 1), "unit": "images/s",
+                "h2d_bytes_per_step": int(args.batch * 3 * 32 * 32 * 4),
+                "d2h_bytes_per_step": int(args.batch * int(np.prod(out_shape_loc[1:])) * 4),
+                "api": gather_api},
         "gpu_launches": net.kernels_per_step() * args.steps,
         "clocks": clk.summary(),
         "roofline": roof,
@@ -724,11 +792,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "fma_peaks_tflops": {k: round(v, 2) for k, v in peaks.items()},
         "repo_native_libs_loaded": repo_libs_loaded(),
     }
-    if not args.no_f16:
+    if proxy is not None:
+        line["proxy_8gpu_shard"] = proxy
+    if not args.no_f16 and world == 1:
         line["f16"] = measure_f16(specs, args, dev, local_rank)
-    if not args.no_alexnet:
+    if not args.no_alexnet and world == 1:
         line["alexnet"] = measure_alexnet(args, dev, local_rank)
-    if not args.no_dense:
+    if not args.no_dense and world == 1:
         line["dense_cudnn"] = dense_cudnn(specs, [L.kernel for L in net.layers], [L.bias for L in net.layers],
                                           args.batch, dev)
     if not args.no_cpu and world == 1:

@@ -10,9 +10,31 @@
 #pragma once
 
 #include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace scb {
+
+// Opt a kernel into the full dynamic shared memory on the CURRENT device.  The
+// attribute is per (function, device), so `lim` is a per-launcher array indexed by
+// device: a process driving several GPUs sets it once on each (benign race:
+// idempotent).  Returns cudaErrorInvalidValue if `smem` exceeds the limit.
+template <typename K>
+inline cudaError_t dyn_smem_ok(K kern, size_t smem, int (&lim)[64]) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (lim[dev] == 0) {
+        cudaFuncAttributes fa;
+        if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
+        const int l = 227 * 1024 - (int)fa.sharedSizeBytes;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l)) != cudaSuccess) return e;
+        lim[dev] = l;
+    }
+    return (int)smem > lim[dev] ? cudaErrorInvalidValue : cudaSuccess;
+}
 
 enum { MODE_EXACT = 0, MODE_FMA = 1 };
 enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3 };

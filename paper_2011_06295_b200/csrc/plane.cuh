@@ -183,17 +183,9 @@ __global__ void __launch_bounds__(256, MINB) k_plane(const __grid_constant__ Til
 template <int H, int W, int R, int S, int PAD, int KT, int NBT, bool F16IO, int WF, int MODE, int MINB>
 cudaError_t launch_plane_t(const TiledParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
     auto kern = k_plane<H, W, R, S, PAD, KT, NBT, F16IO, WF, MODE, MINB>;
-    static int max_dyn = -1;  // benign race: idempotent
-    if (max_dyn < 0) {
-        cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-        if (e != cudaSuccess) return e;
-        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        if (e != cudaSuccess) return e;
-        max_dyn = lim;
-    }
-    if ((int)smem > max_dyn) return cudaErrorInvalidValue;
+    static int lim[64];  // per device (the attribute is per device)
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
+    if (e != cudaSuccess) return e;
     kern<<<grid, threads, smem, st>>>(p);
     return cudaGetLastError();
 }

@@ -347,17 +347,9 @@ template <int R, int S, int PAD, int KT, int NBT, int TH, int TW, bool F16IO, in
           int MINB>
 cudaError_t launch_tiled_t(const TiledParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
     auto kern = k_tiled<R, S, PAD, KT, NBT, TH, TW, F16IO, WF, MODE, DISPATCH, MINB>;
-    static int max_dyn = -1;  // benign race: idempotent
-    if (max_dyn < 0) {
-        cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-        if (e != cudaSuccess) return e;
-        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        if (e != cudaSuccess) return e;
-        max_dyn = lim;
-    }
-    if ((int)smem > max_dyn) return cudaErrorInvalidValue;
+    static int lim[64];  // per device (the attribute is per device)
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
+    if (e != cudaSuccess) return e;
     kern<<<grid, threads, smem, st>>>(p);
     return cudaGetLastError();
 }

@@ -273,17 +273,9 @@ __global__ void __launch_bounds__(128 * M, 1) k_dtm(const __grid_constant__ Dire
 template <int R, int S, int PAD, int TH, int LW, int KW, int M, int MODE>
 cudaError_t launch_dtm_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
     auto kern = k_dtm<R, S, PAD, TH, LW, KW, M, MODE>;
-    static int max_dyn = -1;  // benign race: idempotent
-    if (max_dyn < 0) {
-        cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-        if (e != cudaSuccess) return e;
-        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        if (e != cudaSuccess) return e;
-        max_dyn = lim;
-    }
-    if ((int)smem > max_dyn) return cudaErrorInvalidValue;
+    static int lim[64];  // per device (the attribute is per device)
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
+    if (e != cudaSuccess) return e;
     return launch_pdl(kern, p, grid, threads, smem, st);
 }
 

@@ -490,21 +490,9 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WQ), 1) k_tmi(const __grid_const
 template <int W, int TE, int J, int KW, int WQ, int MODE>
 cudaError_t launch_tmi_t(const TmiParams& p, unsigned grid, size_t smem, cudaStream_t st) {
     auto kern = k_tmi<W, TE, J, KW, WQ, MODE>;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    static int lim[64];  // per device (the attribute is per device)
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
     if (e != cudaSuccess) return e;
-    static int max_dyn[64];  // per device: the attribute is per (function, device)
-    static bool done[64];
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (!done[dev]) {
-        cudaFuncAttributes fa;
-        if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
-        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)) != cudaSuccess) return e;
-        max_dyn[dev] = lim;
-        done[dev] = true;
-    }
-    if ((int)smem > max_dyn[dev]) return cudaErrorInvalidValue;
     return launch_pdl(kern, p, grid, 32 * (4 + 4 * WQ), smem, st);
 }
 

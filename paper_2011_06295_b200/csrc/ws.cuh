@@ -212,17 +212,9 @@ __global__ void __launch_bounds__(288, 2) k_dws(const __grid_constant__ DirectPa
 template <int R, int S, int PAD, int TH, int LW, int KW, int MODE>
 cudaError_t launch_dws_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
     auto kern = k_dws<R, S, PAD, TH, LW, KW, MODE>;
-    static int max_dyn = -1;  // benign race: idempotent
-    if (max_dyn < 0) {
-        cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-        if (e != cudaSuccess) return e;
-        const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        if (e != cudaSuccess) return e;
-        max_dyn = lim;
-    }
-    if ((int)smem > max_dyn) return cudaErrorInvalidValue;
+    static int lim[64];  // per device (the attribute is per device)
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
+    if (e != cudaSuccess) return e;
     kern<<<grid, threads, smem, st>>>(p);
     return cudaGetLastError();
 }

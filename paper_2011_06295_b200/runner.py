@@ -60,6 +60,8 @@ class BatchShardedRunner:
         if not gather or self.world == 1:
             return y
         sizes = shard_sizes(n, self.world) if n is not None else self._all_sizes(y)
+        if y.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            y = y.cpu()  # gloo gathers host tensors (CPU tests, oversubscribed single-GPU runs)
         # gather needs equal shapes: pad every shard to the largest
         m = max(sizes)
         yp = y
@@ -73,7 +75,8 @@ class BatchShardedRunner:
 
     def _all_sizes(self, y):
         import torch
-        t = torch.tensor([y.shape[0]], dtype=torch.int64, device=y.device)
+        dev = "cpu" if self.dist.get_backend(self.group) == "gloo" else y.device
+        t = torch.tensor([y.shape[0]], dtype=torch.int64, device=dev)
         out = [torch.zeros_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return [int(v.item()) for v in out]

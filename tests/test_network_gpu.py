@@ -237,3 +237,59 @@ def test_config5_sweep_points_batch512_bitwise(torch, sparsity, dt):
     want = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 256, 3, 3, 1, 1, b)
     iv = np.uint16 if dt == np.float16 else np.uint32
     assert np.array_equal(got.view(iv), want.view(iv))
+
+
+# ---------------------------------------------------------------------------
+# batch-sharded runner through the real engine: two ranks on one
+# GPU (gloo for the gather), each planning and running its own shard
+# ---------------------------------------------------------------------------
+
+def _sharded_worker(rank, world, port, n, q):
+    import os
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.runner import BatchShardedRunner, shard_range
+    from paper_2011_06295_b200.synth import vgg16_cifar
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        a, b = shard_range(n, world, rank)
+        net = build_net(vgg16_cifar(0.9), seed=0, device=0)
+        net.plan(b - a, tune=False)
+        net.set_chains(2 if b - a >= 2 else 1)
+        x = torch.from_numpy(np.random.default_rng(21).standard_normal((n, 3, 32, 32)).astype(np.float32))
+        out = BatchShardedRunner(lambda xs: net.forward_device(xs.cuda())).run(x, n=n)
+        if rank == 0:
+            q.put(out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [64, 37])
+def test_batch_sharded_runner_two_ranks_bitwise(torch, n):
+    import socket
+
+    import torch.multiprocessing as mp
+    from paper_2011_06295_b200.network import build_net
+    from paper_2011_06295_b200.synth import vgg16_cifar
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    x = np.random.default_rng(21).standard_normal((n, 3, 32, 32)).astype(np.float32)
+    want = oracle_stack(build_net(vgg16_cifar(0.9), seed=0), x)
+    assert got.shape == want.shape and np.array_equal(_bits(got), _bits(want))
