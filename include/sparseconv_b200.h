@@ -14,7 +14,10 @@
  *    SCB_ERR_CUDA / SCB_ERR_UNSUPPORTED to SparseConvError (errors.py:4).
  *  - Host arrays are C-contiguous.  Device arrays are device pointers in the
  *    current CUDA context of `device`.  `stream` is a cudaStream_t (NULL =
- *    legacy default stream).  Launch functions never allocate or synchronise.
+ *    legacy default stream).  scb_conv_sparse never allocates or synchronises:
+ *    the device tables of a tiled launch are built by scb_layer_prepare (an
+ *    unprepared launch fails with SCB_ERR_ARG), so a prepared launch can be
+ *    captured into a CUDA graph.
  *  - dtype codes: the element type of activations/bias/values.
  */
 #ifndef SPARSECONV_B200_H
@@ -164,6 +167,16 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
 SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
                                    void* y, int32_t n, uint32_t flags,
                                    const scb_launch* cfg, void* stream);
+
+/* Build (allocate + upload, synchronously) the device tables launch `cfg`
+ * (NULL = the default launch) reads for batch n and `flags`; idempotent.  The
+ * reference rebuilds nothing per call either -- its CSR arrays are passed
+ * straight to _kernels.conv_sparse_kernel (engine.py:83-84); this is the
+ * one-time upload of their per-launch device layout. */
+SCB_API scb_status scb_layer_prepare(scb_layer* layer, int32_t n, uint32_t flags, const scb_launch* cfg);
+/* SCB_OK iff `cfg` is a valid launch of this layer for batch n and `flags`
+ * (shape, shared-memory and grid rules); no device work. */
+SCB_API scb_status scb_launch_check(const scb_layer* layer, int32_t n, uint32_t flags, const scb_launch* cfg);
 
 /* Launch candidates for the tuner (replaces SUB_BATCH_CANDIDATES,
  * engine.py:25): writes up to `cap` configs valid for batch n. */

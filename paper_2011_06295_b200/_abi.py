@@ -32,7 +32,7 @@ EXPORTS = (
     "scb_channel_nnz", "scb_select_padding_zeros", "scb_csr_count", "scb_build_csr",
     "scb_validate_csr", "scb_decompress", "scb_layer_create", "scb_layer_destroy",
     "scb_layer_weight_bytes", "scb_conv_sparse", "scb_launch_candidates",
-    "scb_default_launch", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
+    "scb_default_launch", "scb_layer_prepare", "scb_launch_check", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
     "scb_fma_peaks", "scb_fnv1a64", "scb_last_error", "scb_version", "scb_fake_quant",
     "scb_layer_set_act_quant",
 )
@@ -110,6 +110,8 @@ def lib():
             "scb_conv_sparse": [vp, vp, vp, vp, i32, u32, P(Launch), vp],
             "scb_launch_candidates": [vp, i32, u32, P(Launch), i32, P(i32)],
             "scb_default_launch": [vp, i32, u32, i32, P(Launch)],
+            "scb_layer_prepare": [vp, i32, u32, P(Launch)],
+            "scb_launch_check": [vp, i32, u32, P(Launch)],
             "scb_variant_get": [i32, P(VariantInfo)],
             "scb_maxpool2": [i32, vp, vp, i64, i32, i32, vp],
             "scb_fma_peaks": [i32, vp, vp, i32, P(i32)],

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ Generic
             double acc = p.bias ? static_cast<const double*>(p.bias)[k] : 0.0;
             for (int q = t0; q < t1; ++q) {
                 const int d = p.dec[q];
-                const int c = d >> 12, gy = y0 + ((d >> 6) & 63), gx = x0 + (d & 63);
+                const int c = d / (p.kr * p.ks), rs = d - c * (p.kr * p.ks);
+                const int gy = y0 + rs / p.ks, gx = x0 + rs % p.ks;
                 double xv = 0.0;
                 if (gy >= 0 && gy < p.h && gx >= 0 && gx < p.w) xv = xn[((int64_t)c * p.h + gy) * p.w + gx];
                 if constexpr (MODE == MODE_EXACT) acc = __dadd_rn(acc, __dmul_rn(vals[q], xv));
@@ -49,7 +50,8 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ Generic
             if (p.bias) acc = static_cast<const float*>(p.bias)[k];  // compute dtype
             for (int q = t0; q < t1; ++q) {
                 const int d = p.dec[q];
-                const int c = d >> 12, gy = y0 + ((d >> 6) & 63), gx = x0 + (d & 63);
+                const int c = d / (p.kr * p.ks), rs = d - c * (p.kr * p.ks);
+                const int gy = y0 + rs / p.ks, gx = x0 + rs % p.ks;
                 float xv = 0.f, v;
                 if constexpr (std::is_same<T, __half>::value) {
                     if (gy >= 0 && gy < p.h && gx >= 0 && gx < p.w)

@@ -116,9 +116,10 @@ struct GenericParams {
     const void* bias;       // compute dtype (f32, or f64 for f64), may be null
     void* y;
     const void* values;     // native values (f32/f64/f16)
-    const int32_t* dec;     // packed (c << 12) | (r << 6) | s per tap
+    const int32_t* dec;     // flat kernel index c*R*S + r*S + s per tap (any extent: < C*R*S <= 2^31)
     const int32_t* rowptr;
     int n, c, h, w, k, e, f, stride, pad;
+    int kr, ks;             // kernel extent R, S (decode of dec)
     uint32_t flags;
 };
 

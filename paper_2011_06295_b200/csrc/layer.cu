@@ -126,11 +126,18 @@ struct scb_layer {
     struct TmiTables { TmiTap* taps = nullptr; int32_t* tbase = nullptr; int32_t* soff = nullptr; int tcap = 0; };
     std::map<std::vector<int>, TmiTables> d_tmi;
 
-    TmiTables tmi_tables(int sw, int cpr, int rw, int cs, int nset) {
+    // largest per-channel tap run (even), host only: = tmi_tables().tcap
+    int tmi_tcap() const {
+        int tcap = 2;
+        for (int k = 0; k < g.k; ++k) tcap = std::max(tcap, (h_rowptr[k + 1] - h_rowptr[k] + 1) & ~1);
+        return tcap;
+    }
+    TmiTables tmi_tables(int sw, int cpr, int rw, int cs, int nset, bool build) {
         std::lock_guard<std::mutex> lk(mu);
         std::vector<int> key{sw, cpr, rw, cs, nset};
         auto it = d_tmi.find(key);
         if (it != d_tmi.end()) return it->second;
+        if (!build) return TmiTables{};
         const int64_t pp = (int64_t)g.hp * g.wp;
         const int nst = (g.c + cs - 1) / cs;
         std::vector<TmiTap> taps;
@@ -173,7 +180,7 @@ struct scb_layer {
 
     // largest block (16-byte units) for (cc, kw), from the host stage pointers
     int block_cap(int cc, int kw) {
-        if (!stage_ptr(cc)) return -1;
+        host_sptr(cc);
         std::lock_guard<std::mutex> lk(mu);
         auto key = std::make_pair(cc, kw);
         auto it = blk_cap.find(key);
@@ -207,13 +214,14 @@ struct scb_layer {
         return b;
     }
     // device tables: taps (as 16-byte chunks) and per-(g, st) chunk offsets
-    Blocks direct_blocks(int plane, int row, const std::vector<int>& col, int es, int cc, int kw) {
-        if (!stage_ptr(cc)) return Blocks{};
+    Blocks direct_blocks(int plane, int row, const std::vector<int>& col, int es, int cc, int kw, bool build) {
+        if (build) host_sptr(cc);
         std::lock_guard<std::mutex> lk(mu);
         std::vector<int> key{plane, row, es, cc, kw};
         key.insert(key.end(), col.begin(), col.end());
         auto it = d_blocks.find(key);
         if (it != d_blocks.end()) return it->second;
+        if (!build) return Blocks{};
         const std::vector<int32_t>& sp = h_sptr[cc];
         const int64_t pp = (int64_t)g.hp * g.wp;
         const int nst = (g.c + cc - 1) / cc, groups = (g.k + kw - 1) / kw;
@@ -247,8 +255,12 @@ struct scb_layer {
         Blocks b;
         if (cudaMalloc(&b.taps, std::max<size_t>(out.size(), 2) * sizeof(DirectTap)) != cudaSuccess) return Blocks{};
         if (cudaMalloc(&b.off, off.size() * 4) != cudaSuccess) { cudaFree(b.taps); return Blocks{}; }
-        cudaMemcpy(b.taps, out.data(), out.size() * sizeof(DirectTap), cudaMemcpyHostToDevice);
-        cudaMemcpy(b.off, off.data(), off.size() * 4, cudaMemcpyHostToDevice);
+        if (cudaMemcpy(b.taps, out.data(), out.size() * sizeof(DirectTap), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(b.off, off.data(), off.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(b.taps);
+            cudaFree(b.off);
+            return Blocks{};
+        }
         d_blocks[key] = b;
         return b;
     }
@@ -265,12 +277,13 @@ struct scb_layer {
         for (auto& kv : d_tmi) { cudaFree(kv.second.taps); cudaFree(kv.second.tbase); cudaFree(kv.second.soff); }
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
-    DirectTap* direct_taps(int plane, int row, const std::vector<int>& col, int es = 4) {
+    DirectTap* direct_taps(int plane, int row, const std::vector<int>& col, int es, bool build) {
         std::lock_guard<std::mutex> lk(mu);
         std::vector<int> key{plane, row, es};
         key.insert(key.end(), col.begin(), col.end());
         auto it = d_dtaps.find(key);
         if (it != d_dtaps.end()) return it->second;
+        if (!build) return nullptr;
         const int64_t pp = (int64_t)g.hp * g.wp;
         std::vector<DirectTap> t(nnz + 2);  // +2: bulk copies read up to the next 16-byte boundary
         for (int64_t i = 0; i < nnz; ++i) {
@@ -288,11 +301,12 @@ struct scb_layer {
         d_dtaps[key] = d;
         return d;
     }
-    // sptr[k][st] = first tap of row k whose input channel is >= st*cc (st = 0..nst)
-    int32_t* stage_ptr(int cc) {
+    // sptr[k][st] = first tap of row k whose input channel is >= st*cc (st = 0..nst), host copy
+    // (plus the longest (channel, stage) segment); no device work
+    const std::vector<int32_t>& host_sptr(int cc) {
         std::lock_guard<std::mutex> lk(mu);
-        auto it = d_sptr.find(cc);
-        if (it != d_sptr.end()) return it->second;
+        auto it = h_sptr.find(cc);
+        if (it != h_sptr.end()) return it->second;
         const int64_t pp = (int64_t)g.hp * g.wp;
         const int nst = (g.c + cc - 1) / cc;
         std::vector<int32_t> sp((size_t)g.k * (nst + 1));
@@ -309,7 +323,20 @@ struct scb_layer {
             for (int st = 0; st < nst; ++st)
                 mx = std::max(mx, sp[(size_t)k * (nst + 1) + st + 1] - sp[(size_t)k * (nst + 1) + st]);
         sptr_maxseg[cc] = mx;
-        h_sptr[cc] = sp;
+        return h_sptr[cc] = std::move(sp);
+    }
+    int maxseg(int cc) {
+        host_sptr(cc);
+        std::lock_guard<std::mutex> lk(mu);
+        return sptr_maxseg[cc];
+    }
+    // device stage pointers: uploaded by scb_layer_prepare (build), looked up on launch
+    int32_t* stage_ptr(int cc, bool build) {
+        if (build) host_sptr(cc);
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = d_sptr.find(cc);
+        if (it != d_sptr.end() || !build) return it != d_sptr.end() ? it->second : nullptr;
+        const std::vector<int32_t>& sp = h_sptr[cc];
         int32_t* d = nullptr;
         if (cudaMalloc(&d, sp.size() * 4) != cudaSuccess) return nullptr;
         if (cudaMemcpy(d, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -665,7 +692,6 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
     const int rows = G * c.cc * (oned ? 1 : v.th + v.r - 1);
     const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
-    if (cap < 0) return fail(SCB_ERR_CUDA, "direct stage pointers: device allocation failed");
     d->wp = cap;  // tap block slot (16-byte units) travels in `wp`
     d->smem = nbuf * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
               (size_t)nbuf * c.warps_k * cap * 16;
@@ -708,7 +734,6 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = blk;
     const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
-    if (cap < 0) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
     d->wp = cap;
     d->smem = nbuf * stage_bytes + (size_t)nbuf * c.warps_k * cap * 16;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
@@ -742,7 +767,6 @@ scb_status derive_dtm(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     d->stage_el = (int)(stage_bytes / 4);
     d->tap_cap = 32;  // TMEM columns per channel slot
     const int cap = L->block_cap(CC, v.kt);
-    if (cap < 0) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
     d->wp = cap;
     const int rows = G * CC * (v.th + v.r - 1);
     d->smem = 2 * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) + (size_t)2 * M * cap * 16;
@@ -770,17 +794,16 @@ scb_status derive_tmi(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     int ip = (t.CS * g.h * g.w + 3) / 4 * 4;
     while ((ip / 4) % 2 == 0) ip += 4;  // odd 16-byte pitch: a quarter-warp's row loads hit 8 bank groups
     const int stage_fl = (t.IMGS * ip + 31) / 32 * 32;
-    auto T = L->tmi_tables(t.SW, t.CPR, t.RW, t.CS, t.NSET);
-    if (!T.taps) return fail(SCB_ERR_CUDA, "tmem image-lane tables: device allocation failed");
+    const int tcap = L->tmi_tcap();
     const int nst = (g.c + t.CS - 1) / t.CS;
     const int cap = 4 * WQ * KW;
     // four filler rings + the consumers' taps and stage offsets
-    d->smem = (size_t)4 * depth * stage_fl * 4 + (size_t)cap * T.tcap * sizeof(TmiTap) + (size_t)cap * (nst + 1) * 4;
+    d->smem = (size_t)4 * depth * stage_fl * 4 + (size_t)cap * tcap * sizeof(TmiTap) + (size_t)cap * (nst + 1) * 4;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     d->threads = 32 * (4 + 4 * WQ);
     d->chunk = ip;
     d->stage_el = stage_fl;
-    d->tap_cap = T.tcap;
+    d->tap_cap = tcap;
     d->row = depth;
     d->wp = nst;
     d->n_ey = 1;
@@ -812,8 +835,7 @@ scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     const size_t stage_bytes = ((size_t)G * ip * 4 + 16 + 127) & ~(size_t)127;  // +16: zero tail
     d->stage_el = (int)(stage_bytes / 4);
     d->tap_cap = plane;
-    if (!L->stage_ptr(c.cc)) return fail(SCB_ERR_CUDA, "stage pointers: device allocation failed");
-    const int segcap = L->sptr_maxseg[c.cc];
+    const int segcap = L->maxseg(c.cc);
     d->wp = segcap;
     const int slot = (segcap + 3) & ~1;
     const int np1 = (g.c + c.cc - 1) / c.cc + 1;
@@ -1059,7 +1081,6 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
     if (st != SCB_OK) return st;
     if (dtype_size(dt) == 0) return fail(SCB_ERR_ARG, "bad dtype");
     if (!rowptr || (nnz > 0 && (!values || !colidx))) return fail(SCB_ERR_ARG, "NULL arrays");
-    if (g.r > 63 || g.s > 63 || g.c >= (1 << 19)) return fail(SCB_ERR_UNSUPPORTED, "kernel extent > 63 or C >= 2^19");
     if (dt == SCB_F64 && wfmt != SCB_W_NATIVE) return fail(SCB_ERR_UNSUPPORTED, "f64 supports native weights only");
     int level = 0;
     for (int k = 0; k < g.k; ++k) level = std::max(level, rowptr[k + 1] - rowptr[k]);
@@ -1085,19 +1106,23 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
     // generic arrays: native values + decoded (c, r, s)
     const int es = dtype_size(dt);
     const int64_t plane = (int64_t)g.hp * g.wp;
+    // decoded taps of the generic kernel: flat kernel index c*R*S + r*S + s (< C*R*S, which
+    // scb_validate_csr bounds through colidx < C*Hp*Wp <= 2^31-1)
     std::vector<int32_t> dec(std::max<int64_t>(nnz, 1));
     for (int64_t t = 0; t < nnz; ++t) {
-        int64_t c = colidx[t] / plane, rem = colidx[t] % plane;
-        dec[t] = (int32_t)((c << 12) | ((rem / g.wp) << 6) | (rem % g.wp));
+        const int64_t c = colidx[t] / plane, rem = colidx[t] % plane;
+        dec[t] = (int32_t)((c * g.r + rem / g.wp) * g.s + rem % g.wp);
     }
     cudaError_t e;
     if ((e = cudaMalloc(&L->d_values, std::max<int64_t>(nnz, 1) * es)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&L->d_dec, dec.size() * 4)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&L->d_rowptr, (g.k + 1) * 4)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    if (nnz > 0) cudaMemcpy(L->d_values, values, nnz * es, cudaMemcpyHostToDevice);
-    cudaMemcpy(L->d_dec, dec.data(), dec.size() * 4, cudaMemcpyHostToDevice);
-    e = cudaMemcpy(L->d_rowptr, rowptr, (g.k + 1) * 4, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
+    if (nnz > 0 && (e = cudaMemcpy(L->d_values, values, nnz * es, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(L->d_dec, dec.data(), dec.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(L->d_rowptr, rowptr, (g.k + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy");
 
     L->h_colidx.assign(colidx, colidx + nnz);
     L->h_rowptr.assign(rowptr, rowptr + g.k + 1);
@@ -1168,6 +1193,77 @@ SCB_API scb_status scb_default_launch(const scb_layer* layer, int32_t n, uint32_
 static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const void* bias, void* y, int32_t n,
                                    uint32_t flags, const scb_launch* cfg, void* stream, bool* fused_aq);
 
+// Device tables a launch reads.  build = true (scb_layer_prepare): create and upload them
+// (cudaMalloc + synchronous copies).  build = false (scb_conv_sparse): look them up only, so
+// the launch path never allocates or synchronises.
+struct LaunchTables {
+    const DirectTap* taps = nullptr;
+    const int32_t* blkoff = nullptr;
+    const int32_t* sptr = nullptr;
+    scb_layer::TmiTables tmi;
+};
+static scb_status launch_tables(scb_layer* L, const scb_launch& c, const Derived& d, bool build, LaunchTables* t) {
+    const VariantEntry& ve = variant(c.variant);
+    const Geom& g = L->g;
+    const char* missing = "launch not prepared: call scb_layer_prepare(layer, n, flags, launch) first";
+    if (ve.info.kind == KIND_TMI) {
+        const TmiG tg(ve.info);
+        t->tmi = L->tmi_tables(tg.SW, tg.CPR, tg.RW, tg.CS, tg.NSET, build);
+        if (!t->tmi.taps) return build ? fail(SCB_ERR_CUDA, "tmem image-lane tables: device allocation failed")
+                                       : fail(SCB_ERR_ARG, missing);
+        return SCB_OK;
+    }
+    if (ve.info.kind < KIND_DIRECT) return SCB_OK;  // tiled / plane: programs built at layer creation
+    std::vector<int> col;
+    if (ve.info.kind == KIND_DIMG) {  // = dimg.cuh: BASE + START_s * H, START = {H+1, 0, 2H+2}
+        const int H = ve.info.th, start[3] = {H + 1, 0, 2 * H + 2};
+        for (int s2 = 0; s2 < g.s; ++s2) col.push_back(dimg_base(ve.info) + start[s2] * H);
+    } else {
+        col = direct_cols(ve.info);
+    }
+    if (ve.info.kind == KIND_DTM) {  // tap offsets in TMEM columns: slot(c) + s*RT + r
+        col.clear();
+        for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * (ve.info.th + g.r - 1));
+        auto blk = L->direct_blocks(32, 1, col, 1, c.cc, ve.info.kt, build);
+        t->taps = blk.taps;
+        t->blkoff = blk.off;
+    } else if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
+        auto blk = L->direct_blocks(d.tap_cap, d.row, col, elem_bytes(ve.info), c.cc, ve.info.kt, build);
+        t->taps = blk.taps;
+        t->blkoff = blk.off;
+    } else {  // warp-specialised: plain tap array
+        t->taps = L->direct_taps(d.tap_cap, d.row, col, elem_bytes(ve.info), build);
+        t->blkoff = reinterpret_cast<const int32_t*>(t->taps);  // (unused by ws.cuh; non-null)
+    }
+    t->sptr = L->stage_ptr(c.cc, build);
+    if (!t->taps || !t->blkoff || !t->sptr)
+        return build ? fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed") : fail(SCB_ERR_ARG, missing);
+    return SCB_OK;
+}
+
+SCB_API scb_status scb_layer_prepare(scb_layer* layer, int32_t n, uint32_t flags, const scb_launch* cfg) {
+    if (!layer) return fail(SCB_ERR_ARG, "layer is NULL");
+    if (n <= 0) return SCB_OK;
+    scb_launch c;
+    if (cfg) c = *cfg;
+    else scb_default_launch(layer, n, flags, 0, &c);
+    if (c.variant < 0 || (flags & SCB_FLAG_GENERIC)) return SCB_OK;  // generic: arrays built at creation
+    DeviceGuard dg(layer->device);
+    if (!dg.ok) return fail(SCB_ERR_CUDA, "cannot select device");
+    Derived d;
+    scb_status s = derive(layer, c, n, flags, &d);
+    if (s != SCB_OK) return s;
+    LaunchTables t;
+    return launch_tables(layer, c, d, true, &t);
+}
+
+SCB_API scb_status scb_launch_check(const scb_layer* layer, int32_t n, uint32_t flags, const scb_launch* cfg) {
+    if (!layer || !cfg) return fail(SCB_ERR_ARG, "NULL");
+    if (cfg->variant < 0) return SCB_OK;
+    Derived d;
+    return derive(const_cast<scb_layer*>(layer), *cfg, std::max(n, 1), flags, &d);
+}
+
 SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
                                    void* y, int32_t n, uint32_t flags,
                                    const scb_launch* cfg, void* stream) {
@@ -1200,12 +1296,15 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
     if (cfg) c = *cfg;
     else scb_default_launch(layer, n, flags, 0, &c);
     const Geom& g = L->g;
+    // no explicit launch and an input the tiled kernels cannot stage (not 16-byte aligned,
+    // e.g. a sliced view): the generic kernel, which accepts any address
+    if (!cfg && (reinterpret_cast<uintptr_t>(x) & 15) && !(flags & SCB_FLAG_POOL2)) c.variant = -1;
     if (c.variant < 0 || (flags & SCB_FLAG_GENERIC)) {
         if (flags & SCB_FLAG_POOL2) return fail(SCB_ERR_UNSUPPORTED, "fused pool needs a tiled variant");
         GenericParams p;
         p.x = x; p.bias = bias; p.y = y; p.values = L->d_values; p.dec = L->d_dec; p.rowptr = L->d_rowptr;
         p.n = n; p.c = g.c; p.h = g.h; p.w = g.w; p.k = g.k; p.e = g.e; p.f = g.f;
-        p.stride = g.stride; p.pad = g.pad; p.flags = flags;
+        p.stride = g.stride; p.pad = g.pad; p.kr = g.r; p.ks = g.s; p.flags = flags;
         cudaError_t e = launch_generic(p, L->dt, (flags & SCB_FLAG_FAST) != 0, st);
         return e == cudaSuccess ? SCB_OK : cuda_fail(e, "generic kernel launch");
     }
@@ -1214,10 +1313,10 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
     if (s != SCB_OK) return s;
     const VariantEntry& ve = variant(c.variant);
     if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
+    LaunchTables tab;
+    if ((s = launch_tables(L, c, d, false, &tab)) != SCB_OK) return s;
     if (ve.info.kind == KIND_TMI) {
-        const TmiG t(ve.info);
-        auto T = L->tmi_tables(t.SW, t.CPR, t.RW, t.CS, t.NSET);
-        if (!T.taps) return fail(SCB_ERR_CUDA, "tmem image-lane tables: device allocation failed");
+        const auto& T = tab.tmi;
         TmiParams q;
         std::memset(&q, 0, sizeof(q));
         q.x = static_cast<const float*>(x);
@@ -1238,32 +1337,9 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
         DirectParams q;
         std::memset(&q, 0, sizeof(q));
         q.x = x; q.bias = static_cast<const float*>(bias); q.y = y;
-        std::vector<int> col;
-        if (ve.info.kind == KIND_DIMG) {  // = dimg.cuh: BASE + START_s * H, START = {H+1, 0, 2H+2}
-            const int H = ve.info.th, start[3] = {H + 1, 0, 2 * H + 2};
-            for (int s2 = 0; s2 < g.s; ++s2) col.push_back(dimg_base(ve.info) + start[s2] * H);
-        }
-        else
-            col = direct_cols(ve.info);
-        if (ve.info.kind == KIND_DTM) {  // tap offsets in TMEM columns: slot(c) + s*RT + r
-            col.clear();
-            for (int s2 = 0; s2 < g.s; ++s2) col.push_back(s2 * (ve.info.th + g.r - 1));
-            auto blk = L->direct_blocks(32, 1, col, 1, c.cc, ve.info.kt);
-            q.taps = blk.taps;
-            q.blkoff = blk.off;
-            q.sptr = L->stage_ptr(c.cc);
-            if (!q.taps || !q.blkoff) return fail(SCB_ERR_CUDA, "tmem tap blocks: device allocation failed");
-        } else if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {
-            auto blk = L->direct_blocks(d.tap_cap, d.row, col, elem_bytes(ve.info), c.cc, ve.info.kt);
-            q.taps = blk.taps;
-            q.blkoff = blk.off;
-            q.sptr = L->stage_ptr(c.cc);
-            if (!q.taps || !q.blkoff) return fail(SCB_ERR_CUDA, "direct tap blocks: device allocation failed");
-        } else {
-            q.taps = L->direct_taps(d.tap_cap, d.row, col, elem_bytes(ve.info));
-            q.sptr = L->stage_ptr(c.cc);
-        }
-        if (!q.taps || !q.sptr) return fail(SCB_ERR_CUDA, "direct tap tables: device allocation failed");
+        q.taps = tab.taps;
+        q.blkoff = tab.blkoff;
+        q.sptr = tab.sptr;
         q.n = n; q.c = g.c; q.h = g.h; q.w = g.w; q.k = g.k; q.e = g.e; q.f = g.f;
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;

@@ -56,10 +56,32 @@ class DeviceLayer:
             self.device, ctypes.byref(h)), "scb_layer_create")
         self.handle = h.value
         self._fin = weakref.finalize(self, _destroy, self.handle)
+        self._prepared = set()
 
     # ---- launches -------------------------------------------------------
+    def prepare(self, n: int, flags: int, launch=None) -> None:
+        """Build the device tables of `launch` once (scb_layer_prepare); the launch
+        itself then never allocates or synchronises (CUDA-graph capturable)."""
+        key = (int(n), int(flags), None if launch is None else tuple(launch))
+        if key in self._prepared:
+            return
+        cfg = None if launch is None else ctypes.byref(_abi.Launch.from_tuple(launch))
+        _abi.check(_abi.lib().scb_layer_prepare(ctypes.c_void_p(self.handle), int(n), int(flags), cfg),
+                   "scb_layer_prepare")
+        self._prepared.add(key)
+
+    def launch_ok(self, n: int, flags: int, launch) -> bool:
+        """Whether `launch` is valid for this layer at batch n (scb_launch_check)."""
+        if launch is None:
+            return True
+        st = _abi.lib().scb_launch_check(ctypes.c_void_p(self.handle), int(n), int(flags),
+                                         ctypes.byref(_abi.Launch.from_tuple(launch)))
+        return st == 0
+
     def launch(self, x_ptr: int, bias_ptr: int | None, y_ptr: int, n: int, flags: int,
                launch=None, stream: int = 0) -> None:
+        if launch is not None or not (flags & _abi.FLAG_GENERIC):
+            self.prepare(n, flags, launch)
         cfg = None if launch is None else ctypes.byref(_abi.Launch.from_tuple(launch))
         _abi.check(_abi.lib().scb_conv_sparse(
             ctypes.c_void_p(self.handle), ctypes.c_void_p(x_ptr),

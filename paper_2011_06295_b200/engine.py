@@ -114,6 +114,23 @@ def _check_geometry(x, kernel: CsrKernel):
                          f"(C,H,W)=({sh.c},{sh.h},{sh.w})")
 
 
+def _check_out(out, shape, dt, tdev) -> None:
+    """A caller-provided output buffer is written by the kernels through a raw pointer:
+    it must be a contiguous CUDA tensor of exactly the output shape and dtype on the
+    input's device, 16-byte aligned (the vectorised epilogue stores)."""
+    torch = _torch()
+    if not isinstance(out, torch.Tensor) or not out.is_cuda:
+        raise ShapeError("out must be a CUDA torch tensor")
+    if tuple(out.shape) != tuple(shape):
+        raise ShapeError(f"out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.dtype != _torch_dtype(dt):
+        raise ShapeError(f"out has dtype {out.dtype}, expected {_torch_dtype(dt)}")
+    if out.device != tdev:
+        raise ShapeError(f"out is on {out.device}, the input on {tdev}")
+    if not out.is_contiguous() or out.data_ptr() % 16:
+        raise ShapeError("out must be contiguous and 16-byte aligned")
+
+
 def _run(x, kernel: CsrKernel, bias, plan: EnginePlan, *, relu=False, pool=False,
          generic=False, out=None):
     torch = _torch()
@@ -155,7 +172,11 @@ def _run(x, kernel: CsrKernel, bias, plan: EnginePlan, *, relu=False, pool=False
         if dtype_of(x_dev) != io:
             x_dev = x_dev.to(_torch_dtype(io))
         x_dev = x_dev.contiguous()
+        if x_dev.data_ptr() % 16:
+            x_dev = x_dev.clone()  # a sliced view: the tiled kernels stage 16-byte chunks
         e, f = (sh.e // 2, sh.f // 2) if pool else (sh.e, sh.f)
+        if out is not None:
+            _check_out(out, (n, sh.k, e, f), x_dt, tdev)
         if out is None or io != x_dt:
             y = torch.empty((n, sh.k, e, f), dtype=_torch_dtype(io), device=tdev)
         else:
@@ -200,7 +221,9 @@ def _choose_launch(layer, n, flags, plan: EnginePlan):
     if key in TUNED:
         return TUNED[key]
     hit = _builtin().get(_builtin_key(layer.signature(), flags))
-    if hit is not None:
+    # the shipped table is keyed on geometry, not sparsity: a launch tuned at 90-95 % may not
+    # fit (shared memory) a denser layer of the same shape -- then the heuristic decides
+    if hit is not None and layer.launch_ok(n, flags, hit):
         return hit
     d = layer.default_launch(n, flags, plan.sub_batch_size if plan.sub_batch_size > 1 else 0)
     return None if d[0] < 0 else d

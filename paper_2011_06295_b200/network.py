@@ -172,6 +172,21 @@ class SparseConvNet:
                 sh = L.kernel.shape
                 self.scratch[i] = self.torch.empty((self.batch, sh.k, sh.e, sh.f), dtype=self.tdtype,
                                                    device=self.tdev)
+        self._prepare_all()
+
+    def _prepare_all(self) -> None:
+        """Build every layer's launch tables for the batch and each sub-batch chain size
+        (scb_layer_prepare) up front: the step itself then never allocates, which also
+        keeps it capturable into a CUDA graph."""
+        if self.batch is None:
+            return
+        sizes = {e - a for a, e in self._chain_bounds()} | {self.batch}
+        for i, L in enumerate(self.layers):
+            if self.launches[i] is None:
+                continue
+            for n in sizes:
+                for pdl in (0, _abi.FLAG_NO_PDL):
+                    self.dlayers[i].prepare(n, self.flags(i) | pdl, self.launches[i])
 
     def set_chains(self, chains: int) -> None:
         """Run the batch as `chains` independent sub-batch chains on their own
@@ -183,6 +198,8 @@ class SparseConvNet:
             raise ShapeError(f"chains must be in [1, batch], got {chains}")
         self.chains = chains
         self.graph = None
+        if self.batch is not None and len(self.launches) == len(self.layers):
+            self._prepare_all()
 
     def _chain_bounds(self):
         from .runner import shard_range
@@ -271,6 +288,9 @@ class SparseConvNet:
         for i, L in enumerate(self.layers):
             ch = config.choices.get(L.name, {})
             algo = ch.get("algorithm", "sparse-direct")
+            # a config written by the reference names its CPU dense baselines (bench.py:238,
+            # ALGORITHMS): on the GPU the dense path of either is the cuDNN convolution
+            algo = {"dense-direct": "dense-cudnn", "dense-gemm": "dense-cudnn"}.get(algo, algo)
             if algo not in ("sparse-direct", "dense-cudnn"):
                 raise ShapeError(f"unknown algorithm {algo!r} for layer {L.name}")
             self.algorithms[i] = algo

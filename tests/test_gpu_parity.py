@@ -694,3 +694,92 @@ def test_fused_act_quant_all_kinds_bitwise(sc, orc, c, hw, k, n, dt):
     layer.set_act_quant(None)
     with pytest.raises(Exception):
         layer.launch(xd.data_ptr(), bd.data_ptr(), xd.data_ptr(), n, _abi.FLAG_ACT_QUANT, None, st)
+
+
+# ---------------------------------------------------------------------------
+# API hygiene (VERDICT r1 "what's weak" 7-10)
+# ---------------------------------------------------------------------------
+
+def test_launch_requires_prepare_and_never_allocates(sc):
+    """scb_conv_sparse of a tiled launch whose tables were not built by
+    scb_layer_prepare fails (SCB_ERR_ARG) instead of allocating; after prepare it runs,
+    also inside a CUDA graph capture."""
+    import ctypes
+
+    import torch
+    from oracle import oracle as orc
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import DeviceLayer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=32, c=256, h=8, w=8, k=256, r=3, s=3, padding=1)
+    kern = sc.build_csr(make_layer_weights(LayerSpec("c3", sh, 0.9), 0), sh)
+    x, b = bench_inputs(sh, 32)
+    layer = DeviceLayer(kern, 0, np.float32)  # fresh handle: nothing prepared
+    cfg = layer.default_launch(32, 0)
+    assert cfg[0] >= 0 and layer.launch_ok(32, 0, cfg)
+    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    y = torch.empty((32, 256, 8, 8), device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    lib = _abi.lib()
+    args = (ctypes.c_void_p(layer.handle), ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(bd.data_ptr()),
+            ctypes.c_void_p(y.data_ptr()), 32, 0, ctypes.byref(_abi.Launch.from_tuple(cfg)), ctypes.c_void_p(st))
+    assert lib.scb_conv_sparse(*args) == _abi.SCB_ERR_ARG
+    assert "prepare" in _abi.last_error()
+    layer.prepare(32, 0, cfg)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        lib.scb_conv_sparse(*args[:7], ctypes.c_void_p(s.cuda_stream))  # warm-up outside capture
+        with torch.cuda.graph(g, stream=s):
+            assert lib.scb_conv_sparse(*args[:7], ctypes.c_void_p(s.cuda_stream)) == 0
+    torch.cuda.current_stream().wait_stream(s)
+    y.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    want = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 256, 3, 3, 1, 1, b)
+    assert beq(y.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("sparsity", [0.0, 0.5])
+def test_dense_vgg_shapes_fall_back_from_table(sc, sparsity):
+    """the shipped table is keyed on geometry; at low sparsity its launch can
+    overflow shared memory -- conv_sparse falls back to a valid launch, bitwise."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    for c, hw, k in ((512, 2, 512), (512, 4, 512), (256, 8, 256)):
+        sh = sc.ConvShape(n=16, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+        kern = sc.build_csr(make_layer_weights(LayerSpec("d", sh, sparsity), 0), sh)
+        x, b = bench_inputs(sh, 16)
+        got = sc.conv_sparse(torch.from_numpy(x).cuda(), kern, b, relu=True).cpu().numpy()
+        want = np.maximum(orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b), 0)
+        assert beq(got, want), (c, hw, sparsity)
+
+
+def test_out_buffer_validated_and_misaligned_input(sc):
+    """a caller `out` of the wrong shape / dtype / layout raises ShapeError
+    (no out-of-bounds device writes); a misaligned input view still computes."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, make_layer_weights
+    sh = sc.ConvShape(n=9, c=64, h=16, w=16, k=32, r=3, s=3, padding=1)
+    kern = sc.build_csr(make_layer_weights(LayerSpec("o", sh, 0.9), 0), sh)
+    x, b = bench_inputs(sh, 9)
+    xd = torch.from_numpy(x).cuda()
+    for bad in (torch.empty((9, 32, 16, 15), device="cuda"), torch.empty((9, 32, 16, 16), device="cuda",
+                dtype=torch.float16), torch.empty((9, 32, 16, 32), device="cuda")[..., ::2],
+                torch.empty((9, 32, 16, 16)), np.empty((9, 32, 16, 16), np.float32)):
+        with pytest.raises(sc.ShapeError):
+            sc.conv_sparse(xd, kern, b, out=bad)
+    good = torch.empty((9, 32, 16, 16), device="cuda")
+    sc.conv_sparse(xd, kern, b, out=good)
+    want = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 32, 3, 3, 1, 1, b)
+    assert beq(good.cpu().numpy(), want)
+    # images 1..8 as a view whose base is 64*16*16*4 bytes (+ an odd offset) into the buffer
+    big = torch.empty(9 * 64 * 256 + 1, device="cuda")
+    view = big[1:].view(9, 64, 16, 16)
+    view.copy_(xd)
+    assert view.data_ptr() % 16
+    got = sc.conv_sparse(view[1:], kern, b).cpu().numpy()
+    assert beq(got, want[1:])
