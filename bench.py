@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=256,
                     help="GLOBAL batch (BASELINE config 3: 256), split into contiguous per-GPU shards")
     ap.add_argument("--no-proxy", action="store_true", help="skip the batch-32 (8-GPU shard) proxy line")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 sparsity sweep summary")
     ap.add_argument("--sparsity", type=float, default=0.9)
     ap.add_argument("--no-tune", action="store_true", help="C heuristic launches instead of the tuner")
     ap.add_argument("--launches", default="", help="JSON of per-layer launches: loaded if present "
@@ -406,11 +407,42 @@ def dense_cudnn(specs, kernels, biases, batch: int, dev, reps: int = 10):
                     a = torch.nn.functional.max_pool2d(a, 2)
             return a
 
+        # per layer (the paper's comparison, sc/bench.py:199-206): the same conv + bias + ReLU
+        # (+ 2x2 max-pool) in cuDNN IEEE fp32, TF32 and fp16 tensor cores (channels_last)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         per_layer = []
+        for (spec, pool), w, b in zip(specs, ws, bs):
+            sh = spec.shape
+            e = 32 if sh.h == 32 else sh.h
+            xi = torch.randn((batch, sh.c, sh.h, sh.w), device=dev)
+            rec = {"layer": spec.name}
+            for tag, dt, tf32, cl in (("cudnn_fp32_us", torch.float32, False, False),
+                                      ("cudnn_tf32_us", torch.float32, True, False),
+                                      ("cudnn_fp16_us", torch.float16, False, True)):
+                xx, ww, bb = xi.to(dt), w.to(dt), b.to(dt)
+                if cl:
+                    xx, ww = xx.to(memory_format=torch.channels_last), ww.to(memory_format=torch.channels_last)
+
+                def lay():
+                    a = torch.relu(torch.nn.functional.conv2d(xx, ww, bb, padding=sh.padding))
+                    return torch.nn.functional.max_pool2d(a, 2) if pool else a
+                torch.backends.cudnn.allow_tf32 = tf32
+                for _ in range(3):
+                    lay()
+                torch.cuda.synchronize()
+                tl = []
+                for _ in range(reps):
+                    evs[0].record()
+                    lay()
+                    evs[1].record()
+                    evs[1].synchronize()
+                    tl.append(evs[0].elapsed_time(evs[1]))
+                rec[tag] = round(statistics.median(tl) * 1e3, 2)
+            torch.backends.cudnn.allow_tf32 = False
+            per_layer.append(rec)
         for _ in range(3):
             step()
         torch.cuda.synchronize()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ts = []
         for _ in range(reps):
             evs[0].record()
@@ -567,6 +599,30 @@ def measure_shard_proxy(args, specs, local_rank, dev, rate_full: float, reps: in
             "implied_8gpu_images_per_s": round(8 * rate, 1),
             "note": "back-to-back steps without L2 flush (the shard's working set is L2-resident on a real "
                     "8-GPU run too); launches tuned at this batch"}
+
+
+def measure_sweep(args, local_rank):
+    """BASELINE config 5 summary: 256->256 3x3 @32x32, batch 512, sparse (heuristic /
+    shipped launches, untuned) vs cuDNN IEEE fp32 / fp16 tensor cores, every point checked
+    bit for bit against the oracle on its first 8 images (benchmark.sparsity_sweep, the
+    reference's sparsity_sweep semantics).  The tuned full sweep: tools/sweep.py."""
+    import paper_2011_06295_b200 as sc
+    from oracle import oracle as orc
+    from paper_2011_06295_b200.synth import LayerSpec
+
+    def oracle_ref(x, kern, b):
+        sh = kern.shape
+        return orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, sh.k, sh.r, sh.s, sh.stride,
+                               sh.padding, b)
+    spec = LayerSpec("sweep-256x32", sc.ConvShape(n=1, c=256, h=32, w=32, k=256, r=3, s=3, padding=1), 0.9)
+    out = {"layer": "256->256 3x3 @32x32", "batch": 512, "launches": "heuristic/shipped (untuned)",
+           "check": "bitwise vs oracle, first 8 images of each point"}
+    for dt in ("f32", "f16"):
+        r = sc.sparsity_sweep(spec, [0.5, 0.7, 0.8, 0.9, 0.95, 0.97, 0.99], batch=512, repetitions=5, warmups=2,
+                              dtype=dt, device=local_rank, reference_fn=oracle_ref, check_images=8)
+        out[dt] = {"sparsities": r.sparsities, "sparse_ms": [round(v, 4) for v in r.sparse_ms],
+                   "dense_cudnn_ms": round(r.dense_ms, 4), "crossover": r.crossover}
+    return out
 
 
 def load_traffic():
@@ -801,6 +857,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.no_dense and world == 1:
         line["dense_cudnn"] = dense_cudnn(specs, [L.kernel for L in net.layers], [L.bias for L in net.layers],
                                           args.batch, dev)
+        sp_us = {l["layer"]: l["us"] for l in layers}
+        for rec in line["dense_cudnn"]["per_layer"]:
+            rec["sparse_us"] = sp_us.get(rec["layer"])
+            rec["speedup_vs_cudnn_fp32"] = round(rec["cudnn_fp32_us"] / rec["sparse_us"], 3)
+        line["dense_cudnn"]["layers_slower_than_cudnn_fp32"] = [
+            r["layer"] for r in line["dense_cudnn"]["per_layer"] if r["sparse_us"] >= r["cudnn_fp32_us"]]
+    if not args.no_sweep and world == 1:
+        line["sweep"] = measure_sweep(args, local_rank)
     if not args.no_cpu and world == 1:
         per_pass, passes, threads = cpu_stack_time(specs, [L.kernel for L in net.layers],
                                                    [L.bias for L in net.layers], args.cpu_images,

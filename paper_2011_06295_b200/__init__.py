@@ -10,6 +10,7 @@ there is no CPU fallback.
 from .engine import (SUB_BATCH_CANDIDATES, EnginePlan, conv_sparse, conv_sparse_1d,
                      conv_sparse_reference, dense_mac_count, sparse_mac_count,
                      tune_sub_batch)
+from .benchmark import BenchRecord, SweepResult, bench_layer, emit_report, sparsity_sweep
 from .configure import NetworkConfig, configure_network
 from .errors import FormatError, IntegrityError, ShapeError, SparseConvError, TrainingError
 from .geometry import ConvShape, check_nchw, compute_dtype, output_shape, pad_input
@@ -19,6 +20,7 @@ from .weights import (CsrKernel, SparsityReport, analyze_sparsity, build_csr, de
 __version__ = "0.1.0"
 
 __all__ = [
+    "BenchRecord", "SweepResult", "bench_layer", "emit_report", "sparsity_sweep",
     "ConvShape", "CsrKernel", "EnginePlan", "NetworkConfig", "configure_network", "FormatError", "IntegrityError", "ShapeError",
     "SparseConvError", "SparsityReport", "SUB_BATCH_CANDIDATES", "TrainingError",
     "analyze_sparsity", "build_csr", "check_nchw", "compute_dtype", "conv_sparse",

@@ -1,0 +1,290 @@
+"""Layer benchmarks on the GPU: the reference's bench_layer / sparsity_sweep /
+emit_report (sc/bench.py:153-215, 235-274, 349-397) with the B200 engine as
+"sparse-direct" and cuDNN (through torch) as the dense baselines.
+
+Semantics kept from the reference:
+* inputs from ``default_rng(seed + 1)`` (x first, then bias), weights from
+  ``make_layer_weights`` unless given (bench.py:175-177);
+* f16 profile = x, w, bias cast to f16 (bench.py:186-188);
+* every timed algorithm is first checked against a reference output and a
+  wrong answer raises ``IntegrityError`` instead of reporting a fast-but-wrong
+  time (bench.py:139-147, 209).  By default the reference output is the dense
+  IEEE cuDNN convolution (as the reference checks against its dense-direct),
+  with the reference's tolerance ``tol*(|ref|+1)``, 1e-4 for fp32 and 1e-2 for
+  f16.  Given ``reference_fn(x, kernel, bias)`` (bench.py and tests pass the
+  CPU oracle -- the reference's conv_sparse_kernel restated), the sparse engine
+  must match it BIT FOR BIT and the dense baselines within the tolerance (TF32
+  is reported but checked at 1e-2: it is not an fp32 result);
+* timing: ``warmups`` untimed calls, then ``repetitions`` timed ones -- here
+  with CUDA events on the launching stream -- median, IQR and mean in ms;
+* sweep crossover: the same linear interpolation as bench.py:263-273.
+
+Dense algorithm names: "dense-cudnn" (IEEE fp32, TF32 off / f16 tensor cores,
+channels_last), "dense-cudnn-tf32" (f32 only).  The reference's CPU names
+"dense-direct" / "dense-gemm" are accepted as aliases of "dense-cudnn".
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import asdict, dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .engine import EnginePlan, conv_sparse, dense_mac_count, sparse_mac_count
+from .errors import IntegrityError, ShapeError
+from .synth import LayerSpec, make_layer_weights
+from .weights import build_csr, decompress
+
+ALGORITHMS = ("sparse-direct", "dense-cudnn", "dense-cudnn-tf32")
+_ALIASES = {"dense-direct": "dense-cudnn", "dense-gemm": "dense-cudnn"}
+REPORT_COLUMNS = ("layer", "sparsity", "subBatchSize", "sparse-f32", "dense-f32", "sparse-f16", "dense-f16")
+
+
+@dataclass
+class BenchRecord:
+    layer: str
+    algorithm: str              # sparse-direct | dense-cudnn | dense-cudnn-tf32
+    dtype: str                  # f32 | f16
+    sub_batch_size: int | None  # images per CTA of the sparse launch (the paper's subBatchSize)
+    median_ms: float
+    iqr_ms: float
+    mean_ms: float
+    repetitions: int
+    mac_count: int
+    sparsity: float
+    launch: tuple | None = None  # the full sparse launch (variant, warps, imgs, bh, bw, cc, stages)
+
+
+@dataclass
+class SweepResult:
+    layer: str
+    sparsities: list
+    sparse_ms: list
+    dense_ms: float             # best dense baseline (IEEE), constant in sparsity
+    crossover: float | None     # None means "never"
+    dtype: str = "f32"
+
+    @property
+    def crossover_label(self) -> str:
+        return "never" if self.crossover is None else f"{self.crossover:.3f}"
+
+
+def _time_ms(fn, repetitions: int, warmups: int):
+    import torch
+    for _ in range(warmups):
+        fn()
+    torch.cuda.synchronize()
+    samples = []
+    for _ in range(repetitions):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        samples.append(a.elapsed_time(b))
+    q1, med, q3 = np.percentile(samples, [25, 50, 75])
+    return float(med), float(q3 - q1), float(np.mean(samples))
+
+
+def _check(out: np.ndarray, ref: np.ndarray, tol: float, bitwise: bool, what: str) -> None:
+    if bitwise:
+        iv = np.uint16 if ref.dtype == np.float16 else np.uint32
+        bad = np.count_nonzero(np.ascontiguousarray(out).view(iv) != np.ascontiguousarray(ref).view(iv))
+        if bad:
+            raise IntegrityError(f"{what}: {bad} of {ref.size} outputs differ from the oracle")
+        return
+    ref64 = ref.astype(np.float64)
+    err = np.abs(out.astype(np.float64) - ref64)
+    bound = tol * (np.abs(ref64) + 1.0)
+    if np.any(err > bound):
+        raise IntegrityError(f"{what}: output disagrees with the oracle (max rel err "
+                             f"{float((err / bound).max()) * tol:.3g})")
+
+
+def bench_layer(spec: LayerSpec, batch: int = 32, profiles=("f32", "f16"), repetitions: int = 5,
+                warmups: int = 2, seed: int = 0, weights: np.ndarray | None = None,
+                algorithms=ALGORITHMS, tune: bool = True, device: int = 0, check: bool = True,
+                check_images: int | None = None, reference_fn=None) -> list[BenchRecord]:
+    """Time the sparse engine (tuned launch unless ``tune=False``) and the cuDNN
+    baselines on one layer; one record per (algorithm, dtype).  ``check_images``
+    limits the check to the first images (large sweeps)."""
+    import torch
+    algorithms = tuple(_ALIASES.get(a, a) for a in algorithms)
+    unknown = set(algorithms) - set(ALGORITHMS)
+    if unknown:
+        raise ShapeError(f"unknown algorithms {sorted(unknown)}")
+    sh = spec.shape.with_batch(batch)
+    if weights is None:
+        weights = make_layer_weights(spec, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    x32 = rng.standard_normal((batch, sh.c, sh.h, sh.w)).astype(np.float32)
+    bias32 = rng.standard_normal(sh.k).astype(np.float32)
+    dev = torch.device("cuda", device)
+    records = []
+    nchk = batch if check_images is None else min(batch, check_images)
+    for dtype in profiles:
+        if dtype == "f32":
+            x, w, b = x32, weights.astype(np.float32), bias32
+        elif dtype == "f16":
+            x, w, b = x32.astype(np.float16), weights.astype(np.float16), bias32.astype(np.float16)
+        else:
+            raise ShapeError(f"unknown dtype profile {dtype!r}")
+        kernel = build_csr(w, sh)
+        xd = torch.from_numpy(x).to(dev)
+        bitwise = reference_fn is not None
+        ref = None
+        if check:
+            if bitwise:
+                ref = np.asarray(reference_fn(x[:nchk], kernel, b))
+            else:  # dense IEEE cuDNN as the checker (sc/bench.py:180 uses dense-direct)
+                fn_ref, _ = _dense_fn(xd[:nchk], torch.from_numpy(decompress(kernel)).to(dev),
+                                      torch.from_numpy(np.asarray(b)).to(dev), sh, dtype, "dense-cudnn")
+                ref = fn_ref().cpu().numpy()
+        launch = None
+        if "sparse-direct" in algorithms:
+            # the launch path itself (device-resident bias, no host round trip per call): what
+            # SparseConvNet runs; conv_sparse() adds its numpy/torch conversions on top
+            from .device import device_layer
+            from .engine import _choose_launch, _flags, _io_dtype, run_layer
+            plan = EnginePlan(device=device)
+            dl = device_layer(kernel, device, _io_dtype(x.dtype, kernel))
+            if tune:
+                from .tuner import tune_launch
+                launch, _ = tune_launch(xd, kernel, b, plan, repetitions=3, warmups=1)
+            else:
+                launch = _choose_launch(dl, batch, _flags(plan, False, False, False), plan)
+            out = torch.empty((batch, sh.k, sh.e, sh.f), dtype=xd.dtype, device=dev)
+            bdev = torch.from_numpy(np.asarray(b, dtype=np.float32)).to(dev)  # compute dtype (f32)
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            flags = 0 if launch is not None else 0x8  # None = the generic kernel
+            fn = lambda: run_layer(dl, xd.data_ptr(), bdev.data_ptr(), out, batch, flags, launch,  # noqa: E731
+                                   stream)
+            fn()
+            torch.cuda.synchronize()
+            if check:
+                _check(out[:nchk].cpu().numpy(), ref, 1e-4 if dtype == "f32" else 1e-2, bitwise,
+                       f"{spec.name}/sparse-direct/{dtype}")
+            med, iqr, mean = _time_ms(fn, repetitions, warmups)
+            records.append(BenchRecord(spec.name, "sparse-direct", dtype,
+                                       None if launch is None else int(launch[2]), med, iqr, mean, repetitions,
+                                       sparse_mac_count(kernel, batch), spec.sparsity,
+                                       None if launch is None else tuple(launch)))
+        dense_algos = [a for a in algorithms if a != "sparse-direct" and (a != "dense-cudnn-tf32" or dtype == "f32")]
+        if dense_algos:
+            wd = torch.from_numpy(decompress(kernel)).to(dev)
+            bd = torch.from_numpy(np.asarray(b)).to(dev)
+            for algo in dense_algos:
+                fn, tol = _dense_fn(xd, wd, bd, sh, dtype, algo)
+                if check:
+                    _check(fn()[:nchk].float().cpu().numpy().astype(ref.dtype), ref, tol, False,
+                           f"{spec.name}/{algo}/{dtype}")
+                med, iqr, mean = _time_ms(fn, repetitions, warmups)
+                records.append(BenchRecord(spec.name, algo, dtype, None, med, iqr, mean, repetitions,
+                                           dense_mac_count(sh, batch), spec.sparsity))
+    return records
+
+
+def _dense_fn(xd, wd, bd, sh, dtype: str, algo: str):
+    """cuDNN convolution closure with its precision settings pinned per call."""
+    import torch
+    torch.backends.cudnn.benchmark = True
+    if dtype == "f16":  # tensor cores, channels_last
+        xc, wc = xd.to(memory_format=torch.channels_last), wd.to(memory_format=torch.channels_last)
+
+        def fn():
+            return torch.nn.functional.conv2d(xc, wc, bd, stride=sh.stride, padding=sh.padding)
+        return fn, 1e-2
+    tf32 = algo == "dense-cudnn-tf32"
+
+    def fn():
+        old = torch.backends.cudnn.allow_tf32
+        torch.backends.cudnn.allow_tf32 = tf32
+        try:
+            return torch.nn.functional.conv2d(xd, wd, bd, stride=sh.stride, padding=sh.padding)
+        finally:
+            torch.backends.cudnn.allow_tf32 = old
+    return fn, (1e-2 if tf32 else 1e-4)
+
+
+def sparsity_sweep(spec: LayerSpec, sparsities, batch: int = 32, repetitions: int = 5, warmups: int = 2,
+                   seed: int = 0, dense_algorithms=("dense-cudnn",), tune: bool = False, dtype: str = "f32",
+                   device: int = 0, check: bool = True, check_images: int | None = 8,
+                   reference_fn=None) -> SweepResult:
+    """Time sparse-direct across sparsity levels (each point oracle-checked) and
+    interpolate the sparsity where it matches the best dense baseline ("never" if it
+    stays slower); the dense baseline is timed once (sc/bench.py:235-274)."""
+    sparsities = sorted(sparsities)
+    if len(sparsities) < 3:
+        raise ShapeError("sparsity sweep needs at least 3 points")
+    dense_algorithms = tuple(_ALIASES.get(a, a) for a in dense_algorithms)
+    sparse_ms, dense_ms = [], math.inf
+    for i, s in enumerate(sparsities):
+        algos = ("sparse-direct",) + (dense_algorithms if i == 0 else ())
+        recs = bench_layer(LayerSpec(spec.name, spec.shape, s, spec.source), batch=batch, profiles=(dtype,),
+                           repetitions=repetitions, warmups=warmups, seed=seed, algorithms=algos, tune=tune,
+                           device=device, check=check, check_images=check_images, reference_fn=reference_fn)
+        by_algo = {r.algorithm: r.median_ms for r in recs}
+        sparse_ms.append(by_algo["sparse-direct"])
+        dense_ms = min([dense_ms] + [by_algo[a] for a in dense_algorithms if a in by_algo])
+    return SweepResult(spec.name, list(sparsities), sparse_ms, dense_ms,
+                       crossover(sparsities, sparse_ms, dense_ms), dtype)
+
+
+def crossover(sparsities, sparse_ms, dense_ms):
+    """Sparsity where the sparse time first drops to the dense time, linearly
+    interpolated between the bracketing points; None = never (bench.py:263-273)."""
+    if sparse_ms[0] <= dense_ms:
+        return sparsities[0]
+    for i in range(1, len(sparsities)):
+        if sparse_ms[i] <= dense_ms:
+            s0, s1 = sparsities[i - 1], sparsities[i]
+            t0, t1 = sparse_ms[i - 1], sparse_ms[i]
+            frac = (t0 - dense_ms) / (t0 - t1) if t0 != t1 else 1.0
+            return s0 + frac * (s1 - s0)
+    return None
+
+
+def _pivot(records) -> list[dict]:
+    """One row per (layer, sparsity); dense columns take the faster IEEE dense
+    baseline (TF32 is not an fp32 result and stays out of the pivot)."""
+    rows: dict = {}
+    for r in records:
+        key = (r.layer, r.sparsity)
+        row = rows.setdefault(key, {c: "" for c in REPORT_COLUMNS})
+        row["layer"], row["sparsity"] = r.layer, float(f"{r.sparsity * 100:g}")
+        if r.algorithm == "sparse-direct":
+            row[f"sparse-{r.dtype}"] = round(r.median_ms, 4)
+            if r.dtype == "f32":
+                row["subBatchSize"] = r.sub_batch_size
+        elif r.algorithm == "dense-cudnn":
+            col = f"dense-{r.dtype}"
+            prev, val = row[col], round(r.median_ms, 4)
+            row[col] = val if prev == "" else min(prev, val)
+    return [rows[k] for k in sorted(rows, key=lambda k: (str(k[0]), k[1]))]
+
+
+def emit_report(records, fmt: str, path) -> None:
+    """Write the pivoted report as csv, json, or a markdown table (sc/bench.py:373-397)."""
+    rows = _pivot(records)
+    path = Path(path)
+    if fmt == "csv":
+        import csv
+        with open(path, "w", newline="") as fh:
+            writer = csv.DictWriter(fh, fieldnames=REPORT_COLUMNS)
+            writer.writeheader()
+            writer.writerows(rows)
+    elif fmt == "json":
+        path.write_text(json.dumps(rows, indent=2))
+    elif fmt == "markdown":
+        lines = ["| " + " | ".join(REPORT_COLUMNS) + " |", "|" + "---|" * len(REPORT_COLUMNS)]
+        for row in rows:
+            lines.append("| " + " | ".join(str(row[c]) for c in REPORT_COLUMNS) + " |")
+        path.write_text("\n".join(lines) + "\n")
+    else:
+        raise ShapeError(f"unknown report format {fmt!r}")
+
+
+def records_to_json(records) -> str:
+    return json.dumps([asdict(r) for r in records], indent=2)
