@@ -391,10 +391,9 @@ def dense_cudnn(specs, kernels, biases, batch: int, dev, reps: int = 10):
     """Dense torch/cuDNN fp32 (IEEE) conv + bias + ReLU (+ max-pool) stack time."""
     import torch
     import paper_2011_06295_b200 as sc
+    from paper_2011_06295_b200.cudnn_mode import cudnn_fp32
     torch.backends.cudnn.benchmark = True
-    old = torch.backends.cudnn.allow_tf32
-    torch.backends.cudnn.allow_tf32 = False
-    try:
+    with cudnn_fp32("ieee"):
         ws = [torch.from_numpy(sc.decompress(k)).to(dev) for k in kernels]
         bs = [torch.from_numpy(b).to(dev) for b in biases]
         x = torch.randn((batch, 3, 32, 32), device=dev)
@@ -426,19 +425,18 @@ def dense_cudnn(specs, kernels, biases, batch: int, dev, reps: int = 10):
                 def lay():
                     a = torch.relu(torch.nn.functional.conv2d(xx, ww, bb, padding=sh.padding))
                     return torch.nn.functional.max_pool2d(a, 2) if pool else a
-                torch.backends.cudnn.allow_tf32 = tf32
-                for _ in range(3):
-                    lay()
-                torch.cuda.synchronize()
-                tl = []
-                for _ in range(reps):
-                    evs[0].record()
-                    lay()
-                    evs[1].record()
-                    evs[1].synchronize()
-                    tl.append(evs[0].elapsed_time(evs[1]))
+                with cudnn_fp32("tf32" if tf32 else "ieee"):
+                    for _ in range(3):
+                        lay()
+                    torch.cuda.synchronize()
+                    tl = []
+                    for _ in range(reps):
+                        evs[0].record()
+                        lay()
+                        evs[1].record()
+                        evs[1].synchronize()
+                        tl.append(evs[0].elapsed_time(evs[1]))
                 rec[tag] = round(statistics.median(tl) * 1e3, 2)
-            torch.backends.cudnn.allow_tf32 = False
             per_layer.append(rec)
         for _ in range(3):
             step()
@@ -452,9 +450,8 @@ def dense_cudnn(specs, kernels, biases, batch: int, dev, reps: int = 10):
             ts.append(evs[0].elapsed_time(evs[1]))
         return {"ms_per_step": round(statistics.median(ts), 4),
                 "images_per_s": round(batch / (statistics.median(ts) * 1e-3), 1),
-                "precision": "fp32 ieee (cudnn.allow_tf32=False), cudnn.benchmark", "per_layer": per_layer}
-    finally:
-        torch.backends.cudnn.allow_tf32 = old
+                "precision": "fp32 ieee (torch.backends.cudnn.conv.fp32_precision='ieee'), cudnn.benchmark",
+                "per_layer": per_layer}
 
 
 def measure_f16(specs, args, dev, local_rank, reps: int = 10):

@@ -198,13 +198,11 @@ def _dense_fn(xd, wd, bd, sh, dtype: str, algo: str):
         return fn, 1e-2
     tf32 = algo == "dense-cudnn-tf32"
 
+    from .cudnn_mode import cudnn_fp32
+
     def fn():
-        old = torch.backends.cudnn.allow_tf32
-        torch.backends.cudnn.allow_tf32 = tf32
-        try:
+        with cudnn_fp32("tf32" if tf32 else "ieee"):
             return torch.nn.functional.conv2d(xd, wd, bd, stride=sh.stride, padding=sh.padding)
-        finally:
-            torch.backends.cudnn.allow_tf32 = old
     return fn, (1e-2 if tf32 else 1e-4)
 
 

@@ -262,12 +262,9 @@ class SparseConvNet:
                 np.asarray(L.bias, dtype=self.dtype)).to(self.tdev)
 
             def run(x, out=None):
-                old = torch.backends.cudnn.allow_tf32
-                torch.backends.cudnn.allow_tf32 = False
-                try:
+                from .cudnn_mode import cudnn_fp32
+                with cudnn_fp32("ieee"):
                     a = torch.nn.functional.conv2d(x, w, b, stride=sh.stride, padding=sh.padding)
-                finally:
-                    torch.backends.cudnn.allow_tf32 = old
                 if L.relu:
                     a = torch.relu(a)
                 if L.pool:

@@ -43,7 +43,7 @@ def main():
     ap.add_argument("--per-kind", type=int, default=24)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
-    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cudnn.conv.fp32_precision = "ieee"  # (allow_tf32=False alone leaves "none" = TF32)
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.benchmark = True
     vs = _abi.variants()

@@ -129,12 +129,11 @@ def main():
         print(json.dumps(row), flush=True)
     # dense comparators (timed once: they do not depend on sparsity)
     wd = torch.randn((256, 256, 3, 3), generator=g).to(dev)
-    old = torch.backends.cudnn.allow_tf32
-    torch.backends.cudnn.allow_tf32 = False
-    d32 = ev_time(lambda: torch.nn.functional.conv2d(x32, wd, bias, padding=1))
-    torch.backends.cudnn.allow_tf32 = True
-    dtf = ev_time(lambda: torch.nn.functional.conv2d(x32, wd, bias, padding=1))
-    torch.backends.cudnn.allow_tf32 = old
+    from paper_2011_06295_b200.cudnn_mode import cudnn_fp32
+    with cudnn_fp32("ieee"):
+        d32 = ev_time(lambda: torch.nn.functional.conv2d(x32, wd, bias, padding=1))
+    with cudnn_fp32("tf32"):
+        dtf = ev_time(lambda: torch.nn.functional.conv2d(x32, wd, bias, padding=1))
     xcl = x16.to(memory_format=torch.channels_last)
     wcl = wd.half().to(memory_format=torch.channels_last)
     d16 = ev_time(lambda: torch.nn.functional.conv2d(xcl, wcl, bias.half(), padding=1))
