@@ -504,12 +504,13 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
         ev[1].synchronize()
         td.append(ev[0].elapsed_time(ev[1]))
     # the config-4 weight formats with the REFERENCE's quantizers (quantize_weights_array
-    # codebook:16 -> 4-bit codes + f16 table, fixed:16 -> int16 codes x 2^-frac; restated
+    # codebook:16 -> 4-bit codes + f16 table, fixed:16 -> int16 codes x 2^-frac, affine:16 ->
+    # int16 codes x f64 step), decoded in registers from 4-byte taps; restated
     # bit-exactly by synth.reference_quantize, pinned by tests/golden/quant_vgg.json)
     from paper_2011_06295_b200.synth import reference_quantized_values_fn
     fixture = ROOT / "tests" / "golden" / "quant_vgg.json"
     fmts = {}
-    for fmt, kind in (("cb4", "codebook"), ("lin16", "fixed")):
+    for fmt, kind in (("cb4", "codebook"), ("lin16", "fixed"), ("aff16", "affine")):
         qn = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_format=fmt,
                        weight_fn=f16_scaled, values_fn=reference_quantized_values_fn(kind, fixture))
         qn.plan(args.batch, tune=not args.no_tune)

@@ -52,7 +52,7 @@ typedef enum { SCB_F32 = 0, SCB_F64 = 1, SCB_F16 = 2 } scb_dtype;
  *  CB4    : 4-bit codebook index + a 16-entry table (the paper's "4b/16b",
  *           quantize.py:194-246; table = the layer's distinct values)
  *  LIN16  : int16 fixed-point code * 2^-frac (quantize.py:28-71)          */
-typedef enum { SCB_W_NATIVE = 0, SCB_W_CB4 = 1, SCB_W_LIN16 = 2 } scb_wfmt;
+typedef enum { SCB_W_NATIVE = 0, SCB_W_CB4 = 1, SCB_W_LIN16 = 2, SCB_W_AFF16 = 3 } scb_wfmt;
 
 /* Geometry of one layer: ConvShape (shapes.py:17-77).  n is ignored by the
  * layer object (the batch comes from each call, engine.py:52-54). */
@@ -152,6 +152,15 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
                                     const void* values, const int32_t* colidx,
                                     const int32_t* rowptr, int64_t nnz, int32_t unified,
                                     int32_t device, scb_layer** out);
+/* scb_layer_create with a quantizer parameter: for wfmt = AFF16 (symmetric affine
+ * int16, quantize.py:99-138) `qstep` is the layer's step and every value must equal
+ * the storage-dtype rounding of float64(code) * qstep for an int16 code -- the
+ * reference's quantize_weights_array(.., "affine", 16) output (quantize.py:279-283);
+ * the f16 kernels decode codes in registers.  qstep is ignored by other formats. */
+SCB_API scb_status scb_layer_create_q(const scb_shape* shape, scb_dtype dt, scb_wfmt wfmt,
+                                      const void* values, const int32_t* colidx,
+                                      const int32_t* rowptr, int64_t nnz, int32_t unified,
+                                      int32_t device, double qstep, scb_layer** out);
 SCB_API scb_status scb_layer_destroy(scb_layer* layer);
 /* device bytes of the tap program used by `variant` (-1 = generic arrays). */
 SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t variant,

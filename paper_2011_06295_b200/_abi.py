@@ -22,7 +22,7 @@ SCB_OK, SCB_ERR_SHAPE, SCB_ERR_FORMAT, SCB_ERR_INTEGRITY = 0, 1, 2, 3
 SCB_ERR_CUDA, SCB_ERR_ARG, SCB_ERR_UNSUPPORTED = 4, 5, 6
 
 SCB_F32, SCB_F64, SCB_F16 = 0, 1, 2
-SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16 = 0, 1, 2
+SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16, SCB_W_AFF16 = 0, 1, 2, 3
 
 FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC, FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8, 0x10
 FLAG_ACT_QUANT = 0x20
@@ -30,7 +30,7 @@ FLAG_ACT_QUANT = 0x20
 # every symbol include/sparseconv_b200.h declares
 EXPORTS = (
     "scb_channel_nnz", "scb_select_padding_zeros", "scb_csr_count", "scb_build_csr",
-    "scb_validate_csr", "scb_decompress", "scb_layer_create", "scb_layer_destroy",
+    "scb_validate_csr", "scb_decompress", "scb_layer_create", "scb_layer_create_q", "scb_layer_destroy",
     "scb_layer_weight_bytes", "scb_conv_sparse", "scb_launch_candidates",
     "scb_default_launch", "scb_layer_prepare", "scb_launch_check", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
     "scb_fma_peaks", "scb_fnv1a64", "scb_last_error", "scb_version", "scb_fake_quant",
@@ -105,6 +105,7 @@ def lib():
             "scb_validate_csr": [P(Shape), vp, vp, i64, i32, i32],
             "scb_decompress": [P(Shape), i32, vp, vp, vp, i64, vp],
             "scb_layer_create": [P(Shape), i32, i32, vp, vp, vp, i64, i32, i32, P(vp)],
+            "scb_layer_create_q": [P(Shape), i32, i32, vp, vp, vp, i64, i32, i32, ctypes.c_double, P(vp)],
             "scb_layer_destroy": [vp],
             "scb_layer_weight_bytes": [vp, i32, P(i64)],
             "scb_conv_sparse": [vp, vp, vp, vp, i32, u32, P(Launch), vp],

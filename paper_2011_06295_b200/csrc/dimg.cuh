@@ -50,8 +50,9 @@ __device__ __forceinline__ unsigned short dimg_half(const typename DimgT<H, true
     return (unsigned short)((x & 1) ? (w >> 16) : (w & 0xffffu));
 }
 
-template <int H, int KW, int MODE, bool F16 = false>
+template <int H, int KW, int MODE, bool F16 = false, int WF = (F16 ? WF_F16 : WF_F32)>
 __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectParams p) {
+    static_assert(F16 == (WF != WF_F32), "f16 storage <=> compact f16 taps (kernels.cuh tap_f16)");
     using E = typename DimgT<H, F16>::E;
     using V = typename DimgT<H, F16>::V;
     constexpr int ES = (int)sizeof(E);
@@ -167,6 +168,12 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
         }
     };
 
+    __shared__ unsigned short cbt[16];  // WF_CB4: f16 codebook (published by the first stage barrier)
+    if constexpr (WF == WF_CB4) {
+        if (tid < 16) cbt[tid] = p.q.cb16[tid];
+    }
+    const float qscale = p.q.scale;
+    const double qstep = p.q.step;
     float acc[KW][HW];
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
@@ -197,6 +204,9 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
         const int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
         const int* cnt = reinterpret_cast<const int*>(tb);
         const DirectTap* seg = reinterpret_cast<const DirectTap*>(tb + HDR);
+        const unsigned* segc = reinterpret_cast<const unsigned*>(tb + HDR);  // f16: compact taps
+        // compact f16 taps hold STAGE-relative element offsets
+        const E* xlc = reinterpret_cast<const E*>(xs + (size_t)buf * p.stage_el + lane * p.ip);
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
@@ -204,13 +214,21 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
             const int nt = cnt[kk];
 #pragma unroll 4
             for (int t = 0; t < nt; ++t) {
-                const DirectTap tp = seg[t];
-                const E* xp = reinterpret_cast<const E*>(xl + tp.off);
+                DirectTap tp;
+                const E* xp;
+                unsigned short vh = 0;
+                if constexpr (F16) {
+                    const unsigned tw = segc[t];
+                    xp = xlc + (tw & 0xffffu);
+                    vh = tap_f16<WF>(tw >> 16, cbt, qscale, qstep);
+                } else {
+                    tp = seg[t];
+                    xp = reinterpret_cast<const E*>(xl + tp.off);
+                }
 #pragma unroll
                 for (int y = 0; y < H; ++y) {
                     const V v = *reinterpret_cast<const V*>(xp + y * RW);
                     if constexpr (F16) {
-                        const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
 #pragma unroll
                         for (int x = 0; x < H; ++x) acc[kk][y * H + x] = fhfma(acc[kk][y * H + x], vh, dimg_half<H>(v, x));
                     } else {
@@ -221,6 +239,7 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
                 }
             }
             seg += nt;
+            segc += nt;
         }
     }
 
@@ -268,9 +287,9 @@ __global__ void __launch_bounds__(512, 1) k_dimg(const __grid_constant__ DirectP
     }
 }
 
-template <int H, int KW, int MODE, bool F16 = false>
+template <int H, int KW, int MODE, bool F16 = false, int WF = (F16 ? WF_F16 : WF_F32)>
 cudaError_t launch_dimg_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_dimg<H, KW, MODE, F16>;
+    auto kern = k_dimg<H, KW, MODE, F16, WF>;
     static int lim[64];  // per device (the attribute is per device)
     const cudaError_t e = dyn_smem_ok(kern, smem, lim);
     if (e != cudaSuccess) return e;

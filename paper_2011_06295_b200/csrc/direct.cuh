@@ -58,6 +58,7 @@ struct DirectParams {
     int nbuf;                 // stage buffers in flight (2 or 3)
     int nfx;                  // k_direct WIDE: column tiles of LW per output row
     ActQuant aq;              // activation fake-quant (flags & SCB_FLAG_ACT_QUANT)
+    QuantAux q;               // f16 kernels: in-register weight decode (codebook / scales)
     const int32_t* blkoff;    // k_direct: [group*nst + st] 16-byte-chunk offset of each tap block (+ end)
     uint32_t flags;
 };
@@ -130,10 +131,12 @@ __device__ __forceinline__ float fhfma(float acc, unsigned short v, unsigned sho
 // nfx); each staged row then carries its real left/right halo columns.
 // ONED (1D convolution, H = R = 1): a lane's TH outputs are columns lx + j*LW of
 // one tile of TH*LW columns, staged as one contiguous row per (image, channel).
+// WF (f16 storage only): weight format of the compact 4-byte taps (kernels.cuh tap_f16).
 template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false,
-          bool WIDE = false, bool ONED = false>
+          bool WIDE = false, bool ONED = false, int WF = WF_F32>
 // (MINB = 2 variants may run 16 warps per CTA: 512 threads, one CTA per SM, same 128 registers)
 __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k_direct(const __grid_constant__ DirectParams p) {
+    static_assert(F16IO == (WF != WF_F32), "f16 storage <=> compact f16 taps");
     static_assert(!F16IO || !WIDE, "f16 storage: narrow rows");
     static_assert(!WIDE || (VX == 1 && !F16IO), "wide tiles: f32, one column per lane");
     static_assert(!ONED || (WIDE && R == 1), "1D tiles are wide tiles of one input row");
@@ -277,6 +280,13 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
         }
     };
 
+    __shared__ unsigned short cbt[16];  // WF_CB4: f16 codebook (published by the first stage barrier)
+    if constexpr (WF == WF_CB4) {
+        if (tid < 16) cbt[tid] = p.q.cb16[tid];
+    }
+    const float qscale = p.q.scale;
+    const double qstep = p.q.step;
+
     float acc[KW][TH * VX];
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
@@ -310,6 +320,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
         const int4* tb = tsm + ((size_t)buf * p.wk + warp) * p.segcap;
         const int* cnt = reinterpret_cast<const int*>(tb);
         const DirectTap* seg = reinterpret_cast<const DirectTap*>(tb + HDR);
+        const unsigned* segc = reinterpret_cast<const unsigned*>(tb + HDR);  // f16: compact taps
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             const int k = k0 + kk;
@@ -317,21 +328,27 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
             const int nt = cnt[kk];
 #pragma unroll 4
             for (int t = 0; t < nt; ++t) {
+                if constexpr (F16IO) {
+                    const unsigned tw = segc[t];
+                    const TIO* xp = xl + (tw & 0xffffu) + st * p.cc * PLANE;  // offsets are stage-relative
+                    const unsigned short vh = tap_f16<WF>(tw >> 16, cbt, qscale, qstep);
+                    if constexpr (VX == 1) {  // one half per MAC: no shifted copy needed
+#pragma unroll
+                        for (int j = 0; j < TH; ++j)
+                            acc[kk][j] = fhfma(acc[kk][j], vh, *reinterpret_cast<const unsigned short*>(xp + j * JS));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < TH; ++j) {
+                            const unsigned w2 = *reinterpret_cast<const unsigned*>(xp + j * ROW);
+                            acc[kk][2 * j] = fhfma(acc[kk][2 * j], vh, (unsigned short)(w2 & 0xffffu));
+                            acc[kk][2 * j + 1] = fhfma(acc[kk][2 * j + 1], vh, (unsigned short)(w2 >> 16));
+                        }
+                    }
+                    continue;
+                }
                 const DirectTap tp = seg[t];
                 const TIO* xp = reinterpret_cast<const TIO*>(reinterpret_cast<const char*>(xl) + tp.off);
-                if constexpr (F16IO && VX == 1) {  // one half per MAC: no shifted copy needed
-                    const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
-#pragma unroll
-                    for (int j = 0; j < TH; ++j)
-                        acc[kk][j] = fhfma(acc[kk][j], vh, *reinterpret_cast<const unsigned short*>(xp + j * JS));
-                } else if constexpr (F16IO) {
-                    const unsigned short vh = (unsigned short)(__float_as_uint(tp.v) & 0xffffu);
-#pragma unroll
-                    for (int j = 0; j < TH; ++j) {
-                        const unsigned w2 = *reinterpret_cast<const unsigned*>(xp + j * ROW);
-                        acc[kk][2 * j] = fhfma(acc[kk][2 * j], vh, (unsigned short)(w2 & 0xffffu));
-                        acc[kk][2 * j + 1] = fhfma(acc[kk][2 * j + 1], vh, (unsigned short)(w2 >> 16));
-                    }
+                if constexpr (F16IO) {
                 } else if constexpr (VX == 1) {
 #pragma unroll
                     for (int j = 0; j < TH; ++j) acc[kk][j] = mac1<MODE>(acc[kk][j], tp.v, xp[j * JS]);
@@ -345,6 +362,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 }
             }
             seg += nt;
+            segc += nt;
         }
     }
 
@@ -422,9 +440,9 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
 }
 
 template <int R, int S, int PAD, int TH, int LW, int KW, int MODE, int VX, int MINB, bool F16IO = false,
-          bool WIDE = false, bool ONED = false>
+          bool WIDE = false, bool ONED = false, int WF = (F16IO ? WF_F16 : WF_F32)>
 cudaError_t launch_direct_t(const DirectParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX, MINB, F16IO, WIDE, ONED>;
+    auto kern = k_direct<R, S, PAD, TH, LW, KW, MODE, VX, MINB, F16IO, WIDE, ONED, WF>;
     static int lim[64];  // per device (the attribute is per device)
     const cudaError_t e = dyn_smem_ok(kern, smem, lim);
     if (e != cudaSuccess) return e;

@@ -35,7 +35,7 @@ HERE = Path(__file__).resolve().parent
 # block), 0 = one shared loop head (smaller code)
 THREADED = int(__import__("os").environ.get("SCB_THREADED", "1"))
 
-WF_F32, WF_F16, WF_CB4, WF_LIN16 = 0, 1, 2, 3   # kernels.cuh WF_*
+WF_F32, WF_F16, WF_CB4, WF_LIN16, WF_AFF16 = 0, 1, 2, 3, 4   # kernels.cuh WF_*
 EXACT, FMA = 0, 1                                # kernels.cuh MODE_*
 JUMP, MASK = 0, 1                                # kernels.cuh DISPATCH_*
 
@@ -403,6 +403,12 @@ DIRECTS_F16 = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for 
               [(3, 3, 1, 4, 4, kw) for kw in (4, 8)]  # 4x4 planes: 8-byte rows, 16 images per warp
 # f16 storage, one column per lane (VX = 1: no shifted row copy): (TH, LW, KW)
 DIRECTS_F16_VX1 = [(8, 32, 4), (16, 32, 4), (8, 32, 8), (8, 16, 4), (8, 16, 8), (8, 8, 8)]
+# quantized f16 weights decoded IN REGISTER from compact 4-byte taps (kernels.cuh tap_f16):
+# 4-bit codebook, int16 fixed point, int16 symmetric affine -- on the shapes the f16 stacks use
+QFMTS = (WF_CB4, WF_LIN16, WF_AFF16)
+DIRECTS_F16_Q = [(3, 3, 1, 8, lw, kw) for lw in (32, 16, 8) for kw in (2, 4)]
+DIRECTS_F16_VX1_Q = [(8, 32, 4), (8, 16, 4), (8, 8, 8)]
+DIMGS_F16_Q = [(4, 2), (4, 4), (2, 2), (2, 4)]
 
 
 N_PARTS = 10
@@ -448,13 +454,17 @@ def main():
     for R, S, PAD, TH, LW, KW in DWS:
         groups[("dws", R, S, PAD, TH, LW, KW)] = ([], [("dws", R, S, PAD, TH, LW, KW, m) for m in (EXACT, FMA)])
     for R, S, PAD, TH, LW, KW in DIRECTS_F16:
-        groups[("direct16", R, S, PAD, TH, LW, KW)] = ([], [("direct16", R, S, PAD, TH, LW, KW)])
+        qs = QFMTS if (R, S, PAD, TH, LW, KW) in DIRECTS_F16_Q else ()
+        groups[("direct16", R, S, PAD, TH, LW, KW)] = (
+            [], [("direct16", R, S, PAD, TH, LW, KW, wf) for wf in (WF_F16,) + qs])
     for TH, LW, KW in DIRECTS_F16_VX1:
-        groups[("direct16v1", TH, LW, KW)] = ([], [("direct16v1", TH, LW, KW)])
+        qs = QFMTS if (TH, LW, KW) in DIRECTS_F16_VX1_Q else ()
+        groups[("direct16v1", TH, LW, KW)] = ([], [("direct16v1", TH, LW, KW, wf) for wf in (WF_F16,) + qs])
     for H, KW in DIMGS:
         groups[("dimg", H, KW)] = ([], [("dimg", H, KW, mode) for mode in (EXACT, FMA)])
     for H, KW in DIMGS_F16:
-        groups[("dimg16", H, KW)] = ([], [("dimg16", H, KW)])
+        qs = QFMTS if (H, KW) in DIMGS_F16_Q else ()
+        groups[("dimg16", H, KW)] = ([], [("dimg16", H, KW, wf) for wf in (WF_F16,) + qs])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -492,21 +502,21 @@ def main():
                                 f"{KIND_DWS}}}, nullptr, &launch_dws_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, {mode}>}},\n")
                     continue
                 if v[0] == "direct16v1":
-                    _, TH, LW, KW = v
-                    ents.append(f"    {{{{3, 3, {KW}, 1, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, 1, "
+                    _, TH, LW, KW, wf = v
+                    ents.append(f"    {{{{3, 3, {KW}, 1, {TH}, {LW}, SCB_F16, {wf}, {FMA}, {JUMP}, 1, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<3, 3, 1, {TH}, {LW}, {KW}, "
-                                f"{FMA}, 1, 2, true>, 512}},\n")
+                                f"{FMA}, 1, 2, true, false, false, {wf}>, 512}},\n")
                     continue
                 if v[0] == "direct16":
-                    _, R, S, PAD, TH, LW, KW = v
-                    ents.append(f"    {{{{{R}, {S}, {KW}, 2, {TH}, {LW}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, {PAD}, "
+                    _, R, S, PAD, TH, LW, KW, wf = v
+                    ents.append(f"    {{{{{R}, {S}, {KW}, 2, {TH}, {LW}, SCB_F16, {wf}, {FMA}, {JUMP}, {PAD}, "
                                 f"{KIND_DIRECT}}}, nullptr, &launch_direct_t<{R}, {S}, {PAD}, {TH}, {LW}, {KW}, "
-                                f"{FMA}, 2, 2, true>, 512}},\n")
+                                f"{FMA}, 2, 2, true, false, false, {wf}>, 512}},\n")
                     continue
                 if v[0] == "dimg16":
-                    _, H, KW = v
-                    ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F16, {WF_F16}, {FMA}, {JUMP}, 1, "
-                                f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {FMA}, true>, 512}},\n")
+                    _, H, KW, wf = v
+                    ents.append(f"    {{{{3, 3, {KW}, 1, {H}, {H}, SCB_F16, {wf}, {FMA}, {JUMP}, 1, "
+                                f"{KIND_DIMG}}}, nullptr, &launch_dimg_t<{H}, {KW}, {FMA}, true, {wf}>, 512}},\n")
                     continue
                 if v[0] == "dimg":
                     _, H, KW, mode = v

@@ -37,7 +37,7 @@ inline cudaError_t dyn_smem_ok(K kern, size_t smem, int (&lim)[64]) {
 }
 
 enum { MODE_EXACT = 0, MODE_FMA = 1 };
-enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3 };
+enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3, WF_AFF16 = 4 };
 // how the tiled kernel dispatches a tap to its unrolled MAC block (gen_taploop.py)
 enum { DISPATCH_JUMP = 0,   // brx.idx jump table, one indirect branch per tap
        DISPATCH_MASK = 1,   // per-channel KT x 16-bit masks walked in order
@@ -109,7 +109,31 @@ struct Tap {          // one nonzero of the device tap program
 struct QuantAux {
     float cb[16];     // codebook table (CB4)
     float scale;      // 2^-frac (LIN16)
+    double step;      // affine symmetric step (AFF16, quantize.py:99-138)
+    unsigned short cb16[16];  // CB4 table as f16 bits (f16-storage kernels)
 };
+
+// Compact f16 tap (4 bytes): bits 0..15 = element offset in the stage window,
+// bits 16..31 = payload decoded IN REGISTER by the weight format:
+//   WF_F16   f16 bits of the value
+//   WF_CB4   4-bit codebook index -> cb16[] (the reference's Codebook.decode, quantize.py:209-210)
+//   WF_LIN16 int16 code x 2^-frac, exact in f32, then f16 (quantize_fixed + astype, quantize.py:64-71,275)
+//   WF_AFF16 int16 code: f16(f64(code) * step) -- dequantize_affine_int in f64 then astype(f16)
+//            (quantize.py:137-138, 279-283), one direct f64 -> f16 rounding like numpy
+template <int WF>
+__device__ __forceinline__ unsigned short tap_f16(unsigned payload, const unsigned short* cbt, float scale,
+                                                  double step) {
+    if constexpr (WF == WF_F16) {
+        return (unsigned short)payload;
+    } else if constexpr (WF == WF_CB4) {
+        return cbt[payload & 15u];
+    } else if constexpr (WF == WF_LIN16) {
+        return __half_as_ushort(__float2half_rn((float)(short)payload * scale));
+    } else {
+        static_assert(WF == WF_AFF16, "f16 tap format");
+        return __half_as_ushort(__double2half(__dmul_rn((double)(short)payload, step)));
+    }
+}
 
 struct GenericParams {
     const void* x;

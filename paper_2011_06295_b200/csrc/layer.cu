@@ -179,10 +179,11 @@ struct scb_layer {
     }
 
     // largest block (16-byte units) for (cc, kw), from the host stage pointers
-    int block_cap(int cc, int kw) {
+    // tw = 32-bit words per tap: 2 ({f32 value, byte offset}) or 1 (compact f16 tap)
+    int block_cap(int cc, int kw, int tw = 2) {
         host_sptr(cc);
         std::lock_guard<std::mutex> lk(mu);
-        auto key = std::make_pair(cc, kw);
+        auto key = std::make_pair(cc, kw * 4 + tw);
         auto it = blk_cap.find(key);
         if (it != blk_cap.end()) return it->second;
         const std::vector<int32_t>& sp = h_sptr[cc];
@@ -196,7 +197,7 @@ struct scb_layer {
                     const int k = gg * kw + kk;
                     if (k < g.k) n += sp[(size_t)k * (nst + 1) + st + 1] - sp[(size_t)k * (nst + 1) + st];
                 }
-                mx = std::max(mx, hdr + (n + 1) / 2);
+                mx = std::max(mx, hdr + (n * tw + 3) / 4);
             }
         blk_cap[key] = mx;
         return mx;
@@ -213,7 +214,10 @@ struct scb_layer {
         std::memcpy(&b, &h_vals[t], 4);
         return b;
     }
-    // device tables: taps (as 16-byte chunks) and per-(g, st) chunk offsets
+    // device tables: taps (as 16-byte chunks) and per-(g, st) chunk offsets.  es = 2 (the f16
+    // kernels): compact 4-byte taps {element offset relative to the stage (16 bits), payload
+    // (16 bits: f16 bits / int16 code / 4-bit codebook index)} decoded in registers
+    // (kernels.cuh tap_f16); otherwise 8-byte {native value, byte offset}.
     Blocks direct_blocks(int plane, int row, const std::vector<int>& col, int es, int cc, int kw, bool build) {
         if (build) host_sptr(cc);
         std::lock_guard<std::mutex> lk(mu);
@@ -222,40 +226,44 @@ struct scb_layer {
         auto it = d_blocks.find(key);
         if (it != d_blocks.end()) return it->second;
         if (!build) return Blocks{};
+        const bool compact = es == 2;
         const std::vector<int32_t>& sp = h_sptr[cc];
         const int64_t pp = (int64_t)g.hp * g.wp;
         const int nst = (g.c + cc - 1) / cc, groups = (g.k + kw - 1) / kw;
         const int hdr = (kw * 4 + 15) / 16;
-        std::vector<DirectTap> out;
+        std::vector<uint32_t> out;  // 32-bit words, 4 per 16-byte chunk
         std::vector<int32_t> off((size_t)groups * nst + 1);
         for (int gg = 0; gg < groups; ++gg)
             for (int st = 0; st < nst; ++st) {
-                off[(size_t)gg * nst + st] = (int32_t)(out.size() / 2);  // in 16-byte chunks
+                off[(size_t)gg * nst + st] = (int32_t)(out.size() / 4);  // in 16-byte chunks
                 const size_t h0 = out.size();
-                out.resize(h0 + 2 * hdr);
-                int32_t* cnt = reinterpret_cast<int32_t*>(&out[h0]);
+                out.resize(h0 + 4 * hdr, 0u);
                 for (int kk = 0; kk < kw; ++kk) {
                     const int k = gg * kw + kk;
                     const int t0 = k < g.k ? sp[(size_t)k * (nst + 1) + st] : 0;
                     const int t1 = k < g.k ? sp[(size_t)k * (nst + 1) + st + 1] : 0;
-                    cnt = reinterpret_cast<int32_t*>(&out[h0]);
-                    cnt[kk] = t1 - t0;
+                    out[h0 + kk] = (uint32_t)(t1 - t0);
                     for (int t = t0; t < t1; ++t) {
                         const int64_t c = h_colidx[t] / pp, rem = h_colidx[t] % pp;
-                        DirectTap d;
-                        const uint32_t vb = native_bits(t);
-                        std::memcpy(&d.v, &vb, 4);
-                        d.off = (int32_t)(es * (c * plane + (rem / g.wp) * row + col[rem % g.wp]));
-                        out.push_back(d);
+                        if (compact) {
+                            const int64_t e = (c - (int64_t)st * cc) * plane + (rem / g.wp) * row + col[rem % g.wp];
+                            if (e < 0 || e > 0xffff) return Blocks{};  // (derive rejects such launches)
+                            out.push_back((h_pay[t] << 16) | (uint32_t)e);
+                        } else {
+                            out.push_back(native_bits(t));
+                            out.push_back((uint32_t)(int32_t)(es * (c * plane + (rem / g.wp) * row + col[rem % g.wp])));
+                        }
                     }
                 }
-                if (out.size() & 1) out.push_back(DirectTap{0.f, 0});
+                while (out.size() & 3) out.push_back(0u);
             }
-        off[(size_t)groups * nst] = (int32_t)(out.size() / 2);  // end of the last block
+        off[(size_t)groups * nst] = (int32_t)(out.size() / 4);  // end of the last block
         Blocks b;
-        if (cudaMalloc(&b.taps, std::max<size_t>(out.size(), 2) * sizeof(DirectTap)) != cudaSuccess) return Blocks{};
+        const size_t nw = std::max<size_t>(out.size(), 4);
+        out.resize(nw, 0u);
+        if (cudaMalloc(&b.taps, nw * 4) != cudaSuccess) return Blocks{};
         if (cudaMalloc(&b.off, off.size() * 4) != cudaSuccess) { cudaFree(b.taps); return Blocks{}; }
-        if (cudaMemcpy(b.taps, out.data(), out.size() * sizeof(DirectTap), cudaMemcpyHostToDevice) != cudaSuccess ||
+        if (cudaMemcpy(b.taps, out.data(), nw * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(b.off, off.data(), off.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
             cudaFree(b.taps);
             cudaFree(b.off);
@@ -413,6 +421,39 @@ bool encode_payloads(scb_layer* L, const unsigned char* vals, std::vector<uint32
         for (size_t i = 0; i < 16; ++i) {
             uint32_t b = i < table.size() ? table[i] : 0u;
             std::memcpy(&L->q.cb[i], &b, 4);
+            L->q.cb16[i] = __half_as_ushort(__float2half_rn(L->q.cb[i]));  // exact for f16 layers
+        }
+        return true;
+    }
+    if (L->wfmt == SCB_W_AFF16) {
+        // code = round(v / step), accepted iff the storage rounding of f64(code)*step gives v back
+        // bit for bit (numpy: dequantize_affine_int in f64, then astype, quantize.py:137-138)
+        const double step = L->q.step;
+        if (!(step > 0.0) || !std::isfinite(step)) { set_error("AFF16 needs a finite step > 0"); return false; }
+        const int es = dtype_size(L->dt);
+        for (int64_t t = 0; t < nnz; ++t) {
+            const double code0 = std::nearbyint((double)as_f32[t] / step);
+            bool ok = false;
+            for (int dlt = 0; dlt < 3 && !ok; ++dlt)
+                for (int sg : {1, -1}) {
+                    const double code = code0 + sg * dlt;
+                    if (std::fabs(code) > 32767.0) continue;
+                    const double v = 0.0 + code * step;
+                    bool same;
+                    if (L->dt == SCB_F16) {
+                        uint16_t h;
+                        std::memcpy(&h, vals + t * es, 2);
+                        same = __half_as_ushort(__double2half(v)) == h;
+                    } else {
+                        uint32_t a, b2;
+                        const float fv = (float)v;
+                        std::memcpy(&a, &fv, 4);
+                        std::memcpy(&b2, vals + t * es, 4);
+                        same = a == b2;
+                    }
+                    if (same) { pay[t] = (uint32_t)(uint16_t)(int16_t)code; ok = true; break; }
+                }
+            if (!ok) { set_error("AFF16: a value is not the storage rounding of an int16 code x step"); return false; }
         }
         return true;
     }
@@ -529,6 +570,7 @@ scb_status build_program(scb_layer* L, int kt, const int32_t* colidx, const int3
 int wf_of(const scb_layer* L) {
     if (L->wfmt == SCB_W_CB4) return WF_CB4;
     if (L->wfmt == SCB_W_LIN16) return WF_LIN16;
+    if (L->wfmt == SCB_W_AFF16) return WF_AFF16;
     return L->dt == SCB_F16 ? WF_F16 : WF_F32;
 }
 
@@ -538,10 +580,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     const Geom& g = L->g;
     if (L->dt == SCB_F64) return false;
     if (g.stride != 1 || v.r != g.r || v.s != g.s || v.pad != g.pad) return false;
-    // direct / image-lane kernels take any weight format: their tap blocks carry the
-    // decoded native value (decoded once on upload, direct_blocks)
+    // f32 direct / image-lane / TMEM kernels take any weight format: their tap blocks carry
+    // the decoded native value (decoded once on upload, direct_blocks); the f16 ones decode
+    // the compact tap's payload in registers, so their format must match the layer's
     const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG || v.kind == KIND_TMI) &&
-                         v.wf == (L->dt == SCB_F16 ? WF_F16 : WF_F32);
+                         L->dt != SCB_F16 && v.wf == WF_F32;
     if (v.io != L->dt || (v.wf != L->wf && !decoded)) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
     if (v.mode != mode) return false;
@@ -691,7 +734,9 @@ scb_status derive_direct(scb_layer* L, const scb_launch& c, int n, uint32_t flag
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = plane;  // plane pitch (elements) travels in `tap_cap`
     const int rows = G * c.cc * (oned ? 1 : v.th + v.r - 1);
-    const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
+    const bool compact = v.io == SCB_F16;  // 4-byte taps with 16-bit stage-relative offsets
+    if (compact && (int64_t)c.cc * plane > 0x10000) return fail(SCB_ERR_SHAPE, "stage too large for 16-bit tap offsets");
+    const int cap = L->block_cap(c.cc, v.kt, compact ? 1 : 2);  // 16-byte chunks per (group, stage) tap block
     d->wp = cap;  // tap block slot (16-byte units) travels in `wp`
     d->smem = nbuf * stage_bytes + (((size_t)rows * 8 + 15) & ~(size_t)15) +
               (size_t)nbuf * c.warps_k * cap * 16;
@@ -733,7 +778,9 @@ scb_status derive_dimg(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const size_t stage_bytes = ((size_t)32 * ip * es + 127) & ~(size_t)127;
     d->stage_el = (int)(stage_bytes / es);
     d->tap_cap = blk;
-    const int cap = L->block_cap(c.cc, v.kt);  // 16-byte chunks per (group, stage) tap block
+    const bool compact = v.io == SCB_F16;  // 4-byte taps with 16-bit stage-relative offsets
+    if (compact && (int64_t)c.cc * blk > 0x10000) return fail(SCB_ERR_SHAPE, "stage too large for 16-bit tap offsets");
+    const int cap = L->block_cap(c.cc, v.kt, compact ? 1 : 2);  // 16-byte chunks per (group, stage) tap block
     d->wp = cap;
     d->smem = nbuf * stage_bytes + (size_t)nbuf * c.warps_k * cap * 16;
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
@@ -1074,6 +1121,13 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
                                     const void* values, const int32_t* colidx,
                                     const int32_t* rowptr, int64_t nnz, int32_t unified,
                                     int32_t device, scb_layer** out) {
+    return scb_layer_create_q(shape, dt, wfmt, values, colidx, rowptr, nnz, unified, device, 0.0, out);
+}
+
+SCB_API scb_status scb_layer_create_q(const scb_shape* shape, scb_dtype dt, scb_wfmt wfmt,
+                                      const void* values, const int32_t* colidx,
+                                      const int32_t* rowptr, int64_t nnz, int32_t unified,
+                                      int32_t device, double qstep, scb_layer** out) {
     if (!out) return fail(SCB_ERR_ARG, "out is NULL");
     *out = nullptr;
     Geom g;
@@ -1097,6 +1151,7 @@ SCB_API scb_status scb_layer_create(const scb_shape* shape, scb_dtype dt, scb_wf
     L->unified = unified != 0;
     L->nnz = nnz;
     L->wf = wf_of(L.get());
+    L->q.step = qstep;
 
     std::vector<uint32_t> pay;
     std::vector<float> as_f32;
@@ -1160,7 +1215,10 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
     }
     if (variant >= num_variants()) return fail(SCB_ERR_ARG, "bad variant");
     if (scb::variant(variant).info.kind >= KIND_DIRECT) {
-        *bytes = L->nnz * (int64_t)sizeof(DirectTap) + (int64_t)(L->g.k + 1) * 4;
+        // f16 direct / image-lane kernels: compact 4-byte taps (offset + f16 / code payload)
+        const scb_variant_info& vi = scb::variant(variant).info;
+        const bool compact = vi.io == SCB_F16 && (vi.kind == KIND_DIRECT || vi.kind == KIND_DIMG);
+        *bytes = L->nnz * (compact ? 4 : (int64_t)sizeof(DirectTap)) + (int64_t)(L->g.k + 1) * 4;
         return SCB_OK;
     }
     Program* P = L->prog(scb::variant(variant).info.kt);
@@ -1344,6 +1402,7 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
         q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nfx = d.n_fx; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
+        q.q = L->q;
         if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {  // fused fake-quant epilogue
             q.aq = L->aq;
             *fused_aq = true;

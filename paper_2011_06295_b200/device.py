@@ -17,7 +17,8 @@ import numpy as np
 from . import _abi
 from .errors import ShapeError
 
-_WFMT = {"native": _abi.SCB_W_NATIVE, "cb4": _abi.SCB_W_CB4, "lin16": _abi.SCB_W_LIN16}
+_WFMT = {"native": _abi.SCB_W_NATIVE, "cb4": _abi.SCB_W_CB4, "lin16": _abi.SCB_W_LIN16,
+         "aff16": _abi.SCB_W_AFF16}
 _IO = {np.dtype(np.float32): _abi.SCB_F32, np.dtype(np.float64): _abi.SCB_F64,
        np.dtype(np.float16): _abi.SCB_F16}
 
@@ -49,11 +50,15 @@ class DeviceLayer:
         self.rowptr = rowptr.copy()
         st = _abi.shape_struct(kernel.shape)
         h = ctypes.c_void_p()
-        _abi.check(_abi.lib().scb_layer_create(
+        # affine int16 codes need the quantizer's step (quantize.py:137-138)
+        self.qstep = float((kernel.quant or {}).get("step", 0.0)) if weight_format == "aff16" else 0.0
+        if weight_format == "aff16" and not self.qstep > 0:
+            raise ShapeError("weight_format 'aff16' needs kernel.quant['step'] (the affine quantizer's step)")
+        _abi.check(_abi.lib().scb_layer_create_q(
             ctypes.byref(st), _IO[io_dtype], _WFMT[weight_format],
             ctypes.c_void_p(vals.ctypes.data), ctypes.c_void_p(colidx.ctypes.data),
             ctypes.c_void_p(rowptr.ctypes.data), self.nnz, int(kernel.unified),
-            self.device, ctypes.byref(h)), "scb_layer_create")
+            self.device, ctypes.c_double(self.qstep), ctypes.byref(h)), "scb_layer_create")
         self.handle = h.value
         self._fin = weakref.finalize(self, _destroy, self.handle)
         self._prepared = set()
@@ -124,7 +129,7 @@ class DeviceLayer:
 def device_layer(kernel, device: int, io_dtype, weight_format: str = "native") -> DeviceLayer:
     """Cached DeviceLayer of `kernel` (keyed on the identity of its arrays)."""
     io_dtype = np.dtype(io_dtype)
-    key = (int(device), str(io_dtype), weight_format)
+    key = (int(device), str(io_dtype), weight_format, float((kernel.quant or {}).get("step", 0.0)))
     ident = (id(kernel.values), id(kernel.colidx), id(kernel.rowptr), int(kernel.sparse_level),
              bool(kernel.unified), kernel.shape)
     cache = kernel._device_cache

@@ -30,7 +30,7 @@ from .weights import CsrKernel
 log = logging.getLogger(__name__)
 
 SUB_BATCH_CANDIDATES = (1, 2, 4, 8, 16)
-WEIGHT_FORMATS = ("native", "cb4", "lin16")
+WEIGHT_FORMATS = ("native", "cb4", "lin16", "aff16")
 
 
 @dataclass(frozen=True)

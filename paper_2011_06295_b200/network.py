@@ -440,8 +440,9 @@ def build_net(specs_pools, seed: int = 0, dtype=np.float32, device: int = 0,
         kern = build_csr(w, spec.shape)
         if values_fn is not None:
             from dataclasses import replace
-            kern = replace(kern, values=np.ascontiguousarray(values_fn(spec.name, kern.values)),
-                           _device_cache={})
+            res = values_fn(spec.name, kern.values)
+            vals, quant = res if isinstance(res, tuple) else (res, None)
+            kern = replace(kern, values=np.ascontiguousarray(vals), _device_cache={}, quant=quant)
         layers.append(NetLayer(spec.name, kern, b, relu=True, pool=pool))
     return SparseConvNet(layers, device=device, dtype=dtype, weight_format=weight_format,
                          fast_math=fast_math)

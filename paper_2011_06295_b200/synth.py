@@ -172,6 +172,8 @@ def reference_quantize(values: np.ndarray, kind: str, centers=None, pin_zero: bo
       tests/golden/make_quant_vgg.py)."""
     dtype = values.dtype
     x = np.asarray(values, dtype=np.float64).ravel()
+    if kind == "affine":  # symmetric int (fit_affine_int / quantize_affine_int / dequantize, quantize.py:99-138)
+        return affine_quantize(values, bits)[0]
     if kind == "fixed":
         m = float(np.max(np.abs(x))) if x.size else 0.0
         int_bits = 0 if m == 0 else max(0, math.ceil(math.log2(m)))
@@ -197,6 +199,23 @@ def reference_quantize(values: np.ndarray, kind: str, centers=None, pin_zero: bo
     return table.astype(np.float16)[labels].astype(dtype).reshape(values.shape)
 
 
+def affine_quantize(values: np.ndarray, bits: int = 16):
+    """quantize_weights_array(values, "affine", bits) restated (quantize.py:99-138, 279-283):
+    symmetric fit (mu = 0, step = max|x| / (2^(bits-1) - 1), 1 if that is 0), codes
+    round-to-nearest clipped to +-(2^(bits-1) - 1), value = mu + float64(code) * step cast
+    to the storage dtype.  Returns (values, step)."""
+    x = np.asarray(values, dtype=np.float64).ravel()
+    vmin, vmax = float(x.min()), float(x.max())
+    mu = 0.0
+    step = max(abs(vmin), abs(vmax)) / (2 ** (bits - 1) - 1)
+    if step == 0:
+        step = 1.0
+    lim = 2 ** (bits - 1) - 1
+    codes = np.clip(np.round((x - mu) / step), -lim, lim).astype(np.int64)
+    out = (mu + codes.astype(np.float64) * step).astype(values.dtype).reshape(values.shape)
+    return out, step
+
+
 def reference_quantized_values_fn(kind: str, fixture) -> "callable":
     """values_fn for network.build_net: replaces each layer's CSR values by the
     reference quantizer's output (config 4 with the reference's own "fixed:16" /
@@ -210,5 +229,8 @@ def reference_quantized_values_fn(kind: str, fixture) -> "callable":
         r = recs[name]
         if kind == "fixed":
             return reference_quantize(values, "fixed")
+        if kind == "affine":
+            out, step = affine_quantize(values, 16)
+            return out, {"scheme": "affine", "bits": 16, "mode": "symmetric", "step": step}
         return reference_quantize(values, "codebook", r["codebook"]["centers"], r["codebook"]["pin_zero"])
     return fn

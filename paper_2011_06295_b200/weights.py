@@ -56,6 +56,9 @@ class CsrKernel:
     shape: ConvShape
     unified: bool = True
     _device_cache: dict = field(default_factory=dict, repr=False, compare=False)
+    # quantizer metadata of the values (the reference's quantize_weights_array meta, e.g.
+    # {"scheme": "affine", "bits": 16, "step": s}, quantize.py:265-288); None = plain floats
+    quant: dict | None = field(default=None, repr=False, compare=False)
 
     def validate(self) -> None:
         """Structural invariants (csr.py:50-73); raises FormatError."""

@@ -8,7 +8,8 @@ Run in the build container (the reference is not on the GPU box):
 For every VGG-16/CIFAR layer at 90 % unified sparsity (make_layer_weights,
 bench.py:105-116, seed 0, scaled by sqrt(2/L) as synth.f16_scaled does) in f16
 storage, the CSR values (build_csr) are passed
-through quantize_weights_array(values, "fixed", 16) and ("codebook", 16, seed=0)
+through quantize_weights_array(values, "fixed", 16), ("codebook", 16, seed=0) and
+("affine", 16)
 (quantize.py:265-288).  Stored per layer: the sha256 of both reference outputs
 (bit patterns), the fixed-point split, and the codebook's float64 k-means centers
 (the labels are the final argmin against them, _cluster.py:45-47), which is what
@@ -51,6 +52,7 @@ def main():
         vals = build_csr(w16, sh).values
         fixed, fmeta, _ = quantize_weights_array(vals, "fixed", 16)
         cbv, cmeta, cb = quantize_weights_array(vals, "codebook", 16, seed=0)
+        aff, ameta, _ = quantize_weights_array(vals, "affine", 16)
         # the float64 centers build_codebook's kmeans call returns (quantize.py:229-243)
         flat = np.asarray(vals, dtype=np.float64).ravel()
         k_eff = min(16, len(np.unique(flat)))
@@ -64,7 +66,8 @@ def main():
         recs.append({"name": name, "nnz": int(vals.size), "values_sha": sha(vals),
                      "fixed": {"int_bits": fmeta["int_bits"], "frac_bits": fmeta["frac_bits"], "sha": sha(fixed)},
                      "codebook": {"pin_zero": pin, "centers": [float(v) for v in centers.ravel()],
-                                  "sha": sha(cbv)}})
+                                  "sha": sha(cbv)},
+                     "affine": {"step": ameta["step"], "sha": sha(aff)}})
         print(name, vals.size, fmeta, cmeta, pin)
     (OUT / "quant_vgg.json").write_text(json.dumps({"sparsity": 0.9, "seed": 0, "dtype": "float16",
                                                     "layers": recs}, indent=1))

@@ -70,10 +70,10 @@ def _fused_ffma(line: str) -> bool:
 _EXACT = {
     "tiled": r"_ZN3scb7k_tiledILi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELi\d+ELb0ELi(\d)ELi0ELi\dELi\dEE",
     "generic": r"_ZN3scb9k_genericI([fd])Li0EE",
-    "direct": r"_ZN3scb8k_directI(?:Li\d+E){6}Li0E(?:Li\d+E){2}Lb0E(?:Lb[01]E){2}E",
+    "direct": r"_ZN3scb8k_directI(?:Li\d+E){6}Li0E(?:Li\d+E){2}Lb0E(?:Lb[01]E){2}Li0EE",
     "dws": r"_ZN3scb5k_dwsI(?:Li\d+E){6}Li0EE",
     "dtm": r"_ZN3scb5k_dtmI(?:Li\d+E){7}Li0EE",
-    "dimg": r"_ZN3scb6k_dimgILi\d+ELi\d+ELi0ELb0EE",
+    "dimg": r"_ZN3scb6k_dimgILi\d+ELi\d+ELi0ELb0ELi0EE",
     "plane": r"_ZN3scb7k_planeI(?:Li\d+E){7}Lb0ELi0ELi0ELi\dEE",
     "tmi": r"_ZN3scb5k_tmiI(?:Li\d+E){5}Li0EE",
 }

@@ -783,3 +783,41 @@ def test_out_buffer_validated_and_misaligned_input(sc):
     assert view.data_ptr() % 16
     got = sc.conv_sparse(view[1:], kern, b).cpu().numpy()
     assert beq(got, want[1:])
+
+
+@pytest.mark.parametrize("fmt", ["native", "cb4", "lin16", "aff16"])
+def test_f16_compact_taps_in_register_decode(sc, fmt):
+    """f16 direct / image-lane kernels read 4-byte taps (16-bit stage offset + f16 value
+    or quantizer code) and decode the weight in registers; bitwise vs the oracle on the
+    reference quantizer's outputs for every matching variant."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import (LayerSpec, affine_quantize, bench_inputs, f16_scaled,
+                                             make_layer_weights, reference_quantize)
+    from dataclasses import replace
+    vs = _abi.variants()
+    for c, hw, k, n in ((64, 32, 64, 3), (128, 8, 64, 40), (256, 4, 96, 33), (128, 2, 64, 70)):
+        sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+        kern = sc.build_csr(f16_scaled(make_layer_weights(LayerSpec("q", sh, 0.9), 0)), sh)
+        if fmt == "cb4":  # 16 centers spread over the values: the codebook decode path
+            cents = np.quantile(kern.values.astype(np.float64), np.linspace(0.02, 0.98, 16))
+            kern = replace(kern, values=reference_quantize(kern.values, "codebook", cents), _device_cache={})
+        elif fmt == "lin16":
+            kern = replace(kern, values=reference_quantize(kern.values, "fixed"), _device_cache={})
+        elif fmt == "aff16":
+            vals, step = affine_quantize(kern.values, 16)
+            kern = replace(kern, values=vals, _device_cache={}, quant={"scheme": "affine", "step": step})
+        x, b = bench_inputs(sh, n)
+        x, b = x.astype(np.float16), b.astype(np.float16)
+        want = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+        layer = device_layer(kern, 0, np.float16, fmt)
+        cands = [cf for cf in layer.candidates(n) if vs[cf[0]]["kind"] in (2, 3)]
+        assert cands, (fmt, hw)
+        assert all(vs[cf[0]]["wf"] == {"native": 1, "cb4": 2, "lin16": 3, "aff16": 4}[fmt] for cf in cands)
+        assert layer.weight_bytes(cands[0][0]) == 4 * kern.values.size + 4 * (k + 1)
+        xd = torch.from_numpy(x).cuda()
+        for cfg in cands[:: max(1, len(cands) // 8)]:
+            o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg, weight_format=fmt)).cpu().numpy()
+            assert beq(o, want), (fmt, hw, cfg)

@@ -187,7 +187,7 @@ def test_config3_vgg_batch256_timed_mode_bitwise(torch, sparsity, chains):
     assert np.array_equal(_bits(got), _bits(oracle_stack(net, x)))
 
 
-@pytest.mark.parametrize("fmt", ["native", "cb4", "lin16"])
+@pytest.mark.parametrize("fmt", ["native", "cb4", "lin16", "aff16"])
 def test_config4_vgg_f16_batch256_bitwise(torch, fmt):
     """BASELINE config 4: the same stack with f16 activations and weights -- plain f16,
     the REFERENCE's codebook:16 weights as 4-bit codes (cb4) and its fixed:16 weights as
@@ -198,7 +198,8 @@ def test_config4_vgg_f16_batch256_bitwise(torch, fmt):
     from paper_2011_06295_b200.synth import f16_scaled, reference_quantized_values_fn, vgg16_cifar
     fixture = Path(__file__).resolve().parent / "golden" / "quant_vgg.json"
     fn = {"native": None, "cb4": reference_quantized_values_fn("codebook", fixture),
-          "lin16": reference_quantized_values_fn("fixed", fixture)}[fmt]
+          "lin16": reference_quantized_values_fn("fixed", fixture),
+          "aff16": reference_quantized_values_fn("affine", fixture)}[fmt]
     net = build_net(vgg16_cifar(0.9), seed=0, dtype=np.float16, weight_format=fmt, weight_fn=f16_scaled,
                     values_fn=fn)
     net.plan(256, tune=False)

@@ -91,7 +91,7 @@ def test_fake_quant_matches_reference():
 
 def test_reference_quantizers_restated_bitwise():
     """synth.reference_quantize reproduces the reference's quantize_weights_array
-    ("fixed", 16) and ("codebook", 16, seed=0) on every VGG-16/CIFAR layer's f16 CSR
+    ("fixed", 16), ("codebook", 16, seed=0) and ("affine", 16) on every VGG-16/CIFAR layer's f16 CSR
     values bit for bit (digests recorded from the reference, make_quant_vgg.py)."""
     import hashlib
     import json
@@ -109,3 +109,7 @@ def test_reference_quantizers_restated_bitwise():
         cb = reference_quantize(vals, "codebook", r["codebook"]["centers"], r["codebook"]["pin_zero"])
         assert hashlib.sha256(cb.tobytes()).hexdigest() == r["codebook"]["sha"], spec.name
         assert len(np.unique(cb)) <= 16
+        aff = reference_quantize(vals, "affine")
+        assert hashlib.sha256(aff.tobytes()).hexdigest() == r["affine"]["sha"], spec.name
+        from paper_2011_06295_b200.synth import affine_quantize
+        assert affine_quantize(vals, 16)[1] == r["affine"]["step"]
