@@ -68,6 +68,11 @@ typedef struct {
 #define SCB_FLAG_NO_PDL    0x10u  /* launch without programmatic dependent launch   */
 #define SCB_FLAG_ACT_QUANT 0x20u  /* fused activation fake-quant epilogue with the
                                      layer's scb_act_quant (store.py:285-286)      */
+#define SCB_FLAG_IMAGE_MINOR 0x40u /* x and y are IMAGE-MINOR: element (n, c, h, w) at
+                                     ((c*H + h)*W + w)*ld + n (ld = the row stride of
+                                     scb_conv_sparse_ld, = n for scb_conv_sparse); the
+                                     layout of the kind-7 image-lane kernels, which only
+                                     accept it (scb_to_image_minor converts NCHW)  */
 
 /* Launch configuration: replaces EnginePlan.sub_batch_size (engine.py:28-39)
  * and the timed tune_sub_batch (engine.py:143-166). variant < 0 = generic. */
@@ -176,6 +181,24 @@ SCB_API scb_status scb_layer_weight_bytes(const scb_layer* layer, int32_t varian
 SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
                                    void* y, int32_t n, uint32_t flags,
                                    const scb_launch* cfg, void* stream);
+
+/* scb_conv_sparse with explicit row strides of IMAGE-MINOR activations
+ * (SCB_FLAG_IMAGE_MINOR): x rows (c, h, w) hold images at x[row*ldx + i], i < n, and
+ * y rows likewise with ldy -- a sub-batch of a larger image-minor buffer is a pointer
+ * offset by its first image with ld = the full batch.  Kind-7 launches need
+ * ldx % 4 == 0 and a 16-byte aligned x (TMA).  Without the flag, ldx / ldy are
+ * ignored and this is scb_conv_sparse. */
+SCB_API scb_status scb_conv_sparse_ld(const scb_layer* layer, const void* x, int64_t ldx,
+                                      const void* bias, void* y, int64_t ldy, int32_t n,
+                                      uint32_t flags, const scb_launch* cfg, void* stream);
+
+/* Layout conversion for the image-minor kernels: x (n, chw) NCHW -> y[j*ldy + i]
+ * (scb_to_image_minor) and back (scb_from_image_minor: x[j*ldx + i] -> y (n, chw)),
+ * i < n, j < chw.  Asynchronous on `stream`. */
+SCB_API scb_status scb_to_image_minor(scb_dtype dt, const void* x, void* y, int32_t n, int64_t chw,
+                                      int64_t ldy, void* stream);
+SCB_API scb_status scb_from_image_minor(scb_dtype dt, const void* x, int64_t ldx, void* y, int32_t n,
+                                        int64_t chw, void* stream);
 
 /* Build (allocate + upload, synchronously) the device tables launch `cfg`
  * (NULL = the default launch) reads for batch n and `flags`; idempotent.  The

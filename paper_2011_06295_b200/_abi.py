@@ -26,6 +26,8 @@ SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16, SCB_W_AFF16 = 0, 1, 2, 3
 
 FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC, FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8, 0x10
 FLAG_ACT_QUANT = 0x20
+FLAG_IMAGE_MINOR = 0x40  # x / y image-minor: ((c*H + h)*W + w)*ld + n (kind-7 launches)
+KIND_LANE = 7
 
 # every symbol include/sparseconv_b200.h declares
 EXPORTS = (
@@ -34,7 +36,7 @@ EXPORTS = (
     "scb_layer_weight_bytes", "scb_conv_sparse", "scb_launch_candidates",
     "scb_default_launch", "scb_layer_prepare", "scb_launch_check", "scb_variant_count", "scb_variant_get", "scb_maxpool2",
     "scb_fma_peaks", "scb_fnv1a64", "scb_last_error", "scb_version", "scb_fake_quant",
-    "scb_layer_set_act_quant",
+    "scb_layer_set_act_quant", "scb_conv_sparse_ld", "scb_to_image_minor", "scb_from_image_minor",
 )
 
 
@@ -109,6 +111,9 @@ def lib():
             "scb_layer_destroy": [vp],
             "scb_layer_weight_bytes": [vp, i32, P(i64)],
             "scb_conv_sparse": [vp, vp, vp, vp, i32, u32, P(Launch), vp],
+            "scb_conv_sparse_ld": [vp, vp, i64, vp, vp, i64, i32, u32, P(Launch), vp],
+            "scb_to_image_minor": [i32, vp, vp, i32, i64, i64, vp],
+            "scb_from_image_minor": [i32, vp, i64, vp, i32, i64, vp],
             "scb_launch_candidates": [vp, i32, u32, P(Launch), i32, P(i32)],
             "scb_default_launch": [vp, i32, u32, i32, P(Launch)],
             "scb_layer_prepare": [vp, i32, u32, P(Launch)],
@@ -183,3 +188,18 @@ def maxpool2(dtype, x_ptr: int, y_ptr: int, planes: int, h: int, w: int, stream:
     check(lib().scb_maxpool2(_DT_CODE[str(np.dtype(dtype))], ctypes.c_void_p(x_ptr),
                              ctypes.c_void_p(y_ptr), int(planes), int(h), int(w),
                              ctypes.c_void_p(stream)), "scb_maxpool2")
+
+
+def to_image_minor(dtype, x_ptr: int, y_ptr: int, n: int, chw: int, ldy: int, stream: int = 0) -> None:
+    """NCHW (n, chw) -> image-minor y[j*ldy + i] (scb_to_image_minor)."""
+    import numpy as np
+    check(lib().scb_to_image_minor(_DT_CODE[str(np.dtype(dtype))], ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                   int(n), int(chw), int(ldy), ctypes.c_void_p(stream)), "scb_to_image_minor")
+
+
+def from_image_minor(dtype, x_ptr: int, ldx: int, y_ptr: int, n: int, chw: int, stream: int = 0) -> None:
+    """image-minor x[j*ldx + i] -> NCHW (n, chw) (scb_from_image_minor)."""
+    import numpy as np
+    check(lib().scb_from_image_minor(_DT_CODE[str(np.dtype(dtype))], ctypes.c_void_p(x_ptr), int(ldx),
+                                     ctypes.c_void_p(y_ptr), int(n), int(chw), ctypes.c_void_p(stream)),
+          "scb_from_image_minor")

@@ -362,7 +362,7 @@ PLANES = [
     (4, 4, 3, 3, 1, 2, 1, 3), (2, 2, 3, 3, 1, 2, 2, 3), (2, 2, 3, 3, 1, 2, 4, 3),
 ]
 PLANE_MODES = [(False, WF_F32, EXACT), (False, WF_F32, FMA), (True, WF_F16, FMA)]
-KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS, KIND_DTM, KIND_TMI = 0, 1, 2, 3, 4, 5, 6
+KIND_TILED, KIND_PLANE, KIND_DIRECT, KIND_DIMG, KIND_DWS, KIND_DTM, KIND_TMI, KIND_LANE = 0, 1, 2, 3, 4, 5, 6, 7
 # TMEM image-lane variants (tmi.cuh): (W plane, TE rows per lane unit, J images per lane, KW, WQ warps per quarter)
 TMIS = [(w, te, j, kw, wq) for (w, te, j) in ((4, 4, 1), (2, 2, 4), (2, 2, 2), (8, 2, 1))
         for kw, wq in ((2, 3), (3, 3), (2, 4), (4, 2))] + [(16, 1, 1, 2, 3), (16, 1, 1, 3, 3), (8, 4, 1, 1, 3), (8, 4, 1, 2, 3)]
@@ -372,6 +372,9 @@ DTMS = [(8, lw, kw, m) for lw in (32, 16, 8) for kw in (4, 8) for m in (2, 4)] +
 DWS = [(3, 3, 1, th, lw, kw) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)]
 # image-lane direct variants (dimg.cuh): (H, KW)
 DIMGS = [(4, 1), (4, 2), (4, 4), (2, 1), (2, 2), (2, 4), (2, 8)]
+# image-lane position-class kernels (lane.cuh, kind 7): (H = W, images per lane NB, KW, U = tap
+# unroll with padded class segments)
+LANES = [(h, nb, 1, u) for h in (2, 4) for nb in (1, 2, 4) for u in (1, 2) if not (h == 4 and nb == 4)]
 DIMGS_F16 = [(2, 2), (2, 4), (2, 8), (4, 2), (4, 4)]  # f16 storage, FHFMA
 
 # dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW, VX)
@@ -465,6 +468,8 @@ def main():
     for H, KW in DIMGS_F16:
         qs = QFMTS if (H, KW) in DIMGS_F16_Q else ()
         groups[("dimg16", H, KW)] = ([], [("dimg16", H, KW, wf) for wf in (WF_F16,) + qs])
+    for H, NB, KW, U in LANES:
+        groups[("lane", H, NB, KW, U)] = ([], [("lane", H, NB, KW, U, m) for m in (EXACT, FMA)])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -474,7 +479,7 @@ def main():
         load[i] += len(t[1])
     total_v = 0
     for i, part in enumerate(parts):
-        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n#include \"tm.cuh\"\n#include \"tmi.cuh\"\n"
+        src = ["// GENERATED by gen_taploop.py -- do not edit.\n#include \"tiled.cuh\"\n#include \"plane.cuh\"\n#include \"direct.cuh\"\n#include \"dimg.cuh\"\n#include \"ws.cuh\"\n#include \"tm.cuh\"\n#include \"tmi.cuh\"\n#include \"lane.cuh\"\n"
                "#include \"variants.h\"\n\nnamespace scb {\n\n"]
         ents = []
         for loops, variants in part:
@@ -489,6 +494,12 @@ def main():
                     _, TH, LW, KW, M, mode = v
                     ents.append(f"    {{{{3, 3, {KW}, {M}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
                                 f"{KIND_DTM}}}, nullptr, &launch_dtm_t<3, 3, 1, {TH}, {LW}, {KW}, {M}, {mode}>}},\n")
+                    continue
+                if v[0] == "lane":  # info: kt = KW, nbt = NB, th = H, tw = W, dispatch = U
+                    _, H, NB, KW, U, mode = v
+                    ents.append(f"    {{{{3, 3, {KW}, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {U}, 1, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, 544, nullptr, "
+                                f"&launch_lane_t<{H}, {H}, {NB}, {KW}, {mode}, {U}>}},\n")
                     continue
                 if v[0] == "tmi":  # info: kt = KW, nbt = J, th = TE, tw = W, dispatch = WQ
                     _, W, TE, J, KW, WQ, mode = v

@@ -147,4 +147,52 @@ cudaError_t launch_maxpool2(int dtype, const void* x, void* y, int64_t planes, i
     return cudaGetLastError();
 }
 
+// 32 x 32 tiles through shared memory (33-word rows: no bank conflicts), 8 rows per thread
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose(const T* __restrict__ x, int64_t ldx, T* __restrict__ y, int64_t ldy,
+                                                   int64_t rows, int64_t cols) {
+    __shared__ T tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int64_t r = r0 + ty + k, c = c0 + tx;
+        if (r < rows && c < cols) tile[ty + k][tx] = x[r * ldx + c];
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int64_t c = c0 + ty + k, r = r0 + tx;
+        if (r < rows && c < cols) y[c * ldy + r] = tile[tx][ty + k];
+    }
+}
+
+cudaError_t launch_transpose(int es, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t rows, int64_t cols,
+                             cudaStream_t st) {
+    const int64_t gx = (cols + 31) / 32, gy = (rows + 31) / 32;
+    if (gy > 65535 || gx > 0x7fffffffLL) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)gx, (unsigned)gy);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (es == 4)
+        e = cudaLaunchKernelEx(&cfg, k_transpose<float>, static_cast<const float*>(x), ldx, static_cast<float*>(y), ldy,
+                               rows, cols);
+    else if (es == 2)
+        e = cudaLaunchKernelEx(&cfg, k_transpose<unsigned short>, static_cast<const unsigned short*>(x), ldx,
+                               static_cast<unsigned short*>(y), ldy, rows, cols);
+    else
+        e = cudaLaunchKernelEx(&cfg, k_transpose<double>, static_cast<const double*>(x), ldx, static_cast<double*>(y),
+                               ldy, rows, cols);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace scb

@@ -1,0 +1,407 @@
+// Image-lane position-class kernel (kind 7, sm_100a) for small output planes.
+//
+// Why: on 4x4 and 2x2 planes (VGG-CIFAR conv4_x / conv5_x) a 3x3 / pad 1 tap
+// lands in the zero padding for 31 % / 56 % of the outputs the reference
+// iterates over (_kernels.py:73-84 runs `o = o + v * x` for every tap and every
+// output, x = 0 in the padding).  The direct kernels (direct.cuh, dimg.cuh)
+// spend a shared-memory load and an FMUL+FADD on each of those.  Here the
+// padding taps are dropped at upload time, so the kernel executes only the
+// MACs whose input is inside the image, in the reference's order:
+//
+//  * the outputs of a plane fall into position classes (rows {0}, {1..H-2},
+//    {H-1} x the same for columns): all positions of a class see the same set of
+//    in-image taps (r, s), at the same relative input offset.  For every output
+//    channel, input-channel stage and class the host writes the class's tap list
+//    -- the CSR row in colidx order with the padding taps removed -- as
+//    {v, byte offset of the input row of the class's first position};
+//  * lane = image (NB images per lane, 32*NB per CTA), the whole plane of
+//    accumulators in registers, the class's positions a compile-time set of
+//    immediate row offsets: per tap one broadcast descriptor, then per
+//    (position, image) one conflict-free LDS.32 (32 consecutive images) and one
+//    MAC -- no data-dependent control flow, no padding MACs;
+//  * activations are IMAGE-MINOR: x[(c*H + y)*W + x][n] with a row stride ldx
+//    (>= n): a stage (cc channels of a block's images) is one 2D TMA box
+//    {32*NB images, cc*H*W rows} (cp.async.bulk.tensor, out-of-bounds images /
+//    channels zero-filled) plus one 1D bulk copy of the CTA's descriptor slots,
+//    issued by a producer warp into an NBUF-deep mbarrier ring (1D bulk copies
+//    per row were measured at ~70 clk each per SM -- far too slow);
+//    consumer warps release a slot with one mbarrier arrive (no CTA barrier,
+//    warps drift up to NBUF-1 stages apart);
+//  * the epilogue writes image-minor rows too (coalesced 128-byte stores), with
+//    bias / ReLU / 2x2 max-pool / activation fake-quant fused as in direct.cuh.
+//
+// Exactness.  Dropping `o = o + v*(+0)` is exact when v is finite and o is not
+// -0.0: v*(+0) is +-0 and o + (+-0) = o.  o can only be -0.0 while every term so
+// far (bias included) was -0.0; then a dropped padding tap with a non-negative v
+// (v*(+0) = +0) would have turned it into +0 for good, and a later -0.0 product
+// keeps +0.  So the only possible difference is a final -0.0 where the reference
+// has +0.0, exactly when some dropped tap of that class has a sign-clear v: the
+// per-(channel, class) bit in `zmask` restores it in the epilogue.  Layers with a
+// non-finite weight are not eligible (the host checks; v*0 would be NaN).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "direct.cuh"
+#include "kernels.cuh"
+#include "sparseconv_b200.h"
+#include "ws.cuh"
+
+namespace scb {
+
+// Position classes along one axis of an H-long output axis (3-tap kernel, pad 1):
+// class i covers positions lo(i)..hi(i), which all see the same in-image taps.
+template <int H>
+struct LaneAxis {
+    static constexpr int N = H == 1 ? 1 : (H == 2 ? 2 : 3);
+    __host__ __device__ static constexpr int lo(int i) { return H <= 2 ? i : (i == 0 ? 0 : (i == 1 ? 1 : H - 1)); }
+    __host__ __device__ static constexpr int hi(int i) { return H <= 2 ? i : (i == 0 ? 0 : (i == 1 ? H - 2 : H - 1)); }
+};
+
+struct __align__(8) LaneTap {
+    float v;
+    int32_t off;  // byte offset of the input row (c_local*H*W + first position's input) * RB
+};
+
+constexpr int LANE_HDR = 32;  // chunk header: uint16 cumulative class ends (<= 16 classes)
+
+struct alignas(64) LaneParams {
+    CUtensorMap tmap;         // x as {images (dim 0), C*H*W rows}, box {32*NB, boxrows}
+    const float* bias;        // f32, may be null
+    float* y;                 // image-minor output, row stride ldy elements
+    const uint4* desc;        // [nst][K][cap] 16-byte units: per (k, stage) slot = header + LaneTaps
+    const uint32_t* zmask;    // [K] classes whose dropped taps include a sign-clear v
+    int n, c, k;              // batch (images of this call), input / output channels
+    int ldx, ldy;             // image-minor row strides (elements)
+    int cc, nst;              // input channels per stage, stages
+    int warps, kw;            // consumer warps, channels per warp (= template KW)
+    int kgroups;              // channel groups (CTA = image block x channel group)
+    int cap;                  // 16-byte units per (channel, stage) descriptor slot
+    int boxrows;              // rows per TMA box (cc*H*W = boxrows * copies)
+    int nbuf;                 // ring depth
+    int slot_bytes;           // bytes of one ring slot (inputs + descriptors)
+    ActQuant aq;
+    uint32_t flags;
+};
+
+// U > 1: every class segment is padded by the host to a multiple of U taps with
+// no-op taps {v = -0.0, input = a zero row} (-0 * +0 = -0 and o + (-0) = o for
+// every o, so exact), and the tap loop runs U taps per iteration with no remainder.
+template <int H, int W, int NB, int KW, int MODE, int U = 1>
+__global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LaneParams p) {
+    constexpr int HW = H * W;
+    constexpr int BI = 32 * NB;   // images per CTA
+    constexpr int RB = BI * 4;    // bytes of one (channel, position) row in shared memory
+    using AY = LaneAxis<H>;
+    using AX = LaneAxis<W>;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int WK = p.warps, NBUF = p.nbuf;
+    const int kg = blockIdx.x % p.kgroups;
+    const int n0 = (blockIdx.x / p.kgroups) * BI;
+    const int KC = WK * KW;
+    const int kbase = kg * KC;
+    const int in_bytes = p.cc * HW * RB;
+    const int d_bytes = in_bytes + (U > 1 ? HW * RB : 0);  // descriptors after inputs (+ zero rows)
+
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (size_t)NBUF * p.slot_bytes);
+    const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + NBUF);
+    if constexpr (U > 1) {  // zero rows read by the no-op taps (never written by the TMA)
+        for (int b = 0; b < NBUF; ++b)
+            for (int i = tid; i < HW * RB / 16; i += blockDim.x)
+                reinterpret_cast<uint4*>(smem + (size_t)b * p.slot_bytes + in_bytes)[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(full0 + 8 * b, 1);
+            mbar_init(empty0 + 8 * b, WK);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == WK) {
+        // ------------------------------------------------------------ producer
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // x is the previous kernel's output
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap) : "memory");
+            const int kn = min(KC, p.k - kbase);
+            const unsigned dbytes = (unsigned)(kn * p.cap * 16);
+            const int copies = p.cc * HW / p.boxrows;
+            const unsigned tx = (unsigned)in_bytes + dbytes;
+            for (int st = 0; st < p.nst; ++st) {
+                const int buf = st % NBUF;
+                if (st >= NBUF) mbar_wait(empty0 + 8 * buf, ((st / NBUF) - 1) & 1);
+                const unsigned fb = full0 + 8 * buf;
+                mbar_arrive_tx(fb, tx);
+                const unsigned dst = smem_u32(smem + (size_t)buf * p.slot_bytes);
+                for (int i = 0; i < copies; ++i)
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + (unsigned)(i * p.boxrows * RB)),
+                        "l"(&p.tmap), "r"(n0), "r"(st * p.cc * HW + i * p.boxrows), "r"(fb)
+                        : "memory");
+                bulk_g2s(dst + (unsigned)d_bytes, p.desc + ((size_t)st * p.k + kbase) * p.cap, dbytes, fb);
+            }
+        }
+        return;
+    }
+
+    // -------------------------------------------------------------- consumers
+    const int k0 = kbase + warp * KW;
+    float acc[KW][HW][NB];
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+        const int k = k0 + kk;
+        const float b = (p.bias != nullptr && k < p.k) ? p.bias[k] : 0.f;
+#pragma unroll
+        for (int q = 0; q < HW; ++q)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[kk][q][j] = b;
+    }
+    for (int st = 0; st < p.nst; ++st) {
+        const int buf = st % NBUF;
+        mbar_wait(full0 + 8 * buf, (st / NBUF) & 1);
+        const unsigned char* slot = smem + (size_t)buf * p.slot_bytes;
+        const unsigned char* xin = slot + lane * 4;
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk) {
+            if (k0 + kk >= p.k) break;
+            const unsigned char* ch = slot + d_bytes + (size_t)(warp * KW + kk) * p.cap * 16;
+            const unsigned short* hd = reinterpret_cast<const unsigned short*>(ch);
+            const LaneTap* tp = reinterpret_cast<const LaneTap*>(ch + LANE_HDR);
+            int beg = 0;
+#pragma unroll
+            for (int cy = 0; cy < AY::N; ++cy) {
+#pragma unroll
+                for (int cx = 0; cx < AX::N; ++cx) {
+                    const int y0 = AY::lo(cy), y1 = AY::hi(cy), x0 = AX::lo(cx), x1 = AX::hi(cx);
+                    const int end = hd[cy * AX::N + cx];
+                    if constexpr (U == 1) {
+#pragma unroll 2
+                        for (int t = beg; t < end; ++t) {
+                            const LaneTap d = tp[t];
+                            const unsigned char* xa = xin + d.off;
+#pragma unroll
+                            for (int yy = y0; yy <= y1; ++yy)
+#pragma unroll
+                                for (int xx = x0; xx <= x1; ++xx)
+#pragma unroll
+                                    for (int j = 0; j < NB; ++j) {
+                                        const float xv = *reinterpret_cast<const float*>(
+                                            xa + ((yy - y0) * W + (xx - x0)) * RB + j * 128);
+                                        acc[kk][yy * W + xx][j] = mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv);
+                                    }
+                        }
+                    } else {
+                        for (int t = beg; t < end; t += U) {
+                            LaneTap d[U];
+#pragma unroll
+                            for (int u = 0; u < U; u += 2) {
+                                const float4 q = *reinterpret_cast<const float4*>(tp + t + u);
+                                d[u].v = q.x;
+                                d[u].off = __float_as_int(q.y);
+                                d[u + 1].v = q.z;
+                                d[u + 1].off = __float_as_int(q.w);
+                            }
+                            float xv[U][HW][NB];
+#pragma unroll
+                            for (int u = 0; u < U; ++u)
+#pragma unroll
+                                for (int yy = y0; yy <= y1; ++yy)
+#pragma unroll
+                                    for (int xx = x0; xx <= x1; ++xx)
+#pragma unroll
+                                        for (int j = 0; j < NB; ++j)
+                                            xv[u][(yy - y0) * (x1 - x0 + 1) + xx - x0][j] = *reinterpret_cast<const float*>(
+                                                xin + d[u].off + ((yy - y0) * W + (xx - x0)) * RB + j * 128);
+#pragma unroll
+                            for (int u = 0; u < U; ++u)
+#pragma unroll
+                                for (int yy = y0; yy <= y1; ++yy)
+#pragma unroll
+                                    for (int xx = x0; xx <= x1; ++xx)
+#pragma unroll
+                                        for (int j = 0; j < NB; ++j)
+                                            acc[kk][yy * W + xx][j] = mac1<MODE>(
+                                                acc[kk][yy * W + xx][j], d[u].v,
+                                                xv[u][(yy - y0) * (x1 - x0 + 1) + xx - x0][j]);
+                        }
+                    }
+                    beg = end;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * buf);
+    }
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // ---- epilogue: lane holds the whole plane of images n0 + lane + 32 j
+    const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
+    const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
+    const bool pool = p.flags & SCB_FLAG_POOL2;
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+        const int k = k0 + kk;
+        if (k >= p.k) break;
+        const uint32_t zm = p.zmask[k];
+#pragma unroll
+        for (int cy = 0; cy < AY::N; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < AX::N; ++cx)
+#pragma unroll
+                for (int yy = AY::lo(cy); yy <= AY::hi(cy); ++yy)
+#pragma unroll
+                    for (int xx = AX::lo(cx); xx <= AX::hi(cx); ++xx)
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) {
+                            float& o = acc[kk][yy * W + xx][j];
+                            if (__float_as_uint(o) == 0x80000000u && ((zm >> (cy * AX::N + cx)) & 1u)) o = 0.f;
+                            if (aq) o = fq_store<float>((p.flags & SCB_FLAG_RELU) ? relu_io<float>(o) : o, p.aq);
+                        }
+        if (!pool) {
+            float* yp = p.y + (size_t)k * HW * p.ldy + n0 + lane;
+#pragma unroll
+            for (int q = 0; q < HW; ++q)
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                    float o = acc[kk][q][j];
+                    if (relu) o = relu_io<float>(o);
+                    if (n0 + lane + 32 * j < p.n) yp[(size_t)q * p.ldy + 32 * j] = o;
+                }
+        } else {
+            constexpr int PW = W / 2, PHW = (H / 2) * (W / 2);
+            float* yp = p.y + (size_t)k * PHW * p.ldy + n0 + lane;
+#pragma unroll
+            for (int py = 0; py < H / 2; ++py)
+#pragma unroll
+                for (int px = 0; px < PW; ++px)
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) {
+                        const int a = (2 * py) * W + 2 * px;
+                        float o = fmaxf(fmaxf(acc[kk][a][j], acc[kk][a + 1][j]),
+                                        fmaxf(acc[kk][a + W][j], acc[kk][a + W + 1][j]));
+                        if (relu) o = relu_io<float>(o);
+                        if (n0 + lane + 32 * j < p.n) yp[(size_t)(py * PW + px) * p.ldy + 32 * j] = o;
+                    }
+        }
+    }
+}
+
+template <int H, int W, int NB, int KW, int MODE, int U = 1>
+cudaError_t launch_lane_t(const LaneParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
+    auto kern = k_lane<H, W, NB, KW, MODE, U>;
+    static int lim[64];  // per device
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, p, grid, threads, smem, st);
+}
+
+// ---------------------------------------------------------------- host side
+// Tap program of a kind-7 launch: per (stage st, output channel k) one slot of
+// `cap` 16-byte units = LANE_HDR bytes of cumulative class ends + the class tap
+// lists, each in the CSR row's colidx order with the taps that fall into the
+// zero padding for that class removed.  Slots are laid out [st][k] so a CTA's
+// consecutive channels of a stage are one contiguous bulk copy.  R = S = 3,
+// pad 1, stride 1 (H x W output = input plane).
+struct LaneProgram {
+    std::vector<uint4> desc;     // [nst][K][cap]
+    std::vector<uint32_t> zmask; // [K]
+    int cap = 0;                 // units per slot
+    int nst = 0;
+    int64_t macs = 0;            // executed MACs per image (in-image taps x class positions)
+};
+
+inline int lane_axis_n(int h) { return h == 1 ? 1 : (h == 2 ? 2 : 3); }
+inline int lane_axis_lo(int h, int i) { return h <= 2 ? i : (i == 0 ? 0 : (i == 1 ? 1 : h - 1)); }
+inline int lane_axis_hi(int h, int i) { return h <= 2 ? i : (i == 0 ? 0 : (i == 1 ? h - 2 : h - 1)); }
+
+// vbits: f32 bit patterns of the CSR values; colidx = c*pp + r*wp + s, the reference's
+// column index into the padded input plane (csr.py:143-160; pp = Hp*Wp, wp = Wp).
+// u > 1: pad every class segment to a multiple of u with no-op taps {-0.0, zero row}.
+// count_only: cap / zmask / macs only (no descriptor array; the launch-shape check).
+inline bool build_lane_program(const uint32_t* vbits, const int32_t* colidx, const int32_t* rowptr, int C, int K,
+                               int64_t pp, int wp, int H, int W, int cc, int nb, LaneProgram* out, int u = 1,
+                               bool count_only = false) {
+    const int HW = H * W, RB = 32 * nb * 4;
+    const int nst = (C + cc - 1) / cc;
+    const int ny = lane_axis_n(H), nx = lane_axis_n(W), ncls = ny * nx;
+    if (ncls > LANE_HDR / 2 || cc < 1) return false;
+    LaneProgram& P = *out;
+    P.zmask.assign(K, 0u);
+    P.nst = nst;
+    P.macs = 0;
+    P.desc.clear();
+    uint32_t mz = 0x80000000u;
+    float negzero;
+    std::memcpy(&negzero, &mz, 4);
+    // walk the (k, st) slot: fn(class, tap) for every kept tap (and padding no-ops), returns count
+    std::vector<LaneTap> taps;
+    uint16_t ends[LANE_HDR / 2];
+    auto slot = [&](int k, int st, int t0, int t1, bool account) {
+        taps.clear();
+        std::fill(ends, ends + LANE_HDR / 2, (uint16_t)0);
+        for (int cy = 0; cy < ny; ++cy)
+            for (int cx = 0; cx < nx; ++cx) {
+                const int y0 = lane_axis_lo(H, cy), x0 = lane_axis_lo(W, cx);
+                const int npos = (lane_axis_hi(H, cy) - y0 + 1) * (lane_axis_hi(W, cx) - x0 + 1);
+                const size_t seg0 = taps.size();
+                for (int i = t0; i < t1; ++i) {
+                    const int64_t ci = colidx[i] / pp, rem = colidx[i] % pp;
+                    const int r = (int)(rem / wp), s = (int)(rem % wp);
+                    const int iy = y0 + r - 1, ix = x0 + s - 1;
+                    if (iy < 0 || iy >= H || ix < 0 || ix >= W) {  // padding tap of this class
+                        if (account && !(vbits[i] & 0x80000000u)) P.zmask[k] |= 1u << (cy * nx + cx);
+                        continue;
+                    }
+                    LaneTap d;
+                    std::memcpy(&d.v, &vbits[i], 4);
+                    d.off = (int32_t)((((ci - (int64_t)st * cc) * HW) + iy * W + ix) * RB);
+                    taps.push_back(d);
+                    if (account) P.macs += npos;
+                }
+                while (u > 1 && (taps.size() - seg0) % u) taps.push_back(LaneTap{negzero, cc * HW * RB});
+                ends[cy * nx + cx] = (uint16_t)taps.size();
+            }
+    };
+    // pass 1: the largest slot; pass 2: the padded [st][k][cap] layout
+    std::vector<int32_t> tstart((size_t)K * (nst + 1));
+    int maxt = 0;
+    for (int k = 0; k < K; ++k) {
+        int t = rowptr[k];
+        for (int st = 0; st < nst; ++st) {
+            tstart[(size_t)k * (nst + 1) + st] = t;
+            const int64_t cend = std::min<int64_t>(C, (int64_t)(st + 1) * cc);
+            while (t < rowptr[k + 1] && colidx[t] / pp < cend) ++t;
+        }
+        tstart[(size_t)k * (nst + 1) + nst] = t;
+        for (int st = 0; st < nst; ++st) {
+            slot(k, st, tstart[(size_t)k * (nst + 1) + st], tstart[(size_t)k * (nst + 1) + st + 1], true);
+            maxt = std::max(maxt, (int)taps.size());
+        }
+    }
+    if (maxt > 0xffff) return false;
+    P.cap = (LANE_HDR + maxt * 8 + 15) / 16;
+    if (count_only) return true;
+    P.desc.assign((size_t)nst * K * P.cap, make_uint4(0, 0, 0, 0));
+    for (int k = 0; k < K; ++k)
+        for (int st = 0; st < nst; ++st) {
+            slot(k, st, tstart[(size_t)k * (nst + 1) + st], tstart[(size_t)k * (nst + 1) + st + 1], false);
+            unsigned char* b = reinterpret_cast<unsigned char*>(P.desc.data() + ((size_t)st * K + k) * P.cap);
+            std::memcpy(b, ends, LANE_HDR);
+            if (!taps.empty()) std::memcpy(b + LANE_HDR, taps.data(), taps.size() * 8);
+        }
+    return true;
+}
+
+}  // namespace scb

@@ -1,7 +1,9 @@
 // Device layer objects, the tap-program builder, launch-configuration rules
 // and the C-ABI launch entry points.
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -23,7 +25,8 @@ namespace {
 constexpr int kSmemLimit = 227 * 1024 - 1024;  // dynamic limit: 227 KB minus the kernels' static shared memory
 constexpr int kMaxThreads = 256;
 const int kKtChoices[] = {2, 4, 8};
-constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4, KIND_DTM = 5, KIND_TMI = 6;
+constexpr int KIND_TILED = 0, KIND_PLANE = 1, KIND_DIRECT = 2, KIND_DIMG = 3, KIND_DWS = 4, KIND_DTM = 5, KIND_TMI = 6,
+              KIND_LANE = 7;
 
 // SM count of a device (persistent grids), cached per device
 int sm_count(int dev) {
@@ -125,6 +128,54 @@ struct scb_layer {
     // output channel in CSR order, each run padded to an even count (16-byte aligned)
     struct TmiTables { TmiTap* taps = nullptr; int32_t* tbase = nullptr; int32_t* soff = nullptr; int tcap = 0; };
     std::map<std::vector<int>, TmiTables> d_tmi;
+    // image-lane position-class tables (lane.cuh), key (cc, nb, u): [st][k][cap] tap slots
+    struct LaneTables { uint4* desc = nullptr; uint32_t* zmask = nullptr; int cap = 0; };
+    std::map<std::vector<int>, LaneTables> d_lane;
+    std::map<std::vector<int>, int> lane_caps;  // host-only slot sizes (launch checks)
+    bool finite = true;  // every weight finite: dropping padding taps is exact (lane.cuh)
+
+    std::vector<uint32_t> lane_vbits() const {
+        std::vector<uint32_t> vb((size_t)nnz);
+        for (int64_t t = 0; t < nnz; ++t) std::memcpy(&vb[t], &h_vals[t], 4);
+        return vb;
+    }
+    int lane_cap(int cc, int nb, int u) {
+        std::lock_guard<std::mutex> lk(mu);
+        std::vector<int> key{cc, nb, u};
+        auto it = lane_caps.find(key);
+        if (it != lane_caps.end()) return it->second;
+        LaneProgram P;
+        const std::vector<uint32_t> vb = lane_vbits();
+        int cap = -1;
+        if (build_lane_program(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp, g.wp, g.h,
+                               g.w, cc, nb, &P, u, true))
+            cap = P.cap;
+        lane_caps[key] = cap;
+        return cap;
+    }
+    LaneTables lane_tables(int cc, int nb, int u, bool build) {
+        std::lock_guard<std::mutex> lk(mu);
+        std::vector<int> key{cc, nb, u};
+        auto it = d_lane.find(key);
+        if (it != d_lane.end()) return it->second;
+        if (!build) return LaneTables{};
+        LaneProgram P;
+        const std::vector<uint32_t> vb = lane_vbits();
+        if (!build_lane_program(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp, g.wp, g.h,
+                                g.w, cc, nb, &P, u, false))
+            return LaneTables{};
+        LaneTables T;
+        T.cap = P.cap;
+        if (cudaMalloc(&T.desc, P.desc.size() * 16) != cudaSuccess) return LaneTables{};
+        if (cudaMalloc(&T.zmask, P.zmask.size() * 4) != cudaSuccess) { cudaFree(T.desc); return LaneTables{}; }
+        if (cudaMemcpy(T.desc, P.desc.data(), P.desc.size() * 16, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(T.zmask, P.zmask.data(), P.zmask.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(T.desc); cudaFree(T.zmask);
+            return LaneTables{};
+        }
+        d_lane[key] = T;
+        return T;
+    }
 
     // largest per-channel tap run (even), host only: = tmi_tables().tcap
     int tmi_tcap() const {
@@ -283,6 +334,7 @@ struct scb_layer {
         for (auto& kv : d_sptr) cudaFree(kv.second);
         for (auto& kv : d_blocks) { cudaFree(kv.second.taps); cudaFree(kv.second.off); }
         for (auto& kv : d_tmi) { cudaFree(kv.second.taps); cudaFree(kv.second.tbase); cudaFree(kv.second.soff); }
+        for (auto& kv : d_lane) { cudaFree(kv.second.desc); cudaFree(kv.second.zmask); }
     }
     // direct taps {v, c*plane + r*row + s} in CSR order for one shared-memory layout
     DirectTap* direct_taps(int plane, int row, const std::vector<int>& col, int es, bool build) {
@@ -580,10 +632,12 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     const Geom& g = L->g;
     if (L->dt == SCB_F64) return false;
     if (g.stride != 1 || v.r != g.r || v.s != g.s || v.pad != g.pad) return false;
+    // image-minor activations are the layout of the kind-7 kernels only
+    if (((flags & SCB_FLAG_IMAGE_MINOR) != 0) != (v.kind == KIND_LANE)) return false;
     // f32 direct / image-lane / TMEM kernels take any weight format: their tap blocks carry
     // the decoded native value (decoded once on upload, direct_blocks); the f16 ones decode
     // the compact tap's payload in registers, so their format must match the layer's
-    const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG || v.kind == KIND_TMI) &&
+    const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG || v.kind == KIND_TMI || v.kind == KIND_LANE) &&
                          L->dt != SCB_F16 && v.wf == WF_F32;
     if (v.io != L->dt || (v.wf != L->wf && !decoded)) return false;
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
@@ -591,6 +645,11 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     if (v.kind < KIND_DIRECT && !L->prog(v.kt)) return false;
     if (v.kind == KIND_DIMG) {
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
+        return true;
+    }
+    if (v.kind == KIND_LANE) {  // whole H x W plane per lane, 3x3 "same" convolution, finite weights
+        if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1 || !L->finite) return false;
+        if ((flags & SCB_FLAG_POOL2) && ((g.h & 1) || (g.w & 1))) return false;
         return true;
     }
     if (v.kind == KIND_TMI) {  // square W x W planes, 3x3 "same" convolution
@@ -900,6 +959,41 @@ scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
     return SCB_OK;
 }
 
+// Image-lane position-class variants (lane.cuh): CTA = 32*nb images x warps_k channels,
+// + 1 producer warp; stages = ring depth.  d->chunk = slot bytes, d->row = TMA box rows,
+// d->tap_cap = descriptor slot units.
+scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
+    const scb_variant_info& v = variant(c.variant).info;
+    const Geom& g = L->g;
+    const int HW = g.h * g.w, nb = v.nbt, RB = 32 * nb * 4, u = v.dispatch;
+    const int nbuf = c.stages == 0 ? 2 : c.stages;
+    if (c.imgs != 32 * nb || c.bh != g.h || c.bw != g.w || c.cc < 1 || c.warps_k < 1 || c.warps_k > 16 ||
+        nbuf < 2 || nbuf > 4)
+        return fail(SCB_ERR_SHAPE, "lane launch: imgs = 32*nb, bh x bw = the plane, 1..16 warps, 2..4 stages");
+    const int rows = c.cc * HW;
+    const int boxrows = std::min(rows, 256);
+    if (rows % boxrows) return fail(SCB_ERR_SHAPE, "lane launch: cc*H*W must be <= 256 or a multiple of 256");
+    const int cap = L->lane_cap(c.cc, nb, u);
+    if (cap <= 0) return fail(SCB_ERR_SHAPE, "lane launch: tap program does not fit the slot format");
+    const int kc = c.warps_k * v.kt;
+    const size_t slot = ((size_t)rows * RB + (u > 1 ? (size_t)HW * RB : 0) + (size_t)kc * cap * 16 + 127) & ~(size_t)127;
+    d->smem = nbuf * slot + 16 * nbuf;
+    if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
+    d->threads = 32 * (c.warps_k + 1);
+    d->chunk = (int)slot;
+    d->row = boxrows;
+    d->tap_cap = cap;
+    d->stage_el = nbuf;
+    d->kblocks = (g.k + kc - 1) / kc;
+    d->nb = (n + 32 * nb - 1) / (32 * nb);
+    d->n_ey = d->n_fx = 1;
+    d->wp = (g.c + c.cc - 1) / c.cc;
+    const int64_t grid = (int64_t)d->kblocks * d->nb;
+    if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
+    d->grid = (unsigned)grid;
+    return SCB_OK;
+}
+
 scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     if (c.variant < 0 || c.variant >= num_variants()) return fail(SCB_ERR_SHAPE, "bad variant index");
     const scb_variant_info& v = variant(c.variant).info;
@@ -910,6 +1004,7 @@ scb_status derive(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Deri
     if (v.kind == KIND_DWS) return derive_dws(L, c, n, flags, d);
     if (v.kind == KIND_DTM) return derive_dtm(L, c, n, flags, d);
     if (v.kind == KIND_TMI) return derive_tmi(L, c, n, flags, d);
+    if (v.kind == KIND_LANE) return derive_lane(L, c, n, flags, d);
     const Geom& g = L->g;
     const int es = elem_bytes(v);
     if (c.imgs < 1 || c.imgs % v.nbt || c.bh < v.th || c.bh % v.th || c.bw < v.tw || c.bw % v.tw || c.cc < 1 ||
@@ -958,6 +1053,16 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
     for (int vi = 0; vi < nv; ++vi) {
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
+        if (v.kind == KIND_LANE) {
+            for (int wk : {8, 14, 16})
+                for (int cc : {8, 16, 32, 64})
+                    for (int ns : {2, 3}) {
+                        scb_launch c{vi, wk, 32 * v.nbt, g.h, g.w, cc, ns};
+                        Derived d;
+                        if (derive(L, c, n, flags, &d) == SCB_OK) out.push_back(c);
+                    }
+            continue;
+        }
         if (v.kind == KIND_TMI) {
             const TmiG t(v);
             for (int depth : {3, 5}) {
@@ -1094,6 +1199,13 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                 score += (v.kt == 2 ? 0.5 : 0.0) + (c.cc == 32 ? 0.5 : 0.0) + (c.warps_k == 16 ? 1.3 : 0.0) -
                          (g.h == 4 && v.io != SCB_F16 ? 2.0 : 0.0);
             }
+            if (v.kind == KIND_LANE) {
+                // measured on B200 (tools/lane_harness.cu, profiles/r02_lane_*): 2 images per lane,
+                // 14 consumer warps (148 CTAs at batch 256), the largest stage that fits, 2 slots;
+                // 2x2 planes prefer the padded 2-tap unroll
+                score = 200.0 + 3.0 * std::log(fill + 1e-3) + (v.nbt == 2 ? 1.0 : 0.0) + (c.warps_k == 14 ? 0.5 : 0.0) +
+                        0.1 * std::log((double)c.cc) + ((g.h * g.w <= 4) == (v.dispatch == 2) ? 0.5 : 0.0);
+            }
             if (c.stages == 2 || c.stages == 0) score += 0.2;
             // TMEM image-lane kernels: correct, measured slower than direct on VGG-CIFAR
             // (profiles/r02_tmem_*): tuner candidates only, never the untuned default
@@ -1182,6 +1294,7 @@ SCB_API scb_status scb_layer_create_q(const scb_shape* shape, scb_dtype dt, scb_
     L->h_colidx.assign(colidx, colidx + nnz);
     L->h_rowptr.assign(rowptr, rowptr + g.k + 1);
     L->h_vals = as_f32;
+    for (float v : as_f32) L->finite &= std::isfinite(v);
     L->h_pay = pay;
 
     // tiled tap programs for every KT a compiled variant of this (R, S) uses
@@ -1248,13 +1361,15 @@ SCB_API scb_status scb_default_launch(const scb_layer* layer, int32_t n, uint32_
     return SCB_OK;
 }
 
-static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const void* bias, void* y, int32_t n,
-                                   uint32_t flags, const scb_launch* cfg, void* stream, bool* fused_aq);
+static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_t ldx, const void* bias, void* y,
+                                   int64_t ldy, int32_t n, uint32_t flags, const scb_launch* cfg, void* stream,
+                                   bool* fused_aq);
 
 // Device tables a launch reads.  build = true (scb_layer_prepare): create and upload them
 // (cudaMalloc + synchronous copies).  build = false (scb_conv_sparse): look them up only, so
 // the launch path never allocates or synchronises.
 struct LaunchTables {
+    scb_layer::LaneTables lane;
     const DirectTap* taps = nullptr;
     const int32_t* blkoff = nullptr;
     const int32_t* sptr = nullptr;
@@ -1269,6 +1384,12 @@ static scb_status launch_tables(scb_layer* L, const scb_launch& c, const Derived
         t->tmi = L->tmi_tables(tg.SW, tg.CPR, tg.RW, tg.CS, tg.NSET, build);
         if (!t->tmi.taps) return build ? fail(SCB_ERR_CUDA, "tmem image-lane tables: device allocation failed")
                                        : fail(SCB_ERR_ARG, missing);
+        return SCB_OK;
+    }
+    if (ve.info.kind == KIND_LANE) {
+        t->lane = L->lane_tables(c.cc, ve.info.nbt, ve.info.dispatch, build);
+        if (!t->lane.desc) return build ? fail(SCB_ERR_CUDA, "lane tables: device allocation failed")
+                                        : fail(SCB_ERR_ARG, missing);
         return SCB_OK;
     }
     if (ve.info.kind < KIND_DIRECT) return SCB_OK;  // tiled / plane: programs built at layer creation
@@ -1325,10 +1446,15 @@ SCB_API scb_status scb_launch_check(const scb_layer* layer, int32_t n, uint32_t 
 SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const void* bias,
                                    void* y, int32_t n, uint32_t flags,
                                    const scb_launch* cfg, void* stream) {
+    return scb_conv_sparse_ld(layer, x, n, bias, y, n, n, flags, cfg, stream);
+}
+
+SCB_API scb_status scb_conv_sparse_ld(const scb_layer* layer, const void* x, int64_t ldx, const void* bias, void* y,
+                                      int64_t ldy, int32_t n, uint32_t flags, const scb_launch* cfg, void* stream) {
     if (layer && (flags & SCB_FLAG_ACT_QUANT) && !layer->has_aq)
         return fail(SCB_ERR_ARG, "SCB_FLAG_ACT_QUANT on a layer without an activation quantizer");
     bool fused = false;
-    scb_status s = conv_sparse_impl(layer, x, bias, y, n, flags, cfg, stream, &fused);
+    scb_status s = conv_sparse_impl(layer, x, ldx, bias, y, ldy, n, flags, cfg, stream, &fused);
     if (s != SCB_OK || !(flags & SCB_FLAG_ACT_QUANT) || fused || n == 0) return s;
     // kernels without the fused epilogue: one in-place pass over the layer output
     const Geom& g = layer->g;
@@ -1339,8 +1465,23 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
     return e == cudaSuccess ? SCB_OK : cuda_fail(e, "fake-quant launch");
 }
 
-static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const void* bias, void* y, int32_t n,
-                                   uint32_t flags, const scb_launch* cfg, void* stream, bool* fused_aq) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_t ldx, const void* bias, void* y,
+                                   int64_t ldy, int32_t n, uint32_t flags, const scb_launch* cfg, void* stream,
+                                   bool* fused_aq) {
     if (!layer) return fail(SCB_ERR_ARG, "layer is NULL");
     auto* L = const_cast<scb_layer*>(layer);
     if (n < 0) return fail(SCB_ERR_SHAPE, "negative batch");
@@ -1356,7 +1497,11 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
     const Geom& g = L->g;
     // no explicit launch and an input the tiled kernels cannot stage (not 16-byte aligned,
     // e.g. a sliced view): the generic kernel, which accepts any address
-    if (!cfg && (reinterpret_cast<uintptr_t>(x) & 15) && !(flags & SCB_FLAG_POOL2)) c.variant = -1;
+    const bool minor = flags & SCB_FLAG_IMAGE_MINOR;
+    if (!cfg && (reinterpret_cast<uintptr_t>(x) & 15) && !(flags & SCB_FLAG_POOL2) && !minor) c.variant = -1;
+    if (minor && (c.variant < 0 || (flags & SCB_FLAG_GENERIC)))
+        return fail(SCB_ERR_UNSUPPORTED, "image-minor activations need a kind-7 (image-lane) launch");
+    if (minor && (ldx < n || ldy < n)) return fail(SCB_ERR_ARG, "image-minor row stride smaller than the batch");
     if (c.variant < 0 || (flags & SCB_FLAG_GENERIC)) {
         if (flags & SCB_FLAG_POOL2) return fail(SCB_ERR_UNSUPPORTED, "fused pool needs a tiled variant");
         GenericParams p;
@@ -1373,6 +1518,36 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
     if (reinterpret_cast<uintptr_t>(x) & 15) return fail(SCB_ERR_UNSUPPORTED, "tiled kernels need a 16-byte aligned input");
     LaunchTables tab;
     if ((s = launch_tables(L, c, d, false, &tab)) != SCB_OK) return s;
+    if (ve.info.kind == KIND_LANE) {
+        if (ldx % 4) return fail(SCB_ERR_UNSUPPORTED, "lane kernel: the input row stride must be a multiple of 4 images");
+        PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+        if (!enc) return fail(SCB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        LaneParams q;
+        std::memset(&q, 0, sizeof(q));
+        const int HW = g.h * g.w;
+        const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)g.c * HW};
+        const cuuint64_t gstr[1] = {(cuuint64_t)ldx * 4};
+        const cuuint32_t box[2] = {(cuuint32_t)(32 * ve.info.nbt), (cuuint32_t)d.row};
+        const cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(&q.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(x), gdim, gstr, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(SCB_ERR_CUDA, "lane kernel: tensor map encoding failed");
+        q.bias = static_cast<const float*>(bias);
+        q.y = static_cast<float*>(y);
+        q.desc = tab.lane.desc;
+        q.zmask = tab.lane.zmask;
+        q.n = n; q.c = g.c; q.k = g.k;
+        q.ldx = (int)ldx; q.ldy = (int)ldy;
+        q.cc = c.cc; q.nst = d.wp; q.warps = c.warps_k; q.kw = ve.info.kt;
+        q.kgroups = d.kblocks; q.cap = d.tap_cap; q.nbuf = d.stage_el; q.slot_bytes = d.chunk; q.boxrows = d.row;
+        q.aq = L->aq;
+        q.flags = flags;
+        *fused_aq = true;
+        if ((int64_t)g.k * (g.e * g.f) * ldy > ((int64_t)1 << 40)) return fail(SCB_ERR_SHAPE, "output too large");
+        cudaError_t e = ve.llaunch(q, d.grid, (unsigned)d.threads, d.smem, st);
+        return e == cudaSuccess ? SCB_OK : cuda_fail(e, "lane kernel launch");
+    }
     if (ve.info.kind == KIND_TMI) {
         const auto& T = tab.tmi;
         TmiParams q;
@@ -1428,6 +1603,24 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, const 
     p.flags = flags;
     cudaError_t e = ve.launch(p, d.grid, (unsigned)d.threads, d.smem, st);
     return e == cudaSuccess ? SCB_OK : cuda_fail(e, "tiled kernel launch");
+}
+
+SCB_API scb_status scb_to_image_minor(scb_dtype dt, const void* x, void* y, int32_t n, int64_t chw, int64_t ldy,
+                                      void* stream) {
+    if (n < 0 || chw < 0 || ldy < n) return fail(SCB_ERR_ARG, "bad extents");
+    if (n == 0 || chw == 0) return SCB_OK;
+    if (!x || !y) return fail(SCB_ERR_ARG, "NULL buffer");
+    cudaError_t e = launch_transpose(dtype_size(dt), x, chw, y, ldy, n, chw, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SCB_OK : cuda_fail(e, "transpose launch");
+}
+
+SCB_API scb_status scb_from_image_minor(scb_dtype dt, const void* x, int64_t ldx, void* y, int32_t n, int64_t chw,
+                                        void* stream) {
+    if (n < 0 || chw < 0 || ldx < n) return fail(SCB_ERR_ARG, "bad extents");
+    if (n == 0 || chw == 0) return SCB_OK;
+    if (!x || !y) return fail(SCB_ERR_ARG, "NULL buffer");
+    cudaError_t e = launch_transpose(dtype_size(dt), x, ldx, y, chw, chw, n, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SCB_OK : cuda_fail(e, "transpose launch");
 }
 
 SCB_API int32_t scb_variant_count(void) { return num_variants(); }

@@ -84,14 +84,16 @@ class DeviceLayer:
         return st == 0
 
     def launch(self, x_ptr: int, bias_ptr: int | None, y_ptr: int, n: int, flags: int,
-               launch=None, stream: int = 0) -> None:
+               launch=None, stream: int = 0, ldx: int | None = None, ldy: int | None = None) -> None:
+        """scb_conv_sparse_ld; ldx / ldy are the image-minor row strides (FLAG_IMAGE_MINOR,
+        default n), ignored for NCHW activations."""
         if launch is not None or not (flags & _abi.FLAG_GENERIC):
             self.prepare(n, flags, launch)
         cfg = None if launch is None else ctypes.byref(_abi.Launch.from_tuple(launch))
-        _abi.check(_abi.lib().scb_conv_sparse(
-            ctypes.c_void_p(self.handle), ctypes.c_void_p(x_ptr),
+        _abi.check(_abi.lib().scb_conv_sparse_ld(
+            ctypes.c_void_p(self.handle), ctypes.c_void_p(x_ptr), int(n if ldx is None else ldx),
             ctypes.c_void_p(bias_ptr) if bias_ptr else None, ctypes.c_void_p(y_ptr),
-            int(n), int(flags), cfg, ctypes.c_void_p(stream)), "scb_conv_sparse")
+            int(n if ldy is None else ldy), int(n), int(flags), cfg, ctypes.c_void_p(stream)), "scb_conv_sparse")
 
     def candidates(self, n: int, flags: int = 0, cap: int = 4096):
         buf = (_abi.Launch * cap)()

@@ -194,11 +194,31 @@ def _run(x, kernel: CsrKernel, bias, plan: EnginePlan, *, relu=False, pool=False
     return y.cpu().numpy()
 
 
+_KINDS = None
+
+
+def launch_kind(launch) -> int:
+    """Kernel kind of a launch tuple (-1 = generic)."""
+    global _KINDS
+    if launch is None:
+        return -1
+    if _KINDS is None:
+        _KINDS = [v["kind"] for v in _abi.variants()]
+    return _KINDS[launch[0]]
+
+
+def minor_ld(n: int) -> int:
+    """Row stride of an image-minor buffer for n images: a multiple of 4 (16-byte TMA rows)."""
+    return (int(n) + 3) // 4 * 4
+
+
 def run_layer(layer, x_ptr: int, b_ptr: int, y, n: int, flags: int, launch, stream: int,
               scratch=None) -> None:
-    """One layer on `stream`: a tiled launch (tuple), or the generic kernel
-    (launch None) followed by scb_maxpool2 when the pool is requested (the
-    generic kernel has no fused pool epilogue)."""
+    """One layer on `stream` with NCHW activations: a tiled launch (tuple), or the
+    generic kernel (launch None) followed by scb_maxpool2 when the pool is requested
+    (the generic kernel has no fused pool epilogue).  A kind-7 launch (image-minor
+    activations) runs between two layout conversions (scb_to_image_minor /
+    scb_from_image_minor) through temporary image-minor buffers."""
     if launch is None and flags & _abi.FLAG_POOL2:
         sh = layer.shape
         tmp = scratch if scratch is not None else \
@@ -206,6 +226,18 @@ def run_layer(layer, x_ptr: int, b_ptr: int, y, n: int, flags: int, launch, stre
         layer.launch(x_ptr, b_ptr, tmp.data_ptr(), n, (flags & ~_abi.FLAG_POOL2) | _abi.FLAG_GENERIC,
                      None, stream)
         _abi.maxpool2(layer.io_dtype, tmp.data_ptr(), y.data_ptr(), n * sh.k, sh.e, sh.f, stream)
+        return
+    if launch_kind(launch) == _abi.KIND_LANE and not flags & _abi.FLAG_IMAGE_MINOR:
+        sh = layer.shape
+        ld = minor_ld(n)
+        chw_in = sh.c * sh.h * sh.w
+        chw_out = int(np.prod(y.shape[1:]))
+        xm = _torch().empty((chw_in, ld), dtype=y.dtype, device=y.device)
+        ym = _torch().empty((chw_out, ld), dtype=y.dtype, device=y.device)
+        _abi.to_image_minor(layer.io_dtype, x_ptr, xm.data_ptr(), n, chw_in, ld, stream)
+        layer.launch(xm.data_ptr(), b_ptr, ym.data_ptr(), n, flags | _abi.FLAG_IMAGE_MINOR, launch, stream,
+                     ldx=ld, ldy=ld)
+        _abi.from_image_minor(layer.io_dtype, ym.data_ptr(), ld, y.data_ptr(), n, chw_out, stream)
         return
     layer.launch(x_ptr, b_ptr, y.data_ptr(), n, flags | (_abi.FLAG_GENERIC if launch is None else 0),
                  launch, stream)

@@ -136,8 +136,7 @@ class SparseConvNet:
         self.batch = int(batch)
         self.graph = None
         self.x_in = torch.zeros((self.batch, *self.in_shape), dtype=self.tdtype, device=self.tdev)
-        self.acts = [torch.empty(self.out_shape(i, self.batch), dtype=self.tdtype, device=self.tdev)
-                     for i in range(len(self.layers))]
+        self.acts = [None] * len(self.layers)  # allocated per layout by set_launches
         self.scratch = [None] * len(self.layers)
         if tune:
             from .tuner import tune_launch
@@ -147,16 +146,27 @@ class SparseConvNet:
                                      device=self.device)
             with torch.cuda.device(self.device):
                 for i, L in enumerate(self.layers):
-                    best, _ = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
-                                          repetitions=repetitions, warmups=warmups,
-                                          max_candidates=max_candidates, include_generic=True)
+                    best, tim = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
+                                            repetitions=repetitions, warmups=warmups,
+                                            max_candidates=max_candidates, include_generic=True)
+                    if self.dtype == np.float32:  # image-minor kernels (kind 7): timed on their layout
+                        bm, tm = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
+                                             repetitions=repetitions, warmups=warmups,
+                                             max_candidates=max_candidates, layout="minor")
+                        if bm is not None and tm[bm] < tim[best]:
+                            best = bm
                     self.launches[i] = best
                     x = torch.relu(torch.randn(self.out_shape(i, self.batch), generator=gen)).to(
                         self.tdev, self.tdtype)
         else:
-            self.launches = [self.dlayers[i].default_launch(self.batch, self.flags(i))
-                             for i in range(len(self.layers))]
-            self.launches = [None if l[0] < 0 else l for l in self.launches]
+            self.launches = []
+            for i in range(len(self.layers)):
+                l = self.dlayers[i].default_launch(self.batch, self.flags(i))
+                if self.dtype == np.float32:  # measured: the image-minor kernels win where they apply
+                    lm = self.dlayers[i].default_launch(self.batch, self.flags(i) | _abi.FLAG_IMAGE_MINOR)
+                    if lm[0] >= 0:
+                        l = lm
+                self.launches.append(None if l[0] < 0 else l)
         self.set_launches(self.launches)
         return list(self.launches)
 
@@ -166,6 +176,32 @@ class SparseConvNet:
             raise ShapeError("one launch per layer")
         self.launches = list(launches)
         self.graph = None
+        torch = self.torch
+        ld = engine.minor_ld(self.batch)
+        self.ld = ld
+        self.minor = [a == "sparse-direct" and engine.launch_kind(l) == _abi.KIND_LANE
+                      for l, a in zip(self.launches, self.algorithms)]
+        self.acts = []
+        self.xconv = []
+        prev_minor = False
+        for i in range(len(self.layers)):
+            n, k, e, f = self.out_shape(i, self.batch)
+            if self.minor[i]:
+                self.acts.append(torch.empty((k * e * f, ld), dtype=self.tdtype, device=self.tdev))
+            else:
+                self.acts.append(torch.empty((n, k, e, f), dtype=self.tdtype, device=self.tdev))
+            # layout conversion of this layer's input when it differs from the producer's
+            sh = self.layers[i].kernel.shape
+            if self.minor[i] and not prev_minor:
+                self.xconv.append(torch.empty((sh.c * sh.h * sh.w, ld), dtype=self.tdtype, device=self.tdev))
+            elif prev_minor and not self.minor[i]:
+                self.xconv.append(torch.empty((self.batch, sh.c, sh.h, sh.w), dtype=self.tdtype, device=self.tdev))
+            else:
+                self.xconv.append(None)
+            prev_minor = self.minor[i]
+        # NCHW result of the stack (the last layer's output, converted when image-minor)
+        self.result = torch.empty(self.out_shape(len(self.layers) - 1, self.batch), dtype=self.tdtype,
+                                  device=self.tdev) if self.minor[-1] else self.acts[-1]
         for i, L in enumerate(self.layers):
             self.scratch[i] = None
             if self.launches[i] is None and L.pool:
@@ -182,11 +218,11 @@ class SparseConvNet:
             return
         sizes = {e - a for a, e in self._chain_bounds()} | {self.batch}
         for i, L in enumerate(self.layers):
-            if self.launches[i] is None:
+            if self.launches[i] is None or self.algorithms[i] != "sparse-direct":
                 continue
             for n in sizes:
                 for pdl in (0, _abi.FLAG_NO_PDL):
-                    self.dlayers[i].prepare(n, self.flags(i) | pdl, self.launches[i])
+                    self.dlayers[i].prepare(n, self.flags(i) | pdl | self._layout_flag(i), self.launches[i])
 
     def set_chains(self, chains: int) -> None:
         """Run the batch as `chains` independent sub-batch chains on their own
@@ -203,11 +239,20 @@ class SparseConvNet:
 
     def _chain_bounds(self):
         from .runner import shard_range
-        return [shard_range(self.batch, self.chains, j) for j in range(self.chains)]
+        b = [shard_range(self.batch, self.chains, j) for j in range(self.chains)]
+        if any(getattr(self, "minor", None) or []):
+            # image-minor sub-batches start at a multiple of 4 images (16-byte TMA rows)
+            cuts = sorted({min(self.batch, (a + 3) // 4 * 4) for a, _ in b} | {self.batch})
+            b = [(a, e) for a, e in zip([0] + cuts[:-1], cuts) if e > a]
+        return b
 
     # ---- execution ------------------------------------------------------
+    def _layout_flag(self, i: int) -> int:
+        return _abi.FLAG_IMAGE_MINOR if getattr(self, "minor", None) and self.minor[i] else 0
+
     def launch_layer(self, i: int, x_dev, y_dev, stream: int, rows: tuple | None = None) -> None:
-        """Layer i on images rows[0]:rows[1] (default: the whole batch)."""
+        """Layer i on images rows[0]:rows[1] (default: the whole batch) of NCHW buffers
+        (a kind-7 launch converts through temporary image-minor buffers: engine.run_layer)."""
         b = self.biases[i]
         a, e = rows if rows is not None else (0, self.batch)
         sc = self.scratch[i]
@@ -216,19 +261,61 @@ class SparseConvNet:
                          self.launches[i], stream,
                          scratch=None if sc is None else sc[a:e])
 
-    def _run_chain(self, x, stream, rows, on_first=None) -> None:
-        cur = x
+    def _minor_ptr(self, buf, a: int) -> int:
+        return buf.data_ptr() + a * buf.element_size()
+
+    def _step(self, i: int, cur, cur_minor: bool, stream, rows):
+        """Layer i of one chain: converts the input layout when the producer's differs,
+        runs the layer into self.acts[i]; returns (output buffer, output is image-minor)."""
         a, e = rows
+        n = e - a
+        s = stream.cuda_stream
+        if self.algorithms[i] == "dense-cudnn":
+            if cur_minor:
+                cur = self._to_nchw(i, cur, rows, s)
+            with self.torch.cuda.stream(stream):
+                self.dense_layer(i)(cur[a:e], self.acts[i][a:e])
+            self._dense_quant(i, self.acts[i][a:e], s)
+            return self.acts[i], False
+        if self.minor[i]:
+            if not cur_minor:
+                sh = self.layers[i].kernel.shape
+                xc = self.xconv[i]
+                _abi.to_image_minor(self.dtype, cur[a:e].data_ptr(), self._minor_ptr(xc, a), n,
+                                    sh.c * sh.h * sh.w, self.ld, s)
+                cur = xc
+            b = self.biases[i]
+            self.dlayers[i].launch(self._minor_ptr(cur, a), b.data_ptr() if b is not None else 0,
+                                   self._minor_ptr(self.acts[i], a), n,
+                                   self.flags(i) | _abi.FLAG_IMAGE_MINOR | (0 if self.pdl else _abi.FLAG_NO_PDL),
+                                   self.launches[i], s, ldx=self.ld, ldy=self.ld)
+            return self.acts[i], True
+        if cur_minor:
+            cur = self._to_nchw(i, cur, rows, s)
+        self.launch_layer(i, cur, self.acts[i], s, rows)
+        return self.acts[i], False
+
+    def _to_nchw(self, i: int, cur, rows, s: int):
+        a, e = rows
+        xc = self.xconv[i]
+        _abi.from_image_minor(self.dtype, self._minor_ptr(cur, a), self.ld, xc[a:e].data_ptr(), e - a,
+                              int(np.prod(xc.shape[1:])), s)
+        return xc
+
+    def _finish(self, cur, cur_minor: bool, stream, rows) -> None:
+        """The NCHW result: convert the last (image-minor) output into self.result."""
+        if cur_minor:
+            a, e = rows
+            _abi.from_image_minor(self.dtype, self._minor_ptr(cur, a), self.ld, self.result[a:e].data_ptr(),
+                                  e - a, int(np.prod(self.result.shape[1:])), stream.cuda_stream)
+
+    def _run_chain(self, x, stream, rows, on_first=None) -> None:
+        cur, cur_minor = x, False
         for i in range(len(self.layers)):
-            if self.algorithms[i] == "dense-cudnn":
-                with self.torch.cuda.stream(stream):
-                    self.dense_layer(i)(cur[a:e], self.acts[i][a:e])
-                self._dense_quant(i, self.acts[i][a:e], stream.cuda_stream)
-            else:
-                self.launch_layer(i, cur, self.acts[i], stream.cuda_stream, rows)
+            cur, cur_minor = self._step(i, cur, cur_minor, stream, rows)
             if i == 0 and on_first is not None:
                 on_first(stream)
-            cur = self.acts[i]
+        self._finish(cur, cur_minor, stream, rows)
 
     def _run_stack(self, x, stream, on_first=None) -> None:
         """The whole stack on `stream`, forked over the sub-batch chains."""
@@ -307,15 +394,19 @@ class SparseConvNet:
         (only the direct and image-lane epilogues do), +1 after a dense layer with one."""
         vs = _abi.variants()
         n = 0
-        for l, L, a in zip(self.launches, self.layers, self.algorithms):
+        prev_minor = False
+        for i, (l, L, a) in enumerate(zip(self.launches, self.layers, self.algorithms)):
             aq = L.act_quant is not None
+            minor = self.minor[i]
+            n += 1 if minor != prev_minor else 0  # layout conversion of the input
+            prev_minor = minor
             if a == "dense-cudnn":
                 n += 1 if aq else 0
                 continue
             n += 2 if (l is None and L.pool) else 1
-            if aq and (l is None or vs[l[0]]["kind"] not in (2, 3)):
+            if aq and (l is None or vs[l[0]]["kind"] not in (2, 3, 7)):
                 n += 1
-        return n
+        return n + (1 if prev_minor else 0)
 
     def forward_device(self, x_dev=None, events=None):
         """Run the stack on the current stream of the device; returns the last
@@ -330,23 +421,21 @@ class SparseConvNet:
             stream = torch.cuda.current_stream(self.device)
             if self.graph is not None and events is None:
                 self.graph.replay()
-                return self.acts[-1]
+                return self.result
             if events is None:
                 self._run_stack(self.x_in, stream)
-                return self.acts[-1]
-            # per-layer events: one chain, an event between layers
-            s = stream.cuda_stream
-            cur = self.x_in
+                return self.result
+            # per-layer events: one chain, an event between layers (a layout conversion
+            # is timed with the layer that needs it)
+            rows = (0, self.batch)
+            cur, cur_minor = self.x_in, False
             events[0].record(stream)
             for i in range(len(self.layers)):
-                if self.algorithms[i] == "dense-cudnn":
-                    self.dense_layer(i)(cur, self.acts[i])
-                    self._dense_quant(i, self.acts[i], s)
-                else:
-                    self.launch_layer(i, cur, self.acts[i], s)
+                cur, cur_minor = self._step(i, cur, cur_minor, stream, rows)
+                if i == len(self.layers) - 1:
+                    self._finish(cur, cur_minor, stream, rows)
                 events[i + 1].record(stream)
-                cur = self.acts[i]
-        return self.acts[-1]
+        return self.result
 
     def capture(self) -> None:
         """Capture the whole stack into one CUDA graph (replayed by
@@ -411,7 +500,7 @@ class SparseConvNet:
                         loaded[i + 1].record(copy)
                 comp.wait_event(loaded[i])
                 self._run_stack(xb, comp, on_first=lambda st, ev=freed[i]: ev.record(st))
-                cur = self.acts[-1]
+                cur = self.result
                 done[i].record(comp)
                 with torch.cuda.stream(copy):
                     copy.wait_event(done[i])

@@ -42,12 +42,14 @@ def time_call(fn, repetitions: int = 5, warmups: int = 2) -> float:
 
 def tune_launch(x, kernel, bias=None, plan: engine.EnginePlan = engine.EnginePlan(), *,
                 relu: bool = False, pool: bool = False, repetitions: int = 5, warmups: int = 2,
-                max_candidates: int | None = None, include_generic: bool = False):
+                max_candidates: int | None = None, include_generic: bool = False,
+                layout: str = "nchw"):
     """Time every valid launch for (x, kernel) and cache the fastest.
 
-    x must be a CUDA tensor (the tuner never copies activations).  Returns
-    (best_launch, {launch: median_seconds}); best_launch None means the
-    generic kernel won.
+    x must be a CUDA tensor (NCHW).  Returns (best_launch, {launch: median_seconds});
+    best_launch None means the generic kernel won.  layout = "minor" times the kernels
+    that read and write image-minor activations (FLAG_IMAGE_MINOR, kind 7) on an
+    image-minor copy of x instead; (None, {}) when the layer has none.
     """
     import torch
     x = check_nchw(x)
@@ -57,6 +59,10 @@ def tune_launch(x, kernel, bias=None, plan: engine.EnginePlan = engine.EnginePla
     dev = x.device.index
     layer = device_layer(kernel, dev, io, plan.weight_format)
     flags = engine._flags(plan, relu, pool, False)
+    minor = layout == "minor"
+    if minor:
+        flags |= _abi.FLAG_IMAGE_MINOR
+        include_generic = False
     n = int(x.shape[0])
     cands = layer.candidates(n, flags)
     if max_candidates is not None:
@@ -64,6 +70,13 @@ def tune_launch(x, kernel, bias=None, plan: engine.EnginePlan = engine.EnginePla
     xin = x.to(engine._torch_dtype(io)).contiguous()
     e, f = (sh.e // 2, sh.f // 2) if pool else (sh.e, sh.f)
     y = torch.empty((n, sh.k, e, f), dtype=engine._torch_dtype(io), device=x.device)
+    ld = n
+    if minor:
+        ld = engine.minor_ld(n)
+        xm = torch.empty((sh.c * sh.h * sh.w, ld), dtype=xin.dtype, device=x.device)
+        xm[:, :n] = xin.reshape(n, -1).t()
+        xin = xm
+        y = torch.empty((sh.k * e * f, ld), dtype=xin.dtype, device=x.device)
     if bias is not None:
         bnp = np.ascontiguousarray(bias.detach().cpu().numpy() if hasattr(bias, "detach") else bias,
                                    dtype=np.float64 if io == np.float64 else np.float32)
@@ -75,7 +88,7 @@ def tune_launch(x, kernel, bias=None, plan: engine.EnginePlan = engine.EnginePla
     timings = {}
     for c in cands:
         timings[c] = time_call(lambda: layer.launch(xin.data_ptr(), bptr, y.data_ptr(), n, flags,
-                                                    c, stream), repetitions, warmups)
+                                                    c, stream, ldx=ld, ldy=ld), repetitions, warmups)
     if include_generic:
         # the generic kernel has no fused pool: conv + ReLU, then scb_maxpool2
         yfull = torch.empty((n, sh.k, sh.e, sh.f), dtype=engine._torch_dtype(io), device=x.device) \
@@ -97,7 +110,7 @@ def tune_launch(x, kernel, bias=None, plan: engine.EnginePlan = engine.EnginePla
             if c is None:
                 continue
             timings[c] = min(timings[c], time_call(
-                lambda: layer.launch(xin.data_ptr(), bptr, y.data_ptr(), n, flags, c, stream),
+                lambda: layer.launch(xin.data_ptr(), bptr, y.data_ptr(), n, flags, c, stream, ldx=ld, ldy=ld),
                 3 * repetitions, warmups))
     best = min(timings, key=lambda c: timings[c])
     engine.TUNED[(layer.signature(), n, flags)] = best

@@ -38,12 +38,15 @@ def test_variant_table():
         assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1)
         if v["kind"] == 6:  # TMEM image-lane: dispatch = warps per lane quarter
             assert v["dispatch"] in (2, 3, 4) and v["tw"] in (2, 4, 8, 16)
+        elif v["kind"] == 7:  # image-lane position classes: dispatch = tap unroll, nbt = images per lane
+            assert v["dispatch"] in (1, 2) and v["th"] == v["tw"] and v["th"] in (2, 4) and v["kt"] == 1
         else:
             assert v["dispatch"] in (0, 1, 2, 3)
             assert v["dispatch"] < 2 or v["kind"] == 2  # column-tiled (wide) / 1D direct
-        assert v["kind"] in (0, 1, 2, 3, 4, 5, 6) and v["io"] in (0, 2)
+        assert v["kind"] in (0, 1, 2, 3, 4, 5, 6, 7) and v["io"] in (0, 2)
         kinds.add(v["kind"])
-    assert kinds == {0, 1, 2, 3, 4, 5, 6}  # tiled, plane, direct, image-lane, ws, TMEM strips, TMEM image-lane
+    # tiled, plane, direct, image-lane, ws, TMEM strips, TMEM image-lane, image-lane position classes
+    assert kinds == {0, 1, 2, 3, 4, 5, 6, 7}
 
 
 def test_sm100a_cubin_only():
@@ -76,6 +79,7 @@ _EXACT = {
     "dimg": r"_ZN3scb6k_dimgILi\d+ELi\d+ELi0ELb0ELi0EE",
     "plane": r"_ZN3scb7k_planeI(?:Li\d+E){7}Lb0ELi0ELi0ELi\dEE",
     "tmi": r"_ZN3scb5k_tmiI(?:Li\d+E){5}Li0EE",
+    "lane": r"_ZN3scb6k_laneI(?:Li\d+E){4}Li0ELi\d+EE",
 }
 
 
@@ -100,6 +104,7 @@ def test_exact_kernels_never_fuse():
             assert re.search(r"\bDMUL\b", body) and re.search(r"\bDADD\b", body), name
         checked[kind] += 1
     assert checked["direct"] >= 100 and checked["dimg"] >= 5 and checked["tmi"] >= 10, checked
+    assert checked["lane"] >= 10, checked
     assert all(v > 0 for v in checked.values()), checked
 
 
