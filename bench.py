@@ -639,8 +639,8 @@ def load_smem_pipe():
     """Per-layer shared-memory pipe utilisation (l1tex throughput % of peak, the kernels'
     real ceiling) from the committed ncu --set full stack summary, layers in order."""
     import csv
-    caps = sorted((ROOT / "profiles").glob("r01_ncu_full_stack_v*.csv"),
-                  key=lambda q: int(q.stem.rsplit("_v", 1)[1]))
+    caps = sorted((ROOT / "profiles").glob("r0*_ncu_full_stack_v*.csv"),
+                  key=lambda q: (q.stem[:3], int(q.stem.rsplit("_v", 1)[1])))
     if not caps:
         return {}, None
     rows = list(csv.reader(caps[-1].open()))
@@ -648,7 +648,9 @@ def load_smem_pipe():
     col = "l1tex__throughput.avg.pct_of_peak_sustained_active"
     if col not in h:
         return {}, None
-    vals = [float(r[h.index(col)]) for r in rows[2:] if len(r) > h.index(col)]
+    kn = h.index("Kernel Name") if "Kernel Name" in h else None
+    vals = [float(r[h.index(col)]) for r in rows[2:]
+            if len(r) > h.index(col) and (kn is None or "k_transpose" not in r[kn])]
     from paper_2011_06295_b200.synth import VGG16_CIFAR_LAYERS
     names = [n for n, *_ in VGG16_CIFAR_LAYERS]
     return dict(zip(names, vals)), f"profiles/{caps[-1].name}"

@@ -498,7 +498,7 @@ def main():
                 if v[0] == "lane":  # info: kt = KW, nbt = NB, th = H, tw = W, dispatch = U
                     _, H, NB, KW, U, mode = v
                     ents.append(f"    {{{{3, 3, {KW}, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {U}, 1, "
-                                f"{KIND_LANE}}}, nullptr, nullptr, 544, nullptr, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, {288 if H >= 8 else 544}, nullptr, "
                                 f"&launch_lane_t<{H}, {H}, {NB}, {KW}, {mode}, {U}>}},\n")
                     continue
                 if v[0] == "tmi":  # info: kt = KW, nbt = J, th = TE, tw = W, dispatch = WQ

@@ -94,8 +94,46 @@ struct alignas(64) LaneParams {
 // U > 1: every class segment is padded by the host to a multiple of U taps with
 // no-op taps {v = -0.0, input = a zero row} (-0 * +0 = -0 and o + (-0) = o for
 // every o, so exact), and the tap loop runs U taps per iteration with no remainder.
+// NB consecutive floats (a lane's images) from shared memory in one vector load
+template <int NB>
+__device__ __forceinline__ void lds_nb(const unsigned char* p, float (&v)[NB]) {
+    if constexpr (NB == 1) {
+        v[0] = *reinterpret_cast<const float*>(p);
+    } else if constexpr (NB == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        static_assert(NB == 4, "images per lane");
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+}
+
+// store a lane's NB consecutive images (nvalid of them exist), one vector store when allowed
+template <int NB>
+__device__ __forceinline__ void store_nb(float* y, const float (&o)[NB], int nvalid, bool vec) {
+    if constexpr (NB == 2) {
+        if (vec && nvalid >= 2) { *reinterpret_cast<float2*>(y) = make_float2(o[0], o[1]); return; }
+    } else if constexpr (NB == 4) {
+        if (vec && nvalid >= 4) { *reinterpret_cast<float4*>(y) = make_float4(o[0], o[1], o[2], o[3]); return; }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+        if (j < nvalid) y[j] = o[j];
+}
+
+// thread limit: 16 consumer warps + the producer; 8 + 1 for 8x8 planes (64 accumulators per lane)
+template <int H, int W>
+constexpr int lane_max_threads() { return H * W >= 64 ? 288 : 544; }
+// largest position set a tap's loads cover at once (bigger classes run in row chunks)
+constexpr int LANE_PMAX = 16;
+#ifndef LANE_UNROLL
+#define LANE_UNROLL 1
+#endif
+constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernels
+
 template <int H, int W, int NB, int KW, int MODE, int U = 1>
-__global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LaneParams p) {
+__global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __grid_constant__ LaneParams p) {
     constexpr int HW = H * W;
     constexpr int BI = 32 * NB;   // images per CTA
     constexpr int RB = BI * 4;    // bytes of one (channel, position) row in shared memory
@@ -172,13 +210,16 @@ __global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LanePar
         const int buf = st % NBUF;
         mbar_wait(full0 + 8 * buf, (st / NBUF) & 1);
         const unsigned char* slot = smem + (size_t)buf * p.slot_bytes;
-        const unsigned char* xin = slot + lane * 4;
+        const unsigned char* xin = slot + lane * 4 * NB;  // lane's images n0 + NB*lane + j
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             if (k0 + kk >= p.k) break;
             const unsigned char* ch = slot + d_bytes + (size_t)(warp * KW + kk) * p.cap * 16;
-            const unsigned short* hd = reinterpret_cast<const unsigned short*>(ch);
+            unsigned short hd[LANE_HDR / 2];  // cumulative class ends, two 16-byte loads
+            *reinterpret_cast<uint4*>(hd) = *reinterpret_cast<const uint4*>(ch);
+            *reinterpret_cast<uint4*>(hd + 8) = *reinterpret_cast<const uint4*>(ch + 16);
             const LaneTap* tp = reinterpret_cast<const LaneTap*>(ch + LANE_HDR);
+            LaneTap dn = tp[0];  // running prefetch over the slot's contiguous class lists
             int beg = 0;
 #pragma unroll
             for (int cy = 0; cy < AY::N; ++cy) {
@@ -187,20 +228,32 @@ __global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LanePar
                     const int y0 = AY::lo(cy), y1 = AY::hi(cy), x0 = AX::lo(cx), x1 = AX::hi(cx);
                     const int end = hd[cy * AX::N + cx];
                     if constexpr (U == 1) {
-#pragma unroll 2
-                        for (int t = beg; t < end; ++t) {
-                            const LaneTap d = tp[t];
-                            const unsigned char* xa = xin + d.off;
+                        const int rc = LANE_PMAX / (x1 - x0 + 1) > 0 ? LANE_PMAX / (x1 - x0 + 1) : 1;  // rows per chunk
 #pragma unroll
-                            for (int yy = y0; yy <= y1; ++yy)
+                        for (int ya = y0; ya <= y1; ya += rc) {
+                            const int yb = ya + rc - 1 < y1 ? ya + rc - 1 : y1;
+                            LaneTap dq = ya == y0 ? dn : tp[beg];
+#pragma unroll kLaneUnroll
+                            for (int t = beg; t < end; ++t) {
+                                const LaneTap d = dq;
+                                dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
+                                const unsigned char* xa = xin + d.off;
+                                float xv[HW][NB];
 #pragma unroll
-                                for (int xx = x0; xx <= x1; ++xx)
+                                for (int yy = ya; yy <= yb; ++yy)
 #pragma unroll
-                                    for (int j = 0; j < NB; ++j) {
-                                        const float xv = *reinterpret_cast<const float*>(
-                                            xa + ((yy - y0) * W + (xx - x0)) * RB + j * 128);
-                                        acc[kk][yy * W + xx][j] = mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv);
-                                    }
+                                    for (int xx = x0; xx <= x1; ++xx)
+                                        lds_nb<NB>(xa + ((yy - y0) * W + (xx - x0)) * RB, xv[(yy - y0) * W + xx - x0]);
+#pragma unroll
+                                for (int yy = ya; yy <= yb; ++yy)
+#pragma unroll
+                                    for (int xx = x0; xx <= x1; ++xx)
+#pragma unroll
+                                        for (int j = 0; j < NB; ++j)
+                                            acc[kk][yy * W + xx][j] =
+                                                mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv[(yy - y0) * W + xx - x0][j]);
+                            }
+                            if (ya + rc > y1) dn = dq;  // = tp[end]: the next class's first tap
                         }
                     } else {
                         for (int t = beg; t < end; t += U) {
@@ -220,10 +273,8 @@ __global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LanePar
                                 for (int yy = y0; yy <= y1; ++yy)
 #pragma unroll
                                     for (int xx = x0; xx <= x1; ++xx)
-#pragma unroll
-                                        for (int j = 0; j < NB; ++j)
-                                            xv[u][(yy - y0) * (x1 - x0 + 1) + xx - x0][j] = *reinterpret_cast<const float*>(
-                                                xin + d[u].off + ((yy - y0) * W + (xx - x0)) * RB + j * 128);
+                                        lds_nb<NB>(xin + d[u].off + ((yy - y0) * W + (xx - x0)) * RB,
+                                                   xv[u][(yy - y0) * W + xx - x0]);
 #pragma unroll
                             for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -233,8 +284,7 @@ __global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LanePar
 #pragma unroll
                                         for (int j = 0; j < NB; ++j)
                                             acc[kk][yy * W + xx][j] = mac1<MODE>(
-                                                acc[kk][yy * W + xx][j], d[u].v,
-                                                xv[u][(yy - y0) * (x1 - x0 + 1) + xx - x0][j]);
+                                                acc[kk][yy * W + xx][j], d[u].v, xv[u][(yy - y0) * W + xx - x0][j]);
                         }
                     }
                     beg = end;
@@ -250,6 +300,8 @@ __global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LanePar
     const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
     const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
     const bool pool = p.flags & SCB_FLAG_POOL2;
+    // vector stores when every row start is NB-float aligned (row stride and base)
+    const bool vec = (p.ldy % NB) == 0 && (reinterpret_cast<uintptr_t>(p.y) % (4 * NB)) == 0;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -270,30 +322,31 @@ __global__ void __launch_bounds__(544, 1) k_lane(const __grid_constant__ LanePar
                             if (aq) o = fq_store<float>((p.flags & SCB_FLAG_RELU) ? relu_io<float>(o) : o, p.aq);
                         }
         if (!pool) {
-            float* yp = p.y + (size_t)k * HW * p.ldy + n0 + lane;
+            float* yp = p.y + (size_t)k * HW * p.ldy + n0 + NB * lane;
 #pragma unroll
-            for (int q = 0; q < HW; ++q)
+            for (int q = 0; q < HW; ++q) {
+                float o[NB];
 #pragma unroll
-                for (int j = 0; j < NB; ++j) {
-                    float o = acc[kk][q][j];
-                    if (relu) o = relu_io<float>(o);
-                    if (n0 + lane + 32 * j < p.n) yp[(size_t)q * p.ldy + 32 * j] = o;
-                }
+                for (int j = 0; j < NB; ++j) o[j] = relu ? relu_io<float>(acc[kk][q][j]) : acc[kk][q][j];
+                store_nb<NB>(yp + (size_t)q * p.ldy, o, p.n - (n0 + NB * lane), vec);
+            }
         } else {
             constexpr int PW = W / 2, PHW = (H / 2) * (W / 2);
-            float* yp = p.y + (size_t)k * PHW * p.ldy + n0 + lane;
+            float* yp = p.y + (size_t)k * PHW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int py = 0; py < H / 2; ++py)
 #pragma unroll
-                for (int px = 0; px < PW; ++px)
+                for (int px = 0; px < PW; ++px) {
+                    float o[NB];
 #pragma unroll
                     for (int j = 0; j < NB; ++j) {
                         const int a = (2 * py) * W + 2 * px;
-                        float o = fmaxf(fmaxf(acc[kk][a][j], acc[kk][a + 1][j]),
-                                        fmaxf(acc[kk][a + W][j], acc[kk][a + W + 1][j]));
-                        if (relu) o = relu_io<float>(o);
-                        if (n0 + lane + 32 * j < p.n) yp[(size_t)(py * PW + px) * p.ldy + 32 * j] = o;
+                        o[j] = fmaxf(fmaxf(acc[kk][a][j], acc[kk][a + 1][j]),
+                                     fmaxf(acc[kk][a + W][j], acc[kk][a + W + 1][j]));
+                        if (relu) o[j] = relu_io<float>(o[j]);
                     }
+                    store_nb<NB>(yp + (size_t)(py * PW + px) * p.ldy, o, p.n - (n0 + NB * lane), vec);
+                }
         }
     }
 }

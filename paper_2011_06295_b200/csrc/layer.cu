@@ -967,9 +967,11 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const Geom& g = L->g;
     const int HW = g.h * g.w, nb = v.nbt, RB = 32 * nb * 4, u = v.dispatch;
     const int nbuf = c.stages == 0 ? 2 : c.stages;
-    if (c.imgs != 32 * nb || c.bh != g.h || c.bw != g.w || c.cc < 1 || c.warps_k < 1 || c.warps_k > 16 ||
+    const int maxw = variant(c.variant).max_threads / 32 - 1;
+    if (c.imgs != 32 * nb || c.bh != g.h || c.bw != g.w || c.cc < 1 || c.warps_k < 1 || c.warps_k > maxw ||
         nbuf < 2 || nbuf > 4)
-        return fail(SCB_ERR_SHAPE, "lane launch: imgs = 32*nb, bh x bw = the plane, 1..16 warps, 2..4 stages");
+        return fail(SCB_ERR_SHAPE, "lane launch: imgs = 32*nb, bh x bw = the plane, warps within the kernel's limit, "
+                                   "2..4 stages");
     const int rows = c.cc * HW;
     const int boxrows = std::min(rows, 256);
     if (rows % boxrows) return fail(SCB_ERR_SHAPE, "lane launch: cc*H*W must be <= 256 or a multiple of 256");
@@ -1054,8 +1056,8 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
         if (v.kind == KIND_LANE) {
-            for (int wk : {8, 14, 16})
-                for (int cc : {8, 16, 32, 64})
+            for (int wk : {4, 8, 14, 16})
+                for (int cc : {4, 8, 12, 16, 32, 48, 64})
                     for (int ns : {2, 3}) {
                         scb_launch c{vi, wk, 32 * v.nbt, g.h, g.w, cc, ns};
                         Derived d;

@@ -29,8 +29,9 @@ cudaError_t launch(const LaneParams& p, unsigned grid, unsigned thr, size_t smem
 
 static cudaError_t dispatch(int H, int nb, int kw, const LaneParams& p, unsigned grid, unsigned thr, size_t smem) {
 #define D(h, b, w) if (H == h && nb == b && kw == w) return launch<h, b, w>(p, grid, thr, smem);
-    D(4, 1, 1) D(4, 2, 1)
+    D(4, 1, 1) D(4, 2, 1) D(4, 4, 1)
     D(2, 2, 1) D(2, 4, 1)
+    D(8, 1, 1)
 #undef D
     return cudaErrorInvalidValue;
 }
@@ -102,7 +103,7 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {1, 2, 4}, kws[] = {1}, wks[] = {8, 14, 16}, ccs[] = {8, 16, 32, 64}, nbufs[] = {2, 3}, us[] = {1, 2, 4};
+    const int nbs[] = {1, 2, 4}, kws[] = {1}, wks[] = {7, 8, 14, 16}, ccs[] = {4, 8, 12, 16, 32, 48, 64}, nbufs[] = {2, 3}, us[] = {1};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -111,7 +112,7 @@ int main(int argc, char** argv) {
     const bool one = argc > 11;
     for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
         if (one && (nb != atoi(argv[6]) || kw != atoi(argv[7]) || cc != atoi(argv[9]) || u != atoi(argv[11]))) continue;
-        if ((H == 4 && nb == 4) || (H == 2 && nb == 1)) continue;
+        if ((H == 2 && nb == 1) || (H == 8 && nb != 1)) continue;
         g_u = u;
         LaneProgram P;
         if (!build_lane_program(reinterpret_cast<const uint32_t*>(vals.data()), colidx.data(), rowptr.data(), C, K, 9, 3, H, H,
@@ -125,6 +126,7 @@ int main(int argc, char** argv) {
             if (one && (wk != atoi(argv[8]) || nbuf != atoi(argv[10]))) continue;
             LaneParams p = {};
             const int boxrows = std::min(cc * HW, 256);
+            if (cc * HW > 1024) continue;
             if ((cc * HW) % boxrows) continue;
             {
                 cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)C * HW};

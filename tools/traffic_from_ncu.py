@@ -23,6 +23,7 @@ iN, iR, iW = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("d
 units = r[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 rows = [(x[iN], float(x[iR]) * scale[units[iR]] + float(x[iW]) * scale[units[iW]]) for x in r[2:]]
+rows = [x for x in rows if "k_transpose" not in x[0]]  # layout conversions are not a layer's kernel
 # drop leading pool launches that belong to the previous pass
 while rows and "maxpool" in rows[0][0]:
     rows.pop(0)
