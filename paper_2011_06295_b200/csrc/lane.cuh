@@ -128,7 +128,7 @@ constexpr int lane_max_threads() { return H * W >= 64 ? 288 : 544; }
 // largest position set a tap's loads cover at once (bigger classes run in row chunks)
 constexpr int LANE_PMAX = 16;
 #ifndef LANE_UNROLL
-#define LANE_UNROLL 1
+#define LANE_UNROLL 4
 #endif
 constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernels
 
