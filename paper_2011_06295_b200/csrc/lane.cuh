@@ -47,6 +47,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "direct.cuh"
@@ -75,7 +76,7 @@ constexpr int LANE_HDR = 32;  // chunk header: uint16 cumulative class ends (<= 
 struct alignas(64) LaneParams {
     CUtensorMap tmap;         // x as {images (dim 0), C*H*W rows}, box {32*NB, boxrows}
     const float* bias;        // f32, may be null
-    float* y;                 // image-minor output, row stride ldy elements
+    void* y;                  // image-minor output (f32 or f16), row stride ldy elements
     const uint4* desc;        // [nst][K][cap] 16-byte units: per (k, stage) slot = header + LaneTaps
     const uint32_t* zmask;    // [K] classes whose dropped taps include a sign-clear v
     int n, c, k;              // batch (images of this call), input / output channels
@@ -88,6 +89,7 @@ struct alignas(64) LaneParams {
     int nbuf;                 // ring depth
     int slot_bytes;           // bytes of one ring slot (inputs + descriptors)
     ActQuant aq;
+    QuantAux q;               // f16 kernels: codebook / scales of the in-register weight decode
     uint32_t flags;
 };
 
@@ -107,6 +109,40 @@ __device__ __forceinline__ void lds_nb(const unsigned char* p, float (&v)[NB]) {
         const float4 t = *reinterpret_cast<const float4*>(p);
         v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
     }
+}
+
+// NB consecutive halves (a lane's images, f16 storage) in one vector load
+template <int NB>
+__device__ __forceinline__ void lds_nb(const unsigned char* p, unsigned short (&v)[NB]) {
+    if constexpr (NB == 2) {
+        const unsigned t = *reinterpret_cast<const unsigned*>(p);
+        v[0] = (unsigned short)(t & 0xffffu); v[1] = (unsigned short)(t >> 16);
+    } else {
+        static_assert(NB == 4, "f16 images per lane");
+        const uint2 t = *reinterpret_cast<const uint2*>(p);
+        v[0] = (unsigned short)(t.x & 0xffffu); v[1] = (unsigned short)(t.x >> 16);
+        v[2] = (unsigned short)(t.y & 0xffffu); v[3] = (unsigned short)(t.y >> 16);
+    }
+}
+
+// f16 store of NB images (rounded to nearest even, like astype(f16))
+template <int NB>
+__device__ __forceinline__ void store_nb(__half* y, const float (&o)[NB], int nvalid, bool vec) {
+    if constexpr (NB == 2) {
+        if (vec && nvalid >= 2) { *reinterpret_cast<__half2*>(y) = __floats2half2_rn(o[0], o[1]); return; }
+    } else if constexpr (NB == 4) {
+        if (vec && nvalid >= 4) {
+            const __half2 a = __floats2half2_rn(o[0], o[1]), b = __floats2half2_rn(o[2], o[3]);
+            uint2 t;
+            t.x = *reinterpret_cast<const unsigned*>(&a);
+            t.y = *reinterpret_cast<const unsigned*>(&b);
+            *reinterpret_cast<uint2*>(y) = t;
+            return;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+        if (j < nvalid) y[j] = __float2half_rn(o[j]);
 }
 
 // store a lane's NB consecutive images (nvalid of them exist), one vector store when allowed
@@ -132,11 +168,18 @@ constexpr int LANE_PMAX = 16;
 #endif
 constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernels
 
-template <int H, int W, int NB, int KW, int MODE, int U = 1>
+// F16: f16 storage (x, y, weights; f32 accumulation by FHFMA -- f16 x f16 is exact in f32, so
+// one fma.rn.f32.f16 per MAC equals the reference's f32 mul + add); WF = the weight format
+// decoded in registers from the descriptor's 32-bit payload (kernels.cuh tap_f16).
+template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32>
 __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __grid_constant__ LaneParams p) {
+    static_assert(!F16 || U == 1, "f16: no padded no-op taps (a quantized payload has no -0.0)");
+    using XT = typename std::conditional<F16, unsigned short, float>::type;  // staged operand
+    using TIO = typename std::conditional<F16, __half, float>::type;         // stored output
     constexpr int HW = H * W;
     constexpr int BI = 32 * NB;   // images per CTA
-    constexpr int RB = BI * 4;    // bytes of one (channel, position) row in shared memory
+    constexpr int ES = F16 ? 2 : 4;
+    constexpr int RB = BI * ES;   // bytes of one (channel, position) row in shared memory
     using AY = LaneAxis<H>;
     using AX = LaneAxis<W>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -149,6 +192,10 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
     const int KC = WK * KW;
     const int kbase = kg * KC;
     const int in_bytes = p.cc * HW * RB;
+    __shared__ unsigned short cbt[16];  // WF_CB4 table (f16 bits), published by the barrier below
+    if (F16 && tid < 16) cbt[tid] = p.q.cb16[tid];
+    const float qscale = p.q.scale;
+    const double qstep = p.q.step;
     const int d_bytes = in_bytes + (U > 1 ? HW * RB : 0);  // descriptors after inputs (+ zero rows)
 
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (size_t)NBUF * p.slot_bytes);
@@ -210,7 +257,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
         const int buf = st % NBUF;
         mbar_wait(full0 + 8 * buf, (st / NBUF) & 1);
         const unsigned char* slot = smem + (size_t)buf * p.slot_bytes;
-        const unsigned char* xin = slot + lane * 4 * NB;  // lane's images n0 + NB*lane + j
+        const unsigned char* xin = slot + lane * ES * NB;  // lane's images n0 + NB*lane + j
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             if (k0 + kk >= p.k) break;
@@ -238,7 +285,9 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                                 const LaneTap d = dq;
                                 dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
                                 const unsigned char* xa = xin + d.off;
-                                float xv[HW][NB];
+                                XT xv[HW][NB];
+                                unsigned short vh = 0;
+                                if constexpr (F16) vh = tap_f16<WF>(__float_as_uint(d.v), cbt, qscale, qstep);
 #pragma unroll
                                 for (int yy = ya; yy <= yb; ++yy)
 #pragma unroll
@@ -249,9 +298,14 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
 #pragma unroll
                                     for (int xx = x0; xx <= x1; ++xx)
 #pragma unroll
-                                        for (int j = 0; j < NB; ++j)
-                                            acc[kk][yy * W + xx][j] =
-                                                mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv[(yy - y0) * W + xx - x0][j]);
+                                        for (int j = 0; j < NB; ++j) {
+                                            if constexpr (F16)
+                                                acc[kk][yy * W + xx][j] =
+                                                    fhfma(acc[kk][yy * W + xx][j], vh, xv[(yy - y0) * W + xx - x0][j]);
+                                            else
+                                                acc[kk][yy * W + xx][j] =
+                                                    mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv[(yy - y0) * W + xx - x0][j]);
+                                        }
                             }
                             if (ya + rc > y1) dn = dq;  // = tp[end]: the next class's first tap
                         }
@@ -266,7 +320,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                                 d[u + 1].v = q.z;
                                 d[u + 1].off = __float_as_int(q.w);
                             }
-                            float xv[U][HW][NB];
+                            XT xv[U][HW][NB];
 #pragma unroll
                             for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -283,8 +337,9 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                                     for (int xx = x0; xx <= x1; ++xx)
 #pragma unroll
                                         for (int j = 0; j < NB; ++j)
-                                            acc[kk][yy * W + xx][j] = mac1<MODE>(
-                                                acc[kk][yy * W + xx][j], d[u].v, xv[u][(yy - y0) * W + xx - x0][j]);
+                                            if constexpr (!F16)
+                                                acc[kk][yy * W + xx][j] = mac1<MODE>(
+                                                    acc[kk][yy * W + xx][j], d[u].v, xv[u][(yy - y0) * W + xx - x0][j]);
                         }
                     }
                     beg = end;
@@ -301,7 +356,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
     const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
     const bool pool = p.flags & SCB_FLAG_POOL2;
     // vector stores when every row start is NB-float aligned (row stride and base)
-    const bool vec = (p.ldy % NB) == 0 && (reinterpret_cast<uintptr_t>(p.y) % (4 * NB)) == 0;
+    const bool vec = (p.ldy % NB) == 0 && (reinterpret_cast<uintptr_t>(p.y) % (ES * NB)) == 0;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -319,20 +374,20 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                         for (int j = 0; j < NB; ++j) {
                             float& o = acc[kk][yy * W + xx][j];
                             if (__float_as_uint(o) == 0x80000000u && ((zm >> (cy * AX::N + cx)) & 1u)) o = 0.f;
-                            if (aq) o = fq_store<float>((p.flags & SCB_FLAG_RELU) ? relu_io<float>(o) : o, p.aq);
+                            if (aq) o = fq_store<TIO>((p.flags & SCB_FLAG_RELU) ? relu_io<TIO>(o) : o, p.aq);
                         }
         if (!pool) {
-            float* yp = p.y + (size_t)k * HW * p.ldy + n0 + NB * lane;
+            TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * HW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int q = 0; q < HW; ++q) {
                 float o[NB];
 #pragma unroll
-                for (int j = 0; j < NB; ++j) o[j] = relu ? relu_io<float>(acc[kk][q][j]) : acc[kk][q][j];
+                for (int j = 0; j < NB; ++j) o[j] = relu ? relu_io<TIO>(acc[kk][q][j]) : acc[kk][q][j];
                 store_nb<NB>(yp + (size_t)q * p.ldy, o, p.n - (n0 + NB * lane), vec);
             }
         } else {
             constexpr int PW = W / 2, PHW = (H / 2) * (W / 2);
-            float* yp = p.y + (size_t)k * PHW * p.ldy + n0 + NB * lane;
+            TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * PHW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int py = 0; py < H / 2; ++py)
 #pragma unroll
@@ -343,7 +398,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                         const int a = (2 * py) * W + 2 * px;
                         o[j] = fmaxf(fmaxf(acc[kk][a][j], acc[kk][a + 1][j]),
                                      fmaxf(acc[kk][a + W][j], acc[kk][a + W + 1][j]));
-                        if (relu) o[j] = relu_io<float>(o[j]);
+                        if (relu) o[j] = relu_io<TIO>(o[j]);
                     }
                     store_nb<NB>(yp + (size_t)(py * PW + px) * p.ldy, o, p.n - (n0 + NB * lane), vec);
                 }
@@ -351,9 +406,9 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
     }
 }
 
-template <int H, int W, int NB, int KW, int MODE, int U = 1>
+template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32>
 cudaError_t launch_lane_t(const LaneParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_lane<H, W, NB, KW, MODE, U>;
+    auto kern = k_lane<H, W, NB, KW, MODE, U, F16, WF>;
     static int lim[64];  // per device
     const cudaError_t e = dyn_smem_ok(kern, smem, lim);
     if (e != cudaSuccess) return e;
@@ -383,10 +438,12 @@ inline int lane_axis_hi(int h, int i) { return h <= 2 ? i : (i == 0 ? 0 : (i == 
 // column index into the padded input plane (csr.py:143-160; pp = Hp*Wp, wp = Wp).
 // u > 1: pad every class segment to a multiple of u with no-op taps {-0.0, zero row}.
 // count_only: cap / zmask / macs only (no descriptor array; the launch-shape check).
+// es: bytes per staged element (4 f32, 2 f16); vbits then holds the f16 kernels' 32-bit
+// payloads (f16 bits / quantized code), whose sign for the -0.0 mask is `sign`.
 inline bool build_lane_program(const uint32_t* vbits, const int32_t* colidx, const int32_t* rowptr, int C, int K,
                                int64_t pp, int wp, int H, int W, int cc, int nb, LaneProgram* out, int u = 1,
-                               bool count_only = false) {
-    const int HW = H * W, RB = 32 * nb * 4;
+                               bool count_only = false, int es = 4, const uint8_t* sign = nullptr) {
+    const int HW = H * W, RB = 32 * nb * es;
     const int nst = (C + cc - 1) / cc;
     const int ny = lane_axis_n(H), nx = lane_axis_n(W), ncls = ny * nx;
     if (ncls > LANE_HDR / 2 || cc < 1) return false;
@@ -414,7 +471,8 @@ inline bool build_lane_program(const uint32_t* vbits, const int32_t* colidx, con
                     const int r = (int)(rem / wp), s = (int)(rem % wp);
                     const int iy = y0 + r - 1, ix = x0 + s - 1;
                     if (iy < 0 || iy >= H || ix < 0 || ix >= W) {  // padding tap of this class
-                        if (account && !(vbits[i] & 0x80000000u)) P.zmask[k] |= 1u << (cy * nx + cx);
+                        const bool neg = sign ? sign[i] != 0 : (vbits[i] & 0x80000000u) != 0;
+                        if (account && !neg) P.zmask[k] |= 1u << (cy * nx + cx);
                         continue;
                     }
                     LaneTap d;

@@ -134,36 +134,45 @@ struct scb_layer {
     std::map<std::vector<int>, int> lane_caps;  // host-only slot sizes (launch checks)
     bool finite = true;  // every weight finite: dropping padding taps is exact (lane.cuh)
 
-    std::vector<uint32_t> lane_vbits() const {
+    // descriptor value words of the lane kernels: f32 bits (f32 kernels, quantized formats
+    // decoded), or the f16 kernels' payload (f16 bits / code, decoded in registers)
+    std::vector<uint32_t> lane_vbits(int es) const {
         std::vector<uint32_t> vb((size_t)nnz);
-        for (int64_t t = 0; t < nnz; ++t) std::memcpy(&vb[t], &h_vals[t], 4);
+        for (int64_t t = 0; t < nnz; ++t) {
+            if (es == 2) vb[t] = h_pay[t];
+            else std::memcpy(&vb[t], &h_vals[t], 4);
+        }
         return vb;
     }
-    int lane_cap(int cc, int nb, int u) {
+    std::vector<uint8_t> lane_sign() const {
+        std::vector<uint8_t> sg((size_t)nnz);
+        for (int64_t t = 0; t < nnz; ++t) sg[t] = std::signbit(h_vals[t]) ? 1 : 0;
+        return sg;
+    }
+    bool lane_build(int cc, int nb, int u, int es, bool count_only, LaneProgram* P) const {
+        const std::vector<uint32_t> vb = lane_vbits(es);
+        const std::vector<uint8_t> sg = lane_sign();
+        return build_lane_program(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp, g.wp,
+                                  g.h, g.w, cc, nb, P, u, count_only, es, sg.data());
+    }
+    int lane_cap(int cc, int nb, int u, int es) {
         std::lock_guard<std::mutex> lk(mu);
-        std::vector<int> key{cc, nb, u};
+        std::vector<int> key{cc, nb, u, es};
         auto it = lane_caps.find(key);
         if (it != lane_caps.end()) return it->second;
         LaneProgram P;
-        const std::vector<uint32_t> vb = lane_vbits();
-        int cap = -1;
-        if (build_lane_program(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp, g.wp, g.h,
-                               g.w, cc, nb, &P, u, true))
-            cap = P.cap;
+        const int cap = lane_build(cc, nb, u, es, true, &P) ? P.cap : -1;
         lane_caps[key] = cap;
         return cap;
     }
-    LaneTables lane_tables(int cc, int nb, int u, bool build) {
+    LaneTables lane_tables(int cc, int nb, int u, int es, bool build) {
         std::lock_guard<std::mutex> lk(mu);
-        std::vector<int> key{cc, nb, u};
+        std::vector<int> key{cc, nb, u, es};
         auto it = d_lane.find(key);
         if (it != d_lane.end()) return it->second;
         if (!build) return LaneTables{};
         LaneProgram P;
-        const std::vector<uint32_t> vb = lane_vbits();
-        if (!build_lane_program(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp, g.wp, g.h,
-                                g.w, cc, nb, &P, u, false))
-            return LaneTables{};
+        if (!lane_build(cc, nb, u, es, false, &P)) return LaneTables{};
         LaneTables T;
         T.cap = P.cap;
         if (cudaMalloc(&T.desc, P.desc.size() * 16) != cudaSuccess) return LaneTables{};
@@ -965,7 +974,8 @@ scb_status derive_dws(scb_layer* L, const scb_launch& c, int n, uint32_t flags, 
 scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags, Derived* d) {
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
-    const int HW = g.h * g.w, nb = v.nbt, RB = 32 * nb * 4, u = v.dispatch;
+    const int es = elem_bytes(v);
+    const int HW = g.h * g.w, nb = v.nbt, RB = 32 * nb * es, u = v.dispatch;
     const int nbuf = c.stages == 0 ? 2 : c.stages;
     const int maxw = variant(c.variant).max_threads / 32 - 1;
     if (c.imgs != 32 * nb || c.bh != g.h || c.bw != g.w || c.cc < 1 || c.warps_k < 1 || c.warps_k > maxw ||
@@ -975,7 +985,7 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const int rows = c.cc * HW;
     const int boxrows = std::min(rows, 256);
     if (rows % boxrows) return fail(SCB_ERR_SHAPE, "lane launch: cc*H*W must be <= 256 or a multiple of 256");
-    const int cap = L->lane_cap(c.cc, nb, u);
+    const int cap = L->lane_cap(c.cc, nb, u, es);
     if (cap <= 0) return fail(SCB_ERR_SHAPE, "lane launch: tap program does not fit the slot format");
     const int kc = c.warps_k * v.kt;
     const size_t slot = ((size_t)rows * RB + (u > 1 ? (size_t)HW * RB : 0) + (size_t)kc * cap * 16 + 127) & ~(size_t)127;
@@ -1389,7 +1399,7 @@ static scb_status launch_tables(scb_layer* L, const scb_launch& c, const Derived
         return SCB_OK;
     }
     if (ve.info.kind == KIND_LANE) {
-        t->lane = L->lane_tables(c.cc, ve.info.nbt, ve.info.dispatch, build);
+        t->lane = L->lane_tables(c.cc, ve.info.nbt, ve.info.dispatch, elem_bytes(ve.info), build);
         if (!t->lane.desc) return build ? fail(SCB_ERR_CUDA, "lane tables: device allocation failed")
                                         : fail(SCB_ERR_ARG, missing);
         return SCB_OK;
@@ -1521,22 +1531,25 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
     LaunchTables tab;
     if ((s = launch_tables(L, c, d, false, &tab)) != SCB_OK) return s;
     if (ve.info.kind == KIND_LANE) {
-        if (ldx % 4) return fail(SCB_ERR_UNSUPPORTED, "lane kernel: the input row stride must be a multiple of 4 images");
+        const int esz = elem_bytes(ve.info);
+        if ((ldx * esz) % 16) return fail(SCB_ERR_UNSUPPORTED, "lane kernel: input rows must be 16-byte multiples");
         PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
         if (!enc) return fail(SCB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
         LaneParams q;
         std::memset(&q, 0, sizeof(q));
         const int HW = g.h * g.w;
         const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)g.c * HW};
-        const cuuint64_t gstr[1] = {(cuuint64_t)ldx * 4};
+        const cuuint64_t gstr[1] = {(cuuint64_t)ldx * esz};
         const cuuint32_t box[2] = {(cuuint32_t)(32 * ve.info.nbt), (cuuint32_t)d.row};
         const cuuint32_t es[2] = {1, 1};
-        CUresult r = enc(&q.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(x), gdim, gstr, box, es,
+        CUresult r = enc(&q.tmap, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<void*>(x), gdim, gstr, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SCB_ERR_CUDA, "lane kernel: tensor map encoding failed");
         q.bias = static_cast<const float*>(bias);
-        q.y = static_cast<float*>(y);
+        q.y = y;
+        q.q = L->q;
         q.desc = tab.lane.desc;
         q.zmask = tab.lane.zmask;
         q.n = n; q.c = g.c; q.k = g.k;

@@ -208,8 +208,9 @@ def launch_kind(launch) -> int:
 
 
 def minor_ld(n: int) -> int:
-    """Row stride of an image-minor buffer for n images: a multiple of 4 (16-byte TMA rows)."""
-    return (int(n) + 3) // 4 * 4
+    """Row stride of an image-minor buffer for n images: a multiple of 8 (16-byte TMA rows
+    in f32 and f16)."""
+    return (int(n) + 7) // 8 * 8
 
 
 def run_layer(layer, x_ptr: int, b_ptr: int, y, n: int, flags: int, launch, stream: int,

@@ -149,12 +149,12 @@ class SparseConvNet:
                     best, tim = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
                                             repetitions=repetitions, warmups=warmups,
                                             max_candidates=max_candidates, include_generic=True)
-                    if self.dtype == np.float32:  # image-minor kernels (kind 7): timed on their layout
-                        bm, tm = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
-                                             repetitions=repetitions, warmups=warmups,
-                                             max_candidates=max_candidates, layout="minor")
-                        if bm is not None and tm[bm] < tim[best]:
-                            best = bm
+                    # image-minor kernels (kind 7), timed on their own layout
+                    bm, tm = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
+                                         repetitions=repetitions, warmups=warmups,
+                                         max_candidates=max_candidates, layout="minor")
+                    if bm is not None and tm[bm] < tim[best]:
+                        best = bm
                     self.launches[i] = best
                     x = torch.relu(torch.randn(self.out_shape(i, self.batch), generator=gen)).to(
                         self.tdev, self.tdtype)
@@ -162,10 +162,10 @@ class SparseConvNet:
             self.launches = []
             for i in range(len(self.layers)):
                 l = self.dlayers[i].default_launch(self.batch, self.flags(i))
-                if self.dtype == np.float32:  # measured: the image-minor kernels win where they apply
-                    lm = self.dlayers[i].default_launch(self.batch, self.flags(i) | _abi.FLAG_IMAGE_MINOR)
-                    if lm[0] >= 0:
-                        l = lm
+                # measured (profiles/r02_lane_*): the image-minor kernels win where they apply
+                lm = self.dlayers[i].default_launch(self.batch, self.flags(i) | _abi.FLAG_IMAGE_MINOR)
+                if lm[0] >= 0:
+                    l = lm
                 self.launches.append(None if l[0] < 0 else l)
         self.set_launches(self.launches)
         return list(self.launches)

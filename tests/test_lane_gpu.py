@@ -212,3 +212,41 @@ def test_vgg_tail_network_uses_lane_layers_bitwise(sc, orc):
     net.capture()
     assert beq(net.forward_device(xd).cpu().numpy(), cur)
     assert net.kernels_per_step() == len(tail) + 2
+
+
+@pytest.mark.parametrize("fmt", ["native", "cb4", "lin16", "aff16"])
+def test_lane_f16_in_register_decode_bitwise(sc, fmt):
+    """f16 storage lane kernels (FHFMA, f16 operands two images per 32-bit load) with every
+    f16 weight format decoded in registers: bitwise vs the oracle on the reference
+    quantizer's outputs, plain and with ReLU + pool."""
+    import torch
+    from dataclasses import replace
+    from oracle import oracle as orc
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import (LayerSpec, affine_quantize, bench_inputs, f16_scaled,
+                                             make_layer_weights, reference_quantize)
+    for c, hw, k, n in ((256, 4, 96, 33), (128, 2, 64, 70), (512, 4, 512, 40)):
+        sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+        kern = sc.build_csr(f16_scaled(make_layer_weights(LayerSpec("q", sh, 0.9), 0)), sh)
+        if fmt == "cb4":
+            cents = np.quantile(kern.values.astype(np.float64), np.linspace(0.02, 0.98, 16))
+            kern = replace(kern, values=reference_quantize(kern.values, "codebook", cents), _device_cache={})
+        elif fmt == "lin16":
+            kern = replace(kern, values=reference_quantize(kern.values, "fixed"), _device_cache={})
+        elif fmt == "aff16":
+            vals, step = affine_quantize(kern.values, 16)
+            kern = replace(kern, values=vals, _device_cache={}, quant={"scheme": "affine", "step": step})
+        x, b = bench_inputs(sh, n)
+        x, b = x.astype(np.float16), b.astype(np.float16)
+        want = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+        layer = device_layer(kern, 0, np.float16, fmt)
+        cands = _lane_cands(layer, n, 0)
+        xd = torch.from_numpy(x).cuda()
+        for cfg in cands[:: max(1, len(cands) // 8)]:
+            o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg, weight_format=fmt)).cpu().numpy()
+            assert beq(o, want), (fmt, hw, cfg)
+        wantp = relu_pool_ref(want)
+        for cfg in _lane_cands(layer, n, 0x5)[::7]:
+            o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg, weight_format=fmt), relu=True,
+                               pool=True).cpu().numpy()
+            assert beq(o, wantp), (fmt, hw, cfg)

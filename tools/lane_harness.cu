@@ -103,7 +103,7 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {2}, kws[] = {1}, wks[] = {7, 8, 14, 16}, ccs[] = {4, 8, 12, 16, 32, 48, 64}, nbufs[] = {2, 3}, us[] = {1, 2};
+    const int nbs[] = {1, 2}, kws[] = {1}, wks[] = {7, 8, 14, 16}, ccs[] = {4, 8, 12, 16, 32, 48, 64}, nbufs[] = {2, 3}, us[] = {1, 2};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
