@@ -458,6 +458,10 @@ class SparseConvNet:
         H2D of `x_host` (pinned for an async copy), the stack, D2H."""
         torch = self.torch
         xt = x_host if isinstance(x_host, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x_host))
+        if xt.dtype != self.tdtype:
+            # the reference computes in the input's dtype (store.py:263-286): a silent cast
+            # would change the arithmetic, so a mismatch is an error
+            raise ShapeError(f"input dtype {xt.dtype} != the network's activation dtype {self.tdtype}")
         if tuple(xt.shape) != (self.batch, *self.in_shape):
             raise ShapeError(f"input {tuple(xt.shape)} != planned {(self.batch, *self.in_shape)}")
         with torch.cuda.device(self.device):

@@ -133,10 +133,18 @@ def load_conv_layers(path, input_chw: tuple | None = None):
     return layers
 
 
-def load_net(path, device: int = 0, weight_format: str = "native", input_chw=None):
-    """SparseConvNet of a stored model's conv stack, resident on `device`."""
+def load_net(path, device: int = 0, weight_format: str = "native", input_chw=None, dtype=None):
+    """SparseConvNet of a stored model's conv stack, resident on `device`.
+
+    The reference's Model.forward computes in the dtype of the input it is given
+    (store.py:263-286); a device network fixes its activation dtype up front, so pass the
+    dtype of the inputs you will feed (`dtype`).  Default: f16 when the stored weights are
+    f16, else f32; SparseConvNet.forward refuses an input of another dtype rather than
+    casting it.  Dense-stored conv layers are converted with build_csr on load and run on
+    the sparse kernels (the reference runs them dense-gemm); the result is the same
+    convolution, summed in the reference's colidx order."""
     from .network import SparseConvNet
     layers = load_conv_layers(path, input_chw)
-    dt = layers[0].kernel.values.dtype
-    return SparseConvNet(layers, device=device, dtype=np.float16 if dt == np.float16 else np.float32,
-                         weight_format=weight_format)
+    if dtype is None:
+        dtype = np.float16 if layers[0].kernel.values.dtype == np.float16 else np.float32
+    return SparseConvNet(layers, device=device, dtype=dtype, weight_format=weight_format)

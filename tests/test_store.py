@@ -95,3 +95,16 @@ def test_act_quant_net_forward_bitwise():
     assert np.array_equal(out.view(np.uint32), exp["conv_out"].view(np.uint32))
     net.set_launches([None] * len(net.layers))  # generic kernels: separate fake-quant pass
     assert np.array_equal(net.forward(exp["x"]).view(np.uint32), exp["conv_out"].view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_loaded_net_refuses_other_input_dtype():
+    """the device net has a fixed activation dtype; an input of another dtype is
+    refused instead of silently cast (the reference computes in the input's dtype)."""
+    from paper_2011_06295_b200.errors import ShapeError
+    from paper_2011_06295_b200.store import load_net
+    exp = _expected()
+    net = load_net(STORE, dtype=np.float32)
+    net.plan(exp["x"].shape[0], tune=False)
+    with pytest.raises(ShapeError, match="dtype"):
+        net.forward(exp["x"].astype(np.float64))
