@@ -159,8 +159,21 @@ __device__ __forceinline__ void store_nb(float* y, const float (&o)[NB], int nva
 }
 
 // thread limit: 16 consumer warps + the producer; 8 + 1 for 8x8 planes (64 accumulators per lane)
+template <int H, int W, int CS = 1>
+constexpr int lane_max_threads() { return H * W >= 64 ? 288 : (CS > 1 ? 1024 : 544); }
+
+// class index (cy * AX::N + cx) of output position q of an H x W plane
 template <int H, int W>
-constexpr int lane_max_threads() { return H * W >= 64 ? 288 : 544; }
+__host__ __device__ constexpr int lane_class_of(int q) {
+    return (q / W == 0 ? 0 : (q / W == H - 1 && H > 1 ? LaneAxis<H>::N - 1 : (H <= 2 ? q / W : 1))) * LaneAxis<W>::N +
+           (q % W == 0 ? 0 : (q % W == W - 1 && W > 1 ? LaneAxis<W>::N - 1 : (W <= 2 ? q % W : 1)));
+}
+// class split: group of class ci when CS warps share an output channel (balanced MACs):
+// 4x4 -- {interior, top edge, top-left corner} | {other edges and corners}; 2x2 -- rows
+template <int H, int W, int CS>
+__host__ __device__ constexpr int lane_class_group(int ci) {
+    return CS == 1 ? 0 : (H == 2 ? ci / 2 : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1));
+}
 // largest position set a tap's loads cover at once (bigger classes run in row chunks)
 constexpr int LANE_PMAX = 16;
 #ifndef LANE_UNROLL
@@ -171,8 +184,8 @@ constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernel
 // F16: f16 storage (x, y, weights; f32 accumulation by FHFMA -- f16 x f16 is exact in f32, so
 // one fma.rn.f32.f16 per MAC equals the reference's f32 mul + add); WF = the weight format
 // decoded in registers from the descriptor's 32-bit payload (kernels.cuh tap_f16).
-template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32>
-__global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __grid_constant__ LaneParams p) {
+template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1>
+__global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const __grid_constant__ LaneParams p) {
     static_assert(!F16 || U == 1, "f16: no padded no-op taps (a quantized payload has no -0.0)");
     using XT = typename std::conditional<F16, unsigned short, float>::type;  // staged operand
     using TIO = typename std::conditional<F16, __half, float>::type;         // stored output
@@ -189,7 +202,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
     const int WK = p.warps, NBUF = p.nbuf;
     const int kg = blockIdx.x % p.kgroups;
     const int n0 = (blockIdx.x / p.kgroups) * BI;
-    const int KC = WK * KW;
+    const int KC = WK / CS * KW;  // output channels per CTA
     const int kbase = kg * KC;
     const int in_bytes = p.cc * HW * RB;
     __shared__ unsigned short cbt[16];  // WF_CB4 table (f16 bits), published by the barrier below
@@ -242,7 +255,12 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
     }
 
     // -------------------------------------------------------------- consumers
-    const int k0 = kbase + warp * KW;
+    // CS = 2: two warps per output channel, each owning a fixed set of position classes
+    // (lane_class_group) -- twice the warps for latency hiding, the same shared-memory traffic
+    const int cq = warp / CS, cgrp = warp % CS;
+    const int k0 = kbase + cq * KW;
+    auto consume = [&](auto GC) {
+    constexpr int G = decltype(GC)::value;
     float acc[KW][HW][NB];
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
@@ -261,7 +279,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
 #pragma unroll
         for (int kk = 0; kk < KW; ++kk) {
             if (k0 + kk >= p.k) break;
-            const unsigned char* ch = slot + d_bytes + (size_t)(warp * KW + kk) * p.cap * 16;
+            const unsigned char* ch = slot + d_bytes + (size_t)(cq * KW + kk) * p.cap * 16;
             unsigned short hd[LANE_HDR / 2];  // cumulative class ends, two 16-byte loads
             *reinterpret_cast<uint4*>(hd) = *reinterpret_cast<const uint4*>(ch);
             *reinterpret_cast<uint4*>(hd + 8) = *reinterpret_cast<const uint4*>(ch + 16);
@@ -274,12 +292,16 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                 for (int cx = 0; cx < AX::N; ++cx) {
                     const int y0 = AY::lo(cy), y1 = AY::hi(cy), x0 = AX::lo(cx), x1 = AX::hi(cx);
                     const int end = hd[cy * AX::N + cx];
+                    if (lane_class_group<H, W, CS>(cy * AX::N + cx) != G) {  // another warp's class
+                        beg = end;
+                        continue;
+                    }
                     if constexpr (U == 1) {
                         const int rc = LANE_PMAX / (x1 - x0 + 1) > 0 ? LANE_PMAX / (x1 - x0 + 1) : 1;  // rows per chunk
 #pragma unroll
                         for (int ya = y0; ya <= y1; ya += rc) {
                             const int yb = ya + rc - 1 < y1 ? ya + rc - 1 : y1;
-                            LaneTap dq = ya == y0 ? dn : tp[beg];
+                            LaneTap dq = (ya == y0 && CS == 1) ? dn : tp[beg];
 #pragma unroll kLaneUnroll
                             for (int t = beg; t < end; ++t) {
                                 const LaneTap d = dq;
@@ -351,21 +373,21 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
     }
 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // ---- epilogue: lane holds the whole plane of images n0 + lane + 32 j
+    // ---- epilogue: lane holds the whole plane (its class group's positions) of images n0 + NB*lane + j
     const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
     const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
     const bool pool = p.flags & SCB_FLAG_POOL2;
-    // vector stores when every row start is NB-float aligned (row stride and base)
+    // vector stores when every row start is NB-element aligned (row stride and base)
     const bool vec = (p.ldy % NB) == 0 && (reinterpret_cast<uintptr_t>(p.y) % (ES * NB)) == 0;
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
-        if (k >= p.k) break;
-        const uint32_t zm = p.zmask[k];
+        const uint32_t zm = k < p.k ? p.zmask[k] : 0u;
 #pragma unroll
         for (int cy = 0; cy < AY::N; ++cy)
 #pragma unroll
-            for (int cx = 0; cx < AX::N; ++cx)
+            for (int cx = 0; cx < AX::N; ++cx) {
+                if (lane_class_group<H, W, CS>(cy * AX::N + cx) != G) continue;
 #pragma unroll
                 for (int yy = AY::lo(cy); yy <= AY::hi(cy); ++yy)
 #pragma unroll
@@ -375,40 +397,73 @@ __global__ void __launch_bounds__(lane_max_threads<H, W>(), 1) k_lane(const __gr
                             float& o = acc[kk][yy * W + xx][j];
                             if (__float_as_uint(o) == 0x80000000u && ((zm >> (cy * AX::N + cx)) & 1u)) o = 0.f;
                             if (aq) o = fq_store<TIO>((p.flags & SCB_FLAG_RELU) ? relu_io<TIO>(o) : o, p.aq);
+                            if (relu && !pool) o = relu_io<TIO>(o);
                         }
+            }
         if (!pool) {
+            if (k >= p.k) continue;
             TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * HW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int q = 0; q < HW; ++q) {
+                if (lane_class_group<H, W, CS>(lane_class_of<H, W>(q)) != G) continue;
                 float o[NB];
 #pragma unroll
-                for (int j = 0; j < NB; ++j) o[j] = relu ? relu_io<TIO>(acc[kk][q][j]) : acc[kk][q][j];
+                for (int j = 0; j < NB; ++j) o[j] = acc[kk][q][j];
                 store_nb<NB>(yp + (size_t)q * p.ldy, o, p.n - (n0 + NB * lane), vec);
             }
-        } else {
-            constexpr int PW = W / 2, PHW = (H / 2) * (W / 2);
+        }
+    }
+    if (pool) {
+        constexpr int PW = W / 2, PHW = (H / 2) * (W / 2);
+        float* ex = reinterpret_cast<float*>(smem);  // CS = 2: [channel][position][image] exchange
+        if constexpr (CS > 1) {
+            asm volatile("bar.sync 1, %0;" ::"r"(WK * 32) : "memory");  // every warp is past the ring
+#pragma unroll
+            for (int q = 0; q < HW; ++q) {
+                if (lane_class_group<H, W, CS>(lane_class_of<H, W>(q)) != G) continue;
+#pragma unroll
+                for (int j = 0; j < NB; ++j) ex[((size_t)cq * HW + q) * BI + NB * lane + j] = acc[0][q][j];
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(WK * 32) : "memory");
+        }
+#pragma unroll
+        for (int kk = 0; kk < KW; ++kk) {
+            const int k = k0 + kk;
+            if (k >= p.k) break;
             TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * PHW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int py = 0; py < H / 2; ++py)
 #pragma unroll
                 for (int px = 0; px < PW; ++px) {
+                    if (CS > 1 && (py * PW + px) % CS != G) continue;  // pooled outputs dealt over the group
                     float o[NB];
 #pragma unroll
                     for (int j = 0; j < NB; ++j) {
                         const int a = (2 * py) * W + 2 * px;
-                        o[j] = fmaxf(fmaxf(acc[kk][a][j], acc[kk][a + 1][j]),
-                                     fmaxf(acc[kk][a + W][j], acc[kk][a + W + 1][j]));
+                        float v[4];
+                        if constexpr (CS > 1) {
+                            const float* e = ex + (size_t)cq * HW * BI + NB * lane + j;
+                            v[0] = e[(size_t)a * BI]; v[1] = e[(size_t)(a + 1) * BI];
+                            v[2] = e[(size_t)(a + W) * BI]; v[3] = e[(size_t)(a + W + 1) * BI];
+                        } else {
+                            v[0] = acc[kk][a][j]; v[1] = acc[kk][a + 1][j];
+                            v[2] = acc[kk][a + W][j]; v[3] = acc[kk][a + W + 1][j];
+                        }
+                        o[j] = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
                         if (relu) o[j] = relu_io<TIO>(o[j]);
                     }
                     store_nb<NB>(yp + (size_t)(py * PW + px) * p.ldy, o, p.n - (n0 + NB * lane), vec);
                 }
         }
     }
+    };  // consume
+    if (cgrp == 0) consume(std::integral_constant<int, 0>{});
+    else if constexpr (CS > 1) consume(std::integral_constant<int, 1>{});
 }
 
-template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32>
+template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1>
 cudaError_t launch_lane_t(const LaneParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_lane<H, W, NB, KW, MODE, U, F16, WF>;
+    auto kern = k_lane<H, W, NB, KW, MODE, U, F16, WF, CS>;
     static int lim[64];  // per device
     const cudaError_t e = dyn_smem_ok(kern, smem, lim);
     if (e != cudaSuccess) return e;

@@ -987,9 +987,14 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     if (rows % boxrows) return fail(SCB_ERR_SHAPE, "lane launch: cc*H*W must be <= 256 or a multiple of 256");
     const int cap = L->lane_cap(c.cc, nb, u, es);
     if (cap <= 0) return fail(SCB_ERR_SHAPE, "lane launch: tap program does not fit the slot format");
-    const int kc = c.warps_k * v.kt;
+    const int cs = v.kt;  // kind 7: warps per output channel (class split)
+    if (c.warps_k % cs) return fail(SCB_ERR_SHAPE, "lane launch: warps must be a multiple of the class split");
+    const int kc = c.warps_k / cs;
     const size_t slot = ((size_t)rows * RB + (u > 1 ? (size_t)HW * RB : 0) + (size_t)kc * cap * 16 + 127) & ~(size_t)127;
     d->smem = nbuf * slot + 16 * nbuf;
+    // class split + pool: the epilogue exchanges f32 planes through the (drained) ring
+    if (cs > 1 && (flags & SCB_FLAG_POOL2))
+        d->smem = std::max(d->smem, (size_t)kc * HW * 32 * nb * 4);
     if (d->smem > (size_t)kSmemLimit) return fail(SCB_ERR_SHAPE, "shared memory over 227 KB");
     d->threads = 32 * (c.warps_k + 1);
     d->chunk = (int)slot;
@@ -1066,7 +1071,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
         if (v.kind == KIND_LANE) {
-            for (int wk : {4, 8, 14, 16})
+            for (int wk : {4, 8, 14, 16, 28})
                 for (int cc : {4, 8, 12, 16, 32, 48, 64})
                     for (int ns : {2, 3}) {
                         scb_launch c{vi, wk, 32 * v.nbt, g.h, g.w, cc, ns};
@@ -1554,7 +1559,7 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
         q.zmask = tab.lane.zmask;
         q.n = n; q.c = g.c; q.k = g.k;
         q.ldx = (int)ldx; q.ldy = (int)ldy;
-        q.cc = c.cc; q.nst = d.wp; q.warps = c.warps_k; q.kw = ve.info.kt;
+        q.cc = c.cc; q.nst = d.wp; q.warps = c.warps_k; q.kw = 1;
         q.kgroups = d.kblocks; q.cap = d.tap_cap; q.nbuf = d.stage_el; q.slot_bytes = d.chunk; q.boxrows = d.row;
         q.aq = L->aq;
         q.flags = flags;

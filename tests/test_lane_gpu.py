@@ -250,3 +250,34 @@ def test_lane_f16_in_register_decode_bitwise(sc, fmt):
             o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg, weight_format=fmt), relu=True,
                                pool=True).cpu().numpy()
             assert beq(o, wantp), (fmt, hw, cfg)
+
+
+@pytest.mark.parametrize("hw", [2, 4])
+def test_lane_class_split_bitwise(sc, orc, hw):
+    """Class-split lane kernels (two warps per output channel, kt = 2): plain, ReLU + pool
+    (pooled windows straddle the two warps' classes: exchanged through shared memory) and
+    fused fake-quant, bitwise."""
+    import torch
+    from paper_2011_06295_b200 import _abi, engine
+    from paper_2011_06295_b200.device import DeviceLayer
+    aq = {"bits": 8, "clip_lo": 0.0, "clip_hi": 6.0, "mu": 0.0, "step": 6.0 / 255, "mode": "asymmetric"}
+    n, c, k = 70, 256, 60
+    sh, w, x, b = _layer(sc, c, hw, k, 0.9, n, seed=7)
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+    layer = DeviceLayer(kern, 0, np.float32)
+    layer.set_act_quant(aq)
+    vs = _abi.variants()
+    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    cases = ((0, ref), (_abi.FLAG_RELU | _abi.FLAG_POOL2, relu_pool_ref(ref)),
+             (_abi.FLAG_RELU | _abi.FLAG_ACT_QUANT, orc.fake_quant(np.maximum(ref, 0), aq)),
+             (_abi.FLAG_RELU | _abi.FLAG_POOL2 | _abi.FLAG_ACT_QUANT, orc.fake_quant(relu_pool_ref(ref), aq)))
+    for flags, exp in cases:
+        cands = [cf for cf in _lane_cands(layer, n, flags) if vs[cf[0]]["kt"] == 2]
+        assert cands, flags
+        for cfg in cands[:: max(1, len(cands) // 5)]:
+            y = torch.empty(exp.shape, device="cuda")
+            engine.run_layer(layer, xd.data_ptr(), bd.data_ptr(), y, n, flags, cfg, st)
+            torch.cuda.synchronize()
+            assert beq(y.cpu().numpy(), exp), (cfg, flags)

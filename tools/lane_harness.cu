@@ -19,19 +19,21 @@ using namespace scb;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s @%d: %s\n", #x, __LINE__, cudaGetErrorString(e_)); exit(1); } } while (0)
 
-static int g_u = 1;
+static int g_u = 1, g_cs = 1;
 template <int H, int NB, int KW>
 cudaError_t launch(const LaneParams& p, unsigned grid, unsigned thr, size_t smem) {
+    if (g_cs == 2) {
+        if (g_u == 2) return launch_lane_t<H, H, NB, KW, MODE_EXACT, 2, false, WF_F32, 2>(p, grid, thr, smem, 0);
+        return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 2>(p, grid, thr, smem, 0);
+    }
     if (g_u == 2) return launch_lane_t<H, H, NB, KW, MODE_EXACT, 2>(p, grid, thr, smem, 0);
-    if (g_u == 4) return launch_lane_t<H, H, NB, KW, MODE_EXACT, 4>(p, grid, thr, smem, 0);
     return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1>(p, grid, thr, smem, 0);
 }
 
 static cudaError_t dispatch(int H, int nb, int kw, const LaneParams& p, unsigned grid, unsigned thr, size_t smem) {
 #define D(h, b, w) if (H == h && nb == b && kw == w) return launch<h, b, w>(p, grid, thr, smem);
-    D(4, 1, 1) D(4, 2, 1) D(4, 4, 1)
-    D(2, 2, 1) D(2, 4, 1)
-    D(8, 1, 1)
+    D(4, 2, 1)
+    D(2, 2, 1)
 #undef D
     return cudaErrorInvalidValue;
 }
@@ -103,14 +105,15 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {1, 2}, kws[] = {1}, wks[] = {7, 8, 14, 16}, ccs[] = {4, 8, 12, 16, 32, 48, 64}, nbufs[] = {2, 3}, us[] = {1, 2};
+    const int nbs[] = {2}, kws[] = {1}, wks[] = {14, 28}, ccs[] = {4, 8, 12, 16, 32, 48, 64}, nbufs[] = {2, 3}, us[] = {1, 2};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     double best = 1e30;
     // optional single config: argv[6..10] = nb kw wk cc nbuf
     const bool one = argc > 11;
-    for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
+    for (int cs : {1, 2}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
+        g_cs = cs;
         if (one && (nb != atoi(argv[6]) || kw != atoi(argv[7]) || cc != atoi(argv[9]) || u != atoi(argv[11]))) continue;
         if ((H == 2 && nb == 1) || (H == 8 && nb != 1)) continue;
         g_u = u;
@@ -142,7 +145,8 @@ int main(int argc, char** argv) {
             p.bias = db; p.y = dy; p.desc = dd; p.zmask = dz;
             p.n = N; p.c = C; p.k = K; p.ldx = N; p.ldy = N;
             p.cc = cc; p.nst = (C + cc - 1) / cc; p.warps = wk; p.kw = kw;
-            const int KC = wk * kw;
+            if (wk % cs || (cs == 1 && wk > 16)) continue;
+            const int KC = wk / cs * kw;
             p.kgroups = (K + KC - 1) / KC;
             p.cap = P.cap; p.nbuf = nbuf;
             p.slot_bytes = ((cc * HW * 128 * nb * (u > 1 ? 1 : 1) + (u > 1 ? HW * 128 * nb : 0) + KC * P.cap * 16) + 127) & ~127;
@@ -175,8 +179,8 @@ int main(int argc, char** argv) {
             CK(cudaEventElapsedTime(&ms, e0, e1));
             const double us = ms * 1000.0 / reps;
             best = std::min(best, us);
-            printf("u %d nb %d kw %d wk %2d cc %2d nbuf %d grid %4u smem %6zu: %8.2f us  counted %5.2f TMAC/s  executed %5.2f TMAC/s  %s\n",
-                   u, nb, kw, wk, cc, nbuf, grid, smem, us, counted / us * 1e-6, (double)P.macs * N / us * 1e-6,
+            printf("cs %d u %d nb %d kw %d wk %2d cc %2d nbuf %d grid %4u smem %6zu: %8.2f us  counted %5.2f TMAC/s  executed %5.2f TMAC/s  %s\n",
+                   cs, u, nb, kw, wk, cc, nbuf, grid, smem, us, counted / us * 1e-6, (double)P.macs * N / us * 1e-6,
                    bad ? "MISMATCH" : "bitwise");
         }
         cudaFree(dd); cudaFree(dz);
