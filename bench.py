@@ -580,7 +580,11 @@ def measure_shard_proxy(args, specs, local_rank, dev, rate_full: float, reps: in
     net = build_net(specs, seed=0, device=local_rank)
     net.plan(nb, tune=not args.no_tune)
     net.pdl = not args.no_pdl
+    net.set_chains(args.chains if args.chains <= nb else 1)
     x = torch.randn((nb, 3, 32, 32), device=dev)
+    net.x_in.copy_(x)
+    if args.graph:
+        net.capture()  # as the main step: forward_device replays the graph
     for _ in range(5):
         net.forward_device(x)
     torch.cuda.synchronize()
@@ -595,6 +599,7 @@ def measure_shard_proxy(args, specs, local_rank, dev, rate_full: float, reps: in
     return {"images_per_gpu": nb, "ms_per_step": round(ms, 4), "images_per_s": round(rate, 1),
             "fraction_of_full_batch_rate": round(rate / rate_full, 4),
             "implied_8gpu_images_per_s": round(8 * rate, 1),
+            "chains": net.chains, "cuda_graph": bool(args.graph),
             "note": "back-to-back steps without L2 flush (the shard's working set is L2-resident on a real "
                     "8-GPU run too); launches tuned at this batch"}
 
