@@ -376,7 +376,7 @@ DIMGS = [(4, 1), (4, 2), (4, 4), (2, 1), (2, 2), (2, 4), (2, 8)]
 # unroll with padded class segments)
 LANES = [(h, nb, 1, u) for h in (2, 4) for nb in (1, 2, 4) for u in (1, 2) if not (h == 4 and nb == 4)]
 # class split: two warps per output channel, each a fixed half of the position classes (CS = 2)
-LANES_CS = [(4, 2, 1), (2, 2, 2)]  # (H, NB, U)
+LANES_CS = [(4, 2, 1, 2), (2, 2, 2, 2), (4, 1, 1, 2), (2, 1, 2, 2), (2, 1, 2, 4)]  # (H, NB, U, CS)
 # f16 storage (FHFMA, in-register weight decode of every f16 format): (H = W, NB)
 LANES_F16 = [(4, 2), (2, 2), (2, 4)]
 DIMGS_F16 = [(2, 2), (2, 4), (2, 8), (4, 2), (4, 4)]  # f16 storage, FHFMA
@@ -474,8 +474,8 @@ def main():
         groups[("dimg16", H, KW)] = ([], [("dimg16", H, KW, wf) for wf in (WF_F16,) + qs])
     for H, NB, KW, U in LANES:
         groups[("lane", H, NB, KW, U)] = ([], [("lane", H, NB, KW, U, m) for m in (EXACT, FMA)])
-    for H, NB, U in LANES_CS:
-        groups[("lanecs", H, NB, U)] = ([], [("lanecs", H, NB, U, m) for m in (EXACT, FMA)])
+    for H, NB, U, CS in LANES_CS:
+        groups[("lanecs", H, NB, U, CS)] = ([], [("lanecs", H, NB, U, CS, m) for m in (EXACT, FMA)])
     for H, NB in LANES_F16:
         groups[("lane16", H, NB)] = ([], [("lane16", H, NB, wf) for wf in (WF_F16,) + QFMTS])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
@@ -503,11 +503,11 @@ def main():
                     ents.append(f"    {{{{3, 3, {KW}, {M}, {TH}, {LW}, SCB_F32, {WF_F32}, {mode}, {JUMP}, 1, "
                                 f"{KIND_DTM}}}, nullptr, &launch_dtm_t<3, 3, 1, {TH}, {LW}, {KW}, {M}, {mode}>}},\n")
                     continue
-                if v[0] == "lanecs":  # info: kt = CS = 2 warps per output channel
-                    _, H, NB, U, mode = v
-                    ents.append(f"    {{{{3, 3, 2, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {U}, 1, "
+                if v[0] == "lanecs":  # info: kt = CS warps per output channel
+                    _, H, NB, U, CS, mode = v
+                    ents.append(f"    {{{{3, 3, {CS}, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {U}, 1, "
                                 f"{KIND_LANE}}}, nullptr, nullptr, 1024, nullptr, "
-                                f"&launch_lane_t<{H}, {H}, {NB}, 1, {mode}, {U}, false, {WF_F32}, 2>}},\n")
+                                f"&launch_lane_t<{H}, {H}, {NB}, 1, {mode}, {U}, false, {WF_F32}, {CS}>}},\n")
                     continue
                 if v[0] == "lane16":
                     _, H, NB, wf = v

@@ -169,10 +169,12 @@ __host__ __device__ constexpr int lane_class_of(int q) {
            (q % W == 0 ? 0 : (q % W == W - 1 && W > 1 ? LaneAxis<W>::N - 1 : (W <= 2 ? q % W : 1)));
 }
 // class split: group of class ci when CS warps share an output channel (balanced MACs):
-// 4x4 -- {interior, top edge, top-left corner} | {other edges and corners}; 2x2 -- rows
+// 4x4 (CS = 2) -- {interior, top edge, top-left corner} | {other edges and corners};
+// 2x2 -- CS = 2: rows, CS = 4: one position each
 template <int H, int W, int CS>
 __host__ __device__ constexpr int lane_class_group(int ci) {
-    return CS == 1 ? 0 : (H == 2 ? ci / 2 : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1));
+    static_assert(CS == 1 || CS == 2 || (CS == 4 && H == 2 && W == 2), "class split");
+    return CS == 1 ? 0 : (H == 2 ? ci * CS / 4 : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1));
 }
 // largest position set a tap's loads cover at once (bigger classes run in row chunks)
 constexpr int LANE_PMAX = 16;
@@ -458,7 +460,12 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
     }
     };  // consume
     if (cgrp == 0) consume(std::integral_constant<int, 0>{});
-    else if constexpr (CS > 1) consume(std::integral_constant<int, 1>{});
+    else if constexpr (CS == 2) consume(std::integral_constant<int, 1>{});
+    else if constexpr (CS == 4) {
+        if (cgrp == 1) consume(std::integral_constant<int, 1>{});
+        else if (cgrp == 2) consume(std::integral_constant<int, 2>{});
+        else consume(std::integral_constant<int, 3>{});
+    }
 }
 
 template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1>

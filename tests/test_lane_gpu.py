@@ -274,9 +274,14 @@ def test_lane_class_split_bitwise(sc, orc, hw):
              (_abi.FLAG_RELU | _abi.FLAG_ACT_QUANT, orc.fake_quant(np.maximum(ref, 0), aq)),
              (_abi.FLAG_RELU | _abi.FLAG_POOL2 | _abi.FLAG_ACT_QUANT, orc.fake_quant(relu_pool_ref(ref), aq)))
     for flags, exp in cases:
-        cands = [cf for cf in _lane_cands(layer, n, flags) if vs[cf[0]]["kt"] == 2]
-        assert cands, flags
-        for cfg in cands[:: max(1, len(cands) // 5)]:
+        all_c = _lane_cands(layer, n, flags)
+        splits = sorted({vs[cf[0]]["kt"] for cf in all_c} - {1})
+        assert splits == ([2, 4] if hw == 2 else [2]), splits
+        cands = []
+        for cs in splits:
+            sub = [cf for cf in all_c if vs[cf[0]]["kt"] == cs]
+            cands += sub[:: max(1, len(sub) // 4)]
+        for cfg in cands:
             y = torch.empty(exp.shape, device="cuda")
             engine.run_layer(layer, xd.data_ptr(), bd.data_ptr(), y, n, flags, cfg, st)
             torch.cuda.synchronize()
