@@ -160,7 +160,7 @@ __device__ __forceinline__ void store_nb(float* y, const float (&o)[NB], int nva
 
 // thread limit: 16 consumer warps + the producer; 8 + 1 for 8x8 planes (64 accumulators per lane)
 template <int H, int W, int CS = 1>
-constexpr int lane_max_threads() { return H * W >= 64 ? 288 : (CS > 1 ? 1024 : 544); }
+constexpr int lane_max_threads() { return CS > 1 ? 1024 : (H * W >= 64 ? 288 : 544); }
 
 // class index (cy * AX::N + cx) of output position q of an H x W plane
 template <int H, int W>
@@ -173,8 +173,25 @@ __host__ __device__ constexpr int lane_class_of(int q) {
 // 2x2 -- CS = 2: rows, CS = 4: one position each
 template <int H, int W, int CS>
 __host__ __device__ constexpr int lane_class_group(int ci) {
-    static_assert(CS == 1 || CS == 2 || (CS == 4 && H == 2 && W == 2), "class split");
-    return CS == 1 ? 0 : (H == 2 ? ci * CS / 4 : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1));
+    static_assert(CS == 1 || CS == 2 || (CS == 4 && ((H == 2 && W == 2) || (H == 8 && W == 8))), "class split");
+    return CS == 1 || H == 8 ? 0 : (H == 2 ? ci * CS / 4 : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1));
+}
+// 8x8 planes split by QUADRANT instead (CS = 4): group G owns rows / columns [lo, hi] of
+// its 4x4 quadrant (every class list is shared; a warp covers class positions in its window)
+template <int H, int W, int CS>
+__host__ __device__ constexpr bool lane_quadrants() { return H == 8 && W == 8 && CS == 4; }
+template <int H, int W, int CS>
+__host__ __device__ constexpr int lane_win_y0(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g / 2) : 0; }
+template <int H, int W, int CS>
+__host__ __device__ constexpr int lane_win_x0(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g % 2) : 0; }
+template <int H, int W, int CS>
+__host__ __device__ constexpr int lane_win_y1(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g / 2) + 3 : H - 1; }
+template <int H, int W, int CS>
+__host__ __device__ constexpr int lane_win_x1(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g % 2) + 3 : W - 1; }
+// group owning output position (y, x)
+template <int H, int W, int CS>
+__host__ __device__ constexpr int lane_pos_group(int y, int x) {
+    return lane_quadrants<H, W, CS>() ? 2 * (y / 4) + x / 4 : lane_class_group<H, W, CS>(lane_class_of<H, W>(y * W + x));
 }
 // largest position set a tap's loads cover at once (bigger classes run in row chunks)
 constexpr int LANE_PMAX = 16;
@@ -182,6 +199,9 @@ constexpr int LANE_PMAX = 16;
 #define LANE_UNROLL 4
 #endif
 constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernels
+#ifndef LANE_PAIRS
+#define LANE_PAIRS 0
+#endif
 
 // F16: f16 storage (x, y, weights; f32 accumulation by FHFMA -- f16 x f16 is exact in f32, so
 // one fma.rn.f32.f16 per MAC equals the reference's f32 mul + add); WF = the weight format
@@ -294,20 +314,23 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                 for (int cx = 0; cx < AX::N; ++cx) {
                     const int y0 = AY::lo(cy), y1 = AY::hi(cy), x0 = AX::lo(cx), x1 = AX::hi(cx);
                     const int end = hd[cy * AX::N + cx];
-                    if (lane_class_group<H, W, CS>(cy * AX::N + cx) != G) {  // another warp's class
+                    // this warp's positions of the class: the class range inside the group window
+                    const int ey0 = y0 > lane_win_y0<H, W, CS>(G) ? y0 : lane_win_y0<H, W, CS>(G);
+                    const int ey1 = y1 < lane_win_y1<H, W, CS>(G) ? y1 : lane_win_y1<H, W, CS>(G);
+                    const int ex0 = x0 > lane_win_x0<H, W, CS>(G) ? x0 : lane_win_x0<H, W, CS>(G);
+                    const int ex1 = x1 < lane_win_x1<H, W, CS>(G) ? x1 : lane_win_x1<H, W, CS>(G);
+                    const bool mine = lane_quadrants<H, W, CS>() || lane_class_group<H, W, CS>(cy * AX::N + cx) == G;
+                    if (!mine || ey0 > ey1 || ex0 > ex1) {  // another warp's class / no position in the window
                         beg = end;
                         continue;
                     }
                     if constexpr (U == 1) {
-                        const int rc = LANE_PMAX / (x1 - x0 + 1) > 0 ? LANE_PMAX / (x1 - x0 + 1) : 1;  // rows per chunk
+                        const int rc = LANE_PMAX / (ex1 - ex0 + 1) > 0 ? LANE_PMAX / (ex1 - ex0 + 1) : 1;  // rows per chunk
 #pragma unroll
-                        for (int ya = y0; ya <= y1; ya += rc) {
-                            const int yb = ya + rc - 1 < y1 ? ya + rc - 1 : y1;
-                            LaneTap dq = (ya == y0 && CS == 1) ? dn : tp[beg];
-#pragma unroll kLaneUnroll
-                            for (int t = beg; t < end; ++t) {
-                                const LaneTap d = dq;
-                                dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
+                        for (int ya = ey0; ya <= ey1; ya += rc) {
+                            const int yb = ya + rc - 1 < ey1 ? ya + rc - 1 : ey1;
+                            // one tap: vector loads of the class positions' inputs, then the MACs
+                            auto tap = [&](const LaneTap& d) {
                                 const unsigned char* xa = xin + d.off;
                                 XT xv[HW][NB];
                                 unsigned short vh = 0;
@@ -315,12 +338,12 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
 #pragma unroll
                                 for (int yy = ya; yy <= yb; ++yy)
 #pragma unroll
-                                    for (int xx = x0; xx <= x1; ++xx)
+                                    for (int xx = ex0; xx <= ex1; ++xx)
                                         lds_nb<NB>(xa + ((yy - y0) * W + (xx - x0)) * RB, xv[(yy - y0) * W + xx - x0]);
 #pragma unroll
                                 for (int yy = ya; yy <= yb; ++yy)
 #pragma unroll
-                                    for (int xx = x0; xx <= x1; ++xx)
+                                    for (int xx = ex0; xx <= ex1; ++xx)
 #pragma unroll
                                         for (int j = 0; j < NB; ++j) {
                                             if constexpr (F16)
@@ -330,8 +353,30 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                                                 acc[kk][yy * W + xx][j] =
                                                     mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv[(yy - y0) * W + xx - x0][j]);
                                         }
+                            };
+#if LANE_PAIRS
+                            // taps in 16-byte pairs (one broadcast LDS.128 = one wavefront per two taps):
+                            // an odd leading tap, whole pairs, an odd trailing tap
+                            int t = beg;
+                            if ((t & 1) && t < end) tap(tp[t++]);
+#pragma unroll 2
+                            for (; t + 1 < end; t += 2) {
+                                const float4 q = *reinterpret_cast<const float4*>(tp + t);
+                                tap(LaneTap{q.x, __float_as_int(q.y)});
+                                tap(LaneTap{q.z, __float_as_int(q.w)});
                             }
-                            if (ya + rc > y1) dn = dq;  // = tp[end]: the next class's first tap
+                            if (t < end) tap(tp[t]);
+                            LaneTap dq = dn;  // (running prefetch unused)
+#else
+                            LaneTap dq = (ya == ey0 && CS == 1) ? dn : tp[beg];
+#pragma unroll kLaneUnroll
+                            for (int t = beg; t < end; ++t) {
+                                const LaneTap d = dq;
+                                dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
+                                tap(d);
+                            }
+#endif
+                            if (ya + rc > ey1) dn = dq;  // = tp[end]: the next class's first tap
                         }
                     } else {
                         for (int t = beg; t < end; t += U) {
@@ -389,13 +434,13 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
         for (int cy = 0; cy < AY::N; ++cy)
 #pragma unroll
             for (int cx = 0; cx < AX::N; ++cx) {
-                if (lane_class_group<H, W, CS>(cy * AX::N + cx) != G) continue;
 #pragma unroll
                 for (int yy = AY::lo(cy); yy <= AY::hi(cy); ++yy)
 #pragma unroll
                     for (int xx = AX::lo(cx); xx <= AX::hi(cx); ++xx)
 #pragma unroll
                         for (int j = 0; j < NB; ++j) {
+                            if (lane_pos_group<H, W, CS>(yy, xx) != G) continue;
                             float& o = acc[kk][yy * W + xx][j];
                             if (__float_as_uint(o) == 0x80000000u && ((zm >> (cy * AX::N + cx)) & 1u)) o = 0.f;
                             if (aq) o = fq_store<TIO>((p.flags & SCB_FLAG_RELU) ? relu_io<TIO>(o) : o, p.aq);
@@ -407,7 +452,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
             TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * HW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int q = 0; q < HW; ++q) {
-                if (lane_class_group<H, W, CS>(lane_class_of<H, W>(q)) != G) continue;
+                if (lane_pos_group<H, W, CS>(q / W, q % W) != G) continue;
                 float o[NB];
 #pragma unroll
                 for (int j = 0; j < NB; ++j) o[j] = acc[kk][q][j];
@@ -422,7 +467,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
             asm volatile("bar.sync 1, %0;" ::"r"(WK * 32) : "memory");  // every warp is past the ring
 #pragma unroll
             for (int q = 0; q < HW; ++q) {
-                if (lane_class_group<H, W, CS>(lane_class_of<H, W>(q)) != G) continue;
+                if (lane_pos_group<H, W, CS>(q / W, q % W) != G) continue;
 #pragma unroll
                 for (int j = 0; j < NB; ++j) ex[((size_t)cq * HW + q) * BI + NB * lane + j] = acc[0][q][j];
             }

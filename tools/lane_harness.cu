@@ -23,8 +23,12 @@ static int g_u = 1, g_cs = 1;
 template <int H, int NB, int KW>
 cudaError_t launch(const LaneParams& p, unsigned grid, unsigned thr, size_t smem) {
     if (g_cs == 2) {
-        if (g_u == 2) return launch_lane_t<H, H, NB, KW, MODE_EXACT, 2, false, WF_F32, 2>(p, grid, thr, smem, 0);
-        return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 2>(p, grid, thr, smem, 0);
+        if constexpr (H == 8) return cudaErrorInvalidValue;
+        else return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 2>(p, grid, thr, smem, 0);
+    }
+    if (g_cs == 4) {
+        if constexpr (H == 4) return cudaErrorInvalidValue;
+        else return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 4>(p, grid, thr, smem, 0);
     }
     if (g_u == 2) return launch_lane_t<H, H, NB, KW, MODE_EXACT, 2>(p, grid, thr, smem, 0);
     return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1>(p, grid, thr, smem, 0);
@@ -34,6 +38,7 @@ static cudaError_t dispatch(int H, int nb, int kw, const LaneParams& p, unsigned
 #define D(h, b, w) if (H == h && nb == b && kw == w) return launch<h, b, w>(p, grid, thr, smem);
     D(4, 2, 1)
     D(2, 2, 1)
+    D(8, 1, 1) D(8, 2, 1)
 #undef D
     return cudaErrorInvalidValue;
 }
@@ -105,17 +110,17 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {2}, kws[] = {1}, wks[] = {14, 28}, ccs[] = {4, 8, 12, 16, 32, 48, 64}, nbufs[] = {2, 3}, us[] = {1, 2};
+    const int nbs[] = {1, 2}, kws[] = {1}, wks[] = {8, 14, 16, 28}, ccs[] = {2, 3, 4, 6, 8}, nbufs[] = {2, 3}, us[] = {1};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     double best = 1e30;
     // optional single config: argv[6..10] = nb kw wk cc nbuf
     const bool one = argc > 11;
-    for (int cs : {1, 2}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
+    for (int cs : {1, 2, 4}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
         g_cs = cs;
         if (one && (nb != atoi(argv[6]) || kw != atoi(argv[7]) || cc != atoi(argv[9]) || u != atoi(argv[11]))) continue;
-        if ((H == 2 && nb == 1) || (H == 8 && nb != 1)) continue;
+        if ((H == 2 && nb == 1) || (H == 8 && cs == 2) || (H == 4 && cs == 4) || (H != 8 && nb != 2)) continue;
         g_u = u;
         LaneProgram P;
         if (!build_lane_program(reinterpret_cast<const uint32_t*>(vals.data()), colidx.data(), rowptr.data(), C, K, 9, 3, H, H,
