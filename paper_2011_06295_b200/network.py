@@ -241,8 +241,9 @@ class SparseConvNet:
         from .runner import shard_range
         b = [shard_range(self.batch, self.chains, j) for j in range(self.chains)]
         if any(getattr(self, "minor", None) or []):
-            # image-minor sub-batches start at a multiple of 4 images (16-byte TMA rows)
-            cuts = sorted({min(self.batch, (a + 3) // 4 * 4) for a, _ in b} | {self.batch})
+            # image-minor sub-batches start at a multiple of 8 images (16-byte aligned TMA
+            # rows in f32 and f16)
+            cuts = sorted({min(self.batch, (a + 7) // 8 * 8) for a, _ in b} | {self.batch})
             b = [(a, e) for a, e in zip([0] + cuts[:-1], cuts) if e > a]
         return b
 

@@ -110,7 +110,7 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {1, 2}, kws[] = {1}, wks[] = {8, 14, 16, 28}, ccs[] = {2, 3, 4, 6, 8}, nbufs[] = {2, 3}, us[] = {1};
+    const int nbs[] = {1, 2}, kws[] = {1}, wks[] = {7, 14, 28}, ccs[] = {4, 8, 16}, nbufs[] = {1, 2}, us[] = {1};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -120,7 +120,7 @@ int main(int argc, char** argv) {
     for (int cs : {1, 2, 4}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
         g_cs = cs;
         if (one && (nb != atoi(argv[6]) || kw != atoi(argv[7]) || cc != atoi(argv[9]) || u != atoi(argv[11]))) continue;
-        if ((H == 2 && nb == 1) || (H == 8 && cs == 2) || (H == 4 && cs == 4) || (H != 8 && nb != 2)) continue;
+        if ((H == 2 && nb == 1) || (H == 8 && cs != 4) || (H == 8 && nb != 1) || (H == 4 && cs == 4) || (H != 8 && nb != 2)) continue;
         g_u = u;
         LaneProgram P;
         if (!build_lane_program(reinterpret_cast<const uint32_t*>(vals.data()), colidx.data(), rowptr.data(), C, K, 9, 3, H, H,
