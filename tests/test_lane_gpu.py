@@ -183,28 +183,30 @@ def test_lane_fused_act_quant_bitwise(sc, orc):
             assert beq(y.cpu().numpy(), exp), (cfg, flags)
 
 
-def test_vgg_tail_network_uses_lane_layers_bitwise(sc, orc):
+@pytest.mark.parametrize("dt", [np.float32, np.float16])
+def test_vgg_tail_network_uses_lane_layers_bitwise(sc, orc, dt):
     """conv4_1 .. conv5_3 of VGG-CIFAR (the stack's tail, pools fused) through
     SparseConvNet: the untuned plan runs them on kind-7 launches in image-minor layout
-    (one conversion in, one out), 1 and 2 sub-batch chains and a CUDA graph replay,
-    bit-identical to the oracle layer by layer."""
+    (one conversion in, one out), 1 and 2 sub-batch chains (the second starts at image 16:
+    16-byte TMA alignment in f16) and a CUDA graph replay, bit-identical to the oracle
+    layer by layer."""
     import torch
     from paper_2011_06295_b200 import _abi, engine
     from paper_2011_06295_b200.network import build_net
-    from paper_2011_06295_b200.synth import vgg16_cifar
+    from paper_2011_06295_b200.synth import f16_scaled, vgg16_cifar
     specs = vgg16_cifar(0.9)
     tail = [(s, p) for s, p in specs if s.name.startswith(("conv4", "conv5"))]
     n = 24
-    net = build_net(tail, seed=0)
+    net = build_net(tail, seed=0, dtype=dt, weight_fn=f16_scaled if dt == np.float16 else None)
     net.plan(n, tune=False)
     assert all(engine.launch_kind(l) == _abi.KIND_LANE for l in net.launches)
     rng = np.random.default_rng(1)
-    x = np.maximum(rng.standard_normal((n, *net.in_shape)), 0).astype(np.float32)
+    x = np.maximum(rng.standard_normal((n, *net.in_shape)), 0).astype(dt)
     cur = x
     for L in net.layers:
         sh = L.kernel.shape
         cur = orc.conv_sparse(cur, L.kernel.values, L.kernel.colidx, L.kernel.rowptr, sh.k, 3, 3, 1, 1, L.bias)
-        cur = relu_pool_ref(cur) if L.pool else np.maximum(cur, 0)
+        cur = relu_pool_ref(cur) if L.pool else np.maximum(cur, cur.dtype.type(0))
     xd = torch.from_numpy(x).cuda()
     for chains in (1, 2):
         net.set_chains(chains)
