@@ -393,7 +393,10 @@ DIRECTS = [d + (2,) for d in DIRECTS] + \
           [(3, 3, 1, 8, lw, 2, 1, 4) for lw in (32, 16, 8)] + \
           [(3, 3, 1, 8, lw, 2, 2, 3) for lw in (32, 16, 8)] + \
           [(3, 3, 1, 16, lw, kw, 1, 2) for lw in (32, 16) for kw in (2, 4)] + \
-          [(3, 3, 1, 4, 4, kw, 2, 2) for kw in (4, 8)]  # + min CTAs/SM (4: <= 64 regs)
+          [(3, 3, 1, 4, 4, kw, 2, 2) for kw in (4, 8)] + \
+          [(3, 3, 1, th, lw, kw, 1, 4) for lw in (32, 16, 8) for th, kw in ((4, 2), (2, 4))]
+# (the last row: small per-lane tiles -- more warps for the 32-image shards of 8 GPUs)
+# + min CTAs/SM (4: <= 64 regs)
 # wide direct variants (column tiles of 32 for output rows wider than 32, e.g. the
 # ImageNet shapes; also rows whose width is no tile width, 28/14/7): (R, S, PAD, TH, LW, KW, min CTAs/SM)
 DIRECTS_WIDE = [(3, 3, 1, th, lw, kw, 2) for lw in (32, 16, 8) for th in (4, 8) for kw in (4, 8)] + \

@@ -6,7 +6,7 @@
 // build: nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo
 //        -Xcompiler -ffp-contract=off -I include -I paper_2011_06295_b200/csrc
 //        tools/lane_harness.cu -o tools/lane_harness
-// run:   tools/lane_harness H C K L N   (sweeps NB, KW, warps, cc, nbuf)
+// run:   tools/lane_harness H C K L N   (sweeps CS, U, NB, warps, cc, nbuf; 8x8 = quadrant split)
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -36,9 +36,9 @@ cudaError_t launch(const LaneParams& p, unsigned grid, unsigned thr, size_t smem
 
 static cudaError_t dispatch(int H, int nb, int kw, const LaneParams& p, unsigned grid, unsigned thr, size_t smem) {
 #define D(h, b, w) if (H == h && nb == b && kw == w) return launch<h, b, w>(p, grid, thr, smem);
-    D(4, 2, 1)
-    D(2, 2, 1)
-    D(8, 1, 1) D(8, 2, 1)
+    D(4, 1, 1) D(4, 2, 1) D(4, 4, 1)
+    D(2, 2, 1) D(2, 4, 1)
+    D(8, 1, 1)
 #undef D
     return cudaErrorInvalidValue;
 }
@@ -110,7 +110,7 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {1, 2}, kws[] = {1}, wks[] = {7, 14, 28}, ccs[] = {4, 8, 16}, nbufs[] = {1, 2}, us[] = {1};
+    const int nbs[] = {1, 2, 4}, kws[] = {1}, wks[] = {7, 14, 16, 28}, ccs[] = {8, 16, 32, 64}, nbufs[] = {1, 2, 3}, us[] = {1, 2};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -120,7 +120,7 @@ int main(int argc, char** argv) {
     for (int cs : {1, 2, 4}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
         g_cs = cs;
         if (one && (nb != atoi(argv[6]) || kw != atoi(argv[7]) || cc != atoi(argv[9]) || u != atoi(argv[11]))) continue;
-        if ((H == 2 && nb == 1) || (H == 8 && cs != 4) || (H == 8 && nb != 1) || (H == 4 && cs == 4) || (H != 8 && nb != 2)) continue;
+        if ((H == 8 && (cs != 4 || nb != 1 || u != 1)) || (H == 4 && cs == 4) || (H == 2 && nb == 1) || (cs > 1 && u > 1)) continue;
         g_u = u;
         LaneProgram P;
         if (!build_lane_program(reinterpret_cast<const uint32_t*>(vals.data()), colidx.data(), rowptr.data(), C, K, 9, 3, H, H,

@@ -31,3 +31,18 @@ for _ in range(a.reps):
 rows = [{"layer": L.name, "us": round(statistics.median(t), 2), "kind": engine.launch_kind(l), "launch": l}
         for L, t, l in zip(net.layers, per, net.launches)]
 print(json.dumps({"batch": a.batch, "sum_us": round(sum(r["us"] for r in rows), 1), "layers": rows}))
+# whole-step time: eager launches vs one CUDA graph replay (launch overhead at small shards)
+for graph in (False, True):
+    if graph:
+        net.capture()
+    for _ in range(5):
+        net.forward_device(x)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(a_reps := 50):
+        net.forward_device(x)
+    b.record()
+    b.synchronize()
+    print(json.dumps({"batch": int(x.shape[0]),
+                      "cuda_graph": graph, "ms_per_step": round(a.elapsed_time(b) / a_reps, 4)}))
