@@ -378,7 +378,7 @@ LANES = [(h, nb, 1, u) for h in (2, 4) for nb in (1, 2, 4) for u in (1, 2) if no
 # class split: two warps per output channel, each a fixed half of the position classes (CS = 2)
 LANES_CS = [(4, 2, 1, 2), (2, 2, 2, 2), (4, 1, 1, 2), (2, 1, 2, 2), (2, 1, 2, 4), (2, 4, 1, 4), (2, 4, 1, 2)]  # (H, NB, U, CS)
 # f16 storage (FHFMA, in-register weight decode of every f16 format): (H = W, NB)
-LANES_F16 = [(4, 2), (2, 2), (2, 4)]
+LANES_F16 = [(4, 2, 1), (2, 2, 1), (2, 4, 1), (4, 2, 2), (2, 4, 4)]  # (H, NB, CS)
 DIMGS_F16 = [(2, 2), (2, 4), (2, 8), (4, 2), (4, 4)]  # f16 storage, FHFMA
 
 # dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW, VX)
@@ -479,8 +479,8 @@ def main():
         groups[("lane", H, NB, KW, U)] = ([], [("lane", H, NB, KW, U, m) for m in (EXACT, FMA)])
     for H, NB, U, CS in LANES_CS:
         groups[("lanecs", H, NB, U, CS)] = ([], [("lanecs", H, NB, U, CS, m) for m in (EXACT, FMA)])
-    for H, NB in LANES_F16:
-        groups[("lane16", H, NB)] = ([], [("lane16", H, NB, wf) for wf in (WF_F16,) + QFMTS])
+    for H, NB, CS in LANES_F16:
+        groups[("lane16", H, NB, CS)] = ([], [("lane16", H, NB, CS, wf) for wf in (WF_F16,) + QFMTS])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
     parts = [[] for _ in range(N_PARTS)]
     load = [0] * N_PARTS
@@ -513,10 +513,10 @@ def main():
                                 f"&launch_lane_t<{H}, {H}, {NB}, 1, {mode}, {U}, false, {WF_F32}, {CS}>}},\n")
                     continue
                 if v[0] == "lane16":
-                    _, H, NB, wf = v
-                    ents.append(f"    {{{{3, 3, 1, {NB}, {H}, {H}, SCB_F16, {wf}, {FMA}, 1, 1, "
-                                f"{KIND_LANE}}}, nullptr, nullptr, 544, nullptr, "
-                                f"&launch_lane_t<{H}, {H}, {NB}, 1, {FMA}, 1, true, {wf}>}},\n")
+                    _, H, NB, CS, wf = v
+                    ents.append(f"    {{{{3, 3, {CS}, {NB}, {H}, {H}, SCB_F16, {wf}, {FMA}, 1, 1, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, {1024 if CS > 1 else 544}, nullptr, "
+                                f"&launch_lane_t<{H}, {H}, {NB}, 1, {FMA}, 1, true, {wf}, {CS}>}},\n")
                     continue
                 if v[0] == "lane":  # info: kt = KW, nbt = NB, th = H, tw = W, dispatch = U
                     _, H, NB, KW, U, mode = v
