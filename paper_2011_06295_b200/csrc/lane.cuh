@@ -160,7 +160,7 @@ __device__ __forceinline__ void store_nb(float* y, const float (&o)[NB], int nva
 
 // thread limit: 16 consumer warps + the producer; 8 + 1 for 8x8 planes (64 accumulators per lane)
 template <int H, int W, int CS = 1>
-constexpr int lane_max_threads() { return CS > 1 ? 1024 : (H * W >= 64 ? 288 : 544); }
+constexpr int lane_max_threads() { return CS == 3 ? 768 : (CS > 1 ? 1024 : (H * W >= 64 ? 288 : 544)); }
 
 // class index (cy * AX::N + cx) of output position q of an H x W plane
 template <int H, int W>
@@ -171,10 +171,16 @@ __host__ __device__ constexpr int lane_class_of(int q) {
 // class split: group of class ci when CS warps share an output channel (balanced MACs):
 // 4x4 (CS = 2) -- {interior, top edge, top-left corner} | {other edges and corners};
 // 2x2 -- CS = 2: rows, CS = 4: one position each
+// 4x4 (CS = 3) -- {interior} | {top, bottom edges, TL, BR corners} | {left, right edges, TR, BL}
 template <int H, int W, int CS>
 __host__ __device__ constexpr int lane_class_group(int ci) {
-    static_assert(CS == 1 || CS == 2 || (CS == 4 && ((H == 2 && W == 2) || (H == 8 && W == 8))), "class split");
-    return CS == 1 || H == 8 ? 0 : (H == 2 ? ci * CS / 4 : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1));
+    static_assert(CS == 1 || CS == 2 || (CS == 3 && H == 4 && W == 4) ||
+                      (CS == 4 && ((H == 2 && W == 2) || (H == 8 && W == 8))),
+                  "class split");
+    return CS == 1 || H == 8 ? 0
+           : H == 2          ? ci * CS / 4
+           : CS == 3         ? (ci == 4 ? 0 : ((ci == 1 || ci == 7 || ci == 0 || ci == 8) ? 1 : 2))
+                             : ((ci == 4 || ci == 1 || ci == 0) ? 0 : 1);
 }
 // 8x8 planes split by QUADRANT instead (CS = 4): group G owns rows / columns [lo, hi] of
 // its 4x4 quadrant (every class list is shared; a warp covers class positions in its window)
@@ -506,6 +512,10 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
     };  // consume
     if (cgrp == 0) consume(std::integral_constant<int, 0>{});
     else if constexpr (CS == 2) consume(std::integral_constant<int, 1>{});
+    else if constexpr (CS == 3) {
+        if (cgrp == 1) consume(std::integral_constant<int, 1>{});
+        else consume(std::integral_constant<int, 2>{});
+    }
     else if constexpr (CS == 4) {
         if (cgrp == 1) consume(std::integral_constant<int, 1>{});
         else if (cgrp == 2) consume(std::integral_constant<int, 2>{});

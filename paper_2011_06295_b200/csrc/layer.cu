@@ -1071,7 +1071,7 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
         if (v.kind == KIND_LANE) {
-            for (int wk : {4, 8, 14, 16, 28})
+            for (int wk : {4, 8, 14, 16, 21, 28})
                 for (int cc : {4, 8, 12, 16, 32, 48, 64})
                     for (int ns : {2, 3}) {
                         scb_launch c{vi, wk, 32 * v.nbt, g.h, g.w, cc, ns};

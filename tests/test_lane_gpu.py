@@ -278,7 +278,7 @@ def test_lane_class_split_bitwise(sc, orc, hw):
     for flags, exp in cases:
         all_c = _lane_cands(layer, n, flags)
         splits = sorted({vs[cf[0]]["kt"] for cf in all_c} - {1})
-        assert splits == ([2, 4] if hw == 2 else [2]), splits
+        assert splits == ([2, 4] if hw == 2 else [2, 3]), splits
         cands = []
         for cs in splits:
             sub = [cf for cf in all_c if vs[cf[0]]["kt"] == cs]

@@ -26,6 +26,10 @@ cudaError_t launch(const LaneParams& p, unsigned grid, unsigned thr, size_t smem
         if constexpr (H == 8) return cudaErrorInvalidValue;
         else return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 2>(p, grid, thr, smem, 0);
     }
+    if (g_cs == 3) {
+        if constexpr (H != 4) return cudaErrorInvalidValue;
+        else return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 3>(p, grid, thr, smem, 0);
+    }
     if (g_cs == 4) {
         if constexpr (H == 4) return cudaErrorInvalidValue;
         else return launch_lane_t<H, H, NB, KW, MODE_EXACT, 1, false, WF_F32, 4>(p, grid, thr, smem, 0);
@@ -110,17 +114,17 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
     printf("layer H=W=%d C=%d K=%d L=%d N=%d  counted MACs %.3e  SMs %d\n", H, C, K, L, N, counted, sms);
-    const int nbs[] = {1, 2, 4}, kws[] = {1}, wks[] = {7, 14, 16, 28}, ccs[] = {8, 16, 32, 64}, nbufs[] = {1, 2, 3}, us[] = {1, 2};
+    const int nbs[] = {2, 4}, kws[] = {1}, wks[] = {21, 28}, ccs[] = {8, 12, 16}, nbufs[] = {2, 3}, us[] = {1};
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     double best = 1e30;
     // optional single config: argv[6..10] = nb kw wk cc nbuf
     const bool one = argc > 11;
-    for (int cs : {1, 2, 4}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
+    for (int cs : {2, 3}) for (int u : us) for (int nb : nbs) for (int kw : kws) for (int cc : ccs) {
         g_cs = cs;
         if (one && (nb != atoi(argv[6]) || kw != atoi(argv[7]) || cc != atoi(argv[9]) || u != atoi(argv[11]))) continue;
-        if ((H == 8 && (cs != 4 || nb != 1 || u != 1)) || (H == 4 && cs == 4) || (H == 2 && nb == 1) || (cs > 1 && u > 1)) continue;
+        if (H != 4 || (cs == 2 && nb == 4)) continue;
         g_u = u;
         LaneProgram P;
         if (!build_lane_program(reinterpret_cast<const uint32_t*>(vals.data()), colidx.data(), rowptr.data(), C, K, 9, 3, H, H,
