@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="reference arm: time budget of warm-up + timed steps (bounds the per-step sample)")
     ap.add_argument("--chains", type=int, default=2, help="sub-batch chains on separate streams per GPU")
+    ap.add_argument("--no-fuse-layouts", action="store_true",
+                    help="separate layout-conversion kernels around the image-minor layers")
     ap.add_argument("--graph", type=int, default=0, help="1: replay the stack as one CUDA graph per step")
     ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch between layers")
     ap.add_argument("--no-dense", action="store_true")
@@ -676,6 +678,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2011_06295_b200.runner import shard_range, shard_sizes
     specs = workload(args.sparsity)
     net = build_net(specs, seed=0, device=local_rank)
+    net.fuse_layouts = not args.no_fuse_layouts
     # strong scaling: the global batch is split into contiguous shards, one per rank
     s0, s1 = shard_range(args.batch, world, rank)
     nloc = s1 - s0

@@ -73,6 +73,11 @@ typedef struct {
                                      scb_conv_sparse_ld, = n for scb_conv_sparse); the
                                      layout of the kind-7 image-lane kernels, which only
                                      accept it (scb_to_image_minor converts NCHW)  */
+#define SCB_FLAG_Y_IMAGE_MINOR 0x80u /* NCHW x, image-minor y (row stride ldy): the
+                                     narrow direct kernels (kind 2, dispatch 0) write the
+                                     next kind-7 layer's input layout directly       */
+#define SCB_FLAG_Y_NCHW    0x100u /* with SCB_FLAG_IMAGE_MINOR: kind-7 kernels write an
+                                     NCHW y (the last layer of an image-minor run)  */
 
 /* Launch configuration: replaces EnginePlan.sub_batch_size (engine.py:28-39)
  * and the timed tune_sub_batch (engine.py:143-166). variant < 0 = generic. */

@@ -27,6 +27,8 @@ SCB_W_NATIVE, SCB_W_CB4, SCB_W_LIN16, SCB_W_AFF16 = 0, 1, 2, 3
 FLAG_RELU, FLAG_FAST, FLAG_POOL2, FLAG_GENERIC, FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8, 0x10
 FLAG_ACT_QUANT = 0x20
 FLAG_IMAGE_MINOR = 0x40  # x / y image-minor: ((c*H + h)*W + w)*ld + n (kind-7 launches)
+FLAG_Y_IMAGE_MINOR = 0x80  # NCHW x, image-minor y (narrow direct kernels)
+FLAG_Y_NCHW = 0x100  # with FLAG_IMAGE_MINOR: NCHW y (kind-7 kernels)
 KIND_LANE = 7
 
 # every symbol include/sparseconv_b200.h declares

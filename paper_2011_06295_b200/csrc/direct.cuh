@@ -61,6 +61,7 @@ struct DirectParams {
     QuantAux q;               // f16 kernels: in-register weight decode (codebook / scales)
     const int32_t* blkoff;    // k_direct: [group*nst + st] 16-byte-chunk offset of each tap block (+ end)
     uint32_t flags;
+    int64_t ldy;              // SCB_FLAG_Y_IMAGE_MINOR: row stride of the image-minor output
 };
 
 // wait until at most NB-1 committed cp.async groups are pending
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
     }
     const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;  // (already applied with the quantizer)
     const bool pool = p.flags & SCB_FLAG_POOL2;
+    const bool ymin = !WIDE && !ONED && (p.flags & SCB_FLAG_Y_IMAGE_MINOR);
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -393,6 +395,20 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                     float o0 = acc[kk][j];
                     if (relu) o0 = relu_io<TIO>(o0);
                     if (ox0 + lx + j * LW < p.f) yp[j * LW] = o0;
+                }
+            }
+        } else if (!pool && ymin) {  // image-minor output: element (n, k, y, x) at ((k*E + y)*F + x)*ldy + n
+            if (n < p.n && ox0 + lx < p.f) {
+                const int jmax = min(TH, p.e - oy0);
+#pragma unroll
+                for (int j = 0; j < TH; ++j) {
+                    if (j >= jmax) break;
+#pragma unroll
+                    for (int v = 0; v < VX; ++v) {
+                        float o0 = acc[kk][j * VX + v];
+                        if (relu) o0 = relu_io<TIO>(o0);
+                        static_cast<TIO*>(p.y)[(((int64_t)k * p.e + oy0 + j) * p.f + ox0 + lx + v) * p.ldy + n] = (TIO)o0;
+                    }
                 }
             }
         } else if (!pool) {
@@ -432,8 +448,12 @@ __global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB) k
                 }
                 if (relu) o = relu_io<TIO>(o);
                 const int py = (oy0 + j) >> 1;
-                if (n < p.n && !(lx & 1) && ox0 + lx < p.f && py < pe)
-                    static_cast<TIO*>(p.y)[(((int64_t)n * p.k + k) * pe + py) * pf + ((ox0 + lx) >> 1)] = (TIO)o;
+                if (n < p.n && !(lx & 1) && ox0 + lx < p.f && py < pe) {
+                    const int64_t pq = (int64_t)py * pf + ((ox0 + lx) >> 1);  // pooled position
+                    const int64_t plane = (int64_t)pe * pf;
+                    static_cast<TIO*>(p.y)[ymin ? ((int64_t)k * plane + pq) * p.ldy + n
+                                                : ((int64_t)n * p.k + k) * plane + pq] = (TIO)o;
+                }
             }
         }
     }

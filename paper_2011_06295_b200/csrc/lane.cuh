@@ -145,6 +145,14 @@ __device__ __forceinline__ void store_nb(__half* y, const float (&o)[NB], int nv
         if (j < nvalid) y[j] = __float2half_rn(o[j]);
 }
 
+// NCHW store of a lane's NB images of output (k, position q): y[(n*K + k)*PLANE + q]
+template <int NB, typename T>
+__device__ __forceinline__ void store_nchw(T* y, int K, int plane, int k, int q, int nfirst, int n, const float (&o)[NB]) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+        if (nfirst + j < n) y[((size_t)(nfirst + j) * K + k) * plane + q] = T(o[j]);
+}
+
 // store a lane's NB consecutive images (nvalid of them exist), one vector store when allowed
 template <int NB>
 __device__ __forceinline__ void store_nb(float* y, const float (&o)[NB], int nvalid, bool vec) {
@@ -432,6 +440,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
     const bool pool = p.flags & SCB_FLAG_POOL2;
     // vector stores when every row start is NB-element aligned (row stride and base)
     const bool vec = (p.ldy % NB) == 0 && (reinterpret_cast<uintptr_t>(p.y) % (ES * NB)) == 0;
+    const bool ynchw = p.flags & SCB_FLAG_Y_NCHW;  // NCHW output (the last layer of an image-minor run)
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -462,7 +471,8 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                 float o[NB];
 #pragma unroll
                 for (int j = 0; j < NB; ++j) o[j] = acc[kk][q][j];
-                store_nb<NB>(yp + (size_t)q * p.ldy, o, p.n - (n0 + NB * lane), vec);
+                if (ynchw) store_nchw<NB>(static_cast<TIO*>(p.y), p.k, HW, k, q, n0 + NB * lane, p.n, o);
+                else store_nb<NB>(yp + (size_t)q * p.ldy, o, p.n - (n0 + NB * lane), vec);
             }
         }
     }
@@ -505,7 +515,8 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                         o[j] = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
                         if (relu) o[j] = relu_io<TIO>(o[j]);
                     }
-                    store_nb<NB>(yp + (size_t)(py * PW + px) * p.ldy, o, p.n - (n0 + NB * lane), vec);
+                    if (ynchw) store_nchw<NB>(static_cast<TIO*>(p.y), p.k, PHW, k, py * PW + px, n0 + NB * lane, p.n, o);
+                    else store_nb<NB>(yp + (size_t)(py * PW + px) * p.ldy, o, p.n - (n0 + NB * lane), vec);
                 }
         }
     }

@@ -641,8 +641,12 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     const Geom& g = L->g;
     if (L->dt == SCB_F64) return false;
     if (g.stride != 1 || v.r != g.r || v.s != g.s || v.pad != g.pad) return false;
-    // image-minor activations are the layout of the kind-7 kernels only
+    // image-minor activations are the layout of the kind-7 kernels only; an image-minor
+    // output from NCHW input is written by the narrow direct kernels, an NCHW output from
+    // image-minor input by kind 7
     if (((flags & SCB_FLAG_IMAGE_MINOR) != 0) != (v.kind == KIND_LANE)) return false;
+    if ((flags & SCB_FLAG_Y_NCHW) && v.kind != KIND_LANE) return false;
+    if ((flags & SCB_FLAG_Y_IMAGE_MINOR) && !(v.kind == KIND_DIRECT && v.dispatch == DISPATCH_JUMP)) return false;
     // f32 direct / image-lane / TMEM kernels take any weight format: their tap blocks carry
     // the decoded native value (decoded once on upload, direct_blocks); the f16 ones decode
     // the compact tap's payload in registers, so their format must match the layer's
@@ -1519,6 +1523,11 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
     if (minor && (c.variant < 0 || (flags & SCB_FLAG_GENERIC)))
         return fail(SCB_ERR_UNSUPPORTED, "image-minor activations need a kind-7 (image-lane) launch");
     if (minor && (ldx < n || ldy < n)) return fail(SCB_ERR_ARG, "image-minor row stride smaller than the batch");
+    if ((flags & SCB_FLAG_Y_IMAGE_MINOR) && (minor || ldy < n))
+        return fail(SCB_ERR_ARG, "SCB_FLAG_Y_IMAGE_MINOR: NCHW input and an output row stride >= the batch");
+    if ((flags & SCB_FLAG_Y_NCHW) && !minor) return fail(SCB_ERR_ARG, "SCB_FLAG_Y_NCHW needs SCB_FLAG_IMAGE_MINOR");
+    if ((flags & (SCB_FLAG_Y_IMAGE_MINOR | SCB_FLAG_Y_NCHW)) && (c.variant < 0 || (flags & SCB_FLAG_GENERIC)))
+        return fail(SCB_ERR_UNSUPPORTED, "output layout flags need a direct / image-lane launch");
     if (c.variant < 0 || (flags & SCB_FLAG_GENERIC)) {
         if (flags & SCB_FLAG_POOL2) return fail(SCB_ERR_UNSUPPORTED, "fused pool needs a tiled variant");
         GenericParams p;
@@ -1597,6 +1606,7 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
         q.cc = c.cc; q.nst = (g.c + c.cc - 1) / c.cc; q.wk = c.warps_k;
         q.ip = d.chunk; q.stage_el = d.stage_el;
         q.kblocks = d.kblocks; q.n_ey = d.n_ey; q.nfx = d.n_fx; q.nb = d.nb; q.segcap = d.wp; q.flags = flags;
+        q.ldy = ldy;
         q.q = L->q;
         if (ve.info.kind == KIND_DIRECT || ve.info.kind == KIND_DIMG) {  // fused fake-quant epilogue
             q.aq = L->aq;

@@ -101,6 +101,7 @@ class SparseConvNet:
         self._dense = [None] * len(self.layers)
         self.chains = 1
         self.pdl = True  # programmatic dependent launch between consecutive layer kernels
+        self.fuse_layouts = True  # layout changes written by the neighbouring layer kernels
         self._side_streams = []
 
     # ---- shapes ---------------------------------------------------------
@@ -181,27 +182,47 @@ class SparseConvNet:
         self.ld = ld
         self.minor = [a == "sparse-direct" and engine.launch_kind(l) == _abi.KIND_LANE
                       for l, a in zip(self.launches, self.algorithms)]
+        nl = len(self.layers)
+        # fused layout changes: a narrow direct layer feeding an image-minor run writes its output
+        # image-minor (SCB_FLAG_Y_IMAGE_MINOR), and the last layer of an image-minor run writes
+        # NCHW (SCB_FLAG_Y_NCHW) -- no conversion kernel at either end when the launch allows it
+        self.yflag = [0] * nl
+        vs = _abi.variants()
+        for i in range(nl):
+            l = self.launches[i]
+            if self.algorithms[i] != "sparse-direct" or l is None or not self.fuse_layouts:
+                continue
+            nxt_minor = i + 1 < nl and self.minor[i + 1]
+            if not self.minor[i] and nxt_minor and vs[l[0]]["kind"] == 2 and vs[l[0]]["dispatch"] == 0:
+                f = self.flags(i) | _abi.FLAG_Y_IMAGE_MINOR
+                if self.dlayers[i].launch_ok(self.batch, f, l):
+                    self.yflag[i] = _abi.FLAG_Y_IMAGE_MINOR
+            elif self.minor[i] and not nxt_minor:
+                f = self.flags(i) | _abi.FLAG_IMAGE_MINOR | _abi.FLAG_Y_NCHW
+                if self.dlayers[i].launch_ok(self.batch, f, l):
+                    self.yflag[i] = _abi.FLAG_Y_NCHW
+        # output layout of each layer, and a conversion buffer where a layer's input differs
+        self.out_minor = [(m and self.yflag[i] != _abi.FLAG_Y_NCHW) or self.yflag[i] == _abi.FLAG_Y_IMAGE_MINOR
+                          for i, m in enumerate(self.minor)]
         self.acts = []
         self.xconv = []
-        prev_minor = False
-        for i in range(len(self.layers)):
+        for i in range(nl):
             n, k, e, f = self.out_shape(i, self.batch)
-            if self.minor[i]:
+            if self.out_minor[i]:
                 self.acts.append(torch.empty((k * e * f, ld), dtype=self.tdtype, device=self.tdev))
             else:
                 self.acts.append(torch.empty((n, k, e, f), dtype=self.tdtype, device=self.tdev))
-            # layout conversion of this layer's input when it differs from the producer's
             sh = self.layers[i].kernel.shape
-            if self.minor[i] and not prev_minor:
+            in_minor = i > 0 and self.out_minor[i - 1]
+            if self.minor[i] and not in_minor:
                 self.xconv.append(torch.empty((sh.c * sh.h * sh.w, ld), dtype=self.tdtype, device=self.tdev))
-            elif prev_minor and not self.minor[i]:
+            elif in_minor and not self.minor[i]:
                 self.xconv.append(torch.empty((self.batch, sh.c, sh.h, sh.w), dtype=self.tdtype, device=self.tdev))
             else:
                 self.xconv.append(None)
-            prev_minor = self.minor[i]
         # NCHW result of the stack (the last layer's output, converted when image-minor)
-        self.result = torch.empty(self.out_shape(len(self.layers) - 1, self.batch), dtype=self.tdtype,
-                                  device=self.tdev) if self.minor[-1] else self.acts[-1]
+        self.result = torch.empty(self.out_shape(nl - 1, self.batch), dtype=self.tdtype,
+                                  device=self.tdev) if self.out_minor[-1] else self.acts[-1]
         for i, L in enumerate(self.layers):
             self.scratch[i] = None
             if self.launches[i] is None and L.pool:
@@ -222,7 +243,8 @@ class SparseConvNet:
                 continue
             for n in sizes:
                 for pdl in (0, _abi.FLAG_NO_PDL):
-                    self.dlayers[i].prepare(n, self.flags(i) | pdl | self._layout_flag(i), self.launches[i])
+                    self.dlayers[i].prepare(n, self.flags(i) | pdl | self._layout_flag(i) | self.yflag[i],
+                                            self.launches[i])
 
     def set_chains(self, chains: int) -> None:
         """Run the batch as `chains` independent sub-batch chains on their own
@@ -278,6 +300,9 @@ class SparseConvNet:
                 self.dense_layer(i)(cur[a:e], self.acts[i][a:e])
             self._dense_quant(i, self.acts[i][a:e], s)
             return self.acts[i], False
+        pdl = 0 if self.pdl else _abi.FLAG_NO_PDL
+        b = self.biases[i]
+        bptr = b.data_ptr() if b is not None else 0
         if self.minor[i]:
             if not cur_minor:
                 sh = self.layers[i].kernel.shape
@@ -285,14 +310,18 @@ class SparseConvNet:
                 _abi.to_image_minor(self.dtype, cur[a:e].data_ptr(), self._minor_ptr(xc, a), n,
                                     sh.c * sh.h * sh.w, self.ld, s)
                 cur = xc
-            b = self.biases[i]
-            self.dlayers[i].launch(self._minor_ptr(cur, a), b.data_ptr() if b is not None else 0,
-                                   self._minor_ptr(self.acts[i], a), n,
-                                   self.flags(i) | _abi.FLAG_IMAGE_MINOR | (0 if self.pdl else _abi.FLAG_NO_PDL),
+            y = self._minor_ptr(self.acts[i], a) if self.out_minor[i] else self.acts[i][a:e].data_ptr()
+            self.dlayers[i].launch(self._minor_ptr(cur, a), bptr, y, n,
+                                   self.flags(i) | _abi.FLAG_IMAGE_MINOR | self.yflag[i] | pdl,
                                    self.launches[i], s, ldx=self.ld, ldy=self.ld)
-            return self.acts[i], True
+            return self.acts[i], self.out_minor[i]
         if cur_minor:
             cur = self._to_nchw(i, cur, rows, s)
+        if self.yflag[i] == _abi.FLAG_Y_IMAGE_MINOR:  # writes the next layer's image-minor input
+            self.dlayers[i].launch(cur[a:e].data_ptr(), bptr, self._minor_ptr(self.acts[i], a), n,
+                                   self.flags(i) | _abi.FLAG_Y_IMAGE_MINOR | pdl, self.launches[i], s,
+                                   ldy=self.ld)
+            return self.acts[i], True
         self.launch_layer(i, cur, self.acts[i], s, rows)
         return self.acts[i], False
 
@@ -395,19 +424,18 @@ class SparseConvNet:
         (only the direct and image-lane epilogues do), +1 after a dense layer with one."""
         vs = _abi.variants()
         n = 0
-        prev_minor = False
+        prev_out_minor = False
         for i, (l, L, a) in enumerate(zip(self.launches, self.layers, self.algorithms)):
             aq = L.act_quant is not None
-            minor = self.minor[i]
-            n += 1 if minor != prev_minor else 0  # layout conversion of the input
-            prev_minor = minor
+            n += 1 if self.minor[i] != prev_out_minor else 0  # layout conversion of the input
+            prev_out_minor = self.out_minor[i]
             if a == "dense-cudnn":
                 n += 1 if aq else 0
                 continue
             n += 2 if (l is None and L.pool) else 1
             if aq and (l is None or vs[l[0]]["kind"] not in (2, 3, 7)):
                 n += 1
-        return n + (1 if prev_minor else 0)
+        return n + (1 if prev_out_minor else 0)
 
     def forward_device(self, x_dev=None, events=None):
         """Run the stack on the current stream of the device; returns the last

@@ -213,7 +213,7 @@ def test_vgg_tail_network_uses_lane_layers_bitwise(sc, orc, dt):
         assert beq(net.forward_device(xd).cpu().numpy(), cur), chains
     net.capture()
     assert beq(net.forward_device(xd).cpu().numpy(), cur)
-    assert net.kernels_per_step() == len(tail) + 2
+    assert net.kernels_per_step() == len(tail) + 1  # input conversion; the last layer writes NCHW
 
 
 @pytest.mark.parametrize("fmt", ["native", "cb4", "lin16", "aff16"])
@@ -288,3 +288,46 @@ def test_lane_class_split_bitwise(sc, orc, hw):
             engine.run_layer(layer, xd.data_ptr(), bd.data_ptr(), y, n, flags, cfg, st)
             torch.cuda.synchronize()
             assert beq(y.cpu().numpy(), exp), (cfg, flags)
+
+
+def test_fused_output_layouts_bitwise(sc, orc):
+    """SCB_FLAG_Y_IMAGE_MINOR (a narrow direct kernel writes an image-minor output, with pool)
+    and SCB_FLAG_Y_NCHW (a kind-7 kernel writes NCHW): the layout changes at both ends of an
+    image-minor run without conversion kernels, bitwise."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    vs = _abi.variants()
+    st = torch.cuda.current_stream().cuda_stream
+    # direct 8x8 -> image-minor pooled 4x4 output (conv3_3-like), sub-batch at image 8
+    n, ld, a = 20, 40, 8
+    sh, w, x, b = _layer(sc, 64, 8, 48, 0.9, n)
+    kern = sc.build_csr(w, sh)
+    ref = relu_pool_ref(orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 48, 3, 3, 1, 1, b))
+    layer = device_layer(kern, 0, np.float32)
+    fl = _abi.FLAG_RELU | _abi.FLAG_POOL2 | _abi.FLAG_Y_IMAGE_MINOR
+    cands = layer.candidates(n, fl)
+    assert cands and all(vs[c[0]]["kind"] == 2 and vs[c[0]]["dispatch"] == 0 for c in cands)
+    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    for cfg in cands[:: max(1, len(cands) // 8)]:
+        ym = torch.full((48 * 16, ld), -3.0, device="cuda")
+        layer.launch(xd.data_ptr(), bd.data_ptr(), ym.data_ptr() + 4 * a, n, fl, cfg, st, ldy=ld)
+        got = ym[:, a:a + n].T.contiguous().cpu().numpy().reshape(ref.shape)
+        assert beq(got, ref), cfg
+        assert torch.all(ym[:, :a] == -3.0) and torch.all(ym[:, a + n:] == -3.0)
+    # kind 7 on image-minor input -> NCHW output (plain and pooled)
+    sh, w, x, b = _layer(sc, 128, 2, 64, 0.9, n)
+    kern = sc.build_csr(w, sh)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, 64, 3, 3, 1, 1, b)
+    layer = device_layer(kern, 0, np.float32)
+    xm = torch.zeros((128 * 4, ld), device="cuda")
+    xm[:, a:a + n] = torch.from_numpy(x.reshape(n, -1).T.copy()).cuda()
+    bd = torch.from_numpy(b).cuda()
+    for extra, exp in ((0, ref), (_abi.FLAG_RELU | _abi.FLAG_POOL2, relu_pool_ref(ref))):
+        fl = _abi.FLAG_IMAGE_MINOR | _abi.FLAG_Y_NCHW | extra
+        cands = layer.candidates(n, fl)
+        assert cands
+        for cfg in cands[:: max(1, len(cands) // 8)]:
+            y = torch.full(exp.shape, -3.0, device="cuda")
+            layer.launch(xm.data_ptr() + 4 * a, bd.data_ptr(), y.data_ptr(), n, fl, cfg, st, ldx=ld, ldy=ld)
+            assert beq(y.cpu().numpy(), exp), (cfg, extra)
