@@ -191,8 +191,9 @@ SCB_API scb_status scb_conv_sparse(const scb_layer* layer, const void* x, const 
  * (SCB_FLAG_IMAGE_MINOR): x rows (c, h, w) hold images at x[row*ldx + i], i < n, and
  * y rows likewise with ldy -- a sub-batch of a larger image-minor buffer is a pointer
  * offset by its first image with ld = the full batch.  Kind-7 launches need
- * ldx % 4 == 0 and a 16-byte aligned x (TMA).  Without the flag, ldx / ldy are
- * ignored and this is scb_conv_sparse. */
+ * ldx % 4 == 0 and a 16-byte aligned x (TMA).  With SCB_FLAG_Y_IMAGE_MINOR (NCHW x)
+ * only ldy is used; with SCB_FLAG_Y_NCHW (image-minor x) y is NCHW and ldy is ignored.
+ * Without any layout flag, ldx / ldy are ignored and this is scb_conv_sparse. */
 SCB_API scb_status scb_conv_sparse_ld(const scb_layer* layer, const void* x, int64_t ldx,
                                       const void* bias, void* y, int64_t ldy, int32_t n,
                                       uint32_t flags, const scb_launch* cfg, void* stream);
