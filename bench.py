@@ -839,6 +839,18 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "hbm_achieved_gbs": round(by / (mean_us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
             "traffic": traffic.get(specs[top][0].name),
             "smem_pipe_pct": smem.get(specs[top][0].name), "smem_pipe_source": smem_src}
+    # per kernel kind: the layers each kind runs and their time-weighted fraction of the peak
+    from paper_2011_06295_b200 import engine as _eng
+    kinds = {}
+    for i, rec in enumerate(layers):
+        kk = {2: "direct", 7: "image-lane position classes (kind 7)"}.get(_eng.launch_kind(launches[i]),
+                                                                         f"kind {_eng.launch_kind(launches[i])}")
+        kinds.setdefault(kk, []).append(rec)
+    roof["per_kernel_kind"] = {
+        kk: {"layers": [r["layer"] for r in recs], "us": round(sum(r["us"] for r in recs), 1),
+             "frac_time_weighted": round(sum(r["fma_frac"] * r["us"] for r in recs) / sum(r["us"] for r in recs), 4),
+             "frac_max": max(r["fma_frac"] for r in recs)}
+        for kk, recs in kinds.items() if all(r["fma_frac"] is not None for r in recs)}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(total_s / args.steps * 1e3, 4),
