@@ -532,8 +532,34 @@ def measure_f16(specs, args, dev, local_rank, reps: int = 10):
                                  oracle_forward(x.cpu().numpy(), specs, [L.kernel for L in qn.layers],
                                                 [L.bias for L in qn.layers]))["bitwise"]
         del qn
+    # opt-in fast mode (SCB_FLAG_FAST on f16): half2 accumulators within a stage (HFMA2) in the
+    # image-lane layers; checked against the oracle with the fp16 tolerance 1e-2*(|ref|+1)
+    hn = build_net(specs, seed=0, dtype=np.float16, device=local_rank, weight_fn=f16_scaled, fast_math=True)
+    hn.plan(args.batch, tune=not args.no_tune)
+    for _ in range(3):
+        hn.forward_device(x)
+    torch.cuda.synchronize()
+    th = []
+    for _ in range(reps):
+        ev[0].record()
+        hn.forward_device(x)
+        ev[1].record()
+        ev[1].synchronize()
+        th.append(ev[0].elapsed_time(ev[1]))
+    got = hn.forward_device(x).cpu().numpy().astype(np.float64)
+    want = oracle_forward(x.cpu().numpy(), specs, [L.kernel for L in hn.layers],
+                          [L.bias for L in hn.layers]).astype(np.float64)
+    err = float(np.max(np.abs(got - want) / (np.abs(want) + 1)))
+    from paper_2011_06295_b200 import _abi as _a
+    vs = _a.variants()
+    half2 = {"ms_per_step": round(statistics.median(th), 4),
+             "images_per_s": round(args.batch / (statistics.median(th) * 1e-3), 1),
+             "max_err_over_abs_ref_plus_1": round(err, 6), "within_1e-2": err <= 1e-2,
+             "half2_layers": [L.name for L, l in zip(hn.layers, hn.launches)
+                              if l is not None and vs[l[0]]["mode"] == 2]}
+    del hn
     return {"images_per_s": round(args.batch / (ms * 1e-3), 1), "ms_per_step": round(ms, 4),
-            "weight_formats": fmts, "parity_bitwise_vs_oracle": gates,
+            "weight_formats": fmts, "parity_bitwise_vs_oracle": gates, "half2_fast_mode": half2,
             "dense_cudnn_fp16_ms": round(statistics.median(td), 4),
             "arith": "f16 storage, FHFMA (f16 x f16 + f32) accumulation, bit-identical to the reference f16 profile",
             "launches": [None if l is None else list(l) for l in net.launches]}

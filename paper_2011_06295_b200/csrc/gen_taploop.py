@@ -379,6 +379,8 @@ LANES = [(h, nb, 1, u) for h in (2, 4) for nb in (1, 2, 4) for u in (1, 2) if no
 LANES_CS = [(4, 4, 1, 3), (4, 2, 1, 2), (2, 2, 2, 2), (4, 1, 1, 2), (2, 1, 2, 2), (2, 1, 2, 4), (2, 4, 1, 4), (2, 4, 1, 2)]  # (H, NB, U, CS)
 # f16 storage (FHFMA, in-register weight decode of every f16 format): (H = W, NB)
 LANES_F16 = [(4, 2, 1), (2, 2, 1), (2, 4, 1), (4, 2, 2), (2, 4, 4)]  # (H, NB, CS)
+# f16 opt-in fast mode (SCB_FLAG_FAST): half2 accumulators, HFMA2 -- native f16 weights
+LANES_H2 = [(4, 2, 1), (4, 2, 2), (2, 4, 4), (2, 2, 2)]  # (H, NB, CS)
 DIMGS_F16 = [(2, 2), (2, 4), (2, 8), (4, 2), (4, 4)]  # f16 storage, FHFMA
 
 # dispatch-free direct variants (direct.cuh): (R, S, PAD, TH, LW, KW, VX)
@@ -479,6 +481,8 @@ def main():
         groups[("lane", H, NB, KW, U)] = ([], [("lane", H, NB, KW, U, m) for m in (EXACT, FMA)])
     for H, NB, U, CS in LANES_CS:
         groups[("lanecs", H, NB, U, CS)] = ([], [("lanecs", H, NB, U, CS, m) for m in (EXACT, FMA)])
+    for H, NB, CS in LANES_H2:
+        groups[("laneh2", H, NB, CS)] = ([], [("laneh2", H, NB, CS)])
     for H, NB, CS in LANES_F16:
         groups[("lane16", H, NB, CS)] = ([], [("lane16", H, NB, CS, wf) for wf in (WF_F16,) + QFMTS])
     items = sorted(groups.values(), key=lambda t: -len(t[1]))
@@ -511,6 +515,12 @@ def main():
                     ents.append(f"    {{{{3, 3, {CS}, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, {U}, 1, "
                                 f"{KIND_LANE}}}, nullptr, nullptr, 1024, nullptr, "
                                 f"&launch_lane_t<{H}, {H}, {NB}, 1, {mode}, {U}, false, {WF_F32}, {CS}>}},\n")
+                    continue
+                if v[0] == "laneh2":  # mode 2 = MODE_HALF2
+                    _, H, NB, CS = v
+                    ents.append(f"    {{{{3, 3, {CS}, {NB}, {H}, {H}, SCB_F16, {WF_F16}, 2, 1, 1, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, {1024 if CS > 1 else 544}, nullptr, "
+                                f"&launch_lane_t<{H}, {H}, {NB}, 1, 2, 1, true, {WF_F16}, {CS}>}},\n")
                     continue
                 if v[0] == "lane16":
                     _, H, NB, CS, wf = v

@@ -36,7 +36,8 @@ inline cudaError_t dyn_smem_ok(K kern, size_t smem, int (&lim)[64]) {
     return (int)smem > lim[dev] ? cudaErrorInvalidValue : cudaSuccess;
 }
 
-enum { MODE_EXACT = 0, MODE_FMA = 1 };
+enum { MODE_EXACT = 0, MODE_FMA = 1,
+       MODE_HALF2 = 2 };  // f16 opt-in fast mode: half2 accumulators, HFMA2 (tolerance 1e-2)
 enum { WF_F32 = 0, WF_F16 = 1, WF_CB4 = 2, WF_LIN16 = 3, WF_AFF16 = 4 };
 // how the tiled kernel dispatches a tap to its unrolled MAC block (gen_taploop.py)
 enum { DISPATCH_JUMP = 0,   // brx.idx jump table, one indirect branch per tap

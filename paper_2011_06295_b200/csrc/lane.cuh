@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
     auto consume = [&](auto GC) {
     constexpr int G = decltype(GC)::value;
     float acc[KW][HW][NB];
+    // MODE_HALF2 (f16 opt-in fast mode, the north star's "half2 FMA"): within a stage the lane's
+    // image pairs accumulate in __half2 with one HFMA2 per two MACs; each stage's partial sums
+    // are folded into the f32 accumulators (a whole 461-tap sum in f16 measured 0.043 off)
+    constexpr bool H2 = F16 && MODE == MODE_HALF2;
+    static_assert(!H2 || NB % 2 == 0, "half2 accumulators pair a lane's images");
+    __half2 acc2[KW][HW][H2 ? NB / 2 : 1];
 #pragma unroll
     for (int kk = 0; kk < KW; ++kk) {
         const int k = k0 + kk;
@@ -306,6 +312,12 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
         for (int q = 0; q < HW; ++q)
 #pragma unroll
             for (int j = 0; j < NB; ++j) acc[kk][q][j] = b;
+        if constexpr (H2) {
+#pragma unroll
+            for (int q = 0; q < HW; ++q)
+#pragma unroll
+                for (int j = 0; j < NB / 2; ++j) acc2[kk][q][j] = __float2half2_rn(0.f);
+        }
     }
     for (int st = 0; st < p.nst; ++st) {
         const int buf = st % NBUF;
@@ -346,6 +358,27 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                             // one tap: vector loads of the class positions' inputs, then the MACs
                             auto tap = [&](const LaneTap& d) {
                                 const unsigned char* xa = xin + d.off;
+                                if constexpr (H2) {  // one HFMA2 per image pair and position
+                                    const unsigned short vh = tap_f16<WF>(__float_as_uint(d.v), cbt, qscale, qstep);
+                                    const __half2 v2 = __half2half2(__ushort_as_half(vh));
+#pragma unroll
+                                    for (int yy = ya; yy <= yb; ++yy)
+#pragma unroll
+                                        for (int xx = ex0; xx <= ex1; ++xx) {
+                                            __half2 xh[NB / 2];
+                                            if constexpr (NB == 2) {
+                                                xh[0] = *reinterpret_cast<const __half2*>(xa + ((yy - y0) * W + (xx - x0)) * RB);
+                                            } else {
+                                                const uint2 t = *reinterpret_cast<const uint2*>(xa + ((yy - y0) * W + (xx - x0)) * RB);
+                                                xh[0] = *reinterpret_cast<const __half2*>(&t.x);
+                                                xh[1] = *reinterpret_cast<const __half2*>(&t.y);
+                                            }
+#pragma unroll
+                                            for (int j = 0; j < NB / 2; ++j)
+                                                acc2[kk][yy * W + xx][j] = __hfma2(v2, xh[j], acc2[kk][yy * W + xx][j]);
+                                        }
+                                    return;
+                                }
                                 XT xv[HW][NB];
                                 unsigned short vh = 0;
                                 if constexpr (F16) vh = tap_f16<WF>(__float_as_uint(d.v), cbt, qscale, qstep);
@@ -428,6 +461,21 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                     beg = end;
                 }
             }
+        }
+        if constexpr (H2) {  // fold the stage's half2 partial sums into the f32 accumulators
+#pragma unroll
+            for (int kk = 0; kk < KW; ++kk)
+#pragma unroll
+                for (int q = 0; q < HW; ++q) {
+                    if (lane_pos_group<H, W, CS>(q / W, q % W) != G) continue;
+#pragma unroll
+                    for (int j = 0; j < NB / 2; ++j) {
+                        const float2 f = __half22float2(acc2[kk][q][j]);
+                        acc[kk][q][2 * j] += f.x;
+                        acc[kk][q][2 * j + 1] += f.y;
+                        acc2[kk][q][j] = __float2half2_rn(0.f);
+                    }
+                }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * buf);

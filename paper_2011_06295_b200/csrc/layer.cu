@@ -653,8 +653,10 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
     const bool decoded = (v.kind == KIND_DIRECT || v.kind == KIND_DIMG || v.kind == KIND_TMI || v.kind == KIND_LANE) &&
                          L->dt != SCB_F16 && v.wf == WF_F32;
     if (v.io != L->dt || (v.wf != L->wf && !decoded)) return false;
+    // f16 storage: FHFMA (exact w.r.t. the reference's f16 profile) always, plus the half2
+    // kernels (f16 accumulators) when the caller opts into the fast mode
     const int mode = (L->dt == SCB_F16) ? MODE_FMA : ((flags & SCB_FLAG_FAST) ? MODE_FMA : MODE_EXACT);
-    if (v.mode != mode) return false;
+    if (v.mode != mode && !(L->dt == SCB_F16 && (flags & SCB_FLAG_FAST) && v.mode == MODE_HALF2)) return false;
     if (v.kind < KIND_DIRECT && !L->prog(v.kt)) return false;
     if (v.kind == KIND_DIMG) {
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;

@@ -35,7 +35,8 @@ def test_variant_table():
     kinds = set()
     for v in vs:
         assert v["r"] >= 1 and v["s"] >= 1 and v["kt"] in (1, 2, 3, 4, 8)
-        assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1)
+        assert v["nbt"] in (1, 2, 4) and v["mode"] in (0, 1, 2)
+        assert v["mode"] < 2 or (v["kind"] == 7 and v["io"] == 2)  # half2: f16 lane kernels only
         if v["kind"] == 6:  # TMEM image-lane: dispatch = warps per lane quarter
             assert v["dispatch"] in (2, 3, 4) and v["tw"] in (2, 4, 8, 16)
         elif v["kind"] == 7:  # image-lane position classes: dispatch = tap unroll, nbt = images per lane

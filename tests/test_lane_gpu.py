@@ -331,3 +331,28 @@ def test_fused_output_layouts_bitwise(sc, orc):
             y = torch.full(exp.shape, -3.0, device="cuda")
             layer.launch(xm.data_ptr() + 4 * a, bd.data_ptr(), y.data_ptr(), n, fl, cfg, st, ldx=ld, ldy=ld)
             assert beq(y.cpu().numpy(), exp), (cfg, extra)
+
+
+@pytest.mark.parametrize("c,hw,k,n", [(512, 4, 512, 40), (512, 2, 512, 70), (96, 4, 40, 7)])
+def test_lane_half2_fast_mode_within_tolerance(sc, orc, c, hw, k, n):
+    """The f16 opt-in fast mode (SCB_FLAG_FAST on f16 layers: half2 accumulators, one HFMA2
+    per two MACs -- the north star's "half2 FMA"): within the fp16 tolerance 1e-2*(|ref|+1)
+    of the reference's f16 profile; without the flag f16 layers never get these kernels."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.synth import LayerSpec, bench_inputs, f16_scaled, make_layer_weights
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    kern = sc.build_csr(f16_scaled(make_layer_weights(LayerSpec("h", sh, 0.9), 0)), sh)
+    x, b = bench_inputs(sh, n)
+    x, b = np.maximum(x, 0).astype(np.float16), b.astype(np.float16)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b).astype(np.float64)
+    layer = device_layer(kern, 0, np.float16)
+    vs = _abi.variants()
+    assert not any(vs[cf[0]]["mode"] == 2 for cf in layer.candidates(n, _abi.FLAG_IMAGE_MINOR))
+    h2 = [cf for cf in layer.candidates(n, _abi.FLAG_IMAGE_MINOR | _abi.FLAG_FAST) if vs[cf[0]]["mode"] == 2]
+    assert h2
+    xd = torch.from_numpy(x).cuda()
+    for cfg in h2[:: max(1, len(h2) // 6)]:
+        o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg, fast_math=True)).cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(o - ref) <= 1e-2 * (np.abs(ref) + 1)), (cfg, float(np.max(np.abs(o - ref))))
