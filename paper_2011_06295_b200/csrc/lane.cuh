@@ -213,9 +213,6 @@ constexpr int LANE_PMAX = 16;
 #define LANE_UNROLL 4
 #endif
 constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernels
-#ifndef LANE_PAIRS
-#define LANE_PAIRS 0
-#endif
 
 // F16: f16 storage (x, y, weights; f32 accumulation by FHFMA -- f16 x f16 is exact in f32, so
 // one fma.rn.f32.f16 per MAC equals the reference's f32 mul + add); WF = the weight format
@@ -401,20 +398,6 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                                                     mac1<MODE>(acc[kk][yy * W + xx][j], d.v, xv[(yy - y0) * W + xx - x0][j]);
                                         }
                             };
-#if LANE_PAIRS
-                            // taps in 16-byte pairs (one broadcast LDS.128 = one wavefront per two taps):
-                            // an odd leading tap, whole pairs, an odd trailing tap
-                            int t = beg;
-                            if ((t & 1) && t < end) tap(tp[t++]);
-#pragma unroll 2
-                            for (; t + 1 < end; t += 2) {
-                                const float4 q = *reinterpret_cast<const float4*>(tp + t);
-                                tap(LaneTap{q.x, __float_as_int(q.y)});
-                                tap(LaneTap{q.z, __float_as_int(q.w)});
-                            }
-                            if (t < end) tap(tp[t]);
-                            LaneTap dq = dn;  // (running prefetch unused)
-#else
                             LaneTap dq = (ya == ey0 && CS == 1) ? dn : tp[beg];
 #pragma unroll kLaneUnroll
                             for (int t = beg; t < end; ++t) {
@@ -422,7 +405,6 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                                 dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
                                 tap(d);
                             }
-#endif
                             if (ya + rc > ey1) dn = dq;  // = tp[end]: the next class's first tap
                         }
                     } else {
