@@ -14,11 +14,15 @@
 //    channel, input-channel stage and class the host writes the class's tap list
 //    -- the CSR row in colidx order with the padding taps removed -- as
 //    {v, byte offset of the input row of the class's first position};
-//  * lane = image (NB images per lane, 32*NB per CTA), the whole plane of
-//    accumulators in registers, the class's positions a compile-time set of
-//    immediate row offsets: per tap one broadcast descriptor, then per
-//    (position, image) one conflict-free LDS.32 (32 consecutive images) and one
-//    MAC -- no data-dependent control flow, no padding MACs;
+//  * lane = image (NB consecutive images per lane, 32*NB per CTA), the whole plane
+//    of accumulators in registers, the class's positions a compile-time set of
+//    immediate row offsets: per tap one broadcast descriptor, then per position
+//    one conflict-free vector load of the lane's NB images and NB MACs -- no
+//    data-dependent control flow, no padding MACs;
+//  * class split (CS): CS warps share an output channel, each owning a fixed set of
+//    classes (lane_class_group; 8x8 planes by quadrant) -- shorter per-warp chains
+//    for small batches, more warps per SM; pooled windows that straddle two warps'
+//    positions are exchanged through the drained ring;
 //  * activations are IMAGE-MINOR: x[(c*H + y)*W + x][n] with a row stride ldx
 //    (>= n): a stage (cc channels of a block's images) is one 2D TMA box
 //    {32*NB images, cc*H*W rows} (cp.async.bulk.tensor, out-of-bounds images /
@@ -27,8 +31,12 @@
 //    per row were measured at ~70 clk each per SM -- far too slow);
 //    consumer warps release a slot with one mbarrier arrive (no CTA barrier,
 //    warps drift up to NBUF-1 stages apart);
-//  * the epilogue writes image-minor rows too (coalesced 128-byte stores), with
-//    bias / ReLU / 2x2 max-pool / activation fake-quant fused as in direct.cuh.
+//  * the epilogue writes image-minor rows too (coalesced 128-byte stores), or NCHW
+//    for the last layer of an image-minor run (SCB_FLAG_Y_NCHW), with bias / ReLU /
+//    2x2 max-pool / activation fake-quant fused as in direct.cuh;
+//  * f16 storage (F16): two images per 32-bit load, FHFMA (exact against the
+//    reference's f16 profile), weight formats decoded in registers; MODE_HALF2 is the
+//    opt-in fast mode (HFMA2 within a stage, f32 across stages, tolerance 1e-2).
 //
 // Exactness.  Dropping `o = o + v*(+0)` is exact when v is finite and o is not
 // -0.0: v*(+0) is +-0 and o + (+-0) = o.  o can only be -0.0 while every term so
