@@ -1223,11 +1223,21 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                          (g.h == 4 && v.io != SCB_F16 ? 2.0 : 0.0);
             }
             if (v.kind == KIND_LANE) {
-                // measured on B200 (tools/lane_harness.cu, profiles/r02_lane_*): 2 images per lane,
-                // 14 consumer warps (148 CTAs at batch 256), the largest stage that fits, 2 slots;
-                // 2x2 planes prefer the padded 2-tap unroll
-                score = 200.0 + 3.0 * std::log(fill + 1e-3) + (v.nbt == 2 ? 1.0 : 0.0) + (c.warps_k == 14 ? 0.5 : 0.0) +
-                        0.1 * std::log((double)c.cc) + ((g.h * g.w <= 4) == (v.dispatch == 2) ? 0.5 : 0.0);
+                // measured on B200 (tools/lane_harness.cu, profiles/r02_lane_harness_sweep.txt) at
+                // batch 256: 4x4 -- 4 images per lane x 3-way class split x 21 warps, cc 12 (111.6 us
+                // on conv4_2) or 2 images x 2-way x 28 warps, cc 16 (113.4); 2x2 -- 4 images x 4-way x
+                // 28 warps, cc 32 (20.2 us).  Small batches (< 4 image blocks) want one image per lane
+                // and the class split (shorter per-warp chains: tools/probe_shard.py).
+                const bool small_plane = g.h * g.w <= 4;
+                const int blocks = (n + 32 * v.nbt - 1) / (32 * v.nbt);
+                score = 200.0 + 3.0 * std::log(fill + 1e-3) + 0.1 * std::log((double)c.cc);
+                if (blocks >= 2) {
+                    if (!small_plane && v.nbt == 4 && v.kt == 3 && c.warps_k == 21 && c.cc == 12) score += 2.0;
+                    if (!small_plane && v.nbt == 2 && v.kt == 2 && c.warps_k == 28 && c.cc == 16) score += 1.8;
+                    if (small_plane && v.nbt == 4 && v.kt == 4 && c.warps_k == 28 && c.cc == 32) score += 2.0;
+                } else {
+                    score += (v.nbt == 1 ? 1.0 : 0.0) + (v.kt > 1 ? 0.8 : 0.0);
+                }
             }
             if (c.stages == 2 || c.stages == 0) score += 0.2;
             // TMEM image-lane kernels: correct, measured slower than direct on VGG-CIFAR
