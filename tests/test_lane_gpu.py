@@ -356,3 +356,32 @@ def test_lane_half2_fast_mode_within_tolerance(sc, orc, c, hw, k, n):
     for cfg in h2[:: max(1, len(h2) // 6)]:
         o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg, fast_math=True)).cpu().numpy().astype(np.float64)
         assert np.all(np.abs(o - ref) <= 1e-2 * (np.abs(ref) + 1)), (cfg, float(np.max(np.abs(o - ref))))
+
+
+def test_layout_flag_misuse_is_refused(sc):
+    """The C ABI refuses inconsistent layout requests instead of computing garbage: a row
+    stride below the batch, an image-minor input without a kind-7 launch, SCB_FLAG_Y_NCHW
+    without an image-minor input, SCB_FLAG_Y_IMAGE_MINOR on a kind-7 or generic launch."""
+    import torch
+    from paper_2011_06295_b200 import _abi
+    from paper_2011_06295_b200.device import device_layer
+    from paper_2011_06295_b200.errors import SparseConvError
+    n = 16
+    sh, w, x, b = _layer(sc, 32, 4, 16, 0.9, n)
+    layer = device_layer(sc.build_csr(w, sh), 0, np.float32)
+    st = torch.cuda.current_stream().cuda_stream
+    buf = torch.zeros(32 * 16 * 64, device="cuda")
+    out = torch.zeros(16 * 16 * 64, device="cuda")
+    lane = layer.default_launch(n, _abi.FLAG_IMAGE_MINOR)
+    nchw = layer.default_launch(n, 0)
+    assert lane[0] >= 0 and nchw[0] >= 0
+    bad = [(_abi.FLAG_IMAGE_MINOR, lane, dict(ldx=8, ldy=8)),               # ld < n
+           (_abi.FLAG_IMAGE_MINOR | _abi.FLAG_GENERIC, None, dict(ldx=n, ldy=n)),  # generic, image-minor
+           (_abi.FLAG_Y_NCHW, nchw, dict(ldx=n, ldy=n)),                    # Y_NCHW needs minor x
+           (_abi.FLAG_IMAGE_MINOR | _abi.FLAG_Y_IMAGE_MINOR, lane, dict(ldx=n, ldy=n)),
+           (_abi.FLAG_Y_IMAGE_MINOR | _abi.FLAG_GENERIC, None, dict(ldx=n, ldy=n))]
+    for flags, cfg, ld in bad:
+        with pytest.raises(SparseConvError):
+            layer.launch(buf.data_ptr(), 0, out.data_ptr(), n, flags, cfg, st, **ld)
+            pytest.fail(f"accepted flags {flags:#x} launch {cfg} {ld}")
+    torch.cuda.synchronize()  # no sticky error left behind
