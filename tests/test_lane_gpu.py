@@ -385,3 +385,27 @@ def test_layout_flag_misuse_is_refused(sc):
             layer.launch(buf.data_ptr(), 0, out.data_ptr(), n, flags, cfg, st, **ld)
             pytest.fail(f"accepted flags {flags:#x} launch {cfg} {ld}")
     torch.cuda.synchronize()  # no sticky error left behind
+
+
+@pytest.mark.parametrize("hw", [2, 4])
+def test_lane_ragged_csr_bitwise(sc, orc, hw):
+    """Ragged (non-unified) CSR -- per-channel tap counts differ (csr.py:120-126) -- on the
+    kind-7 kernels: per-(channel, stage) slots of different lengths, bitwise."""
+    import torch
+    from golden_gen import random_sparse_weights
+    n, c, k = 21, 48, 40
+    rng = np.random.default_rng(9)
+    w = random_sparse_weights(rng, k, c, 3, 3, 0.85).astype(np.float32)
+    sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
+    kern = sc.build_csr(w, sh, unify=False)
+    assert not kern.unified and len(set(np.diff(kern.rowptr))) > 1
+    x = rng.standard_normal((n, c, hw, hw)).astype(np.float32)
+    b = rng.standard_normal(k).astype(np.float32)
+    ref = orc.conv_sparse(x, kern.values, kern.colidx, kern.rowptr, k, 3, 3, 1, 1, b)
+    from paper_2011_06295_b200.device import device_layer
+    layer = device_layer(kern, 0, np.float32)
+    xd = torch.from_numpy(x).cuda()
+    cands = _lane_cands(layer, n, 0)
+    for cfg in cands[:: max(1, len(cands) // 10)]:
+        o = sc.conv_sparse(xd, kern, b, sc.EnginePlan(launch=cfg)).cpu().numpy()
+        assert beq(o, ref), cfg
