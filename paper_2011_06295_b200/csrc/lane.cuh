@@ -200,20 +200,23 @@ __host__ __device__ constexpr int lane_class_group(int ci) {
 }
 // 8x8 planes split by QUADRANT instead (CS = 4): group G owns rows / columns [lo, hi] of
 // its 4x4 quadrant (every class list is shared; a warp covers class positions in its window)
-template <int H, int W, int CS>
-__host__ __device__ constexpr bool lane_quadrants() { return H == 8 && W == 8 && CS == 4; }
-template <int H, int W, int CS>
-__host__ __device__ constexpr int lane_win_y0(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g / 2) : 0; }
-template <int H, int W, int CS>
-__host__ __device__ constexpr int lane_win_x0(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g % 2) : 0; }
-template <int H, int W, int CS>
-__host__ __device__ constexpr int lane_win_y1(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g / 2) + 3 : H - 1; }
-template <int H, int W, int CS>
-__host__ __device__ constexpr int lane_win_x1(int g) { return lane_quadrants<H, W, CS>() ? 4 * (g % 2) + 3 : W - 1; }
+// TQ = 1: the CTA owns one quadrant (a 4x4 output tile) of an 8x8 plane and stages only its
+// 5x5 input window (4D TMA box), one warp per output channel -- group G = the CTA's quadrant
+template <int H, int W, int CS, int TQ = 0>
+__host__ __device__ constexpr bool lane_quadrants() { return H == 8 && W == 8 && (CS == 4 || TQ); }
+template <int H, int W, int CS, int TQ = 0>
+__host__ __device__ constexpr int lane_win_y0(int g) { return lane_quadrants<H, W, CS, TQ>() ? 4 * (g / 2) : 0; }
+template <int H, int W, int CS, int TQ = 0>
+__host__ __device__ constexpr int lane_win_x0(int g) { return lane_quadrants<H, W, CS, TQ>() ? 4 * (g % 2) : 0; }
+template <int H, int W, int CS, int TQ = 0>
+__host__ __device__ constexpr int lane_win_y1(int g) { return lane_quadrants<H, W, CS, TQ>() ? 4 * (g / 2) + 3 : H - 1; }
+template <int H, int W, int CS, int TQ = 0>
+__host__ __device__ constexpr int lane_win_x1(int g) { return lane_quadrants<H, W, CS, TQ>() ? 4 * (g % 2) + 3 : W - 1; }
 // group owning output position (y, x)
-template <int H, int W, int CS>
+template <int H, int W, int CS, int TQ = 0>
 __host__ __device__ constexpr int lane_pos_group(int y, int x) {
-    return lane_quadrants<H, W, CS>() ? 2 * (y / 4) + x / 4 : lane_class_group<H, W, CS>(lane_class_of<H, W>(y * W + x));
+    return lane_quadrants<H, W, CS, TQ>() ? 2 * (y / 4) + x / 4
+                                           : lane_class_group<H, W, CS>(lane_class_of<H, W>(y * W + x));
 }
 // largest position set a tap's loads cover at once (bigger classes run in row chunks)
 constexpr int LANE_PMAX = 16;
@@ -225,8 +228,10 @@ constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernel
 // F16: f16 storage (x, y, weights; f32 accumulation by FHFMA -- f16 x f16 is exact in f32, so
 // one fma.rn.f32.f16 per MAC equals the reference's f32 mul + add); WF = the weight format
 // decoded in registers from the descriptor's 32-bit payload (kernels.cuh tap_f16).
-template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1>
-__global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const __grid_constant__ LaneParams p) {
+template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1,
+          int TQ = 0>
+__global__ void __launch_bounds__(TQ ? 544 : lane_max_threads<H, W, CS>(), 1) k_lane(const __grid_constant__ LaneParams p) {
+    static_assert(!TQ || (H == 8 && W == 8 && CS == 1 && U == 1), "quadrant tiles: 8x8 planes");
     static_assert(!F16 || U == 1, "f16: no padded no-op taps (a quantized payload has no -0.0)");
     using XT = typename std::conditional<F16, unsigned short, float>::type;  // staged operand
     using TIO = typename std::conditional<F16, __half, float>::type;         // stored output
@@ -242,10 +247,12 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
     const int warp = tid >> 5, lane = tid & 31;
     const int WK = p.warps, NBUF = p.nbuf;
     const int kg = blockIdx.x % p.kgroups;
-    const int n0 = (blockIdx.x / p.kgroups) * BI;
+    const int quad = TQ ? (blockIdx.x / p.kgroups) % 4 : 0;  // TQ: the CTA's output quadrant
+    const int n0 = (blockIdx.x / p.kgroups / (TQ ? 4 : 1)) * BI;
+    constexpr int SP = TQ ? 25 : H * W;  // staged input positions per channel (TQ: 5x5 window)
     const int KC = WK / CS * KW;  // output channels per CTA
     const int kbase = kg * KC;
-    const int in_bytes = p.cc * HW * RB;
+    const int in_bytes = p.cc * SP * RB;
     __shared__ unsigned short cbt[16];  // WF_CB4 table (f16 bits), published by the barrier below
     if (F16 && tid < 16) cbt[tid] = p.q.cb16[tid];
     const float qscale = p.q.scale;
@@ -283,13 +290,21 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                 const unsigned fb = full0 + 8 * buf;
                 mbar_arrive_tx(fb, tx);
                 const unsigned dst = smem_u32(smem + (size_t)buf * p.slot_bytes);
+                if constexpr (TQ) {  // the quadrant's 5x5 input window of cc channels: one 4D box
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst), "l"(&p.tmap), "r"(n0),
+                        "r"((quad % 2) ? 3 : 0), "r"((quad / 2) ? 3 : 0), "r"(st * p.cc), "r"(fb)
+                        : "memory");
+                } else {
                 for (int i = 0; i < copies; ++i)
                     asm volatile(
                         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
                         " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + (unsigned)(i * p.boxrows * RB)),
                         "l"(&p.tmap), "r"(n0), "r"(st * p.cc * HW + i * p.boxrows), "r"(fb)
                         : "memory");
-                bulk_g2s(dst + (unsigned)d_bytes, p.desc + ((size_t)st * p.k + kbase) * p.cap, dbytes, fb);
+                }
+                bulk_g2s(dst + (unsigned)d_bytes, p.desc + (((size_t)quad * p.nst + st) * p.k + kbase) * p.cap, dbytes, fb);
             }
         }
         return;
@@ -346,11 +361,11 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                     const int y0 = AY::lo(cy), y1 = AY::hi(cy), x0 = AX::lo(cx), x1 = AX::hi(cx);
                     const int end = hd[cy * AX::N + cx];
                     // this warp's positions of the class: the class range inside the group window
-                    const int ey0 = y0 > lane_win_y0<H, W, CS>(G) ? y0 : lane_win_y0<H, W, CS>(G);
-                    const int ey1 = y1 < lane_win_y1<H, W, CS>(G) ? y1 : lane_win_y1<H, W, CS>(G);
-                    const int ex0 = x0 > lane_win_x0<H, W, CS>(G) ? x0 : lane_win_x0<H, W, CS>(G);
-                    const int ex1 = x1 < lane_win_x1<H, W, CS>(G) ? x1 : lane_win_x1<H, W, CS>(G);
-                    const bool mine = lane_quadrants<H, W, CS>() || lane_class_group<H, W, CS>(cy * AX::N + cx) == G;
+                    const int ey0 = y0 > lane_win_y0<H, W, CS, TQ>(G) ? y0 : lane_win_y0<H, W, CS, TQ>(G);
+                    const int ey1 = y1 < lane_win_y1<H, W, CS, TQ>(G) ? y1 : lane_win_y1<H, W, CS, TQ>(G);
+                    const int ex0 = x0 > lane_win_x0<H, W, CS, TQ>(G) ? x0 : lane_win_x0<H, W, CS, TQ>(G);
+                    const int ex1 = x1 < lane_win_x1<H, W, CS, TQ>(G) ? x1 : lane_win_x1<H, W, CS, TQ>(G);
+                    const bool mine = lane_quadrants<H, W, CS, TQ>() || lane_class_group<H, W, CS>(cy * AX::N + cx) == G;
                     if (!mine || ey0 > ey1 || ex0 > ex1) {  // another warp's class / no position in the window
                         beg = end;
                         continue;
@@ -391,7 +406,8 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                                 for (int yy = ya; yy <= yb; ++yy)
 #pragma unroll
                                     for (int xx = ex0; xx <= ex1; ++xx)
-                                        lds_nb<NB>(xa + ((yy - y0) * W + (xx - x0)) * RB, xv[(yy - y0) * W + xx - x0]);
+                                        lds_nb<NB>(xa + (TQ ? (yy - ey0) * 5 + (xx - ex0) : (yy - y0) * W + (xx - x0)) * RB,
+                                                   xv[(yy - y0) * W + xx - x0]);
 #pragma unroll
                                 for (int yy = ya; yy <= yb; ++yy)
 #pragma unroll
@@ -457,7 +473,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
             for (int kk = 0; kk < KW; ++kk)
 #pragma unroll
                 for (int q = 0; q < HW; ++q) {
-                    if (lane_pos_group<H, W, CS>(q / W, q % W) != G) continue;
+                    if (lane_pos_group<H, W, CS, TQ>(q / W, q % W) != G) continue;
 #pragma unroll
                     for (int j = 0; j < NB / 2; ++j) {
                         const float2 f = __half22float2(acc2[kk][q][j]);
@@ -493,7 +509,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
                     for (int xx = AX::lo(cx); xx <= AX::hi(cx); ++xx)
 #pragma unroll
                         for (int j = 0; j < NB; ++j) {
-                            if (lane_pos_group<H, W, CS>(yy, xx) != G) continue;
+                            if (lane_pos_group<H, W, CS, TQ>(yy, xx) != G) continue;
                             float& o = acc[kk][yy * W + xx][j];
                             if (__float_as_uint(o) == 0x80000000u && ((zm >> (cy * AX::N + cx)) & 1u)) o = 0.f;
                             if (aq) o = fq_store<TIO>((p.flags & SCB_FLAG_RELU) ? relu_io<TIO>(o) : o, p.aq);
@@ -505,7 +521,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
             TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * HW * p.ldy + n0 + NB * lane;
 #pragma unroll
             for (int q = 0; q < HW; ++q) {
-                if (lane_pos_group<H, W, CS>(q / W, q % W) != G) continue;
+                if (lane_pos_group<H, W, CS, TQ>(q / W, q % W) != G) continue;
                 float o[NB];
 #pragma unroll
                 for (int j = 0; j < NB; ++j) o[j] = acc[kk][q][j];
@@ -521,7 +537,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
             asm volatile("bar.sync 1, %0;" ::"r"(WK * 32) : "memory");  // every warp is past the ring
 #pragma unroll
             for (int q = 0; q < HW; ++q) {
-                if (lane_pos_group<H, W, CS>(q / W, q % W) != G) continue;
+                if (lane_pos_group<H, W, CS, TQ>(q / W, q % W) != G) continue;
 #pragma unroll
                 for (int j = 0; j < NB; ++j) ex[((size_t)cq * HW + q) * BI + NB * lane + j] = acc[0][q][j];
             }
@@ -537,6 +553,7 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
 #pragma unroll
                 for (int px = 0; px < PW; ++px) {
                     if (CS > 1 && (py * PW + px) % CS != G) continue;  // pooled outputs dealt over the group
+                    if (TQ && lane_pos_group<H, W, CS, TQ>(2 * py, 2 * px) != G) continue;  // other quadrants
                     float o[NB];
 #pragma unroll
                     for (int j = 0; j < NB; ++j) {
@@ -559,7 +576,13 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
         }
     }
     };  // consume
-    if (cgrp == 0) consume(std::integral_constant<int, 0>{});
+    const int grp = TQ ? quad : cgrp;
+    if (grp == 0) consume(std::integral_constant<int, 0>{});
+    else if constexpr (TQ) {
+        if (grp == 1) consume(std::integral_constant<int, 1>{});
+        else if (grp == 2) consume(std::integral_constant<int, 2>{});
+        else consume(std::integral_constant<int, 3>{});
+    }
     else if constexpr (CS == 2) consume(std::integral_constant<int, 1>{});
     else if constexpr (CS == 3) {
         if (cgrp == 1) consume(std::integral_constant<int, 1>{});
@@ -572,9 +595,10 @@ __global__ void __launch_bounds__(lane_max_threads<H, W, CS>(), 1) k_lane(const 
     }
 }
 
-template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1>
+template <int H, int W, int NB, int KW, int MODE, int U = 1, bool F16 = false, int WF = WF_F32, int CS = 1,
+          int TQ = 0>
 cudaError_t launch_lane_t(const LaneParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
-    auto kern = k_lane<H, W, NB, KW, MODE, U, F16, WF, CS>;
+    auto kern = k_lane<H, W, NB, KW, MODE, U, F16, WF, CS, TQ>;
     static int lim[64];  // per device
     const cudaError_t e = dyn_smem_ok(kern, smem, lim);
     if (e != cudaSuccess) return e;
@@ -678,6 +702,89 @@ inline bool build_lane_program(const uint32_t* vbits, const int32_t* colidx, con
             std::memcpy(b, ends, LANE_HDR);
             if (!taps.empty()) std::memcpy(b + LANE_HDR, taps.data(), taps.size() * 8);
         }
+    return true;
+}
+
+// Tap program of the quadrant-tile mode (TQ): per quadrant q, stage st and channel k one slot
+// ([q][st][k][cap]): the plane's class lists restricted to classes with positions in q, offsets
+// of the input row of the class's first position IN q within q's 5x5 staged window.
+inline bool build_lane_program_tq(const uint32_t* vbits, const int32_t* colidx, const int32_t* rowptr, int C,
+                                  int K, int64_t pp, int wp, int cc, int nb, LaneProgram* out, bool count_only = false,
+                                  int es = 4, const uint8_t* sign = nullptr) {
+    const int H = 8, W = 8, RB = 32 * nb * es;
+    const int nst = (C + cc - 1) / cc;
+    LaneProgram& P = *out;
+    P.zmask.assign(K, 0u);
+    P.nst = nst;
+    P.macs = 0;
+    P.desc.clear();
+    std::vector<int32_t> tstart((size_t)K * (nst + 1));
+    for (int k = 0; k < K; ++k) {
+        int t = rowptr[k];
+        for (int st = 0; st < nst; ++st) {
+            tstart[(size_t)k * (nst + 1) + st] = t;
+            while (t < rowptr[k + 1] && colidx[t] / pp < std::min<int64_t>(C, (int64_t)(st + 1) * cc)) ++t;
+        }
+        tstart[(size_t)k * (nst + 1) + nst] = t;
+    }
+    std::vector<LaneTap> taps;
+    uint16_t ends[LANE_HDR / 2];
+    auto slot = [&](int q, int k, int st, bool account) {
+        taps.clear();
+        std::fill(ends, ends + LANE_HDR / 2, (uint16_t)0);
+        const int qy0 = 4 * (q / 2), qx0 = 4 * (q % 2), wy0 = q / 2 ? 3 : 0, wx0 = q % 2 ? 3 : 0;
+        for (int cy = 0; cy < 3; ++cy)
+            for (int cx = 0; cx < 3; ++cx) {
+                const int y0 = lane_axis_lo(H, cy), y1 = lane_axis_hi(H, cy);
+                const int x0 = lane_axis_lo(W, cx), x1 = lane_axis_hi(W, cx);
+                const int ey0 = std::max(y0, qy0), ey1 = std::min(y1, qy0 + 3);
+                const int ex0 = std::max(x0, qx0), ex1 = std::min(x1, qx0 + 3);
+                if (ey0 <= ey1 && ex0 <= ex1) {
+                    for (int i = tstart[(size_t)k * (nst + 1) + st]; i < tstart[(size_t)k * (nst + 1) + st + 1]; ++i) {
+                        const int64_t ci = colidx[i] / pp, rem = colidx[i] % pp;
+                        const int r = (int)(rem / wp), s = (int)(rem % wp);
+                        const int iy = y0 + r - 1, ix = x0 + s - 1;  // validity is a class property
+                        if (iy < 0 || iy >= H || ix < 0 || ix >= W) {
+                            const bool neg = sign ? sign[i] != 0 : (vbits[i] & 0x80000000u) != 0;
+                            if (account && q == 0 && !neg) P.zmask[k] |= 1u << (cy * 3 + cx);
+                            continue;
+                        }
+                        LaneTap d;
+                        std::memcpy(&d.v, &vbits[i], 4);
+                        d.off = (int32_t)((((ci - (int64_t)st * cc) * 25) + (ey0 + r - 1 - wy0) * 5 + (ex0 + s - 1 - wx0)) * RB);
+                        taps.push_back(d);
+                        if (account) P.macs += (ey1 - ey0 + 1) * (ex1 - ex0 + 1);
+                    }
+                } else if (account && q == 0) {  // zmask must still see every class's padding taps
+                    for (int i = tstart[(size_t)k * (nst + 1) + st]; i < tstart[(size_t)k * (nst + 1) + st + 1]; ++i) {
+                        const int64_t rem = colidx[i] % pp;
+                        const int iy = y0 + (int)(rem / wp) - 1, ix = x0 + (int)(rem % wp) - 1;
+                        const bool neg = sign ? sign[i] != 0 : (vbits[i] & 0x80000000u) != 0;
+                        if ((iy < 0 || iy >= H || ix < 0 || ix >= W) && !neg) P.zmask[k] |= 1u << (cy * 3 + cx);
+                    }
+                }
+                ends[cy * 3 + cx] = (uint16_t)taps.size();
+            }
+    };
+    int maxt = 0;
+    for (int q = 0; q < 4; ++q)
+        for (int k = 0; k < K; ++k)
+            for (int st = 0; st < nst; ++st) {
+                slot(q, k, st, true);
+                maxt = std::max(maxt, (int)taps.size());
+            }
+    if (maxt > 0xffff) return false;
+    P.cap = (LANE_HDR + maxt * 8 + 15) / 16;
+    if (count_only) return true;
+    P.desc.assign((size_t)4 * nst * K * P.cap, make_uint4(0, 0, 0, 0));
+    for (int q = 0; q < 4; ++q)
+        for (int st = 0; st < nst; ++st)
+            for (int k = 0; k < K; ++k) {
+                slot(q, k, st, false);
+                unsigned char* b = reinterpret_cast<unsigned char*>(P.desc.data() + (((size_t)q * nst + st) * K + k) * P.cap);
+                std::memcpy(b, ends, LANE_HDR);
+                if (!taps.empty()) std::memcpy(b + LANE_HDR, taps.data(), taps.size() * 8);
+            }
     return true;
 }
 

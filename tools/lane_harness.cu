@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <random>
 #include <algorithm>
+#include <string>
 
 #include <cudaTypedefs.h>
 #include "lane.cuh"
@@ -54,6 +55,74 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
         cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q);
     }
     return fn;
+}
+
+// quadrant-tile mode (TQ): 8x8 planes, CTA = (32 images, quadrant, channel group), 5x5 windows
+static void run_tq(int C, int K, int L, int N, const std::vector<float>& vals, const std::vector<int32_t>& colidx,
+                   const std::vector<int32_t>& rowptr, float* dx, float* dy, float* db, const std::vector<float>& ref,
+                   const std::vector<int>& sample) {
+    const int HW = 64;
+    const double counted = (double)N * K * HW * L;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int cc : {8, 16, 24, 32, 40}) {
+        LaneProgram P;
+        if (!build_lane_program_tq(reinterpret_cast<const uint32_t*>(vals.data()), colidx.data(), rowptr.data(), C, K, 9,
+                                   3, cc, 1, &P))
+            continue;
+        uint4* dd; uint32_t* dz;
+        CK(cudaMalloc(&dd, P.desc.size() * 16));
+        CK(cudaMalloc(&dz, P.zmask.size() * 4));
+        CK(cudaMemcpy(dd, P.desc.data(), P.desc.size() * 16, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dz, P.zmask.data(), P.zmask.size() * 4, cudaMemcpyHostToDevice));
+        for (int wk : {8, 12, 14, 16})
+            for (int nbuf : {1, 2, 3}) {
+                LaneParams p = {};
+                cuuint64_t gdim[4] = {(cuuint64_t)N, 8, 8, (cuuint64_t)C};
+                cuuint64_t gstr[3] = {(cuuint64_t)N * 4, (cuuint64_t)N * 32, (cuuint64_t)N * 256};
+                cuuint32_t box[4] = {32, 5, 5, (cuuint32_t)cc};
+                cuuint32_t es[4] = {1, 1, 1, 1};
+                if (encode_fn()(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dx, gdim, gstr, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                    continue;
+                p.boxrows = cc * 25;
+                p.bias = db; p.y = dy; p.desc = dd; p.zmask = dz;
+                p.n = N; p.c = C; p.k = K; p.ldx = N; p.ldy = N;
+                p.cc = cc; p.nst = (C + cc - 1) / cc; p.warps = wk; p.kw = 1;
+                p.kgroups = (K + wk - 1) / wk;
+                p.cap = P.cap; p.nbuf = nbuf;
+                p.slot_bytes = ((cc * 25 * 128 + wk * P.cap * 16) + 127) & ~127;
+                const size_t smem = (size_t)nbuf * p.slot_bytes + 16 * nbuf;
+                if (smem > 227 * 1024) continue;
+                const unsigned grid = (unsigned)(((N + 31) / 32) * 4 * p.kgroups);
+                auto go = [&]() { return launch_lane_t<8, 8, 1, 1, MODE_EXACT, 1, false, WF_F32, 1, 1>(p, grid, 32 * (wk + 1), smem, 0); };
+                CK(cudaMemset(dy, 0xff, (size_t)K * HW * N * 4));
+                cudaError_t e = go();
+                if (e != cudaSuccess) { printf("tq cc %d wk %d nbuf %d: %s\n", cc, wk, nbuf, cudaGetErrorString(e)); cudaGetLastError(); continue; }
+                CK(cudaDeviceSynchronize());
+                std::vector<float> y((size_t)K * HW * N);
+                CK(cudaMemcpy(y.data(), dy, y.size() * 4, cudaMemcpyDeviceToHost));
+                size_t bad = 0;
+                for (size_t si = 0; si < sample.size(); ++si)
+                    for (int q = 0; q < K * HW; ++q) {
+                        const float a = y[(size_t)q * N + sample[si]], b = ref[(size_t)q * sample.size() + si];
+                        if (memcmp(&a, &b, 4) != 0) ++bad;
+                    }
+                for (int i = 0; i < 3; ++i) go();
+                CK(cudaEventRecord(e0));
+                for (int i = 0; i < 20; ++i) go();
+                CK(cudaEventRecord(e1));
+                CK(cudaEventSynchronize(e1));
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, e0, e1));
+                const double us = ms * 1000.0 / 20;
+                printf("tq cc %2d wk %2d nbuf %d grid %4u smem %6zu: %8.2f us  counted %5.2f TMAC/s  %s\n", cc, wk, nbuf,
+                       grid, smem, us, counted / us * 1e-6, bad ? "MISMATCH" : "bitwise");
+            }
+        cudaFree(dd); cudaFree(dz);
+    }
 }
 
 int main(int argc, char** argv) {
@@ -110,6 +179,10 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&db, K * 4));
     CK(cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(db, bias.data(), K * 4, cudaMemcpyHostToDevice));
+    if (H == 8 && argc > 6 && std::string(argv[6]) == "tq") {
+        run_tq(C, K, L, N, vals, colidx, rowptr, dx, dy, db, ref, sample);
+        return 0;
+    }
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const double counted = (double)N * K * HW * L;
