@@ -152,6 +152,10 @@ struct scb_layer {
     bool lane_build(int cc, int nb, int u, int es, bool count_only, LaneProgram* P) const {
         const std::vector<uint32_t> vb = lane_vbits(es);
         const std::vector<uint8_t> sg = lane_sign();
+        if (u == 3)  // quadrant tiles of an 8x8 plane (lane.cuh TQ)
+            return g.h == 8 && g.w == 8 &&
+                   build_lane_program_tq(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp,
+                                         g.wp, cc, nb, P, count_only, es, sg.data());
         return build_lane_program(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp, g.wp,
                                   g.h, g.w, cc, nb, P, u, count_only, es, sg.data());
     }
@@ -981,7 +985,9 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
     const int es = elem_bytes(v);
-    const int HW = g.h * g.w, nb = v.nbt, RB = 32 * nb * es, u = v.dispatch;
+    const int u = v.dispatch;  // 1 / 2: tap unroll (padded pairs); 3: quadrant tiles (TQ)
+    const bool tq = u == 3;
+    const int HW = tq ? 25 : g.h * g.w, nb = v.nbt, RB = 32 * nb * es;  // staged positions per channel
     const int nbuf = c.stages == 0 ? 2 : c.stages;
     const int maxw = variant(c.variant).max_threads / 32 - 1;
     if (c.imgs != 32 * nb || c.bh != g.h || c.bw != g.w || c.cc < 1 || c.warps_k < 1 || c.warps_k > maxw ||
@@ -989,14 +995,15 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
         return fail(SCB_ERR_SHAPE, "lane launch: imgs = 32*nb, bh x bw = the plane, warps within the kernel's limit, "
                                    "2..4 stages");
     const int rows = c.cc * HW;
-    const int boxrows = std::min(rows, 256);
-    if (rows % boxrows) return fail(SCB_ERR_SHAPE, "lane launch: cc*H*W must be <= 256 or a multiple of 256");
+    const int boxrows = tq ? rows : std::min(rows, 256);  // TQ: one 4D box {images, 5, 5, cc}
+    if (rows % boxrows || (tq && c.cc > 256))
+        return fail(SCB_ERR_SHAPE, "lane launch: cc*H*W must be <= 256 or a multiple of 256");
     const int cap = L->lane_cap(c.cc, nb, u, es);
     if (cap <= 0) return fail(SCB_ERR_SHAPE, "lane launch: tap program does not fit the slot format");
     const int cs = v.kt;  // kind 7: warps per output channel (class split)
     if (c.warps_k % cs) return fail(SCB_ERR_SHAPE, "lane launch: warps must be a multiple of the class split");
     const int kc = c.warps_k / cs;
-    const size_t slot = ((size_t)rows * RB + (u > 1 ? (size_t)HW * RB : 0) + (size_t)kc * cap * 16 + 127) & ~(size_t)127;
+    const size_t slot = ((size_t)rows * RB + (u == 2 ? (size_t)HW * RB : 0) + (size_t)kc * cap * 16 + 127) & ~(size_t)127;
     d->smem = nbuf * slot + 16 * nbuf;
     // class split + pool: the epilogue exchanges f32 planes through the (drained) ring
     if (cs > 1 && (flags & SCB_FLAG_POOL2))
@@ -1011,7 +1018,7 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     d->nb = (n + 32 * nb - 1) / (32 * nb);
     d->n_ey = d->n_fx = 1;
     d->wp = (g.c + c.cc - 1) / c.cc;
-    const int64_t grid = (int64_t)d->kblocks * d->nb;
+    const int64_t grid = (int64_t)d->kblocks * d->nb * (tq ? 4 : 1);
     if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
     d->grid = (unsigned)grid;
     return SCB_OK;
@@ -1077,8 +1084,8 @@ void enumerate(scb_layer* L, int n, uint32_t flags, std::vector<scb_launch>& out
         const scb_variant_info& v = variant(vi).info;
         if (!variant_matches(L, v, flags)) continue;
         if (v.kind == KIND_LANE) {
-            for (int wk : {4, 8, 14, 16, 21, 28})
-                for (int cc : {4, 8, 12, 16, 32, 48, 64})
+            for (int wk : {4, 8, 12, 14, 16, 21, 28})
+                for (int cc : {4, 8, 12, 16, 24, 32, 48, 64})
                     for (int ns : {2, 3}) {
                         scb_launch c{vi, wk, 32 * v.nbt, g.h, g.w, cc, ns};
                         Derived d;
@@ -1231,7 +1238,9 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                 const bool small_plane = g.h * g.w <= 4;
                 const int blocks = (n + 32 * v.nbt - 1) / (32 * v.nbt);
                 score = 200.0 + 3.0 * std::log(fill + 1e-3) + 0.1 * std::log((double)c.cc);
-                if (blocks >= 2) {
+                if (v.dispatch == 3) {  // 8x8 quadrant tiles: conv3_2 139 us at cc 16, 8 warps, 2 slots
+                    score += (c.cc == 16 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0);
+                } else if (blocks >= 2) {
                     if (!small_plane && v.nbt == 4 && v.kt == 3 && c.warps_k == 21 && c.cc == 12) score += 2.0;
                     if (!small_plane && v.nbt == 2 && v.kt == 2 && c.warps_k == 28 && c.cc == 16) score += 1.8;
                     if (small_plane && v.nbt == 4 && v.kt == 4 && c.warps_k == 28 && c.cc == 32) score += 2.0;
@@ -1564,12 +1573,16 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
         LaneParams q;
         std::memset(&q, 0, sizeof(q));
         const int HW = g.h * g.w;
-        const cuuint64_t gdim[2] = {(cuuint64_t)n, (cuuint64_t)g.c * HW};
-        const cuuint64_t gstr[1] = {(cuuint64_t)ldx * esz};
-        const cuuint32_t box[2] = {(cuuint32_t)(32 * ve.info.nbt), (cuuint32_t)d.row};
-        const cuuint32_t es[2] = {1, 1};
-        CUresult r = enc(&q.tmap, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                         const_cast<void*>(x), gdim, gstr, box, es,
+        const bool tq = ve.info.dispatch == 3;  // quadrant tiles: x as {n, W, H, C}, box {images, 5, 5, cc}
+        const cuuint64_t gdim2[2] = {(cuuint64_t)n, (cuuint64_t)g.c * HW};
+        const cuuint64_t gstr2[1] = {(cuuint64_t)ldx * esz};
+        const cuuint32_t box2[2] = {(cuuint32_t)(32 * ve.info.nbt), (cuuint32_t)d.row};
+        const cuuint64_t gdim4[4] = {(cuuint64_t)n, (cuuint64_t)g.w, (cuuint64_t)g.h, (cuuint64_t)g.c};
+        const cuuint64_t gstr4[3] = {(cuuint64_t)ldx * esz, (cuuint64_t)g.w * ldx * esz, (cuuint64_t)HW * ldx * esz};
+        const cuuint32_t box4[4] = {(cuuint32_t)(32 * ve.info.nbt), 5, 5, (cuuint32_t)c.cc};
+        const cuuint32_t es[4] = {1, 1, 1, 1};
+        CUresult r = enc(&q.tmap, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         tq ? 4 : 2, const_cast<void*>(x), tq ? gdim4 : gdim2, tq ? gstr4 : gstr2, tq ? box4 : box2, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SCB_ERR_CUDA, "lane kernel: tensor map encoding failed");

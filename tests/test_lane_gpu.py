@@ -42,7 +42,7 @@ def _lane_cands(layer, n, flags):
 
 @pytest.mark.parametrize("c,hw,k,sp,n", [(512, 4, 512, 0.9, 70), (96, 4, 40, 0.5, 7), (512, 2, 512, 0.9, 70),
                                          (64, 2, 72, 0.8, 33), (24, 4, 16, 0.9, 3), (256, 4, 512, 0.9, 130),
-                                         (40, 4, 24, 0.0, 5)])
+                                         (40, 4, 24, 0.0, 5), (256, 8, 96, 0.9, 45), (40, 8, 24, 0.5, 7)])
 def test_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     """Every sampled kind-7 launch (NB, unroll, warps, stage, ring depth) through the NCHW
     API (engine.run_layer converts to image-minor and back), plain and with ReLU + pool."""
@@ -97,7 +97,7 @@ def test_lane_image_minor_strided_subbatch(sc, orc):
     assert torch.equal(xm2[:, a:a + n], xm[:, a:a + n])
 
 
-@pytest.mark.parametrize("hw", [2, 4])
+@pytest.mark.parametrize("hw", [2, 4, 8])
 def test_lane_negative_zero_fixup(sc, orc, hw):
     """bias -0.0 and an all-zero input: every product is +-0, so the reference result is
     -0.0 exactly when every tap of the output -- padding taps included -- has a negative
@@ -387,7 +387,7 @@ def test_layout_flag_misuse_is_refused(sc):
     torch.cuda.synchronize()  # no sticky error left behind
 
 
-@pytest.mark.parametrize("hw", [2, 4])
+@pytest.mark.parametrize("hw", [2, 4, 8])
 def test_lane_ragged_csr_bitwise(sc, orc, hw):
     """Ragged (non-unified) CSR -- per-channel tap counts differ (csr.py:120-126) -- on the
     kind-7 kernels: per-(channel, stage) slots of different lengths, bitwise."""
