@@ -81,7 +81,7 @@ _EXACT = {
     "dimg": r"_ZN3scb6k_dimgILi\d+ELi\d+ELi0ELb0ELi0EE",
     "plane": r"_ZN3scb7k_planeI(?:Li\d+E){7}Lb0ELi0ELi0ELi\dEE",
     "tmi": r"_ZN3scb5k_tmiI(?:Li\d+E){5}Li0EE",
-    "lane": r"_ZN3scb6k_laneI(?:Li\d+E){4}Li0ELi\d+ELb0ELi\d+ELi\d+EE",
+    "lane": r"_ZN3scb6k_laneI(?:Li\d+E){4}Li0ELi\d+ELb0E(?:Li\d+E){3}E",
 }
 
 
