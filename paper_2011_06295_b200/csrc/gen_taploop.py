@@ -378,6 +378,7 @@ LANES = [(h, nb, 1, u) for h in (2, 4) for nb in (1, 2, 4) for u in (1, 2) if no
 # class split: two warps per output channel, each a fixed half of the position classes (CS = 2)
 # 8x8 planes in quadrant tiles (lane.cuh TQ; dispatch = 3): one image per lane, one warp per channel
 LANES_TQ = [(8, 1)]
+LANES_TQ16 = [(8, 2)]  # f16 storage (two images per 32-bit load), every f16 weight format
 LANES_CS = [(4, 4, 1, 3), (4, 2, 1, 2), (2, 2, 2, 2), (4, 1, 1, 2), (2, 1, 2, 2), (2, 1, 2, 4), (2, 4, 1, 4), (2, 4, 1, 2)]  # (H, NB, U, CS)
 # f16 storage (FHFMA, in-register weight decode of every f16 format): (H = W, NB)
 LANES_F16 = [(4, 2, 1), (2, 2, 1), (2, 4, 1), (4, 2, 2), (2, 4, 4)]  # (H, NB, CS)
@@ -483,6 +484,8 @@ def main():
         groups[("lane", H, NB, KW, U)] = ([], [("lane", H, NB, KW, U, m) for m in (EXACT, FMA)])
     for H, NB in LANES_TQ:
         groups[("lanetq", H, NB)] = ([], [("lanetq", H, NB, m) for m in (EXACT, FMA)])
+    for H, NB in LANES_TQ16:
+        groups[("lanetq16", H, NB)] = ([], [("lanetq16", H, NB, wf) for wf in (WF_F16,) + QFMTS])
     for H, NB, U, CS in LANES_CS:
         groups[("lanecs", H, NB, U, CS)] = ([], [("lanecs", H, NB, U, CS, m) for m in (EXACT, FMA)])
     for H, NB, CS in LANES_H2:
@@ -519,6 +522,12 @@ def main():
                     ents.append(f"    {{{{3, 3, 1, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, 3, 1, "
                                 f"{KIND_LANE}}}, nullptr, nullptr, 544, nullptr, "
                                 f"&launch_lane_t<{H}, {H}, {NB}, 1, {mode}, 1, false, {WF_F32}, 1, 1>}},\n")
+                    continue
+                if v[0] == "lanetq16":
+                    _, H, NB, wf = v
+                    ents.append(f"    {{{{3, 3, 1, {NB}, {H}, {H}, SCB_F16, {wf}, {FMA}, 3, 1, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, 544, nullptr, "
+                                f"&launch_lane_t<{H}, {H}, {NB}, 1, {FMA}, 1, true, {wf}, 1, 1>}},\n")
                     continue
                 if v[0] == "lanecs":  # info: kt = CS warps per output channel
                     _, H, NB, U, CS, mode = v

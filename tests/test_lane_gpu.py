@@ -227,7 +227,7 @@ def test_lane_f16_in_register_decode_bitwise(sc, fmt):
     from paper_2011_06295_b200.device import device_layer
     from paper_2011_06295_b200.synth import (LayerSpec, affine_quantize, bench_inputs, f16_scaled,
                                              make_layer_weights, reference_quantize)
-    for c, hw, k, n in ((256, 4, 96, 33), (128, 2, 64, 70), (512, 4, 512, 40)):
+    for c, hw, k, n in ((256, 4, 96, 33), (128, 2, 64, 70), (512, 4, 512, 40), (128, 8, 64, 70)):
         sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
         kern = sc.build_csr(f16_scaled(make_layer_weights(LayerSpec("q", sh, 0.9), 0)), sh)
         if fmt == "cb4":
