@@ -379,6 +379,10 @@ LANES = [(h, nb, 1, u) for h in (2, 4) for nb in (1, 2, 4) for u in (1, 2) if no
 # 8x8 planes in quadrant tiles (lane.cuh TQ; dispatch = 3): one image per lane, one warp per channel
 LANES_TQ = [(8, 1)]
 LANES_TQ16 = [(8, 2)]  # f16 storage (two images per 32-bit load), every f16 weight format
+# 4x4 output tiles of 16x16 / 32x32 planes (lane.cuh k_tile; dispatch = 4): images per lane
+LANES_T4 = [1, 2, 4]
+LANES_T4_16 = [2, 4]  # f16 storage, every f16 weight format
+TILE_THREADS = {1: 544, 2: 416, 4: 288}  # = lane.cuh tile_max_threads
 LANES_CS = [(4, 4, 1, 3), (4, 2, 1, 2), (2, 2, 2, 2), (4, 1, 1, 2), (2, 1, 2, 2), (2, 1, 2, 4), (2, 4, 1, 4), (2, 4, 1, 2)]  # (H, NB, U, CS)
 # f16 storage (FHFMA, in-register weight decode of every f16 format): (H = W, NB)
 LANES_F16 = [(4, 2, 1), (2, 2, 1), (2, 4, 1), (4, 2, 2), (2, 4, 4)]  # (H, NB, CS)
@@ -484,6 +488,10 @@ def main():
         groups[("lane", H, NB, KW, U)] = ([], [("lane", H, NB, KW, U, m) for m in (EXACT, FMA)])
     for H, NB in LANES_TQ:
         groups[("lanetq", H, NB)] = ([], [("lanetq", H, NB, m) for m in (EXACT, FMA)])
+    for NB in LANES_T4:
+        groups[("lanet4", NB)] = ([], [("lanet4", NB, m) for m in (EXACT, FMA)])
+    for NB in LANES_T4_16:
+        groups[("lanet4h", NB)] = ([], [("lanet4h", NB, wf) for wf in (WF_F16,) + QFMTS])
     for H, NB in LANES_TQ16:
         groups[("lanetq16", H, NB)] = ([], [("lanetq16", H, NB, wf) for wf in (WF_F16,) + QFMTS])
     for H, NB, U, CS in LANES_CS:
@@ -522,6 +530,18 @@ def main():
                     ents.append(f"    {{{{3, 3, 1, {NB}, {H}, {H}, SCB_F32, {WF_F32}, {mode}, 3, 1, "
                                 f"{KIND_LANE}}}, nullptr, nullptr, 544, nullptr, "
                                 f"&launch_lane_t<{H}, {H}, {NB}, 1, {mode}, 1, false, {WF_F32}, 1, 1>}},\n")
+                    continue
+                if v[0] == "lanet4":  # info: dispatch = 4 (4x4 tiles), th = tw = 4
+                    _, NB, mode = v
+                    ents.append(f"    {{{{3, 3, 1, {NB}, 4, 4, SCB_F32, {WF_F32}, {mode}, 4, 1, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, {TILE_THREADS[NB]}, nullptr, "
+                                f"&launch_tile_t<{NB}, {mode}>}},\n")
+                    continue
+                if v[0] == "lanet4h":
+                    _, NB, wf = v
+                    ents.append(f"    {{{{3, 3, 1, {NB}, 4, 4, SCB_F16, {wf}, {FMA}, 4, 1, "
+                                f"{KIND_LANE}}}, nullptr, nullptr, {TILE_THREADS[NB]}, nullptr, "
+                                f"&launch_tile_t<{NB}, {FMA}, true, {wf}>}},\n")
                     continue
                 if v[0] == "lanetq16":
                     _, H, NB, wf = v

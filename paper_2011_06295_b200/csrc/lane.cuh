@@ -99,6 +99,7 @@ struct alignas(64) LaneParams {
     ActQuant aq;
     QuantAux q;               // f16 kernels: codebook / scales of the in-register weight decode
     uint32_t flags;
+    int h, w;                 // plane (k_tile: the 4x4 tile grid)
 };
 
 // U > 1: every class segment is padded by the host to a multiple of U taps with
@@ -605,6 +606,177 @@ cudaError_t launch_lane_t(const LaneParams& p, unsigned grid, unsigned threads, 
     return launch_pdl(kern, p, grid, threads, smem, st);
 }
 
+// ---------------------------------------------------- 4x4 output tiles of larger planes
+// Dispatch 4 (16x16 / 32x32 planes: VGG conv1_x / conv2_x): a CTA owns one 4x4 output tile
+// of 32*NB images and stages, per channel, the tile's 6x6 input window -- one 4D TMA box
+// {images, 6, 6, cc} whose rows / columns outside the plane the TMA zero-fills, i.e. the
+// reference's zero padding (shapes.py:98-105).  Every tile position sees every tap inside
+// its window, so one tap list per (stage, channel) serves all tiles: the CSR row in colidx
+// order with the padding taps KEPT -- the MACs are exactly the reference's
+// (_kernels.py:73-84, o = o + v*x with x = +0 in the padding), no zmask fix-up, and the
+// ~8 % (16x16) / ~4 % (32x32) padding MACs are the price of a class-free tile.  Lane =
+// image, 16*NB accumulators per lane, per tap one broadcast descriptor then 16
+// conflict-free vector loads and 16*NB MACs; the ring / producer are k_lane's.
+// thread limit (consumer warps + the producer): room for 16*NB accumulators + 16*NB operands
+constexpr int tile_max_threads(int nb) { return nb == 1 ? 544 : (nb == 2 ? 416 : 288); }
+template <int NB, int MODE, bool F16 = false, int WF = WF_F32>
+__global__ void __launch_bounds__(tile_max_threads(NB), 1) k_tile(const __grid_constant__ LaneParams p) {
+    static_assert(!F16 || NB >= 2, "f16: two images per 32-bit load");
+    static_assert(MODE != MODE_HALF2, "tiles: exact / FMA accumulation only");
+    using XT = typename std::conditional<F16, unsigned short, float>::type;
+    using TIO = typename std::conditional<F16, __half, float>::type;
+    constexpr int BI = 32 * NB, ES = F16 ? 2 : 4, RB = BI * ES, SP = 36;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int WK = p.warps, NBUF = p.nbuf;
+    const int ntx = p.w / 4, ntiles = (p.h / 4) * ntx;
+    const int kg = blockIdx.x % p.kgroups;
+    const int tile = (blockIdx.x / p.kgroups) % ntiles;
+    const int n0 = (blockIdx.x / p.kgroups / ntiles) * BI;
+    const int ty0 = 4 * (tile / ntx), tx0 = 4 * (tile % ntx);
+    const int kbase = kg * WK;
+    const int in_bytes = p.cc * SP * RB;
+    __shared__ unsigned short cbt[16];
+    if (F16 && tid < 16) cbt[tid] = p.q.cb16[tid];
+    const float qscale = p.q.scale;
+    const double qstep = p.q.step;
+
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (size_t)NBUF * p.slot_bytes);
+    const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + NBUF);
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(full0 + 8 * b, 1);
+            mbar_init(empty0 + 8 * b, WK);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == WK) {  // producer: the 6x6 window of cc channels + the CTA's descriptor slots
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap) : "memory");
+            const int kn = min(WK, p.k - kbase);
+            const unsigned dbytes = (unsigned)(kn * p.cap * 16);
+            for (int st = 0; st < p.nst; ++st) {
+                const int buf = st % NBUF;
+                if (st >= NBUF) mbar_wait(empty0 + 8 * buf, ((st / NBUF) - 1) & 1);
+                const unsigned fb = full0 + 8 * buf;
+                mbar_arrive_tx(fb, (unsigned)in_bytes + dbytes);
+                const unsigned dst = smem_u32(smem + (size_t)buf * p.slot_bytes);
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst), "l"(&p.tmap), "r"(n0), "r"(tx0 - 1),
+                    "r"(ty0 - 1), "r"(st * p.cc), "r"(fb)
+                    : "memory");
+                bulk_g2s(dst + (unsigned)in_bytes, p.desc + ((size_t)st * p.k + kbase) * p.cap, dbytes, fb);
+            }
+        }
+        return;
+    }
+
+    const int k = kbase + warp;
+    float acc[16][NB];
+    {
+        const float b = (p.bias != nullptr && k < p.k) ? p.bias[k] : 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[q][j] = b;
+    }
+    for (int st = 0; st < p.nst; ++st) {
+        const int buf = st % NBUF;
+        mbar_wait(full0 + 8 * buf, (st / NBUF) & 1);
+        const unsigned char* slot = smem + (size_t)buf * p.slot_bytes;
+        const unsigned char* xin = slot + lane * ES * NB;
+        if (k < p.k) {
+            const unsigned char* ch = slot + in_bytes + (size_t)warp * p.cap * 16;
+            const int cnt = *reinterpret_cast<const int*>(ch);
+            const LaneTap* tp = reinterpret_cast<const LaneTap*>(ch + LANE_HDR);
+            LaneTap dq = tp[0];
+#pragma unroll kLaneUnroll
+            for (int t = 0; t < cnt; ++t) {
+                const LaneTap d = dq;
+                dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
+                const unsigned char* xa = xin + d.off;
+                XT xv[16][NB];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) lds_nb<NB>(xa + ((q / 4) * 6 + q % 4) * RB, xv[q]);
+                if constexpr (F16) {
+                    const unsigned short vh = tap_f16<WF>(__float_as_uint(d.v), cbt, qscale, qstep);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) acc[q][j] = fhfma(acc[q][j], vh, xv[q][j]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) acc[q][j] = mac1<MODE>(acc[q][j], d.v, xv[q][j]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * buf);
+    }
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (k >= p.k) return;
+    const bool aq = p.flags & SCB_FLAG_ACT_QUANT;
+    const bool relu = (p.flags & SCB_FLAG_RELU) && !aq;
+    const bool pool = p.flags & SCB_FLAG_POOL2;
+    const bool vec = (p.ldy % NB) == 0 && (reinterpret_cast<uintptr_t>(p.y) % (ES * NB)) == 0;
+    const bool ynchw = p.flags & SCB_FLAG_Y_NCHW;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            float& o = acc[q][j];
+            if (aq) o = fq_store<TIO>((p.flags & SCB_FLAG_RELU) ? relu_io<TIO>(o) : o, p.aq);
+            if (relu && !pool) o = relu_io<TIO>(o);
+        }
+    const int nf = n0 + NB * lane;
+    if (!pool) {
+        const int HW = p.h * p.w;
+        TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * HW * p.ldy + nf;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int pos = (ty0 + q / 4) * p.w + tx0 + q % 4;
+            if (ynchw) store_nchw<NB>(static_cast<TIO*>(p.y), p.k, HW, k, pos, nf, p.n, acc[q]);
+            else store_nb<NB>(yp + (size_t)pos * p.ldy, acc[q], p.n - nf, vec);
+        }
+    } else {
+        const int PW = p.w / 2, PHW = (p.h / 2) * PW;
+        TIO* yp = static_cast<TIO*>(p.y) + (size_t)k * PHW * p.ldy + nf;
+#pragma unroll
+        for (int py = 0; py < 2; ++py)
+#pragma unroll
+            for (int px = 0; px < 2; ++px) {
+                const int a = 2 * py * 4 + 2 * px;
+                float o[NB];
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                    o[j] = fmaxf(fmaxf(acc[a][j], acc[a + 1][j]), fmaxf(acc[a + 4][j], acc[a + 5][j]));
+                    if (relu) o[j] = relu_io<TIO>(o[j]);
+                }
+                const int pos = (ty0 / 2 + py) * PW + tx0 / 2 + px;
+                if (ynchw) store_nchw<NB>(static_cast<TIO*>(p.y), p.k, PHW, k, pos, nf, p.n, o);
+                else store_nb<NB>(yp + (size_t)pos * p.ldy, o, p.n - nf, vec);
+            }
+    }
+}
+
+template <int NB, int MODE, bool F16 = false, int WF = WF_F32>
+cudaError_t launch_tile_t(const LaneParams& p, unsigned grid, unsigned threads, size_t smem, cudaStream_t st) {
+    auto kern = k_tile<NB, MODE, F16, WF>;
+    static int lim[64];  // per device
+    const cudaError_t e = dyn_smem_ok(kern, smem, lim);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, p, grid, threads, smem, st);
+}
+
 // ---------------------------------------------------------------- host side
 // Tap program of a kind-7 launch: per (stage st, output channel k) one slot of
 // `cap` 16-byte units = LANE_HDR bytes of cumulative class ends + the class tap
@@ -785,6 +957,53 @@ inline bool build_lane_program_tq(const uint32_t* vbits, const int32_t* colidx, 
                 std::memcpy(b, ends, LANE_HDR);
                 if (!taps.empty()) std::memcpy(b + LANE_HDR, taps.data(), taps.size() * 8);
             }
+    return true;
+}
+
+// Tap program of the 4x4-tile kernel (k_tile, dispatch 4): per (stage st, channel k) one slot
+// ([st][k][cap]) = LANE_HDR bytes (int32 tap count first) + the CSR row's taps of the stage in
+// colidx order, padding taps included, offsets into the 6x6 window: (c_local*36 + r*6 + s)*RB.
+// R = S = 3, pad 1, stride 1 (wp = W + 2).
+inline bool build_lane_program_tiles(const uint32_t* vbits, const int32_t* colidx, const int32_t* rowptr, int C,
+                                     int K, int64_t pp, int wp, int H, int W, int cc, int nb, LaneProgram* out,
+                                     bool count_only = false, int es = 4) {
+    const int RB = 32 * nb * es;
+    const int nst = (C + cc - 1) / cc;
+    if (cc < 1 || H % 4 || W % 4) return false;
+    LaneProgram& P = *out;
+    P.zmask.assign(K, 0u);  // padding MACs executed: nothing to restore
+    P.nst = nst;
+    P.macs = (int64_t)(rowptr[K] - rowptr[0]) * H * W;
+    P.desc.clear();
+    std::vector<int32_t> tstart((size_t)K * (nst + 1));
+    int maxt = 0;
+    for (int k = 0; k < K; ++k) {
+        int t = rowptr[k];
+        for (int st = 0; st < nst; ++st) {
+            tstart[(size_t)k * (nst + 1) + st] = t;
+            while (t < rowptr[k + 1] && colidx[t] / pp < std::min<int64_t>(C, (int64_t)(st + 1) * cc)) ++t;
+            maxt = std::max(maxt, t - tstart[(size_t)k * (nst + 1) + st]);
+        }
+        tstart[(size_t)k * (nst + 1) + nst] = t;
+    }
+    P.cap = (LANE_HDR + maxt * 8 + 15) / 16;
+    if (count_only) return true;
+    P.desc.assign((size_t)nst * K * P.cap, make_uint4(0, 0, 0, 0));
+    for (int k = 0; k < K; ++k)
+        for (int st = 0; st < nst; ++st) {
+            const int t0 = tstart[(size_t)k * (nst + 1) + st], t1 = tstart[(size_t)k * (nst + 1) + st + 1];
+            unsigned char* b = reinterpret_cast<unsigned char*>(P.desc.data() + ((size_t)st * K + k) * P.cap);
+            const int32_t cnt = t1 - t0;
+            std::memcpy(b, &cnt, 4);
+            for (int i = t0; i < t1; ++i) {
+                const int64_t ci = colidx[i] / pp, rem = colidx[i] % pp;
+                const int r = (int)(rem / wp), s = (int)(rem % wp);
+                LaneTap d;
+                std::memcpy(&d.v, &vbits[i], 4);
+                d.off = (int32_t)(((ci - (int64_t)st * cc) * 36 + r * 6 + s) * RB);
+                std::memcpy(b + LANE_HDR + (size_t)(i - t0) * 8, &d, 8);
+            }
+        }
     return true;
 }
 

@@ -152,6 +152,9 @@ struct scb_layer {
     bool lane_build(int cc, int nb, int u, int es, bool count_only, LaneProgram* P) const {
         const std::vector<uint32_t> vb = lane_vbits(es);
         const std::vector<uint8_t> sg = lane_sign();
+        if (u == 4)  // 4x4 output tiles of any plane with H, W multiples of 4 (lane.cuh k_tile)
+            return build_lane_program_tiles(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k,
+                                            (int64_t)g.hp * g.wp, g.wp, g.h, g.w, cc, nb, P, count_only, es);
         if (u == 3)  // quadrant tiles of an 8x8 plane (lane.cuh TQ)
             return g.h == 8 && g.w == 8 &&
                    build_lane_program_tq(vb.data(), h_colidx.data(), h_rowptr.data(), g.c, g.k, (int64_t)g.hp * g.wp,
@@ -666,6 +669,10 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
         return true;
     }
+    if (v.kind == KIND_LANE && v.dispatch == 4) {  // 4x4 output tiles: planes of 4-multiples, 16x16 and up
+        if (g.h % 4 || g.w % 4 || g.h * g.w < 256 || g.r != 3 || g.s != 3 || g.pad != 1 || !L->finite) return false;
+        return true;
+    }
     if (v.kind == KIND_LANE) {  // whole H x W plane per lane, 3x3 "same" convolution, finite weights
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1 || !L->finite) return false;
         if ((flags & SCB_FLAG_POOL2) && ((g.h & 1) || (g.w & 1))) return false;
@@ -985,9 +992,9 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     const scb_variant_info& v = variant(c.variant).info;
     const Geom& g = L->g;
     const int es = elem_bytes(v);
-    const int u = v.dispatch;  // 1 / 2: tap unroll (padded pairs); 3: quadrant tiles (TQ)
-    const bool tq = u == 3;
-    const int HW = tq ? 25 : g.h * g.w, nb = v.nbt, RB = 32 * nb * es;  // staged positions per channel
+    const int u = v.dispatch;  // 1 / 2: tap unroll (padded pairs); 3: quadrant tiles (TQ); 4: 4x4 tiles
+    const bool tq = u == 3 || u == 4;
+    const int HW = u == 4 ? 36 : (tq ? 25 : g.h * g.w), nb = v.nbt, RB = 32 * nb * es;  // staged positions per channel
     const int nbuf = c.stages == 0 ? 2 : c.stages;
     const int maxw = variant(c.variant).max_threads / 32 - 1;
     if (c.imgs != 32 * nb || c.bh != g.h || c.bw != g.w || c.cc < 1 || c.warps_k < 1 || c.warps_k > maxw ||
@@ -1018,7 +1025,7 @@ scb_status derive_lane(scb_layer* L, const scb_launch& c, int n, uint32_t flags,
     d->nb = (n + 32 * nb - 1) / (32 * nb);
     d->n_ey = d->n_fx = 1;
     d->wp = (g.c + c.cc - 1) / c.cc;
-    const int64_t grid = (int64_t)d->kblocks * d->nb * (tq ? 4 : 1);
+    const int64_t grid = (int64_t)d->kblocks * d->nb * (u == 4 ? (g.h / 4) * (g.w / 4) : (tq ? 4 : 1));
     if (grid > 0x7fffffffLL) return fail(SCB_ERR_SHAPE, "grid too large");
     d->grid = (unsigned)grid;
     return SCB_OK;
@@ -1240,6 +1247,9 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                 score = 200.0 + 3.0 * std::log(fill + 1e-3) + 0.1 * std::log((double)c.cc);
                 if (v.dispatch == 3) {  // 8x8 quadrant tiles: conv3_2 139 us at cc 16, 8 warps, 2 slots
                     score += (c.cc == 16 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0);
+                } else if (v.dispatch == 4) {  // 4x4 tiles: conv2_2 133 us at 2 images / lane, 8 warps, cc 4, 3 slots
+                    score += (v.nbt == 2 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0) + (c.cc == 4 ? 1.0 : 0.0) +
+                             (c.stages == 3 ? 0.5 : 0.0);
                 } else if (blocks >= 2) {
                     if (!small_plane && v.nbt == 4 && v.kt == 3 && c.warps_k == 21 && c.cc == 12) score += 2.0;
                     if (!small_plane && v.nbt == 2 && v.kt == 2 && c.warps_k == 28 && c.cc == 16) score += 1.8;
@@ -1573,13 +1583,15 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
         LaneParams q;
         std::memset(&q, 0, sizeof(q));
         const int HW = g.h * g.w;
-        const bool tq = ve.info.dispatch == 3;  // quadrant tiles: x as {n, W, H, C}, box {images, 5, 5, cc}
+        // quadrant / 4x4 tiles: x as {n, W, H, C}, box {images, 5, 5, cc} / {images, 6, 6, cc}
+        const bool tq = ve.info.dispatch == 3 || ve.info.dispatch == 4;
+        const cuuint32_t win = ve.info.dispatch == 4 ? 6 : 5;
         const cuuint64_t gdim2[2] = {(cuuint64_t)n, (cuuint64_t)g.c * HW};
         const cuuint64_t gstr2[1] = {(cuuint64_t)ldx * esz};
         const cuuint32_t box2[2] = {(cuuint32_t)(32 * ve.info.nbt), (cuuint32_t)d.row};
         const cuuint64_t gdim4[4] = {(cuuint64_t)n, (cuuint64_t)g.w, (cuuint64_t)g.h, (cuuint64_t)g.c};
         const cuuint64_t gstr4[3] = {(cuuint64_t)ldx * esz, (cuuint64_t)g.w * ldx * esz, (cuuint64_t)HW * ldx * esz};
-        const cuuint32_t box4[4] = {(cuuint32_t)(32 * ve.info.nbt), 5, 5, (cuuint32_t)c.cc};
+        const cuuint32_t box4[4] = {(cuuint32_t)(32 * ve.info.nbt), win, win, (cuuint32_t)c.cc};
         const cuuint32_t es[4] = {1, 1, 1, 1};
         CUresult r = enc(&q.tmap, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                          tq ? 4 : 2, const_cast<void*>(x), tq ? gdim4 : gdim2, tq ? gstr4 : gstr2, tq ? box4 : box2, es,
@@ -1597,6 +1609,7 @@ static scb_status conv_sparse_impl(const scb_layer* layer, const void* x, int64_
         q.kgroups = d.kblocks; q.cap = d.tap_cap; q.nbuf = d.stage_el; q.slot_bytes = d.chunk; q.boxrows = d.row;
         q.aq = L->aq;
         q.flags = flags;
+        q.h = g.h; q.w = g.w;
         *fused_aq = true;
         if ((int64_t)g.k * (g.e * g.f) * ldy > ((int64_t)1 << 40)) return fail(SCB_ERR_SHAPE, "output too large");
         cudaError_t e = ve.llaunch(q, d.grid, (unsigned)d.threads, d.smem, st);

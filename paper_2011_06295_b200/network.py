@@ -145,6 +145,7 @@ class SparseConvNet:
             x = torch.randn((self.batch, *self.in_shape), generator=gen).to(self.tdev, self.tdtype)
             plan = engine.EnginePlan(fast_math=self.fast_math, weight_format=self.weight_format,
                                      device=self.device)
+            opts = []  # per layer: (NCHW launch, seconds, image-minor launch, seconds)
             with torch.cuda.device(self.device):
                 for i, L in enumerate(self.layers):
                     best, tim = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
@@ -154,11 +155,10 @@ class SparseConvNet:
                     bm, tm = tune_launch(x, L.kernel, L.bias, plan, relu=L.relu, pool=L.pool,
                                          repetitions=repetitions, warmups=warmups,
                                          max_candidates=max_candidates, layout="minor")
-                    if bm is not None and tm[bm] < tim[best]:
-                        best = bm
-                    self.launches[i] = best
+                    opts.append((best, tim[best], bm, tm[bm] if bm is not None else float("inf")))
                     x = torch.relu(torch.randn(self.out_shape(i, self.batch), generator=gen)).to(
                         self.tdev, self.tdtype)
+            self.launches = self._pick_layouts(opts)
         else:
             self.launches = []
             for i in range(len(self.layers)):
@@ -170,6 +170,34 @@ class SparseConvNet:
                 self.launches.append(None if l[0] < 0 else l)
         self.set_launches(self.launches)
         return list(self.launches)
+
+    def _layout_change_s(self, i: int) -> float:
+        """Estimated seconds to change the layout of layer i's output (-1: the stack input):
+        one transpose kernel, read + write at ~5 TB/s."""
+        shp = (self.batch, *self.in_shape) if i < 0 else self.out_shape(i, self.batch)
+        return 2.0 * float(np.prod(shp)) * np.dtype(self.dtype).itemsize / 5.0e12
+
+    def _pick_layouts(self, opts) -> list:
+        """Per-layer layout choice over the measured kernel times plus the layout changes
+        between consecutive layers (two-state shortest path: NCHW / image-minor)."""
+        inf = float("inf")
+        nl = len(opts)
+        cost = [opts[0][1], opts[0][3] + self._layout_change_s(-1)]  # ends in NCHW / minor
+        back = []
+        for i in range(1, nl):
+            ch = self._layout_change_s(i - 1)
+            cn = [cost[0], cost[1] + ch]
+            cm = [cost[0] + ch, cost[1]]
+            back.append((int(cn[1] < cn[0]), int(cm[1] < cm[0])))
+            cost = [min(cn) + opts[i][1], min(cm) + opts[i][3]]
+        cost[1] += self._layout_change_s(nl - 1)  # the NCHW result
+        state = int(cost[1] < cost[0] and cost[1] < inf)
+        pick = [state]
+        for i in range(nl - 2, -1, -1):
+            state = back[i][state]
+            pick.append(state)
+        pick.reverse()
+        return [opts[i][2] if m else opts[i][0] for i, m in enumerate(pick)]
 
     def set_launches(self, launches) -> None:
         """Install explicit per-layer launches (tuple, or None = generic)."""
@@ -185,7 +213,9 @@ class SparseConvNet:
         nl = len(self.layers)
         # fused layout changes: a narrow direct layer feeding an image-minor run writes its output
         # image-minor (SCB_FLAG_Y_IMAGE_MINOR), and the last layer of an image-minor run writes
-        # NCHW (SCB_FLAG_Y_NCHW) -- no conversion kernel at either end when the launch allows it
+        # NCHW (SCB_FLAG_Y_NCHW) -- no conversion kernel at either end when the launch allows it.
+        # Only for small output planes (<= 16 positions): those stores scatter one element per
+        # 32-byte sector (measured on a 32x32 plane: 141 us in place of 32 us + a 20 us transpose)
         self.yflag = [0] * nl
         vs = _abi.variants()
         for i in range(nl):
@@ -193,6 +223,9 @@ class SparseConvNet:
             if self.algorithms[i] != "sparse-direct" or l is None or not self.fuse_layouts:
                 continue
             nxt_minor = i + 1 < nl and self.minor[i + 1]
+            _, _, e, f = self.out_shape(i, 1)
+            if e * f > 16:
+                continue
             if not self.minor[i] and nxt_minor and vs[l[0]]["kind"] == 2 and vs[l[0]]["dispatch"] == 0:
                 f = self.flags(i) | _abi.FLAG_Y_IMAGE_MINOR
                 if self.dlayers[i].launch_ok(self.batch, f, l):

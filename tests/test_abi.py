@@ -40,8 +40,9 @@ def test_variant_table():
         if v["kind"] == 6:  # TMEM image-lane: dispatch = warps per lane quarter
             assert v["dispatch"] in (2, 3, 4) and v["tw"] in (2, 4, 8, 16)
         elif v["kind"] == 7:  # image-lane position classes: dispatch = tap unroll, nbt = images per lane
-            assert v["dispatch"] in (1, 2, 3) and v["th"] == v["tw"] and v["th"] in (2, 4, 8) and v["kt"] in (1, 2, 3, 4)
+            assert v["dispatch"] in (1, 2, 3, 4) and v["th"] == v["tw"] and v["th"] in (2, 4, 8) and v["kt"] in (1, 2, 3, 4)
             assert (v["dispatch"] == 3) == (v["th"] == 8)  # 8x8 planes run as quadrant tiles
+            assert v["dispatch"] != 4 or (v["th"] == 4 and v["kt"] == 1)  # 4x4 tiles of 16x16+ planes
         else:
             assert v["dispatch"] in (0, 1, 2, 3)
             assert v["dispatch"] < 2 or v["kind"] == 2  # column-tiled (wide) / 1D direct

@@ -42,7 +42,9 @@ def _lane_cands(layer, n, flags):
 
 @pytest.mark.parametrize("c,hw,k,sp,n", [(512, 4, 512, 0.9, 70), (96, 4, 40, 0.5, 7), (512, 2, 512, 0.9, 70),
                                          (64, 2, 72, 0.8, 33), (24, 4, 16, 0.9, 3), (256, 4, 512, 0.9, 130),
-                                         (40, 4, 24, 0.0, 5), (256, 8, 96, 0.9, 45), (40, 8, 24, 0.5, 7)])
+                                         (40, 4, 24, 0.0, 5), (256, 8, 96, 0.9, 45), (40, 8, 24, 0.5, 7),
+                                         # 4x4 output tiles (dispatch 4) of 16x16 / 32x32 planes
+                                         (64, 16, 48, 0.9, 70), (24, 16, 20, 0.0, 5), (32, 32, 40, 0.9, 33)])
 def test_lane_kernels_bitwise(sc, orc, c, hw, k, sp, n):
     """Every sampled kind-7 launch (NB, unroll, warps, stage, ring depth) through the NCHW
     API (engine.run_layer converts to image-minor and back), plain and with ReLU + pool."""
@@ -97,7 +99,7 @@ def test_lane_image_minor_strided_subbatch(sc, orc):
     assert torch.equal(xm2[:, a:a + n], xm[:, a:a + n])
 
 
-@pytest.mark.parametrize("hw", [2, 4, 8])
+@pytest.mark.parametrize("hw", [2, 4, 8, 16])
 def test_lane_negative_zero_fixup(sc, orc, hw):
     """bias -0.0 and an all-zero input: every product is +-0, so the reference result is
     -0.0 exactly when every tap of the output -- padding taps included -- has a negative
@@ -227,7 +229,7 @@ def test_lane_f16_in_register_decode_bitwise(sc, fmt):
     from paper_2011_06295_b200.device import device_layer
     from paper_2011_06295_b200.synth import (LayerSpec, affine_quantize, bench_inputs, f16_scaled,
                                              make_layer_weights, reference_quantize)
-    for c, hw, k, n in ((256, 4, 96, 33), (128, 2, 64, 70), (512, 4, 512, 40), (128, 8, 64, 70)):
+    for c, hw, k, n in ((256, 4, 96, 33), (128, 2, 64, 70), (512, 4, 512, 40), (128, 8, 64, 70), (64, 16, 48, 70)):
         sh = sc.ConvShape(n=n, c=c, h=hw, w=hw, k=k, r=3, s=3, padding=1)
         kern = sc.build_csr(f16_scaled(make_layer_weights(LayerSpec("q", sh, 0.9), 0)), sh)
         if fmt == "cb4":
@@ -387,7 +389,7 @@ def test_layout_flag_misuse_is_refused(sc):
     torch.cuda.synchronize()  # no sticky error left behind
 
 
-@pytest.mark.parametrize("hw", [2, 4, 8])
+@pytest.mark.parametrize("hw", [2, 4, 8, 16])
 def test_lane_ragged_csr_bitwise(sc, orc, hw):
     """Ragged (non-unified) CSR -- per-channel tap counts differ (csr.py:120-126) -- on the
     kind-7 kernels: per-(channel, stage) slots of different lengths, bitwise."""
