@@ -101,7 +101,11 @@ typedef struct {
     int32_t mode;        /* 0 exact mul+add, 1 fma */
     int32_t dispatch;    /* tap dispatch: 0 brx.idx jump table, 1 per-channel mask walk;
                             direct kind: 2 = column tiles of tw for any output row width,
-                            3 = 1D rows (H = R = 1) in tiles of th*tw columns */
+                            3 = 1D rows (H = R = 1) in tiles of th*tw columns;
+                            kind 7: 1 / 2 = tap unroll of the whole-plane kernel, 3 = 4x4
+                            quadrants of an 8x8 plane (5x5 windows), 4 = 4x4 output tiles of
+                            a plane of 4-multiples >= 16x16 (6x6 zero-filled TMA windows,
+                            padding taps executed; th = tw = 4) */
     int32_t pad;         /* padding the variant is specialised for */
     int32_t kind;        /* 0 tiled (output blocks, halo patches); 1 whole plane (th x tw = the
                             input plane a lane holds; small spatial extents); 2 direct
