@@ -104,7 +104,7 @@ typedef struct {
                             3 = 1D rows (H = R = 1) in tiles of th*tw columns;
                             kind 7: 1 / 2 = tap unroll of the whole-plane kernel, 3 = 4x4
                             quadrants of an 8x8 plane (5x5 windows), 4 = 4x4 output tiles of
-                            a plane of 4-multiples >= 16x16 (6x6 zero-filled TMA windows,
+                            a plane of 4-multiples >= 8x8 (6x6 zero-filled TMA windows,
                             padding taps executed; th = tw = 4) */
     int32_t pad;         /* padding the variant is specialised for */
     int32_t kind;        /* 0 tiled (output blocks, halo patches); 1 whole plane (th x tw = the

@@ -669,8 +669,8 @@ bool variant_matches(const scb_layer* L, const scb_variant_info& v, uint32_t fla
         if (g.h != v.th || g.w != v.tw || g.r != 3 || g.s != 3 || g.pad != 1) return false;
         return true;
     }
-    if (v.kind == KIND_LANE && v.dispatch == 4) {  // 4x4 output tiles: planes of 4-multiples, 16x16 and up
-        if (g.h % 4 || g.w % 4 || g.h * g.w < 256 || g.r != 3 || g.s != 3 || g.pad != 1 || !L->finite) return false;
+    if (v.kind == KIND_LANE && v.dispatch == 4) {  // 4x4 output tiles: planes of 4-multiples, 8x8 and up
+        if (g.h % 4 || g.w % 4 || g.h * g.w < 64 || g.r != 3 || g.s != 3 || g.pad != 1 || !L->finite) return false;
         return true;
     }
     if (v.kind == KIND_LANE) {  // whole H x W plane per lane, 3x3 "same" convolution, finite weights
@@ -1247,6 +1247,9 @@ bool pick_default(scb_layer* L, int n, uint32_t flags, int prefer_imgs, scb_laun
                 score = 200.0 + 3.0 * std::log(fill + 1e-3) + 0.1 * std::log((double)c.cc);
                 if (v.dispatch == 3) {  // 8x8 quadrant tiles: conv3_2 139 us at cc 16, 8 warps, 2 slots
                     score += (c.cc == 16 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0);
+                } else if (v.dispatch == 4 && g.h * g.w <= 64) {  // 4x4 tiles of 8x8: conv3_2 137 us at 1 image
+                    score += 2.5 + (v.nbt == 1 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0) +  // per lane, 8 warps,
+                             (c.cc == 8 ? 1.0 : 0.0) + (c.stages == 2 ? 0.5 : 0.0);          // cc 8, 2 slots
                 } else if (v.dispatch == 4) {  // 4x4 tiles: conv2_2 133 us at 2 images / lane, 8 warps, cc 4, 3 slots
                     score += (v.nbt == 2 ? 1.0 : 0.0) + (c.warps_k == 8 ? 1.0 : 0.0) + (c.cc == 4 ? 1.0 : 0.0) +
                              (c.stages == 3 ? 0.5 : 0.0);

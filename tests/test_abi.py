@@ -42,7 +42,7 @@ def test_variant_table():
         elif v["kind"] == 7:  # image-lane position classes: dispatch = tap unroll, nbt = images per lane
             assert v["dispatch"] in (1, 2, 3, 4) and v["th"] == v["tw"] and v["th"] in (2, 4, 8) and v["kt"] in (1, 2, 3, 4)
             assert (v["dispatch"] == 3) == (v["th"] == 8)  # 8x8 planes run as quadrant tiles
-            assert v["dispatch"] != 4 or (v["th"] == 4 and v["kt"] == 1)  # 4x4 tiles of 16x16+ planes
+            assert v["dispatch"] != 4 or (v["th"] == 4 and v["kt"] == 1)  # 4x4 tiles of 8x8+ planes
         else:
             assert v["dispatch"] in (0, 1, 2, 3)
             assert v["dispatch"] < 2 or v["kind"] == 2  # column-tiled (wide) / 1D direct
