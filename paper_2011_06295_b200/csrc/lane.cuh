@@ -225,6 +225,10 @@ constexpr int LANE_PMAX = 16;
 #define LANE_UNROLL 4
 #endif
 constexpr int kLaneUnroll = LANE_UNROLL;  // tap-loop unroll of the U = 1 kernels
+#ifndef TILE_UNROLL
+#define TILE_UNROLL 2
+#endif
+constexpr int kTileUnroll = TILE_UNROLL;  // tap-loop unroll of k_tile (~7-12 taps per stage)
 
 // F16: f16 storage (x, y, weights; f32 accumulation by FHFMA -- f16 x f16 is exact in f32, so
 // one fma.rn.f32.f16 per MAC equals the reference's f32 mul + add); WF = the weight format
@@ -696,7 +700,7 @@ __global__ void __launch_bounds__(tile_max_threads(NB), 1) k_tile(const __grid_c
             const int cnt = *reinterpret_cast<const int*>(ch);
             const LaneTap* tp = reinterpret_cast<const LaneTap*>(ch + LANE_HDR);
             LaneTap dq = tp[0];
-#pragma unroll kLaneUnroll
+#pragma unroll kTileUnroll
             for (int t = 0; t < cnt; ++t) {
                 const LaneTap d = dq;
                 dq = tp[t + 1];  // (one past the slot's last tap: slack, never used)
